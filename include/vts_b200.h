@@ -1,0 +1,191 @@
+/*
+ * vts_b200.h — C ABI of the B200-native PBM inner Newton step.
+ *
+ * The reference (`vtsopt`, /root/reference/pkg/src/vtsopt) is pure Python and
+ * has no FFI; the path sits behind Python call signatures.
+ * Each entry point below replaces one of those call sites; the file:line of
+ * the reference interface it stands in for is given with it.  A ctypes
+ * binding (the reference-side stub a maintainer would add) is shown in
+ * INTEGRATION.md; the package `paper_1904_06556_b200` is that binding.
+ *
+ * Conventions
+ *  - Every pointer argument is a raw CUDA device pointer to contiguous fp64
+ *    (or int) data owned by the caller, unless documented as host memory.
+ *    The library borrows it for the duration of the call only.
+ *  - "free" vectors use the reference's free-dof numbering (node-major,
+ *    x then y, Dirichlet dofs skipped; mesh.py:266-267): length n, or n+1
+ *    when bordered (volume-multiplier unknown last).  Element arrays have
+ *    length m in the reference's element order (mesh.py:253-259).
+ *  - `stream` is a cudaStream_t passed as an integer (0 = legacy default).
+ *    All work is stream-ordered; calls that return host scalars synchronise
+ *    that stream.
+ *  - Return codes: VTS_OK or one of the VTS_E* codes; vts_last_error()
+ *    returns a message for the calling thread's last failure.
+ *  - A context is not thread safe; one context per problem instance.
+ */
+#ifndef VTS_B200_H
+#define VTS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VTS_OK 0
+#define VTS_E_INDEFINITE 1   /* MinresError("preconditioner is indefinite ...") linalg.py:168,205 */
+#define VTS_E_BREAKDOWN 2    /* MinresError("MINRES recurrence broke down") linalg.py:216 */
+#define VTS_E_NONFINITE 3    /* MinresError("NaN/inf encountered ...") linalg.py:227 */
+#define VTS_E_ARGUMENT 4     /* ValueError */
+#define VTS_E_CUDA 5         /* CUDA runtime failure */
+#define VTS_E_CHOLESKY 6     /* coarse Cholesky failed even after the shift (multigrid.py:102) */
+
+/* warning bits returned through `warn_flags` */
+#define VTS_W_SATURATED 1u   /* penalty input saturated (penalty.py:85-95 RuntimeWarning) */
+#define VTS_W_SHIFTED 2u     /* coarse Cholesky needed the shift (multigrid.py:95-103 log.warning) */
+
+typedef struct vts_ctx vts_ctx;
+
+const char* vts_last_error(void);
+int vts_version(void);
+
+/*
+ * Context over one mesh hierarchy.  Replaces the data the reference builds in
+ * `build_problem` / `MeshLevel` (mesh.py:216-287) and `ElementOps.__init__`
+ * (fem.py:150-162): `ex[k]`, `ey[k]` are the element counts of level k
+ * (coarsest first, each level doubling the previous one), `dof_maps[k]` is a
+ * HOST int64 array (n_nodes_k x 2) holding the free-dof index of each node
+ * component or -1 for a Dirichlet dof (MeshLevel.dof), `ke` a HOST row-major
+ * 8x8 element stiffness (fem.hex_stiffness analogue).
+ */
+int vts_ctx_create(vts_ctx** out, int32_t levels, const int32_t* ex, const int32_t* ey,
+                   const int64_t* const* dof_maps, const double* ke, int64_t stream);
+int vts_ctx_destroy(vts_ctx* ctx);
+/* n (free dofs of the finest level) and m (elements); HOST outputs */
+int vts_ctx_sizes(const vts_ctx* ctx, int64_t* n, int64_t* m);
+
+/*
+ * Augmented Lagrangian value, gradient blocks and curvatures:
+ * `eval_lagrangian` (pbm.py:150-199).  State arrays (length m) and u, f
+ * (length n) are inputs; every output array is written in full.  `w_out`
+ * (m x 8, element-local K_e u_e) may be NULL.  `scalars` (HOST, 8 doubles) =
+ * {value, res_alpha, tau_res, f.u, sum rho_hat, ||res_u||, ||res_lo||, 0}.
+ */
+int vts_eval_lagrangian(vts_ctx* ctx, const double* u, double alpha, const double* nu_lo,
+                        const double* nu_up, const double* rho, const double* mu_lo,
+                        const double* mu_up, const double* p, const double* q_lo,
+                        const double* q_up, const double* f, const double* lower,
+                        const double* upper, double volume, double norm_f, double norm_bounds,
+                        double branch, double* res_u, double* res_lo, double* res_up, double* q,
+                        double* mu_hat_lo, double* mu_hat_up, double* a, double* b_lo,
+                        double* b_up, double* rho_hat, double* w_out, double* scalars,
+                        uint32_t* warn_flags);
+
+/*
+ * Reduced (n+1) Newton system: `schur_system` (pbm.py:202-218) with the
+ * assembly `ElementOps.assemble(..., border_sign=-1)` (fem.py:188-209)
+ * replaced by a matrix-free operator bound into the context.  Inputs are the
+ * eval outputs; writes chat (m), rhs (n+1, free, bordered) and border (n,
+ * may be NULL); `corner` (HOST) = sum chat.  After this call the context
+ * holds the Newton matrix used by vts_newton_apply / vts_mg_setup /
+ * vts_minres.
+ */
+int vts_schur_system(vts_ctx* ctx, const double* u, const double* res_u, double res_alpha,
+                     const double* res_lo, const double* res_up, const double* a,
+                     const double* b_lo, const double* b_up, const double* rho_hat, double* chat,
+                     double* rhs, double* border, double* corner);
+
+/* y = S x for the bound Newton matrix: BorderedMatrix.matvec (linalg.py:56-62). */
+int vts_newton_apply(vts_ctx* ctx, const double* x, double* y);
+
+/*
+ * Galerkin hierarchy + coarsest Cholesky of the bound Newton matrix:
+ * MgPreconditioner.__init__ (multigrid.py:82-103).  HOST `shifted` = 1 when
+ * the coarse factorisation needed the trace-scaled shift.
+ */
+int vts_mg_setup(vts_ctx* ctx, double shift_scale, int32_t* shifted);
+
+/* One V(2,2) cycle from a zero guess: MgPreconditioner.apply (multigrid.py:109-143). */
+int vts_vcycle(vts_ctx* ctx, const double* b, double* z);
+
+/*
+ * Level operator probe for parity tests: y = A_k x on level k (0 = coarsest),
+ * bordered free vectors of that level (MgPreconditioner.mats[k].matvec).
+ */
+int vts_level_apply(vts_ctx* ctx, int32_t level, const double* x, double* y);
+/* free-dof count of level k (HOST output) */
+int vts_level_size(const vts_ctx* ctx, int32_t level, int64_t* n);
+
+/*
+ * Preconditioned MINRES on the bound Newton matrix with the V-cycle
+ * preconditioner: minres_solve(S, b, MinresConfig(tol, max_iters, floor),
+ * mg.apply) (linalg.py:128-242), zero initial guess.  `x` (n+1) receives the
+ * iterate (the last sound one on error).  HOST outputs: iterations, relres,
+ * converged.  `history` (HOST, may be NULL, length >= max_iters) receives the
+ * true relative residual after every iteration (costs one extra apply each).
+ */
+int vts_minres(vts_ctx* ctx, const double* b, double* x, double tol, int32_t max_iters,
+               double floor_tol, int32_t precondition, int32_t* iterations, double* relres,
+               int32_t* converged, double* history);
+
+/*
+ * Bound-multiplier back-substitution + directional derivative:
+ * reconstruct_nu (pbm.py:221-232) and the slope (pbm.py:290-295).
+ * HOST `slope` (may be NULL).
+ */
+int vts_reconstruct_nu(vts_ctx* ctx, const double* u, const double* du, double dalpha,
+                       const double* res_u, double res_alpha, const double* res_lo,
+                       const double* res_up, const double* a, const double* b_lo,
+                       const double* b_up, double* dnu_lo, double* dnu_up, double* slope);
+
+/*
+ * Augmented Lagrangian at the trial point x + kappa dx with multipliers
+ * fixed: _al_value (pbm.py:135-147) fused with the axpys of pbm.py:300-305.
+ * HOST output `value`.
+ */
+int vts_al_value(vts_ctx* ctx, const double* u, double alpha, const double* nu_lo,
+                 const double* nu_up, const double* du, double dalpha, const double* dnu_lo,
+                 const double* dnu_up, double kappa, const double* rho, const double* p,
+                 const double* mu_lo, const double* mu_up, const double* q_lo,
+                 const double* q_up, const double* f, const double* lower, const double* upper,
+                 double volume, double branch, double* value, uint32_t* warn_flags);
+
+/* x += kappa dx for the accepted Newton step (pbm.py:320-323), n and m parts. */
+int vts_axpy(vts_ctx* ctx, int64_t len, double kappa, const double* dx, double* x);
+
+/*
+ * Safeguarded multiplier / penalty update of the outer loop (pbm.py:397-402):
+ * rho <- clip(rho_hat, beta rho, rho/beta) (same for mu_lo, mu_up),
+ * p, q_lo, q_up <- max(gamma x, floor).  Pass rho_hat = NULL to skip the
+ * multiplier part, update_penalties = 0 to skip the penalty part.
+ */
+int vts_outer_update(vts_ctx* ctx, double beta, double gamma, double floor_p, const double* rho_hat,
+                     const double* mu_hat_lo, const double* mu_hat_up, double* rho, double* mu_lo,
+                     double* mu_up, double* p, double* q_lo, double* q_up, int32_t update_penalties);
+
+/*
+ * Dual objective and scaled duality gap at (u, alpha): dual_objective and
+ * duality_gap (model.py:50-79).  HOST outputs: d_val, gap (unscaled), f.u,
+ * sum(rho).
+ */
+int vts_gap(vts_ctx* ctx, const double* u, double alpha, const double* q, const double* f,
+            const double* nu_lo, const double* nu_up, const double* lower, const double* upper,
+            double volume, const double* rho, double* d_val, double* gap, double* fu,
+            double* rho_sum);
+
+/*
+ * phi, phi', phi'' of a device vector tau (length n): PenaltyBarrier.value /
+ * deriv / deriv2 (penalty.py:49-82) with the saturation rule of
+ * penalty.py:85-95 (VTS_W_SATURATED).  Output pointers may be NULL.
+ */
+int vts_penalty_eval(vts_ctx* ctx, int64_t n, const double* tau, double branch, double* value, double* d1,
+                     double* d2, uint32_t* warn_flags);
+
+/* Number of kernels this context launched since creation (evidence counter). */
+int64_t vts_kernel_launches(const vts_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VTS_B200_H */

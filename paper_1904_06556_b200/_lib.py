@@ -1,0 +1,107 @@
+"""ctypes binding of the in-tree C-ABI library `_build/libvts_b200.so`.
+
+This is the reference-side stub INTEGRATION.md describes: every entry point of
+`include/vts_b200.h` with its argument types, plus the status-code mapping to
+the reference's exception classes (`linalg.py:107-115` MinresError,
+`ValueError` for bad arguments).  There is no fallback: if the library is
+missing or fails to load, importing the product path raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_build", "libvts_b200.so")
+
+VTS_OK = 0
+VTS_E_INDEFINITE = 1
+VTS_E_BREAKDOWN = 2
+VTS_E_NONFINITE = 3
+VTS_E_ARGUMENT = 4
+VTS_E_CUDA = 5
+VTS_E_CHOLESKY = 6
+VTS_W_SATURATED = 1
+VTS_W_SHIFTED = 2
+
+_P = ctypes.c_void_p
+_D = ctypes.c_double
+_I32 = ctypes.c_int32
+_I64 = ctypes.c_int64
+_PD = ctypes.POINTER(ctypes.c_double)
+_PI32 = ctypes.POINTER(ctypes.c_int32)
+_PI64 = ctypes.POINTER(ctypes.c_int64)
+_PU32 = ctypes.POINTER(ctypes.c_uint32)
+
+# name -> (restype, argtypes); mirrors include/vts_b200.h
+SIGNATURES = {
+    "vts_last_error": (ctypes.c_char_p, []),
+    "vts_version": (ctypes.c_int, []),
+    "vts_ctx_create": (ctypes.c_int, [ctypes.POINTER(_P), _I32, _PI32, _PI32, ctypes.POINTER(_PI64), _PD, _I64]),
+    "vts_ctx_destroy": (ctypes.c_int, [_P]),
+    "vts_ctx_sizes": (ctypes.c_int, [_P, _PI64, _PI64]),
+    "vts_eval_lagrangian": (ctypes.c_int, [_P, _P, _D] + [_P] * 11 + [_D, _D, _D, _D] + [_P] * 11 + [_PD, _PU32]),
+    "vts_schur_system": (ctypes.c_int, [_P, _P, _P, _D] + [_P] * 6 + [_P, _P, _P, _PD]),
+    "vts_newton_apply": (ctypes.c_int, [_P, _P, _P]),
+    "vts_mg_setup": (ctypes.c_int, [_P, _D, _PI32]),
+    "vts_vcycle": (ctypes.c_int, [_P, _P, _P]),
+    "vts_level_apply": (ctypes.c_int, [_P, _I32, _P, _P]),
+    "vts_level_size": (ctypes.c_int, [_P, _I32, _PI64]),
+    "vts_minres": (ctypes.c_int, [_P, _P, _P, _D, _I32, _D, _I32, _PI32, _PD, _PI32, _PD]),
+    "vts_reconstruct_nu": (ctypes.c_int, [_P, _P, _P, _D, _P, _D] + [_P] * 5 + [_P, _P, _PD]),
+    "vts_al_value": (ctypes.c_int, [_P, _P, _D, _P, _P, _P, _D, _P, _P, _D] + [_P] * 9 + [_D, _D, _PD, _PU32]),
+    "vts_axpy": (ctypes.c_int, [_P, _I64, _D, _P, _P]),
+    "vts_outer_update": (ctypes.c_int, [_P, _D, _D, _D] + [_P] * 9 + [_I32]),
+    "vts_gap": (ctypes.c_int, [_P, _P, _D] + [_P] * 6 + [_D, _P, _PD, _PD, _PD, _PD]),
+    "vts_penalty_eval": (ctypes.c_int, [_P, _I64, _P, _D, _P, _P, _P, _PU32]),
+    "vts_kernel_launches": (ctypes.c_int64, [_P]),
+}
+
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile the library in-tree with nvcc for sm_100a (see Makefile)."""
+    cmd = ["make", "-s", "-C", _HERE]
+    if force:
+        subprocess.run(["make", "-s", "-C", _HERE, "clean"], check=True)
+    subprocess.run(cmd, check=True)
+    return LIB_PATH
+
+
+def load():
+    """Load the library; raises if it is missing (no CPU fallback exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"{LIB_PATH} is missing: build it with `make -C {_HERE}` "
+            "(or __graft_entry__.build()); the B200 path has no fallback"
+        )
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+class VtsError(RuntimeError):
+    """CUDA failure or internal error inside the library."""
+
+
+def last_error() -> str:
+    return load().vts_last_error().decode("utf-8", "replace")
+
+
+def check(rc: int, where: str) -> None:
+    if rc == VTS_OK:
+        return
+    msg = last_error()
+    if rc == VTS_E_ARGUMENT:
+        raise ValueError(f"{where}: {msg}")
+    raise VtsError(f"{where} failed (code {rc}): {msg}")

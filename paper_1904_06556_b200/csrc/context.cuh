@@ -1,0 +1,154 @@
+// Host-side context of the B200 PBM Newton step: mesh hierarchy, device
+// workspace, the bound Newton matrix and the multigrid hierarchy built from it.
+#pragma once
+
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "vts_common.cuh"
+
+struct VtsError {
+  int code;
+  std::string msg;
+};
+
+namespace vts {
+
+struct LevelBuf {
+  LevelDev d{};
+  int32_t* grid2free = nullptr;  // [ngrid] free index or -1
+  double* b = nullptr;           // [ngrid + 1] V-cycle right-hand side
+  double* x = nullptr;           // [ngrid + 1] V-cycle iterate
+  double* r = nullptr;           // [ngrid + 1] residual / scratch
+  unsigned long long* gs_flags = nullptr;  // GS wavefront progress, one per row group
+  int gs_groups = 0;
+};
+
+// MINRES device scalars (linalg.py:128-242 recurrences), one struct per solve
+struct MinresDev {
+  double beta1, beta, oldb, alfa, dbar, epsln, oldeps, phibar, cs, sn, phi, delta, gamma;
+  double verify_at, relres, tol, bnorm, est;
+  int iters, max_iters, stopped, status, no_verify, pad;
+};
+
+enum MinresStatus { kRunning = 0, kConverged = 1, kCap = 2, kIndefinite = -1, kBreakdown = -2, kNonfinite = -3 };
+
+struct Ctx {
+  int L = 0;                    // number of levels (index 0 = coarsest)
+  std::vector<LevelBuf> lv;
+  cudaStream_t stream = nullptr;
+  int n = 0, m = 0;             // finest free dofs, elements
+  double ke[64];
+
+  // bound Newton matrix (finest level)
+  double* u_grid = nullptr;     // [ngrid]
+  double* rho_hat = nullptr;    // [m]
+  double* chat = nullptr;       // [m]
+  double corner = 0.0;
+  double* d_corner = nullptr;   // device copy of corner
+  bool system_bound = false;
+  bool mg_ready = false;
+  int shifted = 0;
+
+  // coarsest dense Cholesky (free order + border)
+  int N0 = 0;
+  double* chol = nullptr;       // [N0 * N0] lower factor (row-major)
+  int* chol_status = nullptr;   // device status
+
+  double* rap_tmp = nullptr;    // unsymmetrised coarse stencil of the largest coarse level
+
+  // finest-level grid work vectors (ngrid + 1 each)
+  std::vector<double*> fvec;
+
+  // reductions
+  double* partials = nullptr;   // [kMaxBlocks * kMaxPartials]
+  unsigned int* counters = nullptr;  // last-block counters
+  double* dscal = nullptr;      // device scalars [64]
+  double* hscal = nullptr;      // pinned host scalars [64]
+  unsigned* dflags = nullptr;   // device warning flags
+  MinresDev* mst = nullptr;     // device MINRES state
+  MinresDev* hmst = nullptr;    // pinned host mirror
+
+  long long launches = 0;
+};
+
+constexpr int kMaxBlocks = 8192;
+constexpr int kMaxPartials = 16;
+constexpr int kNumFineVecs = 14;
+
+// ---- error plumbing (capi.cu) ----
+void set_error(int code, const std::string& msg);
+int cuda_check(cudaError_t e, const char* what);
+#define VTS_CUDA(call)                                   \
+  do {                                                   \
+    cudaError_t _e = (call);                             \
+    if (_e != cudaSuccess) return cuda_check(_e, #call); \
+  } while (0)
+#define VTS_LAUNCHED(ctx)                                     \
+  do {                                                        \
+    (ctx)->launches++;                                        \
+    cudaError_t _e = cudaGetLastError();                      \
+    if (_e != cudaSuccess) return cuda_check(_e, "launch");   \
+  } while (0)
+
+inline int div_up(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+// ---- element / nodal passes (elem_kernels.cu) ----
+int free_to_grid(Ctx* c, int level, const double* src, double* dst, bool bordered);
+int grid_to_free(Ctx* c, int level, const double* src, double* dst, bool bordered);
+int eval_lagrangian(Ctx* c, const double* u, double alpha, const double* nu_lo, const double* nu_up,
+                    const double* rho, const double* mu_lo, const double* mu_up, const double* p,
+                    const double* q_lo, const double* q_up, const double* f, const double* lower,
+                    const double* upper, double volume, double norm_f, double norm_bounds,
+                    double branch, double* res_u, double* res_lo, double* res_up, double* q,
+                    double* mu_hat_lo, double* mu_hat_up, double* a, double* b_lo, double* b_up,
+                    double* rho_hat, double* w_out, double* scalars, unsigned* warn);
+int schur_system(Ctx* c, const double* u, const double* res_u, double res_alpha,
+                 const double* res_lo, const double* res_up, const double* a, const double* b_lo,
+                 const double* b_up, const double* rho_hat, double* chat, double* rhs,
+                 double* border, double* corner);
+int reconstruct_nu(Ctx* c, const double* u, const double* du, double dalpha, const double* res_u,
+                   double res_alpha, const double* res_lo, const double* res_up, const double* a,
+                   const double* b_lo, const double* b_up, double* dnu_lo, double* dnu_up,
+                   double* slope);
+int al_value(Ctx* c, const double* u, double alpha, const double* nu_lo, const double* nu_up,
+             const double* du, double dalpha, const double* dnu_lo, const double* dnu_up,
+             double kappa, const double* rho, const double* p, const double* mu_lo,
+             const double* mu_up, const double* q_lo, const double* q_up, const double* f,
+             const double* lower, const double* upper, double volume, double branch,
+             double* value, unsigned* warn);
+int axpy(Ctx* c, long long len, double kappa, const double* dx, double* x);
+int penalty_eval(Ctx* c, long long n, const double* tau, double branch, double* v, double* d1, double* d2,
+                 unsigned* warn);
+int outer_update(Ctx* c, double beta, double gamma, double floor_p, const double* rho_hat,
+                 const double* mu_hat_lo, const double* mu_hat_up, double* rho, double* mu_lo,
+                 double* mu_up, double* p, double* q_lo, double* q_up, int update_penalties);
+int gap(Ctx* c, const double* u, double alpha, const double* q, const double* f,
+        const double* nu_lo, const double* nu_up, const double* lower, const double* upper,
+        double volume, const double* rho, double* d_val, double* gap, double* fu,
+        double* rho_sum);
+
+// ---- operators (apply.cu) ----
+// y = S x on grid-layout bordered vectors of the finest level (matrix free)
+int newton_apply_grid(Ctx* c, const double* x, double* y, const int* skip);
+// y = A_k x on grid-layout bordered vectors of level k (stencil)
+int level_apply_grid(Ctx* c, int k, const double* x, double* y, const int* skip);
+int level_residual_grid(Ctx* c, int k, const double* x, const double* b, double* r, const int* skip);
+
+// ---- multigrid (mg.cu) ----
+int mg_setup(Ctx* c, double shift_scale);
+int vcycle_grid(Ctx* c, const double* b, double* z, const int* skip);
+
+// ---- MINRES (minres.cu) ----
+int minres(Ctx* c, const double* b_free, double* x_free, double tol, int max_iters,
+           double floor_tol, int precondition, int* iters, double* relres, int* converged,
+           double* history);
+
+// ---- generic reductions (elem_kernels.cu) ----
+// dot of two grid vectors (free dofs only are nonzero) incl. the border slot
+// when `bordered`; result written to dst (device) ; deterministic.
+int dot_grid(Ctx* c, int level, const double* a, const double* b, bool bordered, double* dst,
+             const int* skip);
+
+}  // namespace vts

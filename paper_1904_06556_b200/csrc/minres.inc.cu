@@ -1,0 +1,376 @@
+// Preconditioned MINRES on the bound Newton matrix (unity-built).
+//
+// minres_solve (linalg.py:128-242) with every vector on the device in the
+// grid layout and every scalar of the Lanczos/Givens recurrence in a device
+// struct (MinresDev).  One iteration is a fixed launch sequence
+//   scale -> apply -> lanczos(+alfa) -> axpy -> V-cycle -> givens(beta) ->
+//   update(w, x) -> [verify: apply -> residual norm]
+// whose kernels return immediately once the device-side `stopped` flag is
+// set, so the host only polls that flag and never re-derives a scalar.
+// The vector kernels fuse the reference's updates with the dot products that
+// follow them (fixed-order block trees, last-block finish).
+
+namespace vts {
+
+__global__ void k_mr_scale(int len, const double* __restrict__ y, double* __restrict__ v, const MinresDev* st) {
+  if (st->stopped) return;
+  const double s = 1.0 / st->beta;  // linalg.py:193-194
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x) v[i] = s * y[i];
+}
+
+// y = y - (beta/oldb) r1 (iteration >= 2), alfa = v.y   (linalg.py:196-198)
+__global__ void k_mr_lanczos(int len, double* __restrict__ y, const double* __restrict__ r1,
+                             const double* __restrict__ v, MinresDev* st, double* partials, unsigned* counter) {
+  if (st->stopped) return;
+  __shared__ double scratch[kThreads / 32];
+  const bool second = st->iters >= 1;  // st->iters counts completed iterations
+  const double f = second ? st->beta / st->oldb : 0.0;
+  double acc[1] = {0.0};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x) {
+    double yi = y[i];
+    if (second) yi = __dsub_rn(yi, __dmul_rn(f, r1[i]));
+    y[i] = yi;
+    acc[0] = fma(v[i], yi, acc[0]);
+  }
+  double tot[1];
+  if (last_block_reduce<1>(acc, scratch, partials, counter, tot) && threadIdx.x == 0) st->alfa = tot[0];
+}
+
+// y = y - (alfa/beta) r2   (linalg.py:199)
+__global__ void k_mr_axpy2(int len, double* __restrict__ y, const double* __restrict__ r2, const MinresDev* st) {
+  if (st->stopped) return;
+  const double f = st->alfa / st->beta;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x)
+    y[i] = __dsub_rn(y[i], __dmul_rn(f, r2[i]));
+}
+
+// beta = r2.y, then the Givens update of linalg.py:203-221 (last block)
+__global__ void k_mr_givens(int len, const double* __restrict__ r2, const double* __restrict__ y, MinresDev* st,
+                            double* partials, unsigned* counter) {
+  if (st->stopped) return;
+  __shared__ double scratch[kThreads / 32];
+  double acc[1] = {0.0};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x)
+    acc[0] = fma(r2[i], y[i], acc[0]);
+  double tot[1];
+  if (last_block_reduce<1>(acc, scratch, partials, counter, tot) && threadIdx.x == 0) {
+    st->oldb = st->beta;
+    double beta = tot[0];
+    if (beta < 0.0) {
+      st->status = kIndefinite;
+      st->stopped = 1;
+      st->no_verify = 1;
+      return;
+    }
+    beta = sqrt(beta);
+    st->beta = beta;
+    const double oldeps = st->epsln;
+    const double delta = st->cs * st->dbar + st->sn * st->alfa;
+    const double gbar = st->sn * st->dbar - st->cs * st->alfa;
+    st->epsln = st->sn * beta;
+    st->dbar = -st->cs * beta;
+    const double gamma = sqrt(gbar * gbar + beta * beta);
+    st->oldeps = oldeps;
+    st->delta = delta;
+    st->gamma = gamma;
+    if (!isfinite(gamma) || gamma == 0.0) {
+      st->status = kBreakdown;
+      st->stopped = 1;
+      st->no_verify = 1;
+      return;
+    }
+    st->cs = gbar / gamma;
+    st->sn = beta / gamma;
+    st->phi = st->cs * st->phibar;
+    st->phibar = st->sn * st->phibar;
+  }
+}
+
+// w_new = (v - oldeps w1 - delta w2)/gamma ; x_new = x + phi w_new  (linalg.py:223-229)
+__global__ void k_mr_update(int len, const double* __restrict__ v, const double* __restrict__ w1,
+                            const double* __restrict__ w2, double* __restrict__ wn, const double* __restrict__ x,
+                            double* __restrict__ xn, MinresDev* st, double* partials, unsigned* counter) {
+  if (st->stopped) return;
+  __shared__ double scratch[kThreads / 32];
+  const double oldeps = st->oldeps, delta = st->delta, gamma = st->gamma, phi = st->phi;
+  double acc[1] = {0.0};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x) {
+    const double w = __dsub_rn(__dsub_rn(v[i], __dmul_rn(oldeps, w1[i])), __dmul_rn(delta, w2[i])) / gamma;
+    wn[i] = w;
+    const double xv = __dadd_rn(x[i], __dmul_rn(phi, w));
+    xn[i] = xv;
+    if (!isfinite(xv)) acc[0] = 1.0;
+  }
+  double tot[1];
+  if (last_block_reduce<1>(acc, scratch, partials, counter, tot) && threadIdx.x == 0) {
+    st->iters += 1;
+    if (tot[0] != 0.0 || !isfinite(st->phibar)) {
+      st->status = kNonfinite;
+      st->stopped = 1;
+      st->no_verify = 1;
+      return;
+    }
+    const double est = st->phibar / st->beta1;
+    st->est = est;
+    st->no_verify = (est <= st->verify_at) ? 0 : 1;
+    if (st->no_verify && st->iters >= st->max_iters) {
+      st->status = kCap;
+      st->stopped = 1;
+    }
+  }
+}
+
+// true residual after a verify apply: relres = ||b - Ax|| / ||b||  (linalg.py:231-239)
+__global__ void k_mr_verify(int len, const double* __restrict__ b, const double* __restrict__ ax, MinresDev* st,
+                            double* partials, unsigned* counter) {
+  if (st->no_verify) return;
+  __shared__ double scratch[kThreads / 32];
+  double acc[1] = {0.0};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x) {
+    const double r = b[i] - ax[i];
+    acc[0] = fma(r, r, acc[0]);
+  }
+  double tot[1];
+  if (last_block_reduce<1>(acc, scratch, partials, counter, tot) && threadIdx.x == 0) {
+    const double rel = sqrt(tot[0]) / st->bnorm;
+    st->relres = rel;
+    st->no_verify = 1;
+    if (rel <= st->tol) {
+      st->status = kConverged;
+      st->stopped = 1;
+      return;
+    }
+    st->verify_at = st->est * fmin(0.5, st->tol / rel);
+    if (st->iters >= st->max_iters) {
+      st->status = kCap;
+      st->stopped = 1;
+    }
+  }
+}
+
+// history hook: ||b - A x|| / ||b|| after every iteration (tests only)
+__global__ void k_mr_history(int len, const double* __restrict__ b, const double* __restrict__ ax,
+                             const MinresDev* st, double* hist, double* partials, unsigned* counter) {
+  __shared__ double scratch[kThreads / 32];
+  double acc[1] = {0.0};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x) {
+    const double r = b[i] - ax[i];
+    acc[0] = fma(r, r, acc[0]);
+  }
+  double tot[1];
+  if (last_block_reduce<1>(acc, scratch, partials, counter, tot) && threadIdx.x == 0)
+    hist[0] = sqrt(tot[0]) / st->bnorm;
+}
+
+__global__ void k_norm2(int len, const double* __restrict__ a, double* out, double* partials, unsigned* counter) {
+  __shared__ double scratch[kThreads / 32];
+  double acc[1] = {0.0};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x)
+    acc[0] = fma(a[i], a[i], acc[0]);
+  double tot[1];
+  if (last_block_reduce<1>(acc, scratch, partials, counter, tot) && threadIdx.x == 0) *out = tot[0];
+}
+
+__global__ void k_resnorm(int len, const double* __restrict__ b, const double* __restrict__ ax, double* out,
+                          double* partials, unsigned* counter) {
+  __shared__ double scratch[kThreads / 32];
+  double acc[1] = {0.0};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x) {
+    const double r = b[i] - ax[i];
+    acc[0] = fma(r, r, acc[0]);
+  }
+  double tot[1];
+  if (last_block_reduce<1>(acc, scratch, partials, counter, tot) && threadIdx.x == 0) *out = tot[0];
+}
+
+static int read_state(Ctx* c) {
+  VTS_CUDA(cudaMemcpyAsync(c->hmst, c->mst, sizeof(MinresDev), cudaMemcpyDeviceToHost, c->stream));
+  VTS_CUDA(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int minres(Ctx* c, const double* b_free, double* x_free, double tol, int max_iters, double floor_tol,
+           int precondition, int* iters_out, double* relres_out, int* conv_out, double* history) {
+  (void)floor_tol;  // only used with a warm start, which this entry point does not take
+  if (!c->system_bound || (precondition && !c->mg_ready)) {
+    set_error(4, "minres: bind the Newton system (and set up the multigrid) first");
+    return 4;
+  }
+  const int F = c->L - 1;
+  const int len = c->lv[F].d.ngrid + 1;
+  const int grid = (int)std::min<long long>(div_up(len, kThreads), kReduceGridCap);
+  double* B = c->fvec[4];
+  double* pool[8] = {c->fvec[5], c->fvec[6], c->fvec[7], c->fvec[8], c->fvec[9], c->fvec[10], c->fvec[11], c->fvec[13]};
+  double* W[3] = {c->fvec[1], c->fvec[2], c->fvec[3]};
+  double* X[2] = {c->fvec[0], c->fvec[12]};
+  double* T = c->lv[F].r;  // verify / history apply target
+  if (int rc = free_to_grid(c, F, b_free, B, true)) return rc;
+  k_norm2<<<grid, kThreads, 0, c->stream>>>(len, B, c->dscal + 30, c->partials, c->counters + 7);
+  VTS_LAUNCHED(c);
+  VTS_CUDA(cudaMemcpyAsync(c->hscal + 30, c->dscal + 30, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  VTS_CUDA(cudaStreamSynchronize(c->stream));
+  const double bnorm = sqrt(c->hscal[30]);
+  const int n = c->n;
+  const int cap = max_iters > 0 ? max_iters : 3 * (n + 1);
+  if (bnorm == 0.0) {
+    VTS_CUDA(cudaMemsetAsync(x_free, 0, sizeof(double) * (n + 1), c->stream));
+    *iters_out = 0;
+    *relres_out = 0.0;
+    *conv_out = 1;
+    return 0;
+  }
+  // r1 = b (copy), y = M r1
+  double* r1 = pool[0];
+  double* y = pool[1];
+  VTS_CUDA(cudaMemcpyAsync(r1, B, sizeof(double) * len, cudaMemcpyDeviceToDevice, c->stream));
+  if (precondition) {
+    if (int rc = vcycle_grid(c, r1, y, nullptr)) return rc;
+  } else {
+    VTS_CUDA(cudaMemcpyAsync(y, r1, sizeof(double) * len, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  {
+    // beta1 = r1 . y
+    k_dot<<<grid, kThreads, 0, c->stream>>>(len, r1, y, c->partials, c->counters + 0, c->dscal + 31, nullptr);
+    VTS_LAUNCHED(c);
+    VTS_CUDA(cudaMemcpyAsync(c->hscal + 31, c->dscal + 31, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    VTS_CUDA(cudaStreamSynchronize(c->stream));
+  }
+  double beta1 = c->hscal[31];
+  VTS_CUDA(cudaMemsetAsync(X[0], 0, sizeof(double) * len, c->stream));
+  if (beta1 < 0.0) {
+    VTS_CUDA(cudaMemsetAsync(x_free, 0, sizeof(double) * (n + 1), c->stream));
+    set_error(1, "preconditioner is indefinite: <M r, r> < 0");
+    return 1;
+  }
+  if (beta1 == 0.0) {
+    VTS_CUDA(cudaMemsetAsync(x_free, 0, sizeof(double) * (n + 1), c->stream));
+    *iters_out = 0;
+    *relres_out = 1.0;  // ||b - A 0|| / ||b||
+    *conv_out = 1;
+    return 0;
+  }
+  beta1 = sqrt(beta1);
+  MinresDev h{};
+  h.beta1 = beta1;
+  h.beta = beta1;
+  h.oldb = 0.0;
+  h.dbar = 0.0;
+  h.epsln = 0.0;
+  h.phibar = beta1;
+  h.cs = -1.0;
+  h.sn = 0.0;
+  h.verify_at = tol;
+  h.relres = INFINITY;
+  h.tol = tol;
+  h.bnorm = bnorm;
+  h.iters = 0;
+  h.max_iters = cap;
+  h.stopped = 0;
+  h.status = kRunning;
+  h.no_verify = 1;
+  *c->hmst = h;
+  VTS_CUDA(cudaMemcpyAsync(c->mst, c->hmst, sizeof(MinresDev), cudaMemcpyHostToDevice, c->stream));
+  VTS_CUDA(cudaMemsetAsync(W[0], 0, sizeof(double) * len, c->stream));
+  VTS_CUDA(cudaMemsetAsync(W[1], 0, sizeof(double) * len, c->stream));
+  // buffers: r1 and r2 alias at the start (linalg.py:189)
+  double* r2 = r1;
+  double* v = pool[2];
+  double* w = W[0];   // current w
+  double* w2 = W[1];  // current w2
+  double* wfree = W[2];
+  double* x = X[0];
+  double* xalt = X[1];
+  std::vector<double*> freeb = {pool[3], pool[4], pool[5], pool[6], pool[7]};
+  const int* stopped = &c->mst->stopped;
+  const int* nover = &c->mst->no_verify;
+  std::vector<double> hist_host;
+  double* dhist = c->dscal + 32;  // latest history entry, read back every iteration
+  int status = kRunning;
+  for (int it = 0; it < cap; ++it) {
+    k_mr_scale<<<grid, kThreads, 0, c->stream>>>(len, y, v, c->mst);
+    VTS_LAUNCHED(c);
+    if (int rc = newton_apply_grid(c, v, y, stopped)) return rc;
+    k_mr_lanczos<<<grid, kThreads, 0, c->stream>>>(len, y, r1, v, c->mst, c->partials, c->counters + 8);
+    VTS_LAUNCHED(c);
+    k_mr_axpy2<<<grid, kThreads, 0, c->stream>>>(len, y, r2, c->mst);
+    VTS_LAUNCHED(c);
+    // r1 = r2 ; r2 = y ; new y buffer
+    double* dead = (r1 == r2) ? nullptr : r1;
+    r1 = r2;
+    r2 = y;
+    if (dead) freeb.push_back(dead);
+    y = freeb.back();
+    freeb.pop_back();
+    if (precondition) {
+      if (int rc = vcycle_grid(c, r2, y, stopped)) return rc;
+    } else {
+      VTS_CUDA(cudaMemcpyAsync(y, r2, sizeof(double) * len, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    k_mr_givens<<<grid, kThreads, 0, c->stream>>>(len, r2, y, c->mst, c->partials, c->counters + 9);
+    VTS_LAUNCHED(c);
+    // w1 = w2 ; w2 = w ; w = new (into the dead w1 buffer)
+    double* w1 = w2;
+    w2 = w;
+    double* wn = wfree;
+    k_mr_update<<<grid, kThreads, 0, c->stream>>>(len, v, w1, w2, wn, x, xalt, c->mst, c->partials,
+                                                  c->counters + 10);
+    VTS_LAUNCHED(c);
+    wfree = w1;
+    w = wn;
+    if (history) {
+      if (int rc = newton_apply_grid(c, xalt, T, nullptr)) return rc;
+      k_mr_history<<<grid, kThreads, 0, c->stream>>>(len, B, T, c->mst, dhist, c->partials, c->counters + 11);
+      VTS_LAUNCHED(c);
+    }
+    if (int rc = newton_apply_grid(c, xalt, T, nover)) return rc;
+    k_mr_verify<<<grid, kThreads, 0, c->stream>>>(len, B, T, c->mst, c->partials, c->counters + 12);
+    VTS_LAUNCHED(c);
+    if (int rc = read_state(c)) return rc;
+    const MinresDev& s = *c->hmst;
+    if (s.status == kIndefinite || s.status == kBreakdown || s.status == kNonfinite) {
+      status = s.status;
+      break;
+    }
+    // the update succeeded: x <- x_new
+    std::swap(x, xalt);
+    if (history) {
+      double hv;
+      VTS_CUDA(cudaMemcpy(&hv, dhist, sizeof(double), cudaMemcpyDeviceToHost));
+      history[s.iters - 1] = hv;
+    }
+    if (s.stopped) {
+      status = s.status;
+      break;
+    }
+  }
+  if (status == kRunning) status = kCap;
+  const MinresDev& s = *c->hmst;
+  double relres = s.relres;
+  if (status == kCap) {
+    if (int rc = newton_apply_grid(c, x, T, nullptr)) return rc;
+    k_resnorm<<<grid, kThreads, 0, c->stream>>>(len, B, T, c->dscal + 31, c->partials, c->counters + 7);
+    VTS_LAUNCHED(c);
+    VTS_CUDA(cudaMemcpyAsync(c->hscal + 31, c->dscal + 31, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    VTS_CUDA(cudaStreamSynchronize(c->stream));
+    relres = sqrt(c->hscal[31]) / bnorm;
+  }
+  if (int rc = grid_to_free(c, F, x, x_free, true)) return rc;
+  *iters_out = s.iters;
+  *relres_out = relres;
+  *conv_out = (status == kConverged) || (status == kCap && relres <= tol);
+  if (status == kIndefinite) {
+    set_error(1, "preconditioner is indefinite: <M r, r> < 0");
+    return 1;
+  }
+  if (status == kBreakdown) {
+    set_error(2, "MINRES recurrence broke down");
+    return 2;
+  }
+  if (status == kNonfinite) {
+    set_error(3, "NaN/inf encountered in MINRES recurrences");
+    return 3;
+  }
+  return 0;
+}
+
+}  // namespace vts

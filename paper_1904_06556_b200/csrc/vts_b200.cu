@@ -1,0 +1,401 @@
+// libvts_b200 — B200-native PBM inner Newton step behind a C ABI.
+//
+// Unity build: every kernel file is included here so the element stiffness
+// can live in one __constant__ symbol without relocatable device code.
+// See include/vts_b200.h for the entry points and the reference interfaces
+// they replace, DESIGN.md for the data layout and the kernels' rooflines.
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/vts_b200.h"
+#include "context.cuh"
+
+#include "elem_kernels.inc.cu"
+#include "apply.inc.cu"
+#include "mg.inc.cu"
+#include "minres.inc.cu"
+
+namespace vts {
+
+static thread_local std::string g_last_error;
+static std::mutex g_ke_mutex;
+static const Ctx* g_ke_owner = nullptr;
+
+void set_error(int code, const std::string& msg) {
+  (void)code;
+  g_last_error = msg;
+}
+
+int cuda_check(cudaError_t e, const char* what) {
+  set_error(VTS_E_CUDA, std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+  return VTS_E_CUDA;
+}
+
+// the element stiffness is a module-wide constant; contexts with different K_e
+// re-upload it (stream-ordered) before their kernels run
+static int ensure_ke(Ctx* c) {
+  std::lock_guard<std::mutex> lock(g_ke_mutex);
+  if (g_ke_owner == c) return 0;
+  VTS_CUDA(cudaMemcpyToSymbolAsync(c_ke, c->ke, sizeof(double) * 64, 0, cudaMemcpyHostToDevice, c->stream));
+  g_ke_owner = c;
+  return 0;
+}
+
+template <typename T>
+static int dalloc(T** p, size_t count) {
+  VTS_CUDA(cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T)));
+  return 0;
+}
+
+static void free_ctx(Ctx* c) {
+  for (auto& L : c->lv) {
+    cudaFree(const_cast<uint8_t*>(L.d.free_mask));
+    cudaFree(const_cast<int32_t*>(L.d.free2grid));
+    cudaFree(L.d.stencil);
+    cudaFree(L.d.border);
+    cudaFree(L.grid2free);
+    cudaFree(L.b);
+    cudaFree(L.x);
+    cudaFree(L.r);
+    cudaFree(L.gs_flags);
+  }
+  for (double* p : c->fvec) cudaFree(p);
+  cudaFree(c->u_grid);
+  cudaFree(c->rho_hat);
+  cudaFree(c->chat);
+  cudaFree(c->d_corner);
+  cudaFree(c->chol);
+  cudaFree(c->chol_status);
+  cudaFree(c->rap_tmp);
+  cudaFree(c->partials);
+  cudaFree(c->counters);
+  cudaFree(c->dscal);
+  cudaFree(c->dflags);
+  cudaFree(c->mst);
+  if (c->hscal) cudaFreeHost(c->hscal);
+  if (c->hmst) cudaFreeHost(c->hmst);
+  {
+    std::lock_guard<std::mutex> lock(g_ke_mutex);
+    if (g_ke_owner == c) g_ke_owner = nullptr;
+  }
+  delete c;
+}
+
+static int create(Ctx** out, int levels, const int32_t* ex, const int32_t* ey, const int64_t* const* dof_maps,
+                  const double* ke, int64_t stream) {
+  if (levels < 1 || !ex || !ey || !dof_maps || !ke || !out) {
+    set_error(VTS_E_ARGUMENT, "vts_ctx_create: bad arguments");
+    return VTS_E_ARGUMENT;
+  }
+  for (int k = 0; k < levels; ++k) {
+    if (ex[k] < 1 || ey[k] < 1) {
+      set_error(VTS_E_ARGUMENT, "vts_ctx_create: element counts must be positive");
+      return VTS_E_ARGUMENT;
+    }
+    if (k > 0 && (ex[k] != 2 * ex[k - 1] || ey[k] != 2 * ey[k - 1])) {
+      set_error(VTS_E_ARGUMENT, "vts_ctx_create: each level must refine the previous one by 2 per axis");
+      return VTS_E_ARGUMENT;
+    }
+  }
+  Ctx* c = new Ctx();
+  c->L = levels;
+  c->stream = reinterpret_cast<cudaStream_t>(stream);
+  std::memcpy(c->ke, ke, sizeof(double) * 64);
+  c->lv.resize(levels);
+  auto fail = [&](int rc) {
+    free_ctx(c);
+    return rc;
+  };
+  for (int k = 0; k < levels; ++k) {
+    LevelBuf& L = c->lv[k];
+    L.d.ex = ex[k];
+    L.d.ey = ey[k];
+    L.d.nx = ex[k] + 1;
+    L.d.ny = ey[k] + 1;
+    L.d.nnodes = L.d.nx * L.d.ny;
+    L.d.ngrid = 2 * L.d.nnodes;
+    const int ng = L.d.ngrid;
+    std::vector<uint8_t> mask(ng);
+    std::vector<int32_t> g2f(ng);
+    std::vector<int32_t> f2g;
+    f2g.reserve(ng);
+    int nfree = 0;
+    for (int i = 0; i < ng; ++i) {
+      const int64_t d = dof_maps[k][i];
+      if (d >= 0) {
+        if (d != nfree) {
+          set_error(VTS_E_ARGUMENT, "vts_ctx_create: dof map must number free dofs node-major in order");
+          return fail(VTS_E_ARGUMENT);
+        }
+        mask[i] = 1;
+        g2f[i] = nfree++;
+        f2g.push_back(i);
+      } else {
+        mask[i] = 0;
+        g2f[i] = -1;
+      }
+    }
+    if (nfree == 0) {
+      set_error(VTS_E_ARGUMENT, "vts_ctx_create: a level has no free dofs");
+      return fail(VTS_E_ARGUMENT);
+    }
+    L.d.nfree = nfree;
+    uint8_t* fm_d = nullptr;
+    int32_t* f2g_d = nullptr;
+    const int arc = dalloc(&fm_d, ng) || dalloc(&f2g_d, nfree);
+    L.d.free_mask = fm_d;
+    L.d.free2grid = f2g_d;
+    if (arc || dalloc(&L.grid2free, ng) ||
+        dalloc(&L.d.stencil, (size_t)L.d.nnodes * kStencilStride) || dalloc(&L.d.border, ng + 1) ||
+        dalloc(&L.b, ng + 1) || dalloc(&L.x, ng + 1) || dalloc(&L.r, ng + 1))
+      return fail(VTS_E_CUDA);
+    L.gs_groups = div_up(L.d.ny, 32);
+    if (dalloc(&L.gs_flags, L.gs_groups)) return fail(VTS_E_CUDA);
+    if (cudaMemcpy(const_cast<uint8_t*>(L.d.free_mask), mask.data(), ng, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(const_cast<int32_t*>(L.d.free2grid), f2g.data(), sizeof(int32_t) * nfree, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(L.grid2free, g2f.data(), sizeof(int32_t) * ng, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemset(L.gs_flags, 0, sizeof(unsigned long long) * L.gs_groups) != cudaSuccess ||
+        cudaMemset(L.d.stencil, 0, sizeof(double) * (size_t)L.d.nnodes * kStencilStride) != cudaSuccess ||
+        cudaMemset(L.d.border, 0, sizeof(double) * (ng + 1)) != cudaSuccess ||
+        cudaMemset(L.b, 0, sizeof(double) * (ng + 1)) != cudaSuccess ||
+        cudaMemset(L.x, 0, sizeof(double) * (ng + 1)) != cudaSuccess ||
+        cudaMemset(L.r, 0, sizeof(double) * (ng + 1)) != cudaSuccess) {
+      set_error(VTS_E_CUDA, "vts_ctx_create: device upload failed");
+      return fail(VTS_E_CUDA);
+    }
+  }
+  const LevelBuf& F = c->lv[levels - 1];
+  c->n = F.d.nfree;
+  c->m = F.d.ex * F.d.ey;
+  const int len = F.d.ngrid + 1;
+  c->fvec.assign(kNumFineVecs, nullptr);
+  for (int i = 0; i < kNumFineVecs; ++i) {
+    if (dalloc(&c->fvec[i], std::max(len, c->m + 1))) return fail(VTS_E_CUDA);
+    cudaMemset(c->fvec[i], 0, sizeof(double) * std::max(len, c->m + 1));
+  }
+  if (dalloc(&c->u_grid, len) || dalloc(&c->rho_hat, c->m) || dalloc(&c->chat, c->m) || dalloc(&c->d_corner, 1))
+    return fail(VTS_E_CUDA);
+  c->N0 = c->lv[0].d.nfree + 1;
+  if (dalloc(&c->chol, (size_t)c->N0 * c->N0) || dalloc(&c->chol_status, 1)) return fail(VTS_E_CUDA);
+  const size_t rap = levels > 1 ? (size_t)c->lv[levels - 2].d.nnodes * kStencilStride : 1;
+  if (dalloc(&c->rap_tmp, rap)) return fail(VTS_E_CUDA);
+  if (dalloc(&c->partials, (size_t)kMaxBlocks * kMaxPartials) || dalloc(&c->counters, 64) ||
+      dalloc(&c->dscal, 64) || dalloc(&c->dflags, 4) || dalloc(&c->mst, 1))
+    return fail(VTS_E_CUDA);
+  cudaMemset(c->counters, 0, sizeof(unsigned) * 64);
+  cudaMemset(c->dscal, 0, sizeof(double) * 64);
+  if (cudaMallocHost(reinterpret_cast<void**>(&c->hscal), sizeof(double) * 64) != cudaSuccess ||
+      cudaMallocHost(reinterpret_cast<void**>(&c->hmst), sizeof(MinresDev)) != cudaSuccess) {
+    set_error(VTS_E_CUDA, "vts_ctx_create: pinned allocation failed");
+    return fail(VTS_E_CUDA);
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    set_error(VTS_E_CUDA, "vts_ctx_create: device synchronisation failed");
+    return fail(VTS_E_CUDA);
+  }
+  *out = c;
+  return 0;
+}
+
+}  // namespace vts
+
+using vts::Ctx;
+using vts::cuda_check;
+
+struct vts_ctx {
+  Ctx impl;
+};
+
+static Ctx* C(vts_ctx* p) { return reinterpret_cast<Ctx*>(p); }
+static const Ctx* C(const vts_ctx* p) { return reinterpret_cast<const Ctx*>(p); }
+
+#define VTS_REQUIRE_CTX(ctx)                                 \
+  do {                                                       \
+    if (!(ctx)) {                                            \
+      vts::set_error(VTS_E_ARGUMENT, "null context");       \
+      return VTS_E_ARGUMENT;                                 \
+    }                                                        \
+    if (int _rc = vts::ensure_ke(C(ctx))) return _rc;        \
+  } while (0)
+
+extern "C" {
+
+const char* vts_last_error(void) { return vts::g_last_error.c_str(); }
+
+int vts_version(void) { return 1; }
+
+int vts_ctx_create(vts_ctx** out, int32_t levels, const int32_t* ex, const int32_t* ey,
+                   const int64_t* const* dof_maps, const double* ke, int64_t stream) {
+  Ctx* c = nullptr;
+  const int rc = vts::create(&c, levels, ex, ey, dof_maps, ke, stream);
+  if (rc) return rc;
+  *out = reinterpret_cast<vts_ctx*>(c);
+  return 0;
+}
+
+int vts_ctx_destroy(vts_ctx* ctx) {
+  if (ctx) vts::free_ctx(C(ctx));
+  return 0;
+}
+
+int vts_ctx_sizes(const vts_ctx* ctx, int64_t* n, int64_t* m) {
+  if (!ctx) return VTS_E_ARGUMENT;
+  if (n) *n = C(ctx)->n;
+  if (m) *m = C(ctx)->m;
+  return 0;
+}
+
+int vts_level_size(const vts_ctx* ctx, int32_t level, int64_t* n) {
+  if (!ctx || level < 0 || level >= C(ctx)->L) return VTS_E_ARGUMENT;
+  *n = C(ctx)->lv[level].d.nfree;
+  return 0;
+}
+
+int vts_eval_lagrangian(vts_ctx* ctx, const double* u, double alpha, const double* nu_lo, const double* nu_up,
+                        const double* rho, const double* mu_lo, const double* mu_up, const double* p,
+                        const double* q_lo, const double* q_up, const double* f, const double* lower,
+                        const double* upper, double volume, double norm_f, double norm_bounds, double branch,
+                        double* res_u, double* res_lo, double* res_up, double* q, double* mu_hat_lo,
+                        double* mu_hat_up, double* a, double* b_lo, double* b_up, double* rho_hat, double* w_out,
+                        double* scalars, uint32_t* warn_flags) {
+  VTS_REQUIRE_CTX(ctx);
+  unsigned warn = 0;
+  const int rc = vts::eval_lagrangian(C(ctx), u, alpha, nu_lo, nu_up, rho, mu_lo, mu_up, p, q_lo, q_up, f, lower,
+                                      upper, volume, norm_f, norm_bounds, branch, res_u, res_lo, res_up, q,
+                                      mu_hat_lo, mu_hat_up, a, b_lo, b_up, rho_hat, w_out, scalars, &warn);
+  if (warn_flags) *warn_flags = warn ? VTS_W_SATURATED : 0u;
+  return rc;
+}
+
+int vts_schur_system(vts_ctx* ctx, const double* u, const double* res_u, double res_alpha, const double* res_lo,
+                     const double* res_up, const double* a, const double* b_lo, const double* b_up,
+                     const double* rho_hat, double* chat, double* rhs, double* border, double* corner) {
+  VTS_REQUIRE_CTX(ctx);
+  return vts::schur_system(C(ctx), u, res_u, res_alpha, res_lo, res_up, a, b_lo, b_up, rho_hat, chat, rhs, border,
+                           corner);
+}
+
+int vts_newton_apply(vts_ctx* ctx, const double* x, double* y) {
+  VTS_REQUIRE_CTX(ctx);
+  Ctx* c = C(ctx);
+  if (!c->system_bound) {
+    vts::set_error(VTS_E_ARGUMENT, "vts_newton_apply: no Newton system bound");
+    return VTS_E_ARGUMENT;
+  }
+  const int F = c->L - 1;
+  if (int rc = vts::free_to_grid(c, F, x, c->fvec[10], true)) return rc;
+  if (int rc = vts::newton_apply_grid(c, c->fvec[10], c->fvec[11], nullptr)) return rc;
+  if (int rc = vts::grid_to_free(c, F, c->fvec[11], y, true)) return rc;
+  VTS_CUDA(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int vts_mg_setup(vts_ctx* ctx, double shift_scale, int32_t* shifted) {
+  VTS_REQUIRE_CTX(ctx);
+  const int rc = vts::mg_setup(C(ctx), shift_scale);
+  if (shifted) *shifted = C(ctx)->shifted;
+  return rc;
+}
+
+int vts_vcycle(vts_ctx* ctx, const double* b, double* z) {
+  VTS_REQUIRE_CTX(ctx);
+  Ctx* c = C(ctx);
+  if (!c->mg_ready) {
+    vts::set_error(VTS_E_ARGUMENT, "vts_vcycle: multigrid not set up");
+    return VTS_E_ARGUMENT;
+  }
+  const int F = c->L - 1;
+  if (int rc = vts::free_to_grid(c, F, b, c->fvec[10], true)) return rc;
+  if (int rc = vts::vcycle_grid(c, c->fvec[10], c->fvec[11], nullptr)) return rc;
+  if (int rc = vts::grid_to_free(c, F, c->fvec[11], z, true)) return rc;
+  VTS_CUDA(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int vts_level_apply(vts_ctx* ctx, int32_t level, const double* x, double* y) {
+  VTS_REQUIRE_CTX(ctx);
+  Ctx* c = C(ctx);
+  if (level < 0 || level >= c->L || !c->mg_ready) {
+    vts::set_error(VTS_E_ARGUMENT, "vts_level_apply: bad level or multigrid not set up");
+    return VTS_E_ARGUMENT;
+  }
+  if (int rc = vts::free_to_grid(c, level, x, c->fvec[10], true)) return rc;
+  if (int rc = vts::level_apply_grid(c, level, c->fvec[10], c->fvec[11], nullptr)) return rc;
+  if (int rc = vts::grid_to_free(c, level, c->fvec[11], y, true)) return rc;
+  VTS_CUDA(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int vts_minres(vts_ctx* ctx, const double* b, double* x, double tol, int32_t max_iters, double floor_tol,
+               int32_t precondition, int32_t* iterations, double* relres, int32_t* converged, double* history) {
+  VTS_REQUIRE_CTX(ctx);
+  int it = 0, conv = 0;
+  double rr = 0.0;
+  const int rc = vts::minres(C(ctx), b, x, tol, max_iters, floor_tol, precondition, &it, &rr, &conv, history);
+  if (iterations) *iterations = it;
+  if (relres) *relres = rr;
+  if (converged) *converged = conv;
+  return rc;
+}
+
+int vts_reconstruct_nu(vts_ctx* ctx, const double* u, const double* du, double dalpha, const double* res_u,
+                       double res_alpha, const double* res_lo, const double* res_up, const double* a,
+                       const double* b_lo, const double* b_up, double* dnu_lo, double* dnu_up, double* slope) {
+  VTS_REQUIRE_CTX(ctx);
+  const int rc = vts::reconstruct_nu(C(ctx), u, du, dalpha, res_u, res_alpha, res_lo, res_up, a, b_lo, b_up,
+                                     dnu_lo, dnu_up, slope);
+  if (rc) return rc;
+  if (!slope) VTS_CUDA(cudaStreamSynchronize(C(ctx)->stream));
+  return 0;
+}
+
+int vts_al_value(vts_ctx* ctx, const double* u, double alpha, const double* nu_lo, const double* nu_up,
+                 const double* du, double dalpha, const double* dnu_lo, const double* dnu_up, double kappa,
+                 const double* rho, const double* p, const double* mu_lo, const double* mu_up, const double* q_lo,
+                 const double* q_up, const double* f, const double* lower, const double* upper, double volume,
+                 double branch, double* value, uint32_t* warn_flags) {
+  VTS_REQUIRE_CTX(ctx);
+  unsigned warn = 0;
+  const int rc = vts::al_value(C(ctx), u, alpha, nu_lo, nu_up, du, dalpha, dnu_lo, dnu_up, kappa, rho, p, mu_lo,
+                               mu_up, q_lo, q_up, f, lower, upper, volume, branch, value, &warn);
+  if (warn_flags) *warn_flags = warn ? VTS_W_SATURATED : 0u;
+  return rc;
+}
+
+int vts_axpy(vts_ctx* ctx, int64_t len, double kappa, const double* dx, double* x) {
+  VTS_REQUIRE_CTX(ctx);
+  return vts::axpy(C(ctx), len, kappa, dx, x);
+}
+
+int vts_outer_update(vts_ctx* ctx, double beta, double gamma, double floor_p, const double* rho_hat,
+                     const double* mu_hat_lo, const double* mu_hat_up, double* rho, double* mu_lo, double* mu_up,
+                     double* p, double* q_lo, double* q_up, int32_t update_penalties) {
+  VTS_REQUIRE_CTX(ctx);
+  return vts::outer_update(C(ctx), beta, gamma, floor_p, rho_hat, mu_hat_lo, mu_hat_up, rho, mu_lo, mu_up, p, q_lo,
+                           q_up, update_penalties);
+}
+
+int vts_gap(vts_ctx* ctx, const double* u, double alpha, const double* q, const double* f, const double* nu_lo,
+            const double* nu_up, const double* lower, const double* upper, double volume, const double* rho,
+            double* d_val, double* gap, double* fu, double* rho_sum) {
+  VTS_REQUIRE_CTX(ctx);
+  return vts::gap(C(ctx), u, alpha, q, f, nu_lo, nu_up, lower, upper, volume, rho, d_val, gap, fu, rho_sum);
+}
+
+int vts_penalty_eval(vts_ctx* ctx, int64_t n, const double* tau, double branch, double* value, double* d1,
+                     double* d2, uint32_t* warn_flags) {
+  VTS_REQUIRE_CTX(ctx);
+  unsigned warn = 0;
+  const int rc = vts::penalty_eval(C(ctx), n, tau, branch, value, d1, d2, &warn);
+  if (warn_flags) *warn_flags = warn ? VTS_W_SATURATED : 0u;
+  return rc;
+}
+
+int64_t vts_kernel_launches(const vts_ctx* ctx) { return ctx ? C(ctx)->launches : 0; }
+
+}  // extern "C"

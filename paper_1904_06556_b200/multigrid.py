@@ -1,0 +1,81 @@
+"""Galerkin V(2,2) multigrid preconditioner on the device (multigrid.py of the reference).
+
+`MgPreconditioner(fine, transfers)` builds, for the bound Newton matrix, the
+finest-level block stencil, every coarse operator P^T A P (symmetrised), the
+restricted borders and the dense Cholesky factor of the coarsest bordered
+matrix with the reference's trace-scaled shift fallback
+(multigrid.py:82-103).  `apply(v)` runs one V-cycle from a zero guess with
+the reference's exact lexicographic Gauss-Seidel order (multigrid.py:35-64,
+109-154).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import logging
+
+import torch
+
+from . import _lib
+from .fem import ptr
+from .linalg import NewtonMatrix
+
+log = logging.getLogger("paper_1904_06556_b200.multigrid")
+
+
+class LevelOperator:
+    """Probe handle for one level operator (MgPreconditioner.mats[k])."""
+
+    def __init__(self, pre: "MgPreconditioner", k: int):
+        self._pre = pre
+        self.level = k
+        self.core_dim = pre.ops.level_size(k)
+
+    def matvec(self, x: torch.Tensor) -> torch.Tensor:
+        self._pre._check_current()
+        ops = self._pre.ops
+        x = ops.check_vec(x, self.core_dim + 1, "x")
+        y = ops.vec(self.core_dim + 1)
+        _lib.check(_lib.load().vts_level_apply(ops.handle, self.level, ptr(x), ptr(y)), "vts_level_apply")
+        return y
+
+
+class MgPreconditioner:
+    def __init__(self, fine: NewtonMatrix, transfers, sweeps: int = 2, shift_scale: float = 1e-12):
+        if not isinstance(fine, NewtonMatrix):
+            raise TypeError("MgPreconditioner takes the NewtonMatrix returned by schur_system")
+        if sweeps != 2:
+            raise ValueError("the device V-cycle implements the reference's V(2,2) (sweeps=2)")
+        fine._check_current()
+        self.ops = fine.ops
+        self.transfers = list(transfers)
+        hier = self.ops.problem
+        if len(self.transfers) != len(hier.levels) - 1:
+            raise ValueError("transfers must chain every level of the problem hierarchy")
+        for k, t in enumerate(self.transfers):
+            if tuple(t.shape) != (hier.levels[k + 1].n, hier.levels[k].n):
+                raise ValueError(f"transfer {k} does not match the hierarchy")
+        self.sweeps = sweeps
+        self._version = fine._version
+        shifted = ctypes.c_int32(0)
+        rc = _lib.load().vts_mg_setup(self.ops.handle, shift_scale, ctypes.byref(shifted))
+        _lib.check(rc, "vts_mg_setup")
+        self.shifted = bool(shifted.value)
+        if self.shifted:
+            log.warning("coarse matrix is not positive definite; retrying Cholesky with a trace-scaled shift")
+        self.mats = [LevelOperator(self, k) for k in range(len(hier.levels))]
+
+    @property
+    def levels(self) -> int:
+        return len(self.mats)
+
+    def _check_current(self) -> None:
+        if self.ops._system_version != self._version:
+            raise RuntimeError("this preconditioner was built for a superseded Newton matrix")
+
+    def apply(self, v: torch.Tensor) -> torch.Tensor:
+        self._check_current()
+        v = self.ops.check_vec(v, self.ops.n + 1, "v")
+        z = self.ops.vec(self.ops.n + 1)
+        _lib.check(_lib.load().vts_vcycle(self.ops.handle, ptr(v), ptr(z)), "vts_vcycle")
+        return z

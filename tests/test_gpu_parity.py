@@ -1,0 +1,154 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference fixtures.
+
+Every check compares the device result with the committed golden fixtures
+that the *reference* produced (tests/golden/make_golden.py), at the
+tolerances of BASELINE.json's north star / SURVEY.md §8(c):
+
+* per-element g / phi values and operator applies: rtol 1e-12 with
+  atol 1e-12 * max|ref| (the reference's own style, test_pbm.py:77-79);
+* MINRES residual histories: |h_gpu - h_ref| <= 1e-8 h_ref + 1e-13 over the
+  first 20 iterations (SURVEY.md §6.4 explains the absolute floor);
+* full PBM: compliance and thickness field within 1e-6 relative, outer
+  iteration count within +-1 (observed: identical counts).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from golden_io import KERNEL_FIXTURES, load, state_dict
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU containers
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1904_06556_b200 as vts  # noqa: E402
+
+
+def close(a, b, rtol=1e-12):
+    a = a.detach().cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a, dtype=float)
+    b = np.asarray(b, dtype=float)
+    scale = max(float(np.abs(b).max()), 1e-300)
+    np.testing.assert_allclose(a, b, rtol=rtol, atol=rtol * scale)
+
+
+def dev(x):
+    return torch.as_tensor(np.asarray(x, dtype=np.float64), device="cuda").contiguous()
+
+
+class Case:
+    def __init__(self, name):
+        self.name = name
+        self.prob = vts.build_problem(*KERNEL_FIXTURES[name])
+        self.fx = load(name)
+        st = state_dict(self.fx)
+        self.state = vts.PbmState(**{k: (v if k == "alpha" else dev(v)) for k, v in st.items()})
+        self.ops = vts.ElementOps(self.prob.fine)
+        self.bounds = vts.DensityBounds.for_problem(self.prob.m, self.prob.volume, 0.0)
+        self.pen = vts.PenaltyBarrier()
+        self.ev = vts.eval_lagrangian(self.state, self.ops, self.prob.f, self.bounds, self.pen, keep_w=True)
+
+
+@pytest.fixture(scope="module", params=sorted(KERNEL_FIXTURES))
+def case(request):
+    return Case(request.param)
+
+
+def test_penalty_kernel_matches_reference():
+    fx = load("penalty")
+    pen = vts.PenaltyBarrier()
+    tau = dev(fx["tau"])
+    close(pen.value(tau), fx["value"], 1e-15)
+    close(pen.deriv(tau), fx["deriv"], 1e-15)
+    close(pen.deriv2(tau), fx["deriv2"], 1e-15)
+    with pytest.warns(RuntimeWarning, match="saturated"):
+        big = pen.value(1e200)
+    assert big == pen.value(1e150)
+
+
+def test_phi_pass_matches_reference(case):
+    ev, fx = case.ev, case.fx
+    assert ev.value == pytest.approx(float(fx["value"]), rel=1e-12)
+    assert ev.tau_res == pytest.approx(float(fx["tau_res"]), rel=1e-12)
+    assert ev.res_alpha == pytest.approx(float(fx["res_alpha"]), rel=1e-12, abs=1e-12 * case.prob.volume)
+    for key in ("res_u", "res_lo", "res_up", "q", "mu_hat_lo", "mu_hat_up"):
+        close(getattr(ev, key), fx[key])
+    for key in ("a", "b_lo", "b_up", "rho_hat", "w"):
+        close(getattr(ev.blocks, key), fx[key])
+
+
+def test_schur_rhs_and_newton_apply_match_reference(case):
+    mat, rhs = vts.schur_system(case.ev, case.ops)
+    fx = case.fx
+    close(rhs, fx["rhs"])
+    close(mat.border, fx["border"])
+    assert mat.corner == pytest.approx(float(fx["corner"]), rel=1e-13)
+    close(mat.matvec(dev(fx["x"])), fx["Sx"])
+
+
+def test_reconstruct_and_trial_value_match_reference(case):
+    fx = case.fx
+    du = dev(fx["du"])
+    dnu_lo, dnu_up = vts.reconstruct_nu(case.ev, case.ops, du, float(fx["dalpha"]))
+    close(dnu_lo, fx["dnu_lo"])
+    close(dnu_up, fx["dnu_up"])
+    k = float(fx["kappa"])
+    st = case.state
+    trial = vts.al_value(st.u + k * du, st.alpha + k * float(fx["dalpha"]), st.nu_lo + k * dnu_lo,
+                         st.nu_up + k * dnu_up, st, case.ops, case.prob.f, case.bounds, case.pen)
+    assert trial == pytest.approx(float(fx["trial_value"]), rel=1e-12)
+
+
+def test_galerkin_levels_and_vcycle_match_reference(case):
+    mat, rhs = vts.schur_system(case.ev, case.ops)
+    mg = vts.MgPreconditioner(mat, case.prob.transfers)
+    fx = case.fx
+    assert mg.shifted == bool(fx["shifted"])
+    for k, lev in enumerate(mg.mats):
+        close(lev.matvec(dev(fx[f"level{k}_probe"])), fx[f"level{k}_apply"])
+    close(mg.apply(dev(fx["vcycle_in"])), fx["vcycle_out"])
+    close(mg.apply(rhs), fx["vcycle_rhs_out"])
+
+
+def test_minres_history_matches_reference(case):
+    mat, rhs = vts.schur_system(case.ev, case.ops)
+    mg = vts.MgPreconditioner(mat, case.prob.transfers)
+    fx = case.fx
+    hist = []
+    vts.minres_solve(mat, rhs, vts.MinresConfig(tol=1e-14, max_iters=20), mg.apply, history=hist)
+    cnt = min(len(hist), fx["minres_hist"].size)
+    ref = fx["minres_hist"][:cnt]
+    h = np.array(hist[:cnt])
+    assert np.all(np.abs(h - ref) <= 1e-8 * ref + 1e-13), (h, ref)
+    res = vts.minres_solve(mat, rhs, vts.MinresConfig(tol=1e-6, max_iters=1000), mg.apply)
+    assert res.converged
+    assert res.iterations == int(fx["minres_tol6_iters"])
+    assert res.relres <= 1e-6
+    close(res.x, fx["minres_tol6_x"], 1e-9)
+
+
+@pytest.mark.parametrize("name,args", [
+    ("pbm_c1", ("cantilever", 16, 8, 3, 0.5)),
+    ("pbm_mbb32", ("mbb", 4, 2, 4, 0.4)),
+])
+def test_full_pbm_matches_reference(name, args):
+    fx = load(name)
+    rep = vts.solve_pbm(vts.build_problem(*args))
+    assert rep.converged == bool(fx["converged"])
+    assert abs(rep.outer_iterations - int(fx["outer"])) <= 1
+    assert rep.objective == pytest.approx(float(fx["objective"]), rel=1e-6)
+    close(rep.rho, fx["rho"], 1e-6)
+    # observed rounding-faithful: the discrete trajectory is identical
+    np.testing.assert_array_equal(np.array(rep.extras["minres_per_newton"]), fx["minres_per_newton"])
+
+
+def test_full_pbm_c2_mbb_matches_reference():
+    fx = load("pbm_c2")
+    rep = vts.solve_pbm(vts.build_config("C2"))
+    assert rep.converged
+    assert abs(rep.outer_iterations - int(fx["outer"])) <= 1
+    assert rep.objective == pytest.approx(float(fx["objective"]), rel=1e-6)
+    close(rep.rho[torch.as_tensor(fx["rho_sample_idx"], device="cuda")], fx["rho_sample"], 1e-6)
