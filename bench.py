@@ -1,0 +1,361 @@
+"""Benchmark: MG-preconditioned MINRES on the 1024x512 VTS Newton system (BASELINE.json configs[2]).
+
+A "step" is one preconditioned MINRES iteration (linalg.py:190-242) on the
+bordered Schur system of the C3 microbench state: one matrix-free Newton apply,
+one V(2,2) cycle with exact-order Gauss-Seidel on 9 levels, and the Lanczos /
+Givens vector updates.  `value` = MINRES iterations/s with all inputs resident
+in HBM; `e2e` = the same through the C-ABI call with the right-hand side
+copied host->device and the solution device->host inside the timed region.
+Inputs (the per-level stencils alone are 226 MB) exceed the 126 MB L2, so no
+explicit flush is needed.  Extra keys report the other BASELINE.json figures
+(phi pass, 100 applies, 100 V-cycles, full-PBM wall time of C4) and the
+roofline of the dominant kernel.
+
+`--impl reference` times the reference's CPU algorithm (the oracle port in
+`oracle/`, test infrastructure) on the same workload; under torchrun only
+rank 0 runs it.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "MG-MINRES iters/s + HBM GB/s (frac of 8 TB/s) on VTS Newton system; PBM wall s"
+CONFIG_KEY = "C3"
+N_ELEM_X, N_ELEM_Y = 1024, 512
+
+
+def microbench_inputs(n: int, m: int, seed: int = 0):
+    """BASELINE.json configs[2]: u ~ N(0, 1e-4) per free dof, alpha = 1e-3,
+    rho ~ U(0.5, 2), p = 1e-2, other fields at the reference's initial values,
+    RHS ~ N(0, 1) of length n + 1."""
+    rng = np.random.default_rng(seed)
+    u = rng.normal(0.0, 1e-2, n)
+    rho = rng.uniform(0.5, 2.0, m)
+    rhs = rng.standard_normal(n + 1)
+    one = np.ones(m)
+    state = dict(u=u, alpha=1e-3, nu_lo=one.copy(), nu_up=one.copy(), rho=rho, mu_lo=one.copy(),
+                 mu_up=one.copy(), p=np.full(m, 1e-2), q_lo=one.copy(), q_up=one.copy())
+    return state, rhs
+
+
+def algorithmic_bytes(prob) -> dict:
+    """SURVEY.md Appendix B byte model (fp64 words x 8)."""
+    n, m = prob.n, prob.m
+    lv = prob.levels
+    A_phi = 8 * (4 * n + 16 * m)
+    A_ap = 8 * (3 * n + 2 * m + 2)
+    A_V = 0
+    for k in range(1, len(lv)):  # every level but the coarsest
+        nk, nkm1 = lv[k].n, lv[k - 1].n
+        Bk = 8 * (nk + 2 * m) if k == len(lv) - 1 else 76 * nk
+        A_V += 5 * (Bk + 32 * nk) + 24 * (nk + nkm1)
+    A_MR = A_ap + A_V + 160 * (n + 1)
+    # one forward GS sweep on the finest level: operator (matrix-free credit) + b, x, x', border
+    A_gs = (8 * (n + 2 * m) + 32 * n)
+    return dict(phi=A_phi, apply=A_ap, vcycle=A_V, minres_iter=A_MR, gs_fine_sweep=A_gs)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [p.strip() for p in out.stdout.strip().split(",")]
+                if len(parts) == 7:
+                    self.rows.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def run_reference(args) -> None:
+    """CPU reference arm: the oracle port of the reference algorithm, same workload."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+
+    prob = oracle.build_config(CONFIG_KEY)
+    st, rhs = microbench_inputs(prob.n, prob.m)
+    ops = oracle.ElementOps2D(prob.fine)
+    bounds = oracle.DensityBounds.for_problem(prob.m, prob.volume, 0.0)
+    ev = oracle.eval_lagrangian(oracle.PbmState(**st), ops, prob.f, bounds, oracle.PenaltyBarrier())
+    mat, _ = oracle.schur_system(ev, ops)
+    mg = oracle.MgPreconditioner(mat, prob.transfers)
+    oracle.minres_solve(mat, rhs, oracle.MinresConfig(tol=1e-14, max_iters=max(args.warmup, 1)), mg.apply)
+    t0 = time.perf_counter()
+    res = oracle.minres_solve(mat, rhs, oracle.MinresConfig(tol=1e-14, max_iters=args.steps), mg.apply)
+    dt = time.perf_counter() - t0
+    its = res.iterations
+    value = its / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "MINRES iterations/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / its, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE configs[2])",
+        "config": {"workload": "C3 microbench 1024x512 cantilever, 9 MG levels, preconditioned MINRES",
+                   "n": prob.n, "m": prob.m, "parallelism": "replicas only"},
+        "cpu_baseline": {"value": value, "unit": "MINRES iterations/s", "cores": 1, "kind": "port",
+                         "sample": f"{its} preconditioned MINRES iterations on the C3 Newton system "
+                                   "(oracle/ restatement: numpy/scipy CSR + sequential C Gauss-Seidel, "
+                                   "single-threaded by construction)"},
+        "e2e": {"value": value, "unit": "MINRES iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_sample(seconds_budget: float = 20.0) -> dict:
+    """Bounded oracle sample on the host (rank 0, N=1): 10 MINRES iterations on C3."""
+    import oracle
+
+    prob = oracle.build_config(CONFIG_KEY)
+    st, rhs = microbench_inputs(prob.n, prob.m)
+    ops = oracle.ElementOps2D(prob.fine)
+    bounds = oracle.DensityBounds.for_problem(prob.m, prob.volume, 0.0)
+    t0 = time.perf_counter()
+    ev = oracle.eval_lagrangian(oracle.PbmState(**st), ops, prob.f, bounds, oracle.PenaltyBarrier())
+    t_phi = time.perf_counter() - t0
+    mat, _ = oracle.schur_system(ev, ops)
+    mg = oracle.MgPreconditioner(mat, prob.transfers)
+    its = 10
+    t0 = time.perf_counter()
+    res = oracle.minres_solve(mat, rhs, oracle.MinresConfig(tol=1e-14, max_iters=its), mg.apply)
+    dt = time.perf_counter() - t0
+    return {"value": res.iterations / dt, "unit": "MINRES iterations/s", "cores": 1, "kind": "port",
+            "sample": f"{res.iterations} preconditioned MINRES iterations on the C3 Newton system "
+                      f"({dt:.1f} s) + one phi pass ({t_phi*1e3:.0f} ms); oracle/ restatement, single thread",
+            "phi_pass_ms": 1e3 * t_phi}
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-pbm", action="store_true", help="skip the C4 full-PBM wall-time extra")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1904_06556_b200 as vts
+    from paper_1904_06556_b200 import _lib
+    from paper_1904_06556_b200.fem import ptr
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl")
+    lib = _lib.load()
+    prob = vts.build_config(CONFIG_KEY)
+    n, m = prob.n, prob.m
+    st_h, rhs_h = microbench_inputs(n, m, seed=rank)
+    st = vts.PbmState(**{k: (v if k == "alpha" else torch.as_tensor(v, device="cuda")) for k, v in st_h.items()})
+    ops = vts.ElementOps(prob.fine)
+    bounds = vts.DensityBounds.for_problem(m, prob.volume, 0.0)
+    pen = vts.PenaltyBarrier()
+    stream = torch.cuda.current_stream()
+
+    # --- phi pass (K1) timed with events
+    for _ in range(3):
+        ev = vts.eval_lagrangian(st, ops, prob.f, bounds, pen)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    reps_phi = 10
+    for _ in range(reps_phi):
+        ev = vts.eval_lagrangian(st, ops, prob.f, bounds, pen)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    phi_ms = e0.elapsed_time(e1) / reps_phi
+    mat, _ = vts.schur_system(ev, ops)
+    t_setup0 = time.perf_counter()
+    mg = vts.MgPreconditioner(mat, prob.transfers)
+    setup_wall_ms = 1e3 * (time.perf_counter() - t_setup0)
+    rhs = torch.as_tensor(rhs_h, device="cuda")
+    x = torch.empty(n + 1, dtype=torch.float64, device="cuda")
+    itv, rel, conv = ctypes.c_int32(), ctypes.c_double(), ctypes.c_int32()
+
+    def minres_dev(k: int) -> int:
+        rc = lib.vts_minres(ops.handle, ptr(rhs), ptr(x), 1e-14, k, 1e-9, 1, ctypes.byref(itv), ctypes.byref(rel),
+                            ctypes.byref(conv), None)
+        _lib.check(rc, "vts_minres")
+        return itv.value
+
+    # --- per-kernel device times (roofline) and the 100-apply / 100-V-cycle figures
+    kms = (ctypes.c_double * 6)()
+    _lib.check(lib.vts_time_kernels(ops.handle, 100, kms), "vts_time_kernels")
+    apply_ms, vcycle_ms, gs_fine_ms, gs_l2_ms, resid_ms, setup_ms = list(kms)
+
+    # --- warm-up then the timed region: K MINRES iterations, device resident
+    minres_dev(args.warmup)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ops.kernel_launches
+    with ClockSampler(local) as clk:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        its = minres_dev(args.steps)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    launches = ops.kernel_launches - launches0
+    dt_ms = t0.elapsed_time(t1)
+    if world > 1:
+        tt = torch.tensor([dt_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt_ms = float(tt.item())
+        itt = torch.tensor([its], device="cuda", dtype=torch.float64)
+        dist.all_reduce(itt)
+        total_its = float(itt.item())
+    else:
+        total_its = float(its)
+    value = total_its / (dt_ms * 1e-3)
+
+    # --- e2e through the C-ABI with host buffers (pinned), copies inside the timed region
+    rhs_host = torch.as_tensor(rhs_h).pin_memory()
+    x_host = torch.empty(n + 1, dtype=torch.float64).pin_memory()
+    rhs_dev = torch.empty(n + 1, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    rhs_dev.copy_(rhs_host, non_blocking=True)
+    rc = lib.vts_minres(ops.handle, ptr(rhs_dev), ptr(x), 1e-14, args.steps, 1e-9, 1, ctypes.byref(itv),
+                        ctypes.byref(rel), ctypes.byref(conv), None)
+    _lib.check(rc, "vts_minres")
+    x_host.copy_(x, non_blocking=True)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - w0
+    e2e_its = itv.value
+    if world > 1:
+        tt = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    e2e_value = e2e_its * world / e2e_s
+
+    bytes_ = algorithmic_bytes(prob)
+    peaks_path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    peak, peak_src = 6526.8, "MEASURED_PEAKS.json hbm_gbs"
+    if os.path.exists(peaks_path):
+        with open(peaks_path) as fh:
+            peak = float(json.load(fh).get("hbm_gbs", peak))
+    else:
+        peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+
+    def gbs(nbytes, ms):
+        return nbytes / (ms * 1e-3) / 1e9
+
+    # dominant kernel of the MINRES iteration: the V-cycle, itself dominated by the
+    # finest-level Gauss-Seidel sweeps; report the V-cycle as the roofline unit
+    achieved = gbs(bytes_["vcycle"], vcycle_ms)
+    pbm = None
+    if not args.no_pbm and rank == 0:
+        t_p = time.perf_counter()
+        rep = vts.solve_pbm(vts.build_config("C4"))
+        pbm = {"config": "C4 full PBM 1024x512 cantilever", "wall_s": time.perf_counter() - t_p,
+               "outer": rep.outer_iterations, **rep.totals(), "compliance": rep.objective,
+               "converged": rep.converged}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline_sample()
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": "MINRES iterations/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt_ms / its, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE configs[2] state and RHS)",
+        "config": {"workload": "C3 microbench: preconditioned MINRES on the 1024x512 cantilever Newton system, "
+                               "9 MG levels, V(2,2) exact-order GS", "n": n, "m": m,
+                   "parallelism": "replicas only" if world > 1 else "single GPU",
+                   "l2": "inputs > 126 MB L2 (stencils 226 MB), no flush"},
+        "e2e": {"value": e2e_value, "unit": "MINRES iterations/s", "h2d_bytes_per_step": 8 * (n + 1) / args.steps,
+                "d2h_bytes_per_step": 8 * (n + 1) / args.steps,
+                "note": "one C-ABI vts_minres call of K iterations; RHS H2D and solution D2H once per call"},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "kernel": "V-cycle (9 levels; finest-level GS sweeps dominate)",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "frac_of_8TBs": achieved / 8000.0, "traffic": None, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": bytes_["vcycle"], "launch_ms": vcycle_ms},
+        "kernels": {
+            "phi_pass_ms": phi_ms, "phi_pass_GBs": gbs(bytes_["phi"], phi_ms),
+            "apply_ms": apply_ms, "apply_GBs": gbs(bytes_["apply"], apply_ms), "applies_per_s": 1e3 / apply_ms,
+            "vcycle_ms": vcycle_ms, "vcycles_per_s": 1e3 / vcycle_ms,
+            "gs_fine_sweep_ms": gs_fine_ms, "gs_fine_sweep_GBs": gbs(bytes_["gs_fine_sweep"], gs_fine_ms),
+            "gs_level8_sweep_ms": gs_l2_ms, "residual_fine_ms": resid_ms, "mg_setup_ms": setup_ms,
+            "mg_setup_wall_ms": setup_wall_ms,
+            "minres_iter_GBs": gbs(bytes_["minres_iter"], dt_ms / its),
+            "minres_iter_frac_of_8TBs": gbs(bytes_["minres_iter"], dt_ms / its) / 8000.0,
+            "algorithmic_bytes": bytes_,
+        },
+        "clocks": clk.summary(),
+    }
+    if pbm:
+        line["pbm"] = pbm
+    if cpu:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -181,6 +181,15 @@ int vts_gap(vts_ctx* ctx, const double* u, double alpha, const double* q, const 
 int vts_penalty_eval(vts_ctx* ctx, int64_t n, const double* tau, double branch, double* value, double* d1,
                      double* d2, uint32_t* warn_flags);
 
+/*
+ * Benchmark helper (no reference counterpart): average device time in ms of
+ * {Newton apply, one V-cycle, finest forward GS sweep, second-finest forward
+ * GS sweep, finest residual, mg_setup} over `reps` back-to-back launches,
+ * CUDA events on the context stream; HOST `ms` (6 doubles).  Needs a bound
+ * Newton matrix and a set-up multigrid; overwrites context scratch vectors.
+ */
+int vts_time_kernels(vts_ctx* ctx, int32_t reps, double* ms);
+
 /* Number of kernels this context launched since creation (evidence counter). */
 int64_t vts_kernel_launches(const vts_ctx* ctx);
 

@@ -56,6 +56,7 @@ SIGNATURES = {
     "vts_outer_update": (ctypes.c_int, [_P, _D, _D, _D] + [_P] * 9 + [_I32]),
     "vts_gap": (ctypes.c_int, [_P, _P, _D] + [_P] * 6 + [_D, _P, _PD, _PD, _PD, _PD]),
     "vts_penalty_eval": (ctypes.c_int, [_P, _I64, _P, _D, _P, _P, _P, _PU32]),
+    "vts_time_kernels": (ctypes.c_int, [_P, _I32, _PD]),
     "vts_kernel_launches": (ctypes.c_int64, [_P]),
 }
 

@@ -672,3 +672,53 @@ int mg_setup(Ctx* c, double shift_scale) {
 }
 
 }  // namespace vts
+
+namespace vts {
+
+// Per-kernel device times (CUDA events on the context stream, averaged over
+// `reps` back-to-back launches) for bench.py's roofline: ms[0] Newton apply,
+// ms[1] one V-cycle, ms[2] one forward GS sweep on the finest level, ms[3] one
+// forward GS sweep on the second-finest level, ms[4] finest residual,
+// ms[5] mg_setup (stencil + Galerkin chain + coarse factor, incl. one sync).
+int time_kernels(Ctx* c, int reps, double* ms) {
+  if (!c->mg_ready) {
+    set_error(4, "time_kernels: multigrid not set up");
+    return 4;
+  }
+  const int top = c->L - 1;
+  LevelBuf& F = c->lv[top];
+  double* xin = c->fvec[10];
+  double* yout = c->fvec[11];
+  cudaEvent_t e0, e1;
+  VTS_CUDA(cudaEventCreate(&e0));
+  VTS_CUDA(cudaEventCreate(&e1));
+  auto timed = [&](auto&& body, double* out) -> int {
+    if (int rc = body()) return rc;  // warm
+    VTS_CUDA(cudaEventRecord(e0, c->stream));
+    for (int r = 0; r < reps; ++r)
+      if (int rc = body()) return rc;
+    VTS_CUDA(cudaEventRecord(e1, c->stream));
+    VTS_CUDA(cudaEventSynchronize(e1));
+    float t = 0.f;
+    VTS_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    *out = (double)t / reps;
+    return 0;
+  };
+  int rc = 0;
+  rc = rc ? rc : timed([&] { return newton_apply_grid(c, xin, yout, nullptr); }, ms + 0);
+  rc = rc ? rc : timed([&] { return vcycle_grid(c, xin, yout, nullptr); }, ms + 1);
+  rc = rc ? rc : timed([&] { return gs_sweep(c, top, xin, F.x, true, nullptr); }, ms + 2);
+  if (top >= 1) {
+    LevelBuf& G = c->lv[top - 1];
+    rc = rc ? rc : timed([&] { return gs_sweep(c, top - 1, G.b, G.x, true, nullptr); }, ms + 3);
+  } else {
+    ms[3] = 0.0;
+  }
+  rc = rc ? rc : timed([&] { return level_residual_grid(c, top, F.x, xin, F.r, nullptr); }, ms + 4);
+  rc = rc ? rc : timed([&] { return mg_setup(c, 1e-12); }, ms + 5);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return rc;
+}
+
+}  // namespace vts

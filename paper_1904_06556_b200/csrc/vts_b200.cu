@@ -396,6 +396,11 @@ int vts_penalty_eval(vts_ctx* ctx, int64_t n, const double* tau, double branch, 
   return rc;
 }
 
+int vts_time_kernels(vts_ctx* ctx, int32_t reps, double* ms) {
+  VTS_REQUIRE_CTX(ctx);
+  return vts::time_kernels(C(ctx), reps, ms);
+}
+
 int64_t vts_kernel_launches(const vts_ctx* ctx) { return ctx ? C(ctx)->launches : 0; }
 
 }  // extern "C"
