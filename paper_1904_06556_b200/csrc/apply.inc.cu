@@ -142,8 +142,10 @@ __global__ void __launch_bounds__(kTX* kTY) k_newton_apply(int nx, int ny, int e
 
 // y = A_k x (+ border x_alpha) on a block stencil; with `b` given, computes
 // r = b - (A x + border x_alpha) instead.  Border dot partials for y_alpha.
+// Row sums follow the CSR column order SW S SE W C E NW N NE (linalg.py:58).
 template <bool RESIDUAL>
-__global__ void __launch_bounds__(256) k_level_apply(int nx, int ny, int ngrid, const double* __restrict__ st,
+__global__ void __launch_bounds__(256) k_level_apply(int nx, int ny, int ngrid, const double* __restrict__ stL,
+                                                   const double* __restrict__ stU,
                                                    const double* __restrict__ border,
                                                    const double* __restrict__ corner_ptr,
                                                    const double* __restrict__ x,
@@ -156,7 +158,8 @@ __global__ void __launch_bounds__(256) k_level_apply(int nx, int ny, int ngrid, 
   double acc[1] = {0.0};
   for (int nd = blockIdx.x * blockDim.x + threadIdx.x; nd < nnodes; nd += gridDim.x * blockDim.x) {
     const int ix = nd % nx, iy = nd / nx;
-    const double* a = st + (size_t)nd * kStencilStride;
+    const double* l = stL + (size_t)nd * kHalf;
+    const double* u = stU + (size_t)nd * kHalf;
     double s0 = 0.0, s1 = 0.0;
 #pragma unroll
     for (int blk = 0; blk < 9; ++blk) {
@@ -164,8 +167,15 @@ __global__ void __launch_bounds__(256) k_level_apply(int nx, int ny, int ngrid, 
       const int jx = ix + dx, jy = iy + dy;
       double2 xv = make_double2(0.0, 0.0);
       if (jx >= 0 && jx < nx && jy >= 0 && jy < ny) xv = *reinterpret_cast<const double2*>(x + 2 * (jx + nx * jy));
-      const double2 c01 = *reinterpret_cast<const double2*>(a + 4 * blk);
-      const double2 c23 = *reinterpret_cast<const double2*>(a + 4 * blk + 2);
+      double2 c01, c23;
+      if (blk == kBlockCenter) {
+        c01 = make_double2(l[kHDiag], u[kHC]);
+        c23 = make_double2(l[kHC], u[kHDiag]);
+      } else {
+        const double* h = (blk < 4 ? l : u) + half_offset(blk);
+        c01 = *reinterpret_cast<const double2*>(h);
+        c23 = *reinterpret_cast<const double2*>(h + 2);
+      }
       s0 = fma(c01.x, xv.x, s0);
       s0 = fma(c01.y, xv.y, s0);
       s1 = fma(c23.x, xv.x, s1);
@@ -208,7 +218,7 @@ int newton_apply_grid(Ctx* c, const double* x, double* y, const int* skip) {
 int level_apply_grid(Ctx* c, int k, const double* x, double* y, const int* skip) {
   const LevelBuf& L = c->lv[k];
   const int grid = (int)std::min<long long>(div_up(L.d.nnodes, 256), kReduceGridCap);
-  k_level_apply<false><<<grid, 256, 0, c->stream>>>(L.d.nx, L.d.ny, L.d.ngrid, L.d.stencil, L.d.border,
+  k_level_apply<false><<<grid, 256, 0, c->stream>>>(L.d.nx, L.d.ny, L.d.ngrid, L.d.stL, L.d.stU, L.d.border,
                                                      c->d_corner, x, nullptr, y, c->partials, c->counters + 5,
                                                      skip);
   VTS_LAUNCHED(c);
@@ -218,7 +228,7 @@ int level_apply_grid(Ctx* c, int k, const double* x, double* y, const int* skip)
 int level_residual_grid(Ctx* c, int k, const double* x, const double* b, double* r, const int* skip) {
   const LevelBuf& L = c->lv[k];
   const int grid = (int)std::min<long long>(div_up(L.d.nnodes, 256), kReduceGridCap);
-  k_level_apply<true><<<grid, 256, 0, c->stream>>>(L.d.nx, L.d.ny, L.d.ngrid, L.d.stencil, L.d.border,
+  k_level_apply<true><<<grid, 256, 0, c->stream>>>(L.d.nx, L.d.ny, L.d.ngrid, L.d.stL, L.d.stU, L.d.border,
                                                     c->d_corner, x, b, r, c->partials, c->counters + 5, skip);
   VTS_LAUNCHED(c);
   return 0;

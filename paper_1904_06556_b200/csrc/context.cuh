@@ -23,6 +23,7 @@ struct LevelBuf {
   double* r = nullptr;           // [ngrid + 1] residual / scratch
   unsigned long long* gs_flags = nullptr;  // GS wavefront progress, one per row group
   int gs_groups = 0;
+  size_t pad_nodes = 0;  // zero nodes before/after stL, stU and every vector of this level
 };
 
 // MINRES device scalars (linalg.py:128-242 recurrences), one struct per solve
@@ -71,6 +72,7 @@ struct Ctx {
   MinresDev* hmst = nullptr;    // pinned host mirror
 
   long long launches = 0;
+  std::vector<void*> allocs;  // padded device arrays owned by the context
 };
 
 constexpr int kMaxBlocks = 8192;

@@ -1,4 +1,4 @@
-// Galerkin V(2,2) multigrid on the node-block stencils (unity-built).
+// Galerkin V(2,2) multigrid on node-block half-stencils (unity-built).
 //
 //  mg_setup  : MgPreconditioner.__init__ (multigrid.py:82-103)
 //    k_fine_stencil  finest-level stencil of S straight from the element data
@@ -6,16 +6,23 @@
 //                    element order like _AssemblyPattern.build, fem.py:132-139)
 //    k_rap           coarse block stencil P^T A P (linalg.py:78), structured:
 //                    every coarse node gathers its 3x3 fine support
-//    k_symmetrize    (C + C^T)/2 (linalg.py:79) + reciprocal diagonals
+//    k_symmetrize    (C + C^T)/2 (linalg.py:79) + reciprocal diagonals, split
+//                    into the L / U half-stencils
 //    k_restrict      P^T v (border chain linalg.py:80, residual restriction)
 //    k_dense_coarse + k_cholesky   dense bordered coarsest matrix and its
 //                    Cholesky factor with the trace-scaled shift fallback
 //  vcycle_grid : MgPreconditioner.apply/_cycle (multigrid.py:109-143)
-//    k_gs_sweep      exact-order lexicographic Gauss-Seidel (multigrid.py:35-64):
-//                    wavefront, one lane per grid row, 32 rows per warp,
-//                    rows skewed by two nodes, new values of the row before
-//                    passed lane to lane with shuffles, warps chained through
-//                    release/acquire progress counters in global memory
+//    One lexicographic Gauss-Seidel sweep (multigrid.py:35-64) is split into
+//      k_gs_old   P = b - border x_alpha - (U x_old)   fully parallel, and
+//      k_gs_tri   the lower-triangular solve (D_L + L) x = P as a wavefront:
+//                 one lane per grid row, rows skewed by two nodes, new values
+//                 of the previous row passed lane to lane by shuffles; each
+//                 lane streams its own row's half-stencil and P through a
+//                 shared-memory ring filled by cp.async.bulk (TMA) with
+//                 mbarrier completion; 16-row bands on separate SMs hand the
+//                 band's last row to the next band through release/acquire
+//                 progress counters and a TMA-staged row buffer.
+//    The first sweep after the zero initial guess needs no old-value pass.
 //    k_level_apply<true>  residual, then k_restrict / k_prolong_add
 //    k_coarse_solve  two triangular solves with the coarsest factor
 
@@ -40,6 +47,35 @@ VTS_DEVICE_INLINE int parents(int f, int (&q)[2]) {
   return 1;
 }
 
+// write a full 36-entry block stencil + diagonal reciprocals as the L / U halves
+VTS_DEVICE_INLINE void store_halves(const double (&blk)[36], double rd0, double rd1, double* __restrict__ l,
+                                    double* __restrict__ u) {
+  double lo[kHalf], up[kHalf];
+#pragma unroll
+  for (int b = 0; b < 9; ++b) {
+    if (b == kBlockCenter) continue;
+    const int o = half_offset(b);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (b < 4) lo[o + e] = blk[4 * b + e];
+      else up[o + e] = blk[4 * b + e];
+    }
+  }
+  lo[kHC] = blk[18];     // a10
+  up[kHC] = blk[17];     // a01
+  lo[kHDiag] = blk[16];  // a00
+  up[kHDiag] = blk[19];  // a11
+  lo[kHRd0] = up[kHRd0] = rd0;
+  lo[kHRd1] = up[kHRd1] = rd1;
+#pragma unroll
+  for (int i = 20; i < kHalf; ++i) lo[i] = up[i] = 0.0;
+#pragma unroll
+  for (int i = 0; i < kHalf; i += 2) {
+    *reinterpret_cast<double2*>(l + i) = make_double2(lo[i], lo[i + 1]);
+    *reinterpret_cast<double2*>(u + i) = make_double2(up[i], up[i + 1]);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // finest-level stencil of the Schur matrix from (u, rho_hat, chat)
 // ---------------------------------------------------------------------------
@@ -48,7 +84,7 @@ __global__ void __launch_bounds__(128) k_fine_stencil(int nx, int ny, int ex, in
                                                     const double* __restrict__ rho_hat,
                                                     const double* __restrict__ chat,
                                                     const uint8_t* __restrict__ fm,
-                                                    double* __restrict__ st) {
+                                                    double* __restrict__ stL, double* __restrict__ stU) {
   const int nd = blockIdx.x * blockDim.x + threadIdx.x;
   if (nd >= nx * ny) return;
   const int ix = nd % nx, iy = nd / nx;
@@ -98,19 +134,16 @@ __global__ void __launch_bounds__(128) k_fine_stencil(int nx, int ny, int ex, in
     if (!fi.y || !fj.x) blk[4 * b + 2] = 0.0;
     if (!fi.y || !fj.y) blk[4 * b + 3] = 0.0;
   }
-  double* out = st + (size_t)nd * kStencilStride;
-#pragma unroll
-  for (int i = 0; i < 36; i += 2) *reinterpret_cast<double2*>(out + i) = make_double2(blk[i], blk[i + 1]);
   const double rd0 = fi.x ? 1.0 / blk[16] : 0.0;
   const double rd1 = fi.y ? 1.0 / blk[19] : 0.0;
-  *reinterpret_cast<double2*>(out + 36) = make_double2(rd0, rd1);
-  *reinterpret_cast<double2*>(out + 38) = make_double2(0.0, 0.0);
+  store_halves(blk, rd0, rd1, stL + (size_t)nd * kHalf, stU + (size_t)nd * kHalf);
 }
 
 // ---------------------------------------------------------------------------
 // coarse operator P^T A P (unsymmetrised) on coarse node I
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_rap(int fnx, int fny, const double* __restrict__ fst,
+__global__ void __launch_bounds__(128) k_rap(int fnx, int fny, const double* __restrict__ fL,
+                                           const double* __restrict__ fU,
                                            const uint8_t* __restrict__ ffm, int cnx, int cny,
                                            const uint8_t* __restrict__ cfm, double* __restrict__ out) {
   const int cn = blockIdx.x * blockDim.x + threadIdx.x;
@@ -129,11 +162,11 @@ __global__ void __launch_bounds__(128) k_rap(int fnx, int fny, const double* __r
       const double wI = pweight(fx, fy, cx, cy);
       const double pr0 = (ff.x && fI.x) ? wI : 0.0, pr1 = (ff.y && fI.y) ? wI : 0.0;
       if (pr0 == 0.0 && pr1 == 0.0) continue;
-      const double* a = fst + (size_t)fi * kStencilStride;
       for (int b = 0; b < 9; ++b) {
         const int jx = fx + b % 3 - 1, jy = fy + b / 3 - 1;
         if (jx < 0 || jx >= fnx || jy < 0 || jy >= fny) continue;
-        const double a00 = a[4 * b], a01 = a[4 * b + 1], a10 = a[4 * b + 2], a11 = a[4 * b + 3];
+        const double a00 = stencil_entry(fL, fU, fi, b, 0, 0), a01 = stencil_entry(fL, fU, fi, b, 0, 1);
+        const double a10 = stencil_entry(fL, fU, fi, b, 1, 0), a11 = stencil_entry(fL, fU, fi, b, 1, 1);
         const uchar2 fj = *reinterpret_cast<const uchar2*>(ffm + 2 * (jx + fnx * jy));
         // coarse parents of fine node j (one per even, two per odd coordinate)
         int qxs[2], qys[2];
@@ -161,32 +194,34 @@ __global__ void __launch_bounds__(128) k_rap(int fnx, int fny, const double* __r
   for (int i = 0; i < 36; i += 2) *reinterpret_cast<double2*>(o + i) = make_double2(acc[i], acc[i + 1]);
 }
 
-// (C + C^T)/2 and reciprocal diagonals
+// (C + C^T)/2 (linalg.py:79) and reciprocal diagonals, written as halves
 __global__ void k_symmetrize(int nx, int ny, const double* __restrict__ raw, const uint8_t* __restrict__ fm,
-                             double* __restrict__ st) {
+                             double* __restrict__ stL, double* __restrict__ stU) {
   const int nd = blockIdx.x * blockDim.x + threadIdx.x;
   if (nd >= nx * ny) return;
   const int ix = nd % nx, iy = nd / nx;
   const double* a = raw + (size_t)nd * kStencilStride;
-  double* o = st + (size_t)nd * kStencilStride;
+  double blk[36];
+#pragma unroll
   for (int b = 0; b < 9; ++b) {
     const int dx = b % 3 - 1, dy = b / 3 - 1;
     const int jx = ix + dx, jy = iy + dy;
-    double t[4] = {0.0, 0.0, 0.0, 0.0};
+    double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
     if (jx >= 0 && jx < nx && jy >= 0 && jy < ny) {
       const double* bt = raw + (size_t)(jx + nx * jy) * kStencilStride + 4 * (8 - b);  // mirrored block
-      t[0] = (a[4 * b + 0] + bt[0]) * 0.5;
-      t[1] = (a[4 * b + 1] + bt[2]) * 0.5;
-      t[2] = (a[4 * b + 2] + bt[1]) * 0.5;
-      t[3] = (a[4 * b + 3] + bt[3]) * 0.5;
+      t0 = (a[4 * b + 0] + bt[0]) * 0.5;
+      t1 = (a[4 * b + 1] + bt[2]) * 0.5;
+      t2 = (a[4 * b + 2] + bt[1]) * 0.5;
+      t3 = (a[4 * b + 3] + bt[3]) * 0.5;
     }
-    *reinterpret_cast<double2*>(o + 4 * b) = make_double2(t[0], t[1]);
-    *reinterpret_cast<double2*>(o + 4 * b + 2) = make_double2(t[2], t[3]);
+    blk[4 * b + 0] = t0;
+    blk[4 * b + 1] = t1;
+    blk[4 * b + 2] = t2;
+    blk[4 * b + 3] = t3;
   }
   const uchar2 f = *reinterpret_cast<const uchar2*>(fm + 2 * nd);
-  const double a00 = o[16], a11 = o[19];
-  *reinterpret_cast<double2*>(o + 36) = make_double2(f.x ? 1.0 / a00 : 0.0, f.y ? 1.0 / a11 : 0.0);
-  *reinterpret_cast<double2*>(o + 38) = make_double2(0.0, 0.0);
+  store_halves(blk, f.x ? 1.0 / blk[16] : 0.0, f.y ? 1.0 / blk[19] : 0.0, stL + (size_t)nd * kHalf,
+               stU + (size_t)nd * kHalf);
 }
 
 // ---------------------------------------------------------------------------
@@ -258,7 +293,7 @@ __global__ void k_prolong_add(int fnx, int fny, const uint8_t* __restrict__ ffm,
 }
 
 // ---------------------------------------------------------------------------
-// exact-order Gauss-Seidel sweep (wavefront), v1
+// exact-order Gauss-Seidel sweep, v2: old-value pass + staged wavefront solve
 // ---------------------------------------------------------------------------
 VTS_DEVICE_INLINE unsigned long long ld_acquire(const unsigned long long* p) {
   unsigned long long v;
@@ -268,162 +303,418 @@ VTS_DEVICE_INLINE unsigned long long ld_acquire(const unsigned long long* p) {
 VTS_DEVICE_INLINE void st_release(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-
-template <bool FWD>
-__global__ void __launch_bounds__(32) k_gs_sweep(int nx, int ny, int ngrid, const double* __restrict__ st,
-                                               const double* __restrict__ b, const double* __restrict__ border,
-                                               double* x, unsigned long long* flags, const int* skip) {
-  if (skip && *skip) return;
-  const int lane = threadIdx.x, grp = blockIdx.x;
-  const int r = grp * 32 + lane;  // row in sweep order
-  const bool row_ok = r < ny;
-  const int iy = FWD ? r : ny - 1 - r;
-  const double xa = x[ngrid];
-  const int nsteps = nx + 62;
-  double pm0 = 0.0, pm1 = 0.0, pz0 = 0.0, pz1 = 0.0, pp0 = 0.0, pp1 = 0.0;  // previous row (new), cols j-1, j, j+1
-  double w0 = 0.0, w1 = 0.0;                                                // own row, col j-1 (new)
-  unsigned long long seen = 0;
-  const int prev_row_y = FWD ? iy - 1 : iy + 1;  // grid row of the sweep-previous row
-  const int next_row_y = FWD ? iy + 1 : iy - 1;
-  if (lane == 0 && grp > 0) {
-    // first two sweep columns of the previous group's last row (later ones arrive each step)
-    const unsigned long long need = (unsigned long long)((nx > 1 ? 1 : 0) + 62 + 1);
-    while (seen < need) seen = ld_acquire(flags + grp - 1);
-    const int q0 = FWD ? 0 : nx - 1;
-    const double2 v0 = __ldcg(reinterpret_cast<const double2*>(x + 2 * (q0 + nx * prev_row_y)));
-    pz0 = v0.x;
-    pz1 = v0.y;
-    if (nx > 1) {
-      const int q1 = FWD ? 1 : nx - 2;
-      const double2 v1 = __ldcg(reinterpret_cast<const double2*>(x + 2 * (q1 + nx * prev_row_y)));
-      pp0 = v1.x;
-      pp1 = v1.y;
-    }
+VTS_DEVICE_INLINE uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+VTS_DEVICE_INLINE void mbar_init(unsigned long long* m, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
+}
+VTS_DEVICE_INLINE void mbar_expect_tx(unsigned long long* m, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
+}
+VTS_DEVICE_INLINE bool mbar_try_wait(unsigned long long* m, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(m)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+VTS_DEVICE_INLINE void mbar_wait(unsigned long long* m, unsigned parity) {
+  while (!mbar_try_wait(m, parity)) {
   }
-  for (int t = 0; t < nsteps; ++t) {
-    const int j = t - 2 * lane;
-    const bool active = row_ok && j >= 0 && j < nx;
-    double n0 = 0.0, n1 = 0.0;
-    if (active) {
-      const int ix = FWD ? j : nx - 1 - j;
-      const int nd = ix + nx * iy;
-      const double* a = st + (size_t)nd * kStencilStride;
-      double c[38];
+}
+// bulk global -> shared copy (TMA engine), completion counted on mbarrier m
+VTS_DEVICE_INLINE void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* m) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(m))
+               : "memory");
+}
+
+// Old-value pass of one sweep: P = b - border x_alpha - U x_old (forward) or
+// - L x_old (backward).  Sums follow the CSR column order of multigrid.py:41-47.
+template <bool FWD>
+__global__ void __launch_bounds__(256) k_gs_old(int nx, int ny, int ngrid, const double* __restrict__ half,
+                                              const double* __restrict__ b, const double* __restrict__ bd,
+                                              const double* __restrict__ x, double* __restrict__ P,
+                                              const int* skip) {
+  if (skip && *skip) return;
+  const int nd = blockIdx.x * blockDim.x + threadIdx.x;
+  if (nd >= nx * ny) return;
+  const int ix = nd % nx, iy = nd / nx;
+  const double xa = x[ngrid];
+  const double* a = half + (size_t)nd * kHalf;
+  const double2 bv = *reinterpret_cast<const double2*>(b + 2 * nd);
+  const double2 dv = *reinterpret_cast<const double2*>(bd + 2 * nd);
+  const double2 xo = *reinterpret_cast<const double2*>(x + 2 * nd);
+  // half slots q = 0..3: FWD (U) NE N NW E at (+1,+1) (0,+1) (-1,+1) (+1,0); BWD (L) mirrored
+  const int sg = FWD ? 1 : -1;
+  double2 v[4];
 #pragma unroll
-      for (int k = 0; k < 19; ++k) {
-        const double2 v = *reinterpret_cast<const double2*>(a + 2 * k);
-        c[2 * k] = v.x;
-        c[2 * k + 1] = v.y;
-      }
-      const double2 bv = *reinterpret_cast<const double2*>(b + 2 * nd);
-      const double2 bd = *reinterpret_cast<const double2*>(border + 2 * nd);
-      const double badj0 = __dsub_rn(bv.x, __dmul_rn(bd.x, xa));
-      const double badj1 = __dsub_rn(bv.y, __dmul_rn(bd.y, xa));
-      const double2 xo = *reinterpret_cast<const double2*>(x + 2 * nd);  // own old values
-      // neighbour values by block index (dy+1)*3 + (dx+1) in grid coordinates
-      double v0[9], v1[9];
+  for (int q = 0; q < 4; ++q) {
+    const int dx = sg * (q == 0 ? 1 : q == 1 ? 0 : q == 2 ? -1 : 1);
+    const int dy = sg * (q == 3 ? 0 : 1);
+    const int jx = ix + dx, jy = iy + dy;
+    v[q] = (jx >= 0 && jx < nx && jy >= 0 && jy < ny) ? *reinterpret_cast<const double2*>(x + 2 * (jx + nx * jy))
+                                                      : make_double2(0.0, 0.0);
+  }
+  double p0 = __dsub_rn(bv.x, __dmul_rn(dv.x, xa));
+  double p1 = __dsub_rn(bv.y, __dmul_rn(dv.y, xa));
+  if (FWD) {
+    // CSR order of the upper part: C(a01 x1), E, NW, N, NE  (slots 3, 2, 1, 0)
+    p0 = fma(-a[kHC], xo.y, p0);
 #pragma unroll
-      for (int k = 0; k < 9; ++k) { v0[k] = 0.0; v1[k] = 0.0; }
-      // sweep-previous row (new): sweep cols j-1, j, j+1
-      if (FWD) {  // row iy-1: SW(0) S(1) SE(2) at ix-1, ix, ix+1
-        v0[0] = pm0; v1[0] = pm1; v0[1] = pz0; v1[1] = pz1; v0[2] = pp0; v1[2] = pp1;
-        v0[3] = w0; v1[3] = w1;  // W new
-      } else {    // row iy+1: sweep col j-1 -> ix+1 (NE 8), j -> N 7, j+1 -> ix-1 (NW 6)
-        v0[8] = pm0; v1[8] = pm1; v0[7] = pz0; v1[7] = pz1; v0[6] = pp0; v1[6] = pp1;
-        v0[5] = w0; v1[5] = w1;  // E new
+    for (int q = 3; q >= 0; --q) {
+      p0 = fma(-a[4 * q + 0], v[q].x, p0);
+      p0 = fma(-a[4 * q + 1], v[q].y, p0);
+      p1 = fma(-a[4 * q + 2], v[q].x, p1);
+      p1 = fma(-a[4 * q + 3], v[q].y, p1);
+    }
+  } else {
+    // CSR order of the lower part: SW, S, SE, W, C(a10 x0)  (slots 0..3)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      p0 = fma(-a[4 * q + 0], v[q].x, p0);
+      p0 = fma(-a[4 * q + 1], v[q].y, p0);
+      p1 = fma(-a[4 * q + 2], v[q].x, p1);
+      p1 = fma(-a[4 * q + 3], v[q].y, p1);
+    }
+    p1 = fma(-a[kHC], xo.x, p1);
+  }
+  *reinterpret_cast<double2*>(P + 2 * nd) = make_double2(p0, p1);
+}
+
+#ifdef VTS_GS_PROBE
+__device__ long long g_gs_probe[4 * 256];
+VTS_DEVICE_INLINE long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+namespace gs {
+constexpr int R = 16;      // grid rows (compute lanes) per band / CTA
+constexpr int W = 17;      // wavefront steps per window (odd: conflict-free lane stride)
+constexpr int NS = 3;      // window slots in flight (in and out rings)
+constexpr int NSA = 4;     // window slots of the previous band's row
+constexpr int SKEW = 2;    // columns between consecutive rows of the wavefront
+constexpr int kWarps = 5;  // compute, loader, storer, publisher, stager
+// one window slot = three TMA boxes: R rows x W nodes x {22 stencil, 2 P, 2 border} doubles
+struct __align__(128) InSlot {
+  double st[R][W][kHalf];
+  double p[R][W][2];
+  double q[R][W][2];
+};
+struct Smem {
+  InSlot in[NS];
+  double2 out[NS][R][W];
+  double2 above[NSA][W];
+  unsigned long long full_in[NS], empty_in[NS], full_out[NS], empty_out[NS];
+  unsigned long long full_above[NSA], empty_above[NSA];
+};
+static_assert(sizeof(InSlot) % 128 == 0, "TMA destinations must stay 128-B aligned");
+static_assert(((W * kHalf * 8) / 16) % 2 == 1, "lane stride must be an odd multiple of 16 B");
+}  // namespace gs
+
+VTS_DEVICE_INLINE void mbar_arrive(unsigned long long* m) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(m)) : "memory");
+}
+// 3-D TMA tile load (box of the tensor map at {c0, c1, c2}) with mbarrier completion
+VTS_DEVICE_INLINE void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, unsigned long long* m) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(m))
+      : "memory");
+}
+
+// Wavefront lower-triangular solve (D_L + L) x = P in sweep order (forward:
+// lexicographic; backward: reversed, where the U half plays the role of L).
+// ZERO: first sweep from the zero guess, P = b - border x_alpha formed here.
+//
+// Lane l of warp 0 owns band row l (grid row band*R + l in sweep order) and
+// works on sweep column j = t - SKEW*l at step t.  A window of W steps needs,
+// for row l, the W nodes starting at column W*w - SKEW*l: a parallelogram
+// whose node indices are affine in (position, row) with row stride nx - SKEW,
+// i.e. ONE 3-D TMA box of a tensor map with that row stride (mapS / mapP /
+// mapQ: half-stencil, P or b, border).  All synchronisation of the compute
+// warp is one uniform mbarrier wait per ring per window.
+//   warp 1  loader (1 thread): 2-3 TMA boxes per window, NS windows ahead
+//   warp 2  storer: rows 0..R-2 of each finished window -> global x
+//   warp 3  publisher: row R-1 -> global x, fence, release of the number of
+//           that row's final columns (the next band's input)
+//   warp 4  stager: acquires the previous band's counter, copies the columns
+//           lane 0 needs in the next window into the above ring
+template <bool FWD, bool ZERO>
+__global__ void __launch_bounds__(32 * gs::kWarps, 1)
+    k_gs_tri(int nx, int ny, int ngrid, int pad_nodes, const __grid_constant__ CUtensorMap mapS,
+             const __grid_constant__ CUtensorMap mapP, const __grid_constant__ CUtensorMap mapQ,
+             double* __restrict__ x, unsigned long long* flags, const int* skip) {
+  using namespace gs;
+  if (skip && *skip) return;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Smem& S = *reinterpret_cast<Smem*>(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int band = blockIdx.x;
+  const int rows_here = min(R, ny - band * R);
+  const bool has_above = band > 0;
+  const int T = nx + SKEW * (R - 1);
+  const int nwin = (T + W - 1) / W;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&S.full_in[s], 1);
+      mbar_init(&S.empty_in[s], 1);
+      mbar_init(&S.full_out[s], 1);
+      mbar_init(&S.empty_out[s], 2);
+    }
+    for (int s = 0; s < NSA; ++s) {
+      mbar_init(&S.full_above[s], 1);
+      mbar_init(&S.empty_above[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // band row l -> grid row; box row of band row l; slot position of step st
+  auto grid_row = [&](int l) {
+    const int r = band * R + l;
+    return FWD ? r : ny - 1 - r;
+  };
+  // grid column of slot position p in window w for band row l
+  auto grid_ix = [&](int w, int l, int p) { return FWD ? W * w - SKEW * l + p : nx - W * (w + 1) + SKEW * l + p; };
+
+  if (warp == 1) {  // ---------------- loader (one thread, TMA boxes)
+    if (lane == 0) {
+      const int iy0 = band * R, iyb = ny - 1 - band * R;
+      for (int w = 0; w < nwin; ++w) {
+        const int s = w % NS;
+        if (w >= NS) mbar_wait(&S.empty_in[s], ((w / NS) - 1) & 1);
+        // node index of box element (p = 0, box row 0)
+        const int node0 = FWD ? iy0 * nx + W * w : (iyb - R + 2) * nx - W * (w + 1) + SKEW * (R - 1);
+        const int c1 = node0 + pad_nodes;
+        mbar_expect_tx(&S.full_in[s], (unsigned)(sizeof(S.in[s].st) + sizeof(S.in[s].p) + (ZERO ? sizeof(S.in[s].q) : 0)));
+        tma_load_3d(&S.in[s].st[0][0][0], &mapS, 0, c1, 0, &S.full_in[s]);
+        tma_load_3d(&S.in[s].p[0][0][0], &mapP, 0, c1, 0, &S.full_in[s]);
+        if (ZERO) tma_load_3d(&S.in[s].q[0][0][0], &mapQ, 0, c1, 0, &S.full_in[s]);
       }
-      // old values: own row next node, sweep-next row three nodes
-      {
-        const int ox = FWD ? ix + 1 : ix - 1;
-        if (ox >= 0 && ox < nx) {
-          const double2 v = *reinterpret_cast<const double2*>(x + 2 * (ox + nx * iy));
-          if (FWD) { v0[5] = v.x; v1[5] = v.y; } else { v0[3] = v.x; v1[3] = v.y; }
+    }
+    return;
+  }
+  if (warp == 2 || warp == 3) {  // ---------------- storer (rows 0..R-2) / publisher (row R-1)
+    const bool pub = warp == 3;
+    const bool publish = pub && rows_here == R && band * R + R < ny;
+    unsigned long long published = 0;
+    for (int w = 0; w < nwin; ++w) {
+      const int s = w % NS;
+      mbar_wait(&S.full_out[s], (w / NS) & 1);
+      if (!pub) {
+        for (int i = lane; i < (R - 1) * W; i += 32) {
+          const int l = i / W, p = i - (i / W) * W;
+          if (l >= rows_here) continue;
+          const int ix = grid_ix(w, l, p);
+          const int j = FWD ? ix : nx - 1 - ix;
+          if (j < 0 || j >= nx || ix < 0 || ix >= nx) continue;
+          *reinterpret_cast<double2*>(x + 2 * ((size_t)grid_row(l) * nx + ix)) = S.out[s][l][p];
         }
-        if (next_row_y >= 0 && next_row_y < ny) {
-#pragma unroll
-          for (int d = -1; d <= 1; ++d) {
-            const int qx = ix + d;
-            if (qx < 0 || qx >= nx) continue;
-            const double2 v = *reinterpret_cast<const double2*>(x + 2 * (qx + nx * next_row_y));
-            const int blk = (FWD ? 6 : 0) + (d + 1);
-            v0[blk] = v.x;
-            v1[blk] = v.y;
+      } else if (R - 1 < rows_here) {
+        const int l = R - 1;
+        if (lane < W) {
+          const int ix = grid_ix(w, l, lane);
+          if (ix >= 0 && ix < nx)
+            *reinterpret_cast<double2*>(x + 2 * ((size_t)grid_row(l) * nx + ix)) = S.out[s][l][lane];
+        }
+        if (publish) {
+          __threadfence();
+          __syncwarp();
+          // sweep columns < W*(w+1) - SKEW*(R-1) of the last row are final
+          const long long c = (long long)W * (w + 1) - SKEW * (R - 1);
+          const unsigned long long done = (unsigned long long)(c < 0 ? 0 : (c > nx ? nx : c));
+          if (lane == 0 && done > published) {
+            st_release(flags + band, done);
+            published = done;
           }
         }
       }
-      if (FWD) {
-        // dof 0 then dof 1 (node-major, x then y)
-        double s = badj0;
-#pragma unroll
-        for (int k = 0; k < 9; ++k) {
-          if (k == kBlockCenter) { s = fma(-c[4 * k + 1], xo.y, s); continue; }
-          s = fma(-c[4 * k], v0[k], s);
-          s = fma(-c[4 * k + 1], v1[k], s);
-        }
-        n0 = s * c[kRd0];
-        s = badj1;
-#pragma unroll
-        for (int k = 0; k < 9; ++k) {
-          if (k == kBlockCenter) { s = fma(-c[4 * k + 2], n0, s); continue; }
-          s = fma(-c[4 * k + 2], v0[k], s);
-          s = fma(-c[4 * k + 3], v1[k], s);
-        }
-        n1 = s * c[kRd1];
-      } else {
-        // backward order: dof 1 then dof 0
-        double s = badj1;
-#pragma unroll
-        for (int k = 0; k < 9; ++k) {
-          if (k == kBlockCenter) { s = fma(-c[4 * k + 2], xo.x, s); continue; }
-          s = fma(-c[4 * k + 2], v0[k], s);
-          s = fma(-c[4 * k + 3], v1[k], s);
-        }
-        n1 = s * c[kRd1];
-        s = badj0;
-#pragma unroll
-        for (int k = 0; k < 9; ++k) {
-          if (k == kBlockCenter) { s = fma(-c[4 * k + 1], n1, s); continue; }
-          s = fma(-c[4 * k], v0[k], s);
-          s = fma(-c[4 * k + 1], v1[k], s);
-        }
-        n0 = s * c[kRd0];
-      }
-      *reinterpret_cast<double2*>(x + 2 * nd) = make_double2(n0, n1);
-      w0 = n0;
-      w1 = n1;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.empty_out[s]);
     }
-    // hand the new value to the next row (it needs sweep col j+1 at its step t+1 ... as its col j+2)
-    double r0 = __shfl_up_sync(0xffffffffu, n0, 1);
-    double r1 = __shfl_up_sync(0xffffffffu, n1, 1);
-    if (lane == 0) {
-      r0 = 0.0;
-      r1 = 0.0;
-      const int jn = t + 2;  // sweep column needed next step (+1 ahead)
-      if (grp > 0 && row_ok && jn < nx && prev_row_y >= 0 && prev_row_y < ny) {
-        const unsigned long long need = (unsigned long long)(jn + 62 + 1);
-        while (seen < need) seen = ld_acquire(flags + grp - 1);
-        const int qx = FWD ? jn : nx - 1 - jn;
-        const double2 v = __ldcg(reinterpret_cast<const double2*>(x + 2 * (qx + nx * prev_row_y)));
-        r0 = v.x;
-        r1 = v.y;
-      }
-    }
-    pm0 = pz0; pm1 = pz1;
-    pz0 = pp0; pz1 = pp1;
-    pp0 = r0; pp1 = r1;
-    __syncwarp();
-    if (lane == 31 && ((t & 7) == 7 || t == nsteps - 1)) st_release(flags + grp, (unsigned long long)(t + 1));
+    return;
   }
-  // lane 0 consumed flags[grp-1]; nobody reads it again in this launch
-  if (lane == 0 && grp > 0) flags[grp - 1] = 0ull;
+  if (warp == 4) {  // ---------------- stager (previous band's last row -> above ring)
+    if (has_above && rows_here > 0) {
+      const int prev_y = FWD ? grid_row(0) - 1 : grid_row(0) + 1;
+      unsigned long long seen = 0;
+      // above slot a = w + 1 holds sweep columns W*w + SKEW + [0, W); a = 0 is the preload
+      for (int a = 0; a <= nwin; ++a) {
+        const int s = a % NSA;
+        if (a >= NSA) mbar_wait(&S.empty_above[s], ((a / NSA) - 1) & 1);
+        const int c0 = W * (a - 1) + SKEW;
+        const unsigned long long need = (unsigned long long)max(0, min(nx, c0 + W));
+        if (lane == 0)
+          while (seen < need) seen = ld_acquire(flags + band - 1);
+        __syncwarp();
+        if (lane < W) {
+          const int j = c0 + lane;
+          double2 v = make_double2(0.0, 0.0);
+          if (j >= 0 && j < nx) {
+            const int ix = FWD ? j : nx - 1 - j;
+            v = __ldcg(reinterpret_cast<const double2*>(x + 2 * ((size_t)prev_y * nx + ix)));
+          }
+          S.above[s][lane] = v;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.full_above[s]);
+      }
+      if (lane == 0) flags[band - 1] = 0ull;  // consumed by this band only
+    }
+    return;
+  }
+
+  // ---------------- warp 0: compute
+  const int l = lane;
+  const bool act = l < rows_here;
+  static_assert(SKEW == 2, "the step pipeline below assumes a two-column skew");
+  const int lc = l < R ? l : R - 1;
+  const int brow = FWD ? lc : R - 1 - lc;  // box row holding band row l
+  const double xa = ZERO ? x[ngrid] : 0.0;
+  double2 win[SKEW + 1];  // previous row, new values, sweep columns j-1 .. j+SKEW-1
+#pragma unroll
+  for (int i = 0; i <= SKEW; ++i) win[i] = make_double2(0.0, 0.0);
+  double2 wprev = make_double2(0.0, 0.0);  // own row, previous sweep column (new)
+  if (has_above) {  // sweep columns 0 .. SKEW-1 of the previous row
+    mbar_wait(&S.full_above[0], 0);
+    if (l == 0) {
+#pragma unroll
+      for (int c = 0; c < SKEW; ++c) win[1 + c] = S.above[0][W - SKEW + c];
+    }
+    __syncwarp();
+    if (l == 0) mbar_arrive(&S.empty_above[0]);
+  }
+#ifdef VTS_GS_PROBE
+  long long t_first = 0, t_wait_above = 0;
+  if (l == 0) g_gs_probe[4 * band] = gtimer();
+#endif
+  for (int w = 0; w < nwin; ++w) {
+    const int s = w % NS;
+    mbar_wait(&S.full_in[s], (w / NS) & 1);
+    if (w >= NS) mbar_wait(&S.empty_out[s], ((w / NS) - 1) & 1);
+    const int sa = (w + 1) % NSA;
+#ifdef VTS_GS_PROBE
+    const long long tw0 = gtimer();
+    if (has_above) mbar_wait(&S.full_above[sa], ((w + 1) / NSA) & 1);
+    t_wait_above += gtimer() - tw0;
+    if (w == 0 && l == 0) t_first = gtimer();
+#endif
+    if (has_above) mbar_wait(&S.full_above[sa], ((w + 1) / NSA) & 1);
+    const InSlot& in = S.in[s];
+    // branch-free, software-pipelined steps: while step st runs its 5-op
+    // recurrence, step st+1's coefficients are loaded and its
+    // recurrence-independent partial sums are formed from the window (all
+    // previous-row values it needs are already final).  Every lane computes
+    // on finite slot data (padding / out-of-range nodes are zeros or real
+    // neighbours); results are selected.
+    constexpr int d0 = FWD ? 0 : 1;
+    constexpr int d1 = 1 - d0;
+    struct StepData {
+      double q0, q1;        // partial sums without the own-row and the newest previous-row neighbour
+      double e00, e01, e10, e11;  // coupling to the previous row's column j+1 (arrives by shuffle)
+      double w00, w01, w10, w11, c, r0, r1;  // own-row block rows d0/d1, centre coupling, reciprocals
+    };
+    auto prepare = [&](int st, const double2 xm, const double2 xz) {
+      const int pos = FWD ? st : W - 1 - st;
+      const double2* a2 = reinterpret_cast<const double2*>(in.st[brow][pos]);
+      double a[20];
+#pragma unroll
+      for (int i = 0; i < 10; ++i) {
+        const double2 v = a2[i];
+        a[2 * i] = v.x;
+        a[2 * i + 1] = v.y;
+      }
+      double p0, p1;
+      const double2 pp = *reinterpret_cast<const double2*>(in.p[brow][pos]);
+      if (ZERO) {
+        const double2 qq = *reinterpret_cast<const double2*>(in.q[brow][pos]);
+        p0 = __dsub_rn(pp.x, __dmul_rn(qq.x, xa));
+        p1 = __dsub_rn(pp.y, __dmul_rn(qq.y, xa));
+      } else {
+        p0 = pp.x;
+        p1 = pp.y;
+      }
+      auto pre = [&](int d, double p) {
+        const double t1 = fma(-a[0 + 2 * d], xm.x, -a[1 + 2 * d] * xm.y);
+        const double t2 = fma(-a[4 + 2 * d], xz.x, -a[5 + 2 * d] * xz.y);
+        return p + (t1 + t2);
+      };
+      StepData o;
+      o.e00 = a[8 + 2 * d0];
+      o.e01 = a[9 + 2 * d0];
+      o.e10 = a[8 + 2 * d1];
+      o.e11 = a[9 + 2 * d1];
+      o.q0 = pre(d0, d0 == 0 ? p0 : p1);
+      o.q1 = pre(d1, d1 == 0 ? p0 : p1);
+      o.w00 = a[12 + 2 * d0];
+      o.w01 = a[13 + 2 * d0];
+      o.w10 = a[12 + 2 * d1];
+      o.w11 = a[13 + 2 * d1];
+      o.c = a[kHC];
+      o.r0 = a[d0 == 0 ? kHRd0 : kHRd1];
+      o.r1 = a[d1 == 0 ? kHRd0 : kHRd1];
+      return o;
+    };
+    StepData cur = prepare(0, win[0], win[1]);
+#pragma unroll
+    for (int st = 0; st < W; ++st) {
+      const int j = W * w - SKEW * l + st;
+      const int pos = FWD ? st : W - 1 - st;
+      const bool valid = act && j >= 0 && j < nx;
+      // the recurrence of step st (xp: previous row, column j+1, shuffled in last step):
+      //   x_d0 = r0 (q0 - E[d0].xp - W[d0].w),  x_d1 = r1 (q1 - E[d1].xp - W[d1].w - c x_d0)
+      const double2 xp = win[2];
+      const double u0 = fma(-cur.e00, xp.x, fma(-cur.e01, xp.y, cur.q0));
+      const double u1 = fma(-cur.e10, xp.x, fma(-cur.e11, xp.y, cur.q1));
+      const double n0 = fma(-cur.w00, wprev.x, fma(-cur.w01, wprev.y, u0)) * cur.r0;
+      const double n1 = fma(-cur.c, n0, fma(-cur.w10, wprev.x, fma(-cur.w11, wprev.y, u1))) * cur.r1;
+      // step st+1's independent part (previous-row columns j, j+1 are in win[1..2])
+      StepData nxt;
+      if (st + 1 < W) nxt = prepare(st + 1, win[1], win[2]);
+      const double2 calc = FWD ? make_double2(n0, n1) : make_double2(n1, n0);
+      const double2 nv = valid ? calc : make_double2(0.0, 0.0);
+      wprev = valid ? calc : wprev;
+      if (l < R) S.out[s][l][pos] = nv;
+      const double r0s = __shfl_up_sync(0xffffffffu, nv.x, 1);
+      const double r1s = __shfl_up_sync(0xffffffffu, nv.y, 1);
+      const double2 av = S.above[sa][st];  // zeros for band 0 (never filled, never read as valid)
+      const bool from_above = l == 0 && has_above;
+      const double r0 = l == 0 ? (from_above ? av.x : 0.0) : r0s;
+      const double r1 = l == 0 ? (from_above ? av.y : 0.0) : r1s;
+#pragma unroll
+      for (int i = 0; i < SKEW; ++i) win[i] = win[i + 1];
+      win[SKEW] = make_double2(r0, r1);
+      if (st + 1 < W) cur = nxt;
+    }
+    __syncwarp();
+    if (l == 0) {
+      mbar_arrive(&S.empty_in[s]);
+      mbar_arrive(&S.full_out[s]);
+      if (has_above) mbar_arrive(&S.empty_above[sa]);
+    }
+  }
+#ifdef VTS_GS_PROBE
+  if (l == 0) {
+    g_gs_probe[4 * band + 1] = t_first;
+    g_gs_probe[4 * band + 2] = gtimer();
+    g_gs_probe[4 * band + 3] = t_wait_above;
+  }
+#endif
 }
 
 // ---------------------------------------------------------------------------
 // finest-level border unknown relaxation (multigrid.py:121-122, 141-142)
 // ---------------------------------------------------------------------------
-__global__ void k_alpha_init(int ngrid, const double* b, double* x, const double* corner, const int* skip) {
+// top level: x_alpha = b_alpha / corner (multigrid.py:121-122); coarse levels start at 0
+__global__ void k_alpha_init(int ngrid, const double* b, double* x, const double* corner, int top, const int* skip) {
   if (skip && *skip) return;
-  x[ngrid] = b[ngrid] / *corner;
+  x[ngrid] = top ? b[ngrid] / *corner : 0.0;
 }
 
 __global__ void k_alpha_relax(int ngrid, const double* __restrict__ border, const double* b, double* x,
@@ -443,7 +734,8 @@ __global__ void k_alpha_relax(int ngrid, const double* __restrict__ border, cons
 // ---------------------------------------------------------------------------
 // coarsest level: dense bordered matrix, Cholesky, triangular solves
 // ---------------------------------------------------------------------------
-__global__ void k_dense_coarse(int nx, int ny, const double* __restrict__ st, const double* __restrict__ border,
+__global__ void k_dense_coarse(int nx, int ny, const double* __restrict__ stL, const double* __restrict__ stU,
+                               const double* __restrict__ border,
                                const int32_t* __restrict__ g2f, const double* corner, int N, double shift,
                                double* __restrict__ A) {
   // one thread per (free row, neighbour block) ; zero-fill first via memset
@@ -459,7 +751,7 @@ __global__ void k_dense_coarse(int nx, int ny, const double* __restrict__ st, co
       for (int cc = 0; cc < 2; ++cc) {
         const int fj = g2f[2 * (jx + nx * jy) + cc];
         if (fj < 0) continue;
-        A[(size_t)fi * N + fj] = st[(size_t)nd * kStencilStride + 4 * b + 2 * r + cc];
+        A[(size_t)fi * N + fj] = stencil_entry(stL, stU, nd, b, r, cc);
       }
     }
     A[(size_t)fi * N + (N - 1)] = border[2 * nd + r];
@@ -545,20 +837,76 @@ __global__ void __launch_bounds__(1024) k_coarse_solve(int N, int nfree, int ngr
 // ---------------------------------------------------------------------------
 // host drivers
 // ---------------------------------------------------------------------------
-static int gs_sweep(Ctx* c, int k, const double* b, double* x, bool forward, const int* skip) {
-  LevelBuf& L = c->lv[k];
-  const int groups = div_up(L.d.ny, 32);
-  if (forward)
-    k_gs_sweep<true><<<groups, 32, 0, c->stream>>>(L.d.nx, L.d.ny, L.d.ngrid, L.d.stencil, b, L.d.border, x,
-                                                    L.gs_flags, skip);
-  else
-    k_gs_sweep<false><<<groups, 32, 0, c->stream>>>(L.d.nx, L.d.ny, L.d.ngrid, L.d.stencil, b, L.d.border, x,
-                                                     L.gs_flags, skip);
-  VTS_LAUNCHED(c);
+static bool g_gs_attr_set = false;
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static int gs_prepare() {
+  if (g_gs_attr_set) return 0;
+  const int bytes = (int)sizeof(gs::Smem);
+  VTS_CUDA(cudaFuncSetAttribute(k_gs_tri<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  VTS_CUDA(cudaFuncSetAttribute(k_gs_tri<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  VTS_CUDA(cudaFuncSetAttribute(k_gs_tri<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  cudaDriverEntryPointQueryResult q;
+  VTS_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&g_encode), cudaEnableDefault, &q));
+  if (q != cudaDriverEntryPointSuccess || !g_encode) {
+    set_error(5, "cuTensorMapEncodeTiled unavailable");
+    return 5;
+  }
+  g_gs_attr_set = true;
   return 0;
 }
 
-int level_residual_grid(Ctx* c, int k, const double* x, const double* b, double* r, const int* skip);
+// 3-D map over a padded node array of `width` doubles per node: dims {width,
+// nodes incl. padding, R rows}, strides {width, (nx - SKEW) * width} doubles,
+// box {width, W, R}.  `data` points at node 0 (pad_nodes nodes precede it).
+static int encode_skewed(CUtensorMap* map, const double* data, int width, const LevelBuf& L) {
+  const cuuint64_t nodes = (cuuint64_t)(L.d.nnodes + 2 * L.pad_nodes);
+  const cuuint64_t dims[3] = {(cuuint64_t)width, nodes, (cuuint64_t)gs::R};
+  const cuuint64_t strides[2] = {(cuuint64_t)width * 8, (cuuint64_t)(L.d.nx - gs::SKEW) * width * 8};
+  const cuuint32_t box[3] = {(cuuint32_t)width, (cuuint32_t)gs::W, (cuuint32_t)gs::R};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  void* base = const_cast<double*>(data - L.pad_nodes * width);
+  const CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error(5, "cuTensorMapEncodeTiled failed");
+    return 5;
+  }
+  return 0;
+}
+
+// one Gauss-Seidel sweep on level k: x <- sweep(x; b) (zero_guess: x_old = 0)
+static int gs_sweep(Ctx* c, int k, const double* b, double* x, bool forward, bool zero_guess, const int* skip) {
+  if (int rc = gs_prepare()) return rc;
+  LevelBuf& L = c->lv[k];
+  const int bands = div_up(L.d.ny, gs::R);
+  const size_t smem = sizeof(gs::Smem);
+  double* P = L.r;
+  CUtensorMap mS, mP, mQ;
+  if (forward && zero_guess) {
+    if (encode_skewed(&mS, L.d.stL, kHalf, L) || encode_skewed(&mP, b, 2, L) || encode_skewed(&mQ, L.d.border, 2, L))
+      return 5;
+    k_gs_tri<true, true><<<bands, 32 * gs::kWarps, smem, c->stream>>>(L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, mS,
+                                                                      mP, mQ, x, L.gs_flags, skip);
+  } else if (forward) {
+    k_gs_old<true><<<div_up(L.d.nnodes, 256), 256, 0, c->stream>>>(L.d.nx, L.d.ny, L.d.ngrid, L.d.stU, b,
+                                                                    L.d.border, x, P, skip);
+    VTS_LAUNCHED(c);
+    if (encode_skewed(&mS, L.d.stL, kHalf, L) || encode_skewed(&mP, P, 2, L)) return 5;
+    k_gs_tri<true, false><<<bands, 32 * gs::kWarps, smem, c->stream>>>(L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, mS,
+                                                                       mP, mP, x, L.gs_flags, skip);
+  } else {
+    k_gs_old<false><<<div_up(L.d.nnodes, 256), 256, 0, c->stream>>>(L.d.nx, L.d.ny, L.d.ngrid, L.d.stL, b,
+                                                                     L.d.border, x, P, skip);
+    VTS_LAUNCHED(c);
+    if (encode_skewed(&mS, L.d.stU, kHalf, L) || encode_skewed(&mP, P, 2, L)) return 5;
+    k_gs_tri<false, false><<<bands, 32 * gs::kWarps, smem, c->stream>>>(L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes,
+                                                                        mS, mP, mP, x, L.gs_flags, skip);
+  }
+  VTS_LAUNCHED(c);
+  return 0;
+}
 
 int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
   const int top = c->L - 1;
@@ -567,13 +915,10 @@ int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
     LevelBuf& L = c->lv[k];
     const double* b = (k == top) ? b_top : L.b;
     double* x = (k == top) ? z_top : L.x;
-    VTS_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * (L.d.ngrid + 1), c->stream));
-    if (k == top) {
-      k_alpha_init<<<1, 1, 0, c->stream>>>(L.d.ngrid, b, x, c->d_corner, skip);
-      VTS_LAUNCHED(c);
-    }
-    for (int s = 0; s < 2; ++s)
-      if (int rc = gs_sweep(c, k, b, x, true, skip)) return rc;
+    k_alpha_init<<<1, 1, 0, c->stream>>>(L.d.ngrid, b, x, c->d_corner, k == top ? 1 : 0, skip);
+    VTS_LAUNCHED(c);
+    if (int rc = gs_sweep(c, k, b, x, true, true, skip)) return rc;
+    if (int rc = gs_sweep(c, k, b, x, true, false, skip)) return rc;
     if (int rc = level_residual_grid(c, k, x, b, L.r, skip)) return rc;
     LevelBuf& C = c->lv[k - 1];
     k_restrict<<<div_up(C.d.nnodes + 1, 256), 256, 0, c->stream>>>(L.d.nx, L.d.ny, L.d.free_mask, L.r, C.d.nx,
@@ -598,7 +943,7 @@ int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
                                                                         C.d.ny, C.d.free_mask, C.x, skip);
     VTS_LAUNCHED(c);
     for (int s = 0; s < 2; ++s)
-      if (int rc = gs_sweep(c, k, b, x, false, skip)) return rc;
+      if (int rc = gs_sweep(c, k, b, x, false, false, skip)) return rc;
     if (k == top) {
       const int grid = (int)std::min<long long>(div_up(L.d.ngrid, 256), kReduceGridCap);
       k_alpha_relax<<<grid, 256, 0, c->stream>>>(L.d.ngrid, L.d.border, b, x, c->d_corner, c->partials,
@@ -618,18 +963,19 @@ int mg_setup(Ctx* c, double shift_scale) {
   {
     LevelBuf& F = c->lv[top];
     k_fine_stencil<<<div_up(F.d.nnodes, 128), 128, 0, c->stream>>>(F.d.nx, F.d.ny, F.d.ex, F.d.ey, c->u_grid,
-                                                                    c->rho_hat, c->chat, F.d.free_mask,
-                                                                    F.d.stencil);
+                                                                    c->rho_hat, c->chat, F.d.free_mask, F.d.stL,
+                                                                    F.d.stU);
     VTS_LAUNCHED(c);
   }
   for (int k = top; k >= 1; --k) {
     LevelBuf& F = c->lv[k];
     LevelBuf& C = c->lv[k - 1];
     double* tmp = c->rap_tmp;
-    k_rap<<<div_up(C.d.nnodes, 128), 128, 0, c->stream>>>(F.d.nx, F.d.ny, F.d.stencil, F.d.free_mask, C.d.nx,
+    k_rap<<<div_up(C.d.nnodes, 128), 128, 0, c->stream>>>(F.d.nx, F.d.ny, F.d.stL, F.d.stU, F.d.free_mask, C.d.nx,
                                                            C.d.ny, C.d.free_mask, tmp);
     VTS_LAUNCHED(c);
-    k_symmetrize<<<div_up(C.d.nnodes, 128), 128, 0, c->stream>>>(C.d.nx, C.d.ny, tmp, C.d.free_mask, C.d.stencil);
+    k_symmetrize<<<div_up(C.d.nnodes, 128), 128, 0, c->stream>>>(C.d.nx, C.d.ny, tmp, C.d.free_mask, C.d.stL,
+                                                                  C.d.stU);
     VTS_LAUNCHED(c);
     k_restrict<<<div_up(C.d.nnodes + 1, 256), 256, 0, c->stream>>>(F.d.nx, F.d.ny, F.d.free_mask, F.d.border,
                                                                      C.d.nx, C.d.ny, C.d.free_mask, C.d.border, 0,
@@ -641,7 +987,7 @@ int mg_setup(Ctx* c, double shift_scale) {
   const int N = c->N0;
   auto build = [&](double shift_scale_now) -> int {
     VTS_CUDA(cudaMemsetAsync(c->chol, 0, sizeof(double) * N * N, c->stream));
-    k_dense_coarse<<<div_up(C.d.nnodes, 128), 128, 0, c->stream>>>(C.d.nx, C.d.ny, C.d.stencil, C.d.border,
+    k_dense_coarse<<<div_up(C.d.nnodes, 128), 128, 0, c->stream>>>(C.d.nx, C.d.ny, C.d.stL, C.d.stU, C.d.border,
                                                                     C.grid2free, c->d_corner, N, 0.0, c->chol);
     VTS_LAUNCHED(c);
     if (shift_scale_now != 0.0) {
@@ -671,15 +1017,11 @@ int mg_setup(Ctx* c, double shift_scale) {
   return 0;
 }
 
-}  // namespace vts
-
-namespace vts {
-
 // Per-kernel device times (CUDA events on the context stream, averaged over
 // `reps` back-to-back launches) for bench.py's roofline: ms[0] Newton apply,
-// ms[1] one V-cycle, ms[2] one forward GS sweep on the finest level, ms[3] one
-// forward GS sweep on the second-finest level, ms[4] finest residual,
-// ms[5] mg_setup (stencil + Galerkin chain + coarse factor, incl. one sync).
+// ms[1] one V-cycle, ms[2] one forward GS sweep (old-value pass + wavefront)
+// on the finest level, ms[3] the same on the second-finest level, ms[4]
+// finest residual, ms[5] mg_setup (stencil + Galerkin chain + coarse factor).
 int time_kernels(Ctx* c, int reps, double* ms) {
   if (!c->mg_ready) {
     set_error(4, "time_kernels: multigrid not set up");
@@ -707,10 +1049,10 @@ int time_kernels(Ctx* c, int reps, double* ms) {
   int rc = 0;
   rc = rc ? rc : timed([&] { return newton_apply_grid(c, xin, yout, nullptr); }, ms + 0);
   rc = rc ? rc : timed([&] { return vcycle_grid(c, xin, yout, nullptr); }, ms + 1);
-  rc = rc ? rc : timed([&] { return gs_sweep(c, top, xin, F.x, true, nullptr); }, ms + 2);
+  rc = rc ? rc : timed([&] { return gs_sweep(c, top, xin, F.x, true, false, nullptr); }, ms + 2);
   if (top >= 1) {
     LevelBuf& G = c->lv[top - 1];
-    rc = rc ? rc : timed([&] { return gs_sweep(c, top - 1, G.b, G.x, true, nullptr); }, ms + 3);
+    rc = rc ? rc : timed([&] { return gs_sweep(c, top - 1, G.b, G.x, true, false, nullptr); }, ms + 3);
   } else {
     ms[3] = 0.0;
   }

@@ -12,6 +12,9 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "../../include/vts_b200.h"
 #include "context.cuh"
 
@@ -52,19 +55,26 @@ static int dalloc(T** p, size_t count) {
   return 0;
 }
 
+// zeroed array of `count` doubles with `pad` zero doubles before and after
+// (the skewed TMA boxes of the Gauss-Seidel wavefront read into the padding)
+static int dalloc_pad(Ctx* c, double** p, size_t count, size_t pad) {
+  double* base = nullptr;
+  const size_t total = count + 2 * pad;
+  VTS_CUDA(cudaMalloc(reinterpret_cast<void**>(&base), total * sizeof(double)));
+  VTS_CUDA(cudaMemset(base, 0, total * sizeof(double)));
+  c->allocs.push_back(base);
+  *p = base + pad;
+  return 0;
+}
+
 static void free_ctx(Ctx* c) {
   for (auto& L : c->lv) {
     cudaFree(const_cast<uint8_t*>(L.d.free_mask));
     cudaFree(const_cast<int32_t*>(L.d.free2grid));
-    cudaFree(L.d.stencil);
-    cudaFree(L.d.border);
     cudaFree(L.grid2free);
-    cudaFree(L.b);
-    cudaFree(L.x);
-    cudaFree(L.r);
     cudaFree(L.gs_flags);
   }
-  for (double* p : c->fvec) cudaFree(p);
+  for (void* p : c->allocs) cudaFree(p);
   cudaFree(c->u_grid);
   cudaFree(c->rho_hat);
   cudaFree(c->chat);
@@ -150,21 +160,19 @@ static int create(Ctx** out, int levels, const int32_t* ex, const int32_t* ey, c
     const int arc = dalloc(&fm_d, ng) || dalloc(&f2g_d, nfree);
     L.d.free_mask = fm_d;
     L.d.free2grid = f2g_d;
+    L.pad_nodes = (size_t)kPadRows * L.d.nx;
     if (arc || dalloc(&L.grid2free, ng) ||
-        dalloc(&L.d.stencil, (size_t)L.d.nnodes * kStencilStride) || dalloc(&L.d.border, ng + 1) ||
-        dalloc(&L.b, ng + 1) || dalloc(&L.x, ng + 1) || dalloc(&L.r, ng + 1))
+        dalloc_pad(c, &L.d.stL, (size_t)L.d.nnodes * kHalf, L.pad_nodes * kHalf) ||
+        dalloc_pad(c, &L.d.stU, (size_t)L.d.nnodes * kHalf, L.pad_nodes * kHalf) ||
+        dalloc_pad(c, &L.d.border, ng + 1, 2 * L.pad_nodes) || dalloc_pad(c, &L.b, ng + 1, 2 * L.pad_nodes) ||
+        dalloc_pad(c, &L.x, ng + 1, 2 * L.pad_nodes) || dalloc_pad(c, &L.r, ng + 1, 2 * L.pad_nodes))
       return fail(VTS_E_CUDA);
-    L.gs_groups = div_up(L.d.ny, 32);
+    L.gs_groups = div_up(L.d.ny, 8);  // >= bands of any GS row-band height used
     if (dalloc(&L.gs_flags, L.gs_groups)) return fail(VTS_E_CUDA);
     if (cudaMemcpy(const_cast<uint8_t*>(L.d.free_mask), mask.data(), ng, cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy(const_cast<int32_t*>(L.d.free2grid), f2g.data(), sizeof(int32_t) * nfree, cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy(L.grid2free, g2f.data(), sizeof(int32_t) * ng, cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemset(L.gs_flags, 0, sizeof(unsigned long long) * L.gs_groups) != cudaSuccess ||
-        cudaMemset(L.d.stencil, 0, sizeof(double) * (size_t)L.d.nnodes * kStencilStride) != cudaSuccess ||
-        cudaMemset(L.d.border, 0, sizeof(double) * (ng + 1)) != cudaSuccess ||
-        cudaMemset(L.b, 0, sizeof(double) * (ng + 1)) != cudaSuccess ||
-        cudaMemset(L.x, 0, sizeof(double) * (ng + 1)) != cudaSuccess ||
-        cudaMemset(L.r, 0, sizeof(double) * (ng + 1)) != cudaSuccess) {
+        cudaMemset(L.gs_flags, 0, sizeof(unsigned long long) * L.gs_groups) != cudaSuccess) {
       set_error(VTS_E_CUDA, "vts_ctx_create: device upload failed");
       return fail(VTS_E_CUDA);
     }
@@ -175,8 +183,7 @@ static int create(Ctx** out, int levels, const int32_t* ex, const int32_t* ey, c
   const int len = F.d.ngrid + 1;
   c->fvec.assign(kNumFineVecs, nullptr);
   for (int i = 0; i < kNumFineVecs; ++i) {
-    if (dalloc(&c->fvec[i], std::max(len, c->m + 1))) return fail(VTS_E_CUDA);
-    cudaMemset(c->fvec[i], 0, sizeof(double) * std::max(len, c->m + 1));
+    if (dalloc_pad(c, &c->fvec[i], std::max(len, c->m + 1), 2 * F.pad_nodes)) return fail(VTS_E_CUDA);
   }
   if (dalloc(&c->u_grid, len) || dalloc(&c->rho_hat, c->m) || dalloc(&c->chat, c->m) || dalloc(&c->d_corner, 1))
     return fail(VTS_E_CUDA);

@@ -7,10 +7,14 @@
 //    right after the grid (index 2*NX*NY);
 //  * element arrays are indexed e = ex_i + EX*ey_i, the reference's order
 //    (mesh.py:253-259);
-//  * a level operator is a node-block 9-point stencil: 9 blocks of 2x2
-//    (block b = (dy+1)*3 + (dx+1), entries r0c0 r0c1 r1c0 r1c1) plus the two
-//    reciprocal diagonals, 40 doubles (320 B) per node, array-of-structs so a
-//    Gauss-Seidel lane reads one contiguous row.
+//  * a level operator is a node-block 9-point stencil (block b = (dy+1)*3 +
+//    (dx+1), entries r0c0 r0c1 r1c0 r1c1) stored as two half-stencils of 20
+//    doubles (160 B) per node, array-of-structs:
+//      L = [SW S SE W | a10 rd0 rd1 a00 | pad pad]   (couplings to earlier nodes)
+//      U = [NE N NW E | a01 rd0 rd1 a11 | pad pad]   (couplings to later nodes)
+//    A forward Gauss-Seidel sweep is "P = b - U x_old" (parallel) followed by
+//    a wavefront solve with L only; a backward sweep swaps the halves, and the
+//    mirrored block order makes the two wavefront kernels identical.
 #pragma once
 
 #include <cstdint>
@@ -22,10 +26,33 @@
 
 namespace vts {
 
-constexpr int kStencilStride = 40;  // doubles per node in a level stencil
-constexpr int kRd0 = 36;            // reciprocal of a00 (0 on a fixed dof)
-constexpr int kRd1 = 37;            // reciprocal of a11
+constexpr int kStencilStride = 40;  // doubles per node of the full (setup-time) stencil
+constexpr int kHalf = 22;           // doubles per node of one half-stencil (20 used + 2 pad: 176 B rows)
+constexpr int kPadRows = 17;        // node rows of zero padding before/after every level array (skewed TMA boxes)
+constexpr int kHC = 16;             // a10 (L) / a01 (U)
+constexpr int kHRd0 = 17, kHRd1 = 18;
+constexpr int kHDiag = 19;          // a00 (L) / a11 (U)
 constexpr int kBlockCenter = 4;
+
+// offset of full-stencil block b inside its half (-1 = center), and which half
+VTS_DEVICE_INLINE int half_offset(int b) {
+  // SW S SE W -> L 0 4 8 12 ; E NW N NE -> U 12 8 4 0
+  return b < 4 ? 4 * b : (b > 4 ? 4 * (8 - b) : -1);
+}
+VTS_DEVICE_INLINE bool in_lower(int b) { return b < 4; }
+
+// entry (r, c) of block b of node nd from the two halves
+VTS_DEVICE_INLINE double stencil_entry(const double* __restrict__ L, const double* __restrict__ U, int nd, int b,
+                                       int r, int c) {
+  const double* l = L + (size_t)nd * kHalf;
+  const double* u = U + (size_t)nd * kHalf;
+  if (b == kBlockCenter) {
+    if (r == 0) return c == 0 ? l[kHDiag] : u[kHC];
+    return c == 0 ? l[kHC] : u[kHDiag];
+  }
+  const int o = half_offset(b) + 2 * r + c;
+  return b < 4 ? l[o] : u[o];
+}
 
 // Element stiffness of the unit Q1 square, row-major 8x8 (set by the context).
 // Defined here: the library is one translation unit (csrc/vts_b200.cu).
@@ -39,7 +66,8 @@ struct LevelDev {
   int nfree;          // number of free dofs (the reference's n)
   const uint8_t* free_mask;  // [ngrid] 1 = free dof
   const int32_t* free2grid;  // [nfree]
-  double* stencil;           // [nnodes * kStencilStride]
+  double* stL;               // [nnodes * kHalf] lower half-stencil
+  double* stU;               // [nnodes * kHalf] upper half-stencil
   double* border;            // [ngrid] level border vector (P^T chain)
 };
 

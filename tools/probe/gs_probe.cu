@@ -1,0 +1,101 @@
+// Standalone probe of the GS wavefront through the library internals: builds a
+// cantilever hierarchy, a synthetic Newton system, the multigrid, then times
+// single sweeps per level and the V-cycle.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o gs_probe gs_probe.cu
+#include "../../paper_1904_06556_b200/csrc/vts_b200.cu"
+#include <cstdio>
+#include <random>
+#include <vector>
+
+int main(int argc, char** argv) {
+  const int levels = argc > 1 ? atoi(argv[1]) : 9;
+  std::vector<int32_t> ex(levels), ey(levels);
+  std::vector<std::vector<int64_t>> dofs(levels);
+  std::vector<const int64_t*> ptrs(levels);
+  for (int k = 0; k < levels; ++k) {
+    ex[k] = 4 << k;
+    ey[k] = 2 << k;
+    const int nx = ex[k] + 1, ny = ey[k] + 1;
+    dofs[k].assign(2 * nx * ny, -1);
+    int64_t n = 0;
+    for (int iy = 0; iy < ny; ++iy)
+      for (int ix = 0; ix < nx; ++ix)
+        for (int c = 0; c < 2; ++c)
+          if (ix > 0) dofs[k][2 * (iy * nx + ix) + c] = n++;
+    ptrs[k] = dofs[k].data();
+  }
+  double ke[64];
+  for (int i = 0; i < 8; ++i)
+    for (int j = 0; j < 8; ++j) ke[8 * i + j] = (i == j ? 0.5 : -0.5 / 7.0);
+  vts_ctx* h = nullptr;
+  if (vts_ctx_create(&h, levels, ex.data(), ey.data(), ptrs.data(), ke, 0)) {
+    printf("create failed: %s\n", vts_last_error());
+    return 1;
+  }
+  vts::Ctx* c = reinterpret_cast<vts::Ctx*>(h);
+  vts::ensure_ke(c);
+  std::mt19937_64 g(1);
+  std::uniform_real_distribution<double> u(-0.01, 0.01), pos(0.5, 2.0);
+  std::vector<double> ug(c->lv[levels - 1].d.ngrid), rh(c->m), ch(c->m);
+  for (auto& v : ug) v = u(g);
+  for (auto& v : rh) v = pos(g);
+  for (auto& v : ch) v = 1e-3 * pos(g);
+  cudaMemcpy(c->u_grid, ug.data(), ug.size() * 8, cudaMemcpyHostToDevice);
+  cudaMemcpy(c->rho_hat, rh.data(), rh.size() * 8, cudaMemcpyHostToDevice);
+  cudaMemcpy(c->chat, ch.data(), ch.size() * 8, cudaMemcpyHostToDevice);
+  double corner = 1.0;
+  cudaMemcpy(c->d_corner, &corner, 8, cudaMemcpyHostToDevice);
+  c->system_bound = true;
+  if (vts::mg_setup(c, 1e-12)) {
+    printf("mg_setup failed: %s\n", vts_last_error());
+    return 1;
+  }
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int k = levels - 1; k >= std::max(0, levels - 4); --k) {
+    vts::LevelBuf& L = c->lv[k];
+    for (int variant = 0; variant < 3; ++variant) {
+      const bool fwd = variant < 2, zero = variant == 0;
+      vts::gs_sweep(c, k, L.b, L.x, fwd, zero, nullptr);
+      cudaEventRecord(e0);
+      const int reps = 5;
+      for (int r = 0; r < reps; ++r) vts::gs_sweep(c, k, L.b, L.x, fwd, zero, nullptr);
+      cudaEventRecord(e1);
+      cudaError_t err = cudaEventSynchronize(e1);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      ms /= reps;
+      const int steps = L.d.nx + 2 * L.d.ny;
+      printf("level %d (%d x %d) %s%s sweep: %8.1f us  (%s) ~%.0f cycles/step\n", k, L.d.nx, L.d.ny,
+             fwd ? "fwd" : "bwd", zero ? "-zero" : "     ", ms * 1e3, cudaGetErrorString(err), ms * 1.965e6 / steps);
+    }
+  }
+#ifdef VTS_GS_PROBE
+  {
+    vts::LevelBuf& L = c->lv[levels - 1];
+    vts::gs_sweep(c, levels - 1, L.b, L.x, true, false, nullptr);
+    cudaDeviceSynchronize();
+    std::vector<long long> pr(4 * 256);
+    cudaMemcpyFromSymbol(pr.data(), vts::g_gs_probe, pr.size() * 8);
+    const int bands = (L.d.ny + vts::gs::R - 1) / vts::gs::R;
+    long long t0 = pr[0];
+    for (int b = 0; b < bands; ++b)
+      printf("band %2d: start %7.1f us  first-window %7.1f  end %7.1f  (dur %6.1f, waiting-above %6.1f us)\n", b,
+             (pr[4 * b] - t0) / 1e3, (pr[4 * b + 1] - t0) / 1e3, (pr[4 * b + 2] - t0) / 1e3,
+             (pr[4 * b + 2] - pr[4 * b + 1]) / 1e3, pr[4 * b + 3] / 1e3);
+  }
+#endif
+  double* xin = c->fvec[10];
+  double* yout = c->fvec[11];
+  vts::vcycle_grid(c, xin, yout, nullptr);
+  cudaEventRecord(e0);
+  for (int r = 0; r < 5; ++r) vts::vcycle_grid(c, xin, yout, nullptr);
+  cudaEventRecord(e1);
+  cudaError_t err = cudaEventSynchronize(e1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  printf("V-cycle: %.1f us (%s)\n", ms * 1e3 / 5, cudaGetErrorString(err));
+  vts_ctx_destroy(h);
+  return 0;
+}
