@@ -411,6 +411,7 @@ struct Smem {
   double2 above[NSA][W];
   unsigned long long full_in[NS], empty_in[NS], full_out[NS], empty_out[NS];
   unsigned long long full_above[NSA], empty_above[NSA];
+  int armed;  // (producer side) highest above-ring chunk the consumer has armed
 };
 static_assert(sizeof(InSlot) % 128 == 0, "TMA destinations must stay 128-B aligned");
 static_assert(((W * kHalf * 8) / 16) % 2 == 1, "lane stride must be an odd multiple of 16 B");
@@ -446,8 +447,13 @@ VTS_DEVICE_INLINE void tma_load_3d(void* dst, const CUtensorMap* map, int c0, in
 //   warp 4  stager: acquires the previous band's counter, copies the columns
 //           lane 0 needs in the next window into the above ring
 template <bool FWD, bool ZERO>
+__device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int band, int rows_here, bool has_above,
+                                           bool dsm_in, unsigned crank, int nwin,
+                                           double* __restrict__ x);
+
+template <bool FWD, bool ZERO>
 __global__ void __launch_bounds__(32 * gs::kWarps, 1)
-    k_gs_tri(int nx, int ny, int ngrid, int pad_nodes, const __grid_constant__ CUtensorMap mapS,
+    k_gs_tri(int nx, int ny, int ngrid, int pad_nodes, int bands, const __grid_constant__ CUtensorMap mapS,
              const __grid_constant__ CUtensorMap mapP, const __grid_constant__ CUtensorMap mapQ,
              double* __restrict__ x, unsigned long long* flags, const int* skip) {
   using namespace gs;
@@ -456,10 +462,23 @@ __global__ void __launch_bounds__(32 * gs::kWarps, 1)
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int band = blockIdx.x;
-  const int rows_here = min(R, ny - band * R);
-  const bool has_above = band > 0;
+  const bool real = band < bands;  // grids are padded to whole clusters
+  const int rows_here = real ? min(R, ny - band * R) : 0;
+  const bool has_above = real && band > 0;
   const int T = nx + SKEW * (R - 1);
   const int nwin = (T + W - 1) / W;
+  unsigned crank, csize;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(csize));
+  // band-to-band handoff: through DSMEM inside a cluster, through global memory across clusters
+  const bool dsm_in = has_above && crank > 0;
+  const bool dsm_out = real && crank + 1 < csize && band + 1 < bands;
+  // bytes of the above-ring slot a (sweep columns W*(a-1) + SKEW + [0, W) that exist)
+  auto above_bytes = [&](int a) -> unsigned {
+    const int c0 = W * (a - 1) + SKEW;
+    const int lo = max(c0, 0), hi = min(c0 + W, nx);
+    return (unsigned)(hi > lo ? 16 * (hi - lo) : 0);
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
@@ -472,9 +491,14 @@ __global__ void __launch_bounds__(32 * gs::kWarps, 1)
       mbar_init(&S.full_above[s], 1);
       mbar_init(&S.empty_above[s], 1);
     }
+    S.armed = NSA - 1;  // the consumer arms above slots 0 .. NSA-1 before the first cluster barrier
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (dsm_in) {
+      for (int a = 0; a < NSA && a <= nwin; ++a) mbar_expect_tx(&S.full_above[a], above_bytes(a));
+    }
   }
-  __syncthreads();
+  // every CTA's barriers exist before any remote st.async lands
+  asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
   // band row l -> grid row; box row of band row l; slot position of step st
   auto grid_row = [&](int l) {
     const int r = band * R + l;
@@ -483,7 +507,9 @@ __global__ void __launch_bounds__(32 * gs::kWarps, 1)
   // grid column of slot position p in window w for band row l
   auto grid_ix = [&](int w, int l, int p) { return FWD ? W * w - SKEW * l + p : nx - W * (w + 1) + SKEW * l + p; };
 
-  if (warp == 1) {  // ---------------- loader (one thread, TMA boxes)
+  if (!real) {
+    // padding CTA of the last cluster: only the cluster barriers
+  } else if (warp == 1) {  // ---------------- loader (one thread, TMA boxes)
     if (lane == 0) {
       const int iy0 = band * R, iyb = ny - 1 - band * R;
       for (int w = 0; w < nwin; ++w) {
@@ -498,11 +524,14 @@ __global__ void __launch_bounds__(32 * gs::kWarps, 1)
         if (ZERO) tma_load_3d(&S.in[s].q[0][0][0], &mapQ, 0, c1, 0, &S.full_in[s]);
       }
     }
-    return;
-  }
-  if (warp == 2 || warp == 3) {  // ---------------- storer (rows 0..R-2) / publisher (row R-1)
+  } else if (warp == 2 || warp == 3) {  // ---------------- storer (rows 0..R-2) / publisher (row R-1)
     const bool pub = warp == 3;
-    const bool publish = pub && rows_here == R && band * R + R < ny;
+    const bool publish = pub && rows_here == R && band * R + R < ny && !dsm_out;
+    uint32_t r_above = 0, r_mbar = 0;  // the next band's above ring / its barriers (cluster addresses)
+    if (pub && dsm_out) {
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r_above) : "r"(smem_u32(&S.above[0][0])), "r"(crank + 1));
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r_mbar) : "r"(smem_u32(&S.full_above[0])), "r"(crank + 1));
+    }
     unsigned long long published = 0;
     for (int w = 0; w < nwin; ++w) {
       const int s = w % NS;
@@ -523,6 +552,28 @@ __global__ void __launch_bounds__(32 * gs::kWarps, 1)
           if (ix >= 0 && ix < nx)
             *reinterpret_cast<double2*>(x + 2 * ((size_t)grid_row(l) * nx + ix)) = S.out[s][l][lane];
         }
+        if (dsm_out) {
+          // hand the row to the next band of the cluster: one st.async per column into
+          // its above ring, completing on that slot's mbarrier (above slot a holds
+          // sweep columns W*(a-1) + SKEW + [0, W)), once the consumer has armed it
+          const int jlo = W * w - SKEW * (R - 1);
+          const int jmax = min(jlo + W - 1, nx - 1);
+          const int amax = jmax < 0 ? -1 : (jmax + W - SKEW) / W;
+          if (lane == 0)
+            while (*reinterpret_cast<volatile int*>(&S.armed) < amax) {
+            }
+          __syncwarp();
+          const int j = jlo + (FWD ? lane : W - 1 - lane);
+          if (lane < W && j >= 0 && j < nx) {
+            const int a = (j + W - SKEW) / W;
+            const int sl = a % NSA;
+            const uint32_t dst = r_above + (uint32_t)((sl * W + (j - SKEW - W * (a - 1))) * 16);
+            const double2 v = S.out[s][l][lane];
+            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(dst),
+                         "d"(v.x), "d"(v.y), "r"(r_mbar + (uint32_t)(sl * 8))
+                         : "memory");
+          }
+        }
         if (publish) {
           __threadfence();
           __syncwarp();
@@ -538,10 +589,8 @@ __global__ void __launch_bounds__(32 * gs::kWarps, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.empty_out[s]);
     }
-    return;
-  }
-  if (warp == 4) {  // ---------------- stager (previous band's last row -> above ring)
-    if (has_above && rows_here > 0) {
+  } else if (warp == 4) {  // ---------------- stager (previous band's last row -> above ring)
+    if (has_above && rows_here > 0 && !dsm_in) {
       const int prev_y = FWD ? grid_row(0) - 1 : grid_row(0) + 1;
       unsigned long long seen = 0;
       // above slot a = w + 1 holds sweep columns W*w + SKEW + [0, W); a = 0 is the preload
@@ -567,10 +616,30 @@ __global__ void __launch_bounds__(32 * gs::kWarps, 1)
       }
       if (lane == 0) flags[band - 1] = 0ull;  // consumed by this band only
     }
-    return;
+  } else {
+    gs_compute<FWD, ZERO>(S, nx, ngrid, band, rows_here, has_above, dsm_in, crank, nwin, x);
   }
+  // no CTA leaves while a cluster peer may still write into its shared memory
+  asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+}
 
-  // ---------------- warp 0: compute
+// warp 0 of k_gs_tri: the wavefront itself
+template <bool FWD, bool ZERO>
+__device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int band, int rows_here, bool has_above,
+                                           bool dsm_in, unsigned crank, int nwin,
+                                           double* __restrict__ x) {
+  using namespace gs;
+  const int lane = threadIdx.x & 31;
+  auto above_bytes = [&](int a) -> unsigned {
+    const int c0 = W * (a - 1) + SKEW;
+    const int lo = max(c0, 0), hi = min(c0 + W, nx);
+    return (unsigned)(hi > lo ? 16 * (hi - lo) : 0);
+  };
+  // the producer's `armed` counter as a cluster address
+  uint32_t r_armed = 0;
+  if (dsm_in) {
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r_armed) : "r"(smem_u32(&S.armed)), "r"(crank - 1));
+  }
   const int l = lane;
   const bool act = l < rows_here;
   static_assert(SKEW == 2, "the step pipeline below assumes a two-column skew");
@@ -588,7 +657,14 @@ __global__ void __launch_bounds__(32 * gs::kWarps, 1)
       for (int c = 0; c < SKEW; ++c) win[1 + c] = S.above[0][W - SKEW + c];
     }
     __syncwarp();
-    if (l == 0) mbar_arrive(&S.empty_above[0]);
+    if (l == 0) {
+      if (dsm_in) {
+        if (NSA <= nwin) mbar_expect_tx(&S.full_above[0], above_bytes(NSA));
+        asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(r_armed), "r"(NSA) : "memory");
+      } else {
+        mbar_arrive(&S.empty_above[0]);
+      }
+    }
   }
 #ifdef VTS_GS_PROBE
   long long t_first = 0, t_wait_above = 0;
@@ -696,7 +772,13 @@ __global__ void __launch_bounds__(32 * gs::kWarps, 1)
     if (l == 0) {
       mbar_arrive(&S.empty_in[s]);
       mbar_arrive(&S.full_out[s]);
-      if (has_above) mbar_arrive(&S.empty_above[sa]);
+      if (dsm_in) {
+        const int an = w + 1 + NSA;  // re-arm this slot for its next chunk and tell the producer
+        if (an <= nwin) mbar_expect_tx(&S.full_above[sa], above_bytes(an));
+        asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(r_armed), "r"(an) : "memory");
+      } else if (has_above) {
+        mbar_arrive(&S.empty_above[sa]);
+      }
     }
   }
 #ifdef VTS_GS_PROBE
@@ -846,6 +928,9 @@ static int gs_prepare() {
   VTS_CUDA(cudaFuncSetAttribute(k_gs_tri<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   VTS_CUDA(cudaFuncSetAttribute(k_gs_tri<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   VTS_CUDA(cudaFuncSetAttribute(k_gs_tri<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  VTS_CUDA(cudaFuncSetAttribute(k_gs_tri<true, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  VTS_CUDA(cudaFuncSetAttribute(k_gs_tri<true, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  VTS_CUDA(cudaFuncSetAttribute(k_gs_tri<false, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaDriverEntryPointQueryResult q;
   VTS_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&g_encode), cudaEnableDefault, &q));
   if (q != cudaDriverEntryPointSuccess || !g_encode) {
@@ -876,36 +961,54 @@ static int encode_skewed(CUtensorMap* map, const double* data, int width, const 
   return 0;
 }
 
+// launch the wavefront on `bands` row bands, grouped in clusters of <= 16 CTAs
+template <bool FWD, bool ZERO>
+static int launch_tri(Ctx* c, LevelBuf& L, const CUtensorMap& mS, const CUtensorMap& mP, const CUtensorMap& mQ,
+                      double* x, const int* skip) {
+  const int bands = div_up(L.d.ny, gs::R);
+  const int ncl = div_up(bands, 16);
+  const int cs = div_up(bands, ncl);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cs * ncl);
+  cfg.blockDim = dim3(32 * gs::kWarps);
+  cfg.dynamicSmemBytes = sizeof(gs::Smem);
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  VTS_CUDA(cudaLaunchKernelEx(&cfg, k_gs_tri<FWD, ZERO>, L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, bands, mS, mP,
+                              mQ, x, L.gs_flags, skip));
+  VTS_LAUNCHED(c);
+  return 0;
+}
+
 // one Gauss-Seidel sweep on level k: x <- sweep(x; b) (zero_guess: x_old = 0)
 static int gs_sweep(Ctx* c, int k, const double* b, double* x, bool forward, bool zero_guess, const int* skip) {
   if (int rc = gs_prepare()) return rc;
   LevelBuf& L = c->lv[k];
-  const int bands = div_up(L.d.ny, gs::R);
-  const size_t smem = sizeof(gs::Smem);
   double* P = L.r;
   CUtensorMap mS, mP, mQ;
   if (forward && zero_guess) {
     if (encode_skewed(&mS, L.d.stL, kHalf, L) || encode_skewed(&mP, b, 2, L) || encode_skewed(&mQ, L.d.border, 2, L))
       return 5;
-    k_gs_tri<true, true><<<bands, 32 * gs::kWarps, smem, c->stream>>>(L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, mS,
-                                                                      mP, mQ, x, L.gs_flags, skip);
-  } else if (forward) {
+    return launch_tri<true, true>(c, L, mS, mP, mQ, x, skip);
+  }
+  if (forward) {
     k_gs_old<true><<<div_up(L.d.nnodes, 256), 256, 0, c->stream>>>(L.d.nx, L.d.ny, L.d.ngrid, L.d.stU, b,
                                                                     L.d.border, x, P, skip);
     VTS_LAUNCHED(c);
     if (encode_skewed(&mS, L.d.stL, kHalf, L) || encode_skewed(&mP, P, 2, L)) return 5;
-    k_gs_tri<true, false><<<bands, 32 * gs::kWarps, smem, c->stream>>>(L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, mS,
-                                                                       mP, mP, x, L.gs_flags, skip);
-  } else {
-    k_gs_old<false><<<div_up(L.d.nnodes, 256), 256, 0, c->stream>>>(L.d.nx, L.d.ny, L.d.ngrid, L.d.stL, b,
-                                                                     L.d.border, x, P, skip);
-    VTS_LAUNCHED(c);
-    if (encode_skewed(&mS, L.d.stU, kHalf, L) || encode_skewed(&mP, P, 2, L)) return 5;
-    k_gs_tri<false, false><<<bands, 32 * gs::kWarps, smem, c->stream>>>(L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes,
-                                                                        mS, mP, mP, x, L.gs_flags, skip);
+    return launch_tri<true, false>(c, L, mS, mP, mP, x, skip);
   }
+  k_gs_old<false><<<div_up(L.d.nnodes, 256), 256, 0, c->stream>>>(L.d.nx, L.d.ny, L.d.ngrid, L.d.stL, b,
+                                                                   L.d.border, x, P, skip);
   VTS_LAUNCHED(c);
-  return 0;
+  if (encode_skewed(&mS, L.d.stU, kHalf, L) || encode_skewed(&mP, P, 2, L)) return 5;
+  return launch_tri<false, false>(c, L, mS, mP, mP, x, skip);
 }
 
 int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
