@@ -65,7 +65,30 @@ def algorithmic_bytes(prob) -> dict:
     A_MR = A_ap + A_V + 160 * (n + 1)
     # one forward GS sweep on the finest level: operator (matrix-free credit) + b, x, x', border
     A_gs = (8 * (n + 2 * m) + 32 * n)
-    return dict(phi=A_phi, apply=A_ap, vcycle=A_V, minres_iter=A_MR, gs_fine_sweep=A_gs)
+    # one finest-level wavefront launch (k_gs_tri): per grid node the 20-double
+    # half-stencil it solves with, the 2-double right-hand side P, the 2-double result
+    fine = lv[-1]
+    A_tri = fine.nx * fine.ny * 8 * (20 + 2 + 2)
+    return dict(phi=A_phi, apply=A_ap, vcycle=A_V, minres_iter=A_MR, gs_fine_sweep=A_gs, gs_tri_fine=A_tri)
+
+
+def ncu_traffic():
+    """dram bytes per finest-level k_gs_tri launch from the committed ncu --set full capture."""
+    import csv
+
+    path = os.path.join(REPO, "profiles", "r01_ncu_full_k_gs_tri_fine_raw_subset.csv")
+    try:
+        with open(path) as fh:
+            rows = list(csv.reader(fh))
+        head, units, vals = rows[0], rows[1], rows[2]
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        tot = 0.0
+        for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = head.index(key)
+            tot += float(vals[i].replace(",", "")) * scale[units[i]]
+        return tot
+    except (OSError, ValueError, KeyError, IndexError):
+        return None
 
 
 class ClockSampler:
@@ -114,6 +137,21 @@ class ClockSampler:
 
 def dist_env():
     return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def aggregate_over_ranks(elapsed, units, world: int, device: str):
+    """Replicas-only multi-GPU (DESIGN.md): every rank solves its own system;
+    the job's time is the max over ranks and its work the sum over ranks."""
+    if world <= 1:
+        return float(elapsed), float(units)
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([float(elapsed)], dtype=torch.float64, device=device)
+    u = torch.tensor([float(units)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(u, op=dist.ReduceOp.SUM)
+    return float(t.item()), float(u.item())
 
 
 def run_reference(args) -> None:
@@ -256,17 +294,21 @@ def main() -> None:
         t1.record(stream)
         torch.cuda.synchronize()
     launches = ops.kernel_launches - launches0
-    dt_ms = t0.elapsed_time(t1)
-    if world > 1:
-        tt = torch.tensor([dt_ms], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        dt_ms = float(tt.item())
-        itt = torch.tensor([its], device="cuda", dtype=torch.float64)
-        dist.all_reduce(itt)
-        total_its = float(itt.item())
-    else:
-        total_its = float(its)
+    dt_ms, total_its = aggregate_over_ranks(t0.elapsed_time(t1), its, world, "cuda")
     value = total_its / (dt_ms * 1e-3)
+
+    # --- profiling pass (not the timed value): the same K iterations with every
+    # wavefront launch bracketed by CUDA events on the context stream, giving the
+    # dominant kernel's average launch time and its share of the step
+    prof = (ctypes.c_double * 4)()
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    _lib.check(lib.vts_profile_begin(ops.handle), "vts_profile_begin")
+    p0.record(stream)
+    minres_dev(args.steps)
+    p1.record(stream)
+    _lib.check(lib.vts_profile_end(ops.handle, prof), "vts_profile_end")
+    prof_region_ms = p0.elapsed_time(p1)
+    tri_total_ms, tri_n, tri_fine_ms, tri_fine_n = list(prof)
 
     # --- e2e through the C-ABI with host buffers (pinned), copies inside the timed region
     rhs_host = torch.as_tensor(rhs_h).pin_memory()
@@ -281,12 +323,8 @@ def main() -> None:
     x_host.copy_(x, non_blocking=True)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - w0
-    e2e_its = itv.value
-    if world > 1:
-        tt = torch.tensor([e2e_s], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_s = float(tt.item())
-    e2e_value = e2e_its * world / e2e_s
+    e2e_s, e2e_its = aggregate_over_ranks(e2e_s, itv.value, world, "cuda")
+    e2e_value = e2e_its / e2e_s
 
     bytes_ = algorithmic_bytes(prob)
     peaks_path = os.path.join(REPO, "MEASURED_PEAKS.json")
@@ -300,9 +338,11 @@ def main() -> None:
     def gbs(nbytes, ms):
         return nbytes / (ms * 1e-3) / 1e9
 
-    # dominant kernel of the MINRES iteration: the V-cycle, itself dominated by the
-    # finest-level Gauss-Seidel sweeps; report the V-cycle as the roofline unit
-    achieved = gbs(bytes_["vcycle"], vcycle_ms)
+    # dominant kernel of the MINRES iteration: the wavefront Gauss-Seidel kernel
+    # k_gs_tri (~75 % of the step); roofline unit = one finest-level launch
+    tri_fine_avg_ms = tri_fine_ms / max(tri_fine_n, 1.0)
+    achieved = gbs(bytes_["gs_tri_fine"], tri_fine_avg_ms)
+    traffic = ncu_traffic()
     pbm = None
     if not args.no_pbm and rank == 0:
         t_p = time.perf_counter()
@@ -330,10 +370,14 @@ def main() -> None:
                 "d2h_bytes_per_step": 8 * (n + 1) / args.steps,
                 "note": "one C-ABI vts_minres call of K iterations; RHS H2D and solution D2H once per call"},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "hbm", "kernel": "V-cycle (9 levels; finest-level GS sweeps dominate)",
+        "roofline": {"bound": "hbm", "kernel": "k_gs_tri, finest level (1025x513 wavefront sweep)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "frac_of_8TBs": achieved / 8000.0, "traffic": None, "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": bytes_["vcycle"], "launch_ms": vcycle_ms},
+                     "frac_of_8TBs": achieved / 8000.0, "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": bytes_["gs_tri_fine"], "launch_ms": tri_fine_avg_ms,
+                     "launches_in_profiled_region": int(tri_n), "finest_launches": int(tri_fine_n),
+                     "share_of_step": tri_total_ms / prof_region_ms,
+                     "note": "latency-bound: a sweep is a wavefront of nx + 2 ny dependent steps "
+                             "(DESIGN.md, 'Gauss-Seidel depth'); traffic from profiles/ ncu --set full"},
         "kernels": {
             "phi_pass_ms": phi_ms, "phi_pass_GBs": gbs(bytes_["phi"], phi_ms),
             "apply_ms": apply_ms, "apply_GBs": gbs(bytes_["apply"], apply_ms), "applies_per_s": 1e3 / apply_ms,

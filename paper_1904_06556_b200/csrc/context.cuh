@@ -73,6 +73,15 @@ struct Ctx {
 
   long long launches = 0;
   std::vector<void*> allocs;  // padded device arrays owned by the context
+
+  // optional per-launch timing of the wavefront kernel (vts_profile_begin/end)
+  bool prof = false;
+  struct ProfEv {
+    cudaEvent_t a, b;
+    int level;
+  };
+  std::vector<ProfEv> prof_ev;
+  size_t prof_used = 0;  // padded device arrays owned by the context
 };
 
 constexpr int kMaxBlocks = 8192;
@@ -141,6 +150,8 @@ int level_residual_grid(Ctx* c, int k, const double* x, const double* b, double*
 // ---- multigrid (mg.cu) ----
 int mg_setup(Ctx* c, double shift_scale);
 int vcycle_grid(Ctx* c, const double* b, double* z, const int* skip);
+int profile_begin(Ctx* c);
+int profile_end(Ctx* c, double* out);
 
 // ---- MINRES (minres.cu) ----
 int minres(Ctx* c, const double* b_free, double* x_free, double tol, int max_iters,

@@ -980,9 +980,22 @@ static int launch_tri(Ctx* c, LevelBuf& L, const CUtensorMap& mS, const CUtensor
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  Ctx::ProfEv* pe = nullptr;
+  if (c->prof) {
+    if (c->prof_used == c->prof_ev.size()) {
+      Ctx::ProfEv e{};
+      VTS_CUDA(cudaEventCreate(&e.a));
+      VTS_CUDA(cudaEventCreate(&e.b));
+      c->prof_ev.push_back(e);
+    }
+    pe = &c->prof_ev[c->prof_used++];
+    pe->level = (int)(&L - c->lv.data());
+    VTS_CUDA(cudaEventRecord(pe->a, c->stream));
+  }
   VTS_CUDA(cudaLaunchKernelEx(&cfg, k_gs_tri<FWD, ZERO>, L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, bands, mS, mP,
                               mQ, x, L.gs_flags, skip));
   VTS_LAUNCHED(c);
+  if (pe) VTS_CUDA(cudaEventRecord(pe->b, c->stream));
   return 0;
 }
 
@@ -1125,6 +1138,36 @@ int mg_setup(Ctx* c, double shift_scale) {
 // ms[1] one V-cycle, ms[2] one forward GS sweep (old-value pass + wavefront)
 // on the finest level, ms[3] the same on the second-finest level, ms[4]
 // finest residual, ms[5] mg_setup (stencil + Galerkin chain + coarse factor).
+// per-launch timing of k_gs_tri between profile_begin and profile_end:
+// out = {total ms, launches, finest-level ms, finest-level launches}
+int profile_begin(Ctx* c) {
+  c->prof = true;
+  c->prof_used = 0;
+  return 0;
+}
+
+int profile_end(Ctx* c, double* out) {
+  c->prof = false;
+  VTS_CUDA(cudaStreamSynchronize(c->stream));
+  double tot = 0.0, fine = 0.0;
+  long long nf = 0;
+  for (size_t i = 0; i < c->prof_used; ++i) {
+    float t = 0.f;
+    VTS_CUDA(cudaEventElapsedTime(&t, c->prof_ev[i].a, c->prof_ev[i].b));
+    tot += t;
+    if (c->prof_ev[i].level == c->L - 1) {
+      fine += t;
+      ++nf;
+    }
+  }
+  out[0] = tot;
+  out[1] = (double)c->prof_used;
+  out[2] = fine;
+  out[3] = (double)nf;
+  c->prof_used = 0;
+  return 0;
+}
+
 int time_kernels(Ctx* c, int reps, double* ms) {
   if (!c->mg_ready) {
     set_error(4, "time_kernels: multigrid not set up");

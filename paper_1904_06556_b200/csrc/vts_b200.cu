@@ -75,6 +75,10 @@ static void free_ctx(Ctx* c) {
     cudaFree(L.gs_flags);
   }
   for (void* p : c->allocs) cudaFree(p);
+  for (auto& e : c->prof_ev) {
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
   cudaFree(c->u_grid);
   cudaFree(c->rho_hat);
   cudaFree(c->chat);
@@ -409,5 +413,19 @@ int vts_time_kernels(vts_ctx* ctx, int32_t reps, double* ms) {
 }
 
 int64_t vts_kernel_launches(const vts_ctx* ctx) { return ctx ? C(ctx)->launches : 0; }
+
+int vts_profile_begin(vts_ctx* ctx) {
+  VTS_REQUIRE_CTX(ctx);
+  return vts::profile_begin(C(ctx));
+}
+
+int vts_profile_end(vts_ctx* ctx, double* out) {
+  VTS_REQUIRE_CTX(ctx);
+  if (!out) {
+    vts::set_error(4, "vts_profile_end: out is NULL");
+    return 4;
+  }
+  return vts::profile_end(C(ctx), out);
+}
 
 }  // extern "C"
