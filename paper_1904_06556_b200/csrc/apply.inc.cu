@@ -4,13 +4,14 @@
 //   S = [[sum_e rho_hat_e K_e + sum_e chat_e w_e w_e^T, -sum_e chat_e w_e],
 //        [.^T, sum_e chat_e]],  w_e = K_e u_e
 // i.e. BorderedMatrix.matvec (linalg.py:56-62) of ElementOps.assemble
-// (fem.py:188-209) without ever forming the CSR matrix.  One CTA owns a
-// 32 x 8 tile of nodes: it stages x and u of the (34 x 10)-node halo in shared
-// memory, computes the 33 x 9 touching elements once each (w_e, theta_e =
-// w_e.x_e - x_alpha, K_e x_e, the 8-vector rho_hat K_e x_e + chat theta w_e),
-// then every thread gathers its node's four element contributions in the
-// reference's scatter order.  No atomics; y_alpha = -sum chat_e theta_e is a
-// deterministic last-block reduction over the elements each tile owns.
+// (fem.py:188-209) without ever forming the CSR matrix.  One CTA (32 x 8
+// threads) owns a 31 x 7 tile of nodes: it stages x and u of the (33 x 9)-node
+// halo in shared memory, computes the 32 x 8 touching elements, one per thread
+// (w_e, theta_e = w_e.x_e - x_alpha, K_e x_e, the 8-vector
+// rho_hat K_e x_e + chat theta w_e), then every owning thread gathers its
+// node's four element contributions in the reference's scatter order.  No
+// atomics; y_alpha = -sum chat_e theta_e is a deterministic last-block
+// reduction over the elements each tile owns.
 //
 // k_level_apply: y = A_k x + border x_alpha, y_alpha = border.x + corner x_alpha
 // on a stored 9-point block stencil (the residual of multigrid.py:125 and the
@@ -18,126 +19,170 @@
 
 namespace vts {
 
-constexpr int kTX = 32, kTY = 8;
-constexpr int kHX = kTX + 2, kHY = kTY + 2;  // halo nodes
-constexpr int kEX = kTX + 1, kEY = kTY + 1;  // touching elements
+constexpr int kBX = 32, kBY = 8;            // threads = touching elements
+constexpr int kTX = kBX - 1, kTY = kBY - 1;  // owned nodes
+constexpr int kHX = kTX + 2, kHY = kTY + 2;  // halo nodes (33 x 9)
+constexpr int kEX = kBX, kEY = kBY;
+constexpr int kES = kEX * kEY;               // elements per tile
 
-__global__ void __launch_bounds__(kTX* kTY) k_newton_apply(int nx, int ny, int ex, int ey, int ngrid,
-                                                         const double* __restrict__ ug,
-                                                         const double* __restrict__ rho_hat,
-                                                         const double* __restrict__ chat,
-                                                         const uint8_t* __restrict__ fmask,
-                                                         const double* __restrict__ x,
-                                                         double* __restrict__ y, double* partials,
-                                                         unsigned* counter, const int* skip) {
-  if (skip && *skip) return;
-  __shared__ double2 xs[kHY * kHX];
-  __shared__ double2 us[kHY * kHX];
-  __shared__ double contrib[kEY * kEX * 8];
-  __shared__ double scratch[kTX * kTY / 32];
-  const int tid = threadIdx.x;
-  const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * kTY;
-  const double xa = x[ngrid];
+// TMA boxes of the tile's halo nodes (x, u).  The element arrays are read
+// directly: a 2-D box starting at element column x0 - 1 has an inner start
+// offset that is not 16-B aligned, which TMA rejects for negative starts.
+struct __align__(128) ApplyStage {
+  double2 xs[kHY * kHX];
+  double pad0[(128 - (kHY * kHX * 16) % 128) / 8];
+  double2 us[kHY * kHX];
+};
+struct ApplySmem {
+  ApplyStage st[2];
+  double contrib[8 * kES];  // structure of arrays: conflict-free
+  unsigned long long full[2];
+  double scratch[kES / 32];
+};
+static_assert(offsetof(ApplyStage, us) % 128 == 0, "TMA alignment");
+constexpr unsigned kApplyTxBytes = 2 * kHY * kHX * 16;
 
-  for (int h = tid; h < kHY * kHX; h += blockDim.x) {
-    const int gx = x0 - 1 + h % kHX, gy = y0 - 1 + h / kHX;
-    double2 xv = make_double2(0.0, 0.0), uv = make_double2(0.0, 0.0);
-    if (gx >= 0 && gx < nx && gy >= 0 && gy < ny) {
-      const int nd = gx + nx * gy;
-      xv = *reinterpret_cast<const double2*>(x + 2 * nd);
-      uv = *reinterpret_cast<const double2*>(ug + 2 * nd);
-    }
-    xs[h] = xv;
-    us[h] = uv;
-  }
-  __syncthreads();
-
-  double acc[1] = {0.0};
-  for (int le = tid; le < kEY * kEX; le += blockDim.x) {
-    const int lx = le % kEX, ly = le / kEX;
-    const int gx = x0 - 1 + lx, gy = y0 - 1 + ly;
-    if (gx < 0 || gx >= ex || gy < 0 || gy >= ey) continue;
-    const int e = gx + ex * gy;
-    const int h0 = lx + kHX * ly;
-    const int hn[4] = {h0, h0 + 1, h0 + kHX + 1, h0 + kHX};
-    double ue[8], xe[8];
+// Element phase of one tile (thread = element): contrib = rho_hat K_e x_e +
+// chat theta w_e with w_e = K_e u_e, theta = w_e.x_e - x_alpha; returns theta.
+// `ke` is c_ke offset by an opaque zero produced inside the tile loop: NVVM
+// would otherwise hoist the 64 loop-invariant K_e loads into registers (and
+// spill); ptxas still folds them into constant-bank operands.
+VTS_DEVICE_INLINE double apply_element(const ApplyStage& G, double* contrib, int tid, int h0, double xa, double rh,
+                                       double ch, const double* __restrict__ ke) {
+  const int hn[4] = {h0, h0 + 1, h0 + kHX + 1, h0 + kHX};
+  double w[8], kx[8], xe[8];
+  {
+    double ue[8];
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
-      const double2 uv = us[hn[a]], xv = xs[hn[a]];
+      const double2 uv = G.us[hn[a]];
       ue[2 * a] = uv.x;
       ue[2 * a + 1] = uv.y;
-      xe[2 * a] = xv.x;
-      xe[2 * a + 1] = xv.y;
     }
-    double w[8], kx[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      double sw = ue[0] * c_ke[j], sk = xe[0] * c_ke[j];
+      double sw = ue[0] * ke[j];
 #pragma unroll
-      for (int i = 1; i < 8; ++i) {
-        sw = fma(ue[i], c_ke[i * 8 + j], sw);
-        sk = fma(xe[i], c_ke[i * 8 + j], sk);
-      }
+      for (int i = 1; i < 8; ++i) sw = fma(ue[i], ke[i * 8 + j], sw);
       w[j] = sw;
-      kx[j] = sk;
     }
-    double wx = w[0] * xe[0];
-#pragma unroll
-    for (int i = 1; i < 8; ++i) wx = fma(w[i], xe[i], wx);
-    const double ch = chat[e], rh = rho_hat[e];
-    const double theta = wx - xa;
-    const double ct = ch * theta;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) contrib[le * 8 + j] = fma(ct, w[j], rh * kx[j]);
-    if (gx >= x0 && gx < x0 + kTX && gy >= y0 && gy < y0 + kTY) acc[0] = fma(ch, theta, acc[0]);
   }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const double2 xv = G.xs[hn[a]];
+    xe[2 * a] = xv.x;
+    xe[2 * a + 1] = xv.y;
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    double sk = xe[0] * ke[j];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) sk = fma(xe[i], ke[i * 8 + j], sk);
+    kx[j] = sk;
+  }
+  double wx = w[0] * xe[0];
+#pragma unroll
+  for (int i = 1; i < 8; ++i) wx = fma(w[i], xe[i], wx);
+  const double theta = wx - xa;
+  const double ct = ch * theta;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) contrib[j * kES + tid] = fma(ct, w[j], rh * kx[j]);
+  return theta;
+}
+
+// Persistent: CTA b takes tiles b, b + grid, ...; the halo boxes (TMA, OOB
+// zero fill) and element coefficients of the next tile are in flight while
+// the current tile computes (2 stages).
+__global__ void __launch_bounds__(kBX* kBY, 3) k_newton_apply(const __grid_constant__ CUtensorMap mapX,
+                                                             const __grid_constant__ CUtensorMap mapU,
+                                                             const double* __restrict__ rho_hat,
+                                                             const double* __restrict__ chat, int nx, int ny,
+                                                             int ex, int ey, int ngrid, int tiles_x, int ntiles,
+                                                             const uint8_t* __restrict__ fmask,
+                                                             const double* __restrict__ x, double* __restrict__ y,
+                                                             double* partials, unsigned* counter, const int* skip) {
+  if (skip && *skip) return;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  ApplySmem& S = *reinterpret_cast<ApplySmem*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int lx = tid % kEX, ly = tid / kEX;
+  const int h0 = lx + kHX * ly;
+  auto issue = [&](int t, int s) {
+    const int x0 = (t % tiles_x) * kTX, y0 = (t / tiles_x) * kTY;
+    mbar_expect_tx(&S.full[s], kApplyTxBytes);
+    tma_load_3d(S.st[s].xs, &mapX, 0, x0 - 1, y0 - 1, &S.full[s]);
+    tma_load_3d(S.st[s].us, &mapU, 0, x0 - 1, y0 - 1, &S.full[s]);
+  };
+  auto coeffs = [&](int t, double& rh, double& ch) {
+    const int gx = (t % tiles_x) * kTX - 1 + lx, gy = (t / tiles_x) * kTY - 1 + ly;
+    rh = 0.0;
+    ch = 0.0;
+    if (t < ntiles && gx >= 0 && gx < ex && gy >= 0 && gy < ey) {
+      rh = rho_hat[gx + ex * gy];
+      ch = chat[gx + ex * gy];
+    }
+  };
+  if (tid == 0) {
+    mbar_init(&S.full[0], 1);
+    mbar_init(&S.full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if ((int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    if ((int)blockIdx.x + (int)gridDim.x < ntiles) issue(blockIdx.x + gridDim.x, 1);
+  }
+  const double xa = x[ngrid];
+  double rh, ch;
+  coeffs(blockIdx.x, rh, ch);
   __syncthreads();
 
-  const int tx = tid % kTX, ty = tid / kTX;
-  const int ix = x0 + tx, iy = y0 + ty;
-  if (ix < nx && iy < ny) {
-    // elements (ix-1,iy-1) c2, (ix,iy-1) c3, (ix-1,iy) c1, (ix,iy) c0  -> local (tx,ty) (tx+1,ty) (tx,ty+1) (tx+1,ty+1)
-    double s0 = 0.0, s1 = 0.0;
-    if (ix >= 1 && iy >= 1) {
-      const double* cb = contrib + (tx + kEX * ty) * 8;
-      s0 += cb[4]; s1 += cb[5];
+  double acc = 0.0;
+  int k = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+    const int s = k & 1;
+    const int x0 = (t % tiles_x) * kTX, y0 = (t / tiles_x) * kTY;
+    double rh_n, ch_n;
+    coeffs(t + gridDim.x, rh_n, ch_n);  // next tile's coefficients, in flight during this one
+    mbar_wait(&S.full[s], (k >> 1) & 1);
+    int z;
+    asm volatile("mov.u32 %0, 0;" : "=r"(z));
+    double* contrib = S.contrib;
+    const double theta = apply_element(S.st[s], contrib, tid, h0, xa, rh, ch, c_ke + z);
+    // y_alpha sums the elements this tile owns (ch = 0 outside the mesh)
+    {
+      const int gx = x0 - 1 + lx, gy = y0 - 1 + ly;
+      if (gx >= x0 && gx < x0 + kTX && gy >= y0 && gy < y0 + kTY) acc = fma(ch, theta, acc);
     }
-    if (ix < ex && iy >= 1) {
-      const double* cb = contrib + (tx + 1 + kEX * ty) * 8;
-      s0 += cb[6]; s1 += cb[7];
+    rh = rh_n;
+    ch = ch_n;
+    __syncthreads();  // stage s consumed, contrib complete
+    if (tid == 0 && t + 2 * (int)gridDim.x < ntiles) issue(t + 2 * gridDim.x, s);
+    const int ix = x0 + lx, iy = y0 + ly;
+    if (lx < kTX && ly < kTY && ix < nx && iy < ny) {
+      // elements (ix-1,iy-1) c2, (ix,iy-1) c3, (ix-1,iy) c1, (ix,iy) c0: the reference's scatter order
+      double s0 = 0.0, s1 = 0.0;
+      if (ix >= 1 && iy >= 1) {
+        const double* cb = contrib + (lx + kEX * ly);
+        s0 += cb[4 * kES]; s1 += cb[5 * kES];
+      }
+      if (ix < ex && iy >= 1) {
+        const double* cb = contrib + (lx + 1 + kEX * ly);
+        s0 += cb[6 * kES]; s1 += cb[7 * kES];
+      }
+      if (ix >= 1 && iy < ey) {
+        const double* cb = contrib + (lx + kEX * (ly + 1));
+        s0 += cb[2 * kES]; s1 += cb[3 * kES];
+      }
+      if (ix < ex && iy < ey) {
+        const double* cb = contrib + (lx + 1 + kEX * (ly + 1));
+        s0 += cb[0]; s1 += cb[kES];
+      }
+      const int nd = ix + nx * iy;
+      const uchar2 fm = *reinterpret_cast<const uchar2*>(fmask + 2 * nd);
+      *reinterpret_cast<double2*>(y + 2 * nd) = make_double2(fm.x ? s0 : 0.0, fm.y ? s1 : 0.0);
     }
-    if (ix >= 1 && iy < ey) {
-      const double* cb = contrib + (tx + kEX * (ty + 1)) * 8;
-      s0 += cb[2]; s1 += cb[3];
-    }
-    if (ix < ex && iy < ey) {
-      const double* cb = contrib + (tx + 1 + kEX * (ty + 1)) * 8;
-      s0 += cb[0]; s1 += cb[1];
-    }
-    const int nd = ix + nx * iy;
-    const uchar2 fm = *reinterpret_cast<const uchar2*>(fmask + 2 * nd);
-    *reinterpret_cast<double2*>(y + 2 * nd) = make_double2(fm.x ? s0 : 0.0, fm.y ? s1 : 0.0);
+    __syncthreads();  // contrib reused by the next tile
   }
-  double tot[1];
-  // flatten the 2D grid for the last-block protocol
-  __shared__ bool s_last;
-  block_sum<1>(acc, scratch);
-  const int bid = blockIdx.x + gridDim.x * blockIdx.y, nb = gridDim.x * gridDim.y;
-  if (tid == 0) {
-    partials[bid] = acc[0];
-    __threadfence();
-    s_last = (atomicAdd(counter, 1u) == (unsigned)nb - 1);
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  tot[0] = 0.0;
-  for (int b = tid; b < nb; b += blockDim.x) tot[0] += __ldcg(partials + b);
-  block_sum<1>(tot, scratch);
-  if (tid == 0) {
-    y[ngrid] = -tot[0];
-    *counter = 0u;
-  }
+  double a1[1] = {acc}, tot[1];
+  if (last_block_reduce<1>(a1, S.scratch, partials, counter, tot) && tid == 0) y[ngrid] = -tot[0];
 }
 
 // y = A_k x (+ border x_alpha) on a block stencil; with `b` given, computes
@@ -201,16 +246,34 @@ __global__ void __launch_bounds__(256) k_level_apply(int nx, int ny, int ngrid, 
   }
 }
 
+static bool g_apply_attr_set = false;
+
 int newton_apply_grid(Ctx* c, const double* x, double* y, const int* skip) {
   const LevelBuf& F = c->lv[c->L - 1];
-  dim3 grid(div_up(F.d.nx, kTX), div_up(F.d.ny, kTY));
-  if ((long long)grid.x * grid.y > kMaxBlocks * kMaxPartials) {
-    set_error(4, "mesh too large for the apply partial buffer");
+  if (!g_apply_attr_set) {
+    VTS_CUDA(cudaFuncSetAttribute(k_newton_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ApplySmem)));
+    g_apply_attr_set = true;
+  }
+  const int tiles_x = div_up(F.d.nx, kTX), tiles_y = div_up(F.d.ny, kTY);
+  const int ntiles = tiles_x * tiles_y;
+  int dev = 0, sms = 148, per_sm = 2;
+  VTS_CUDA(cudaGetDevice(&dev));
+  VTS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  VTS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_newton_apply, kBX * kBY, sizeof(ApplySmem)));
+  const int grid = std::max(1, std::min(ntiles, sms * std::max(per_sm, 1)));
+  if (grid > kMaxBlocks * 8) {
+    set_error(4, "apply grid exceeds the partial buffer");
     return 4;
   }
-  k_newton_apply<<<grid, kTX * kTY, 0, c->stream>>>(F.d.nx, F.d.ny, F.d.ex, F.d.ey, F.d.ngrid, c->u_grid,
-                                                     c->rho_hat, c->chat, F.d.free_mask, x, y,
-                                                     c->partials + kMaxBlocks * 8, c->counters + 4, skip);
+  CUtensorMap mX, mU;
+  const cuuint64_t nd3[3] = {2, (cuuint64_t)F.d.nx, (cuuint64_t)F.d.ny};
+  const cuuint64_t ns3[2] = {16, (cuuint64_t)F.d.nx * 16};
+  const cuuint32_t nb3[3] = {2, kHX, kHY};
+  if (int rc = encode_tiled(&mX, x, 3, nd3, ns3, nb3)) return rc;
+  if (int rc = encode_tiled(&mU, c->u_grid, 3, nd3, ns3, nb3)) return rc;
+  k_newton_apply<<<grid, kBX * kBY, sizeof(ApplySmem), c->stream>>>(
+      mX, mU, c->rho_hat, c->chat, F.d.nx, F.d.ny, F.d.ex, F.d.ey, F.d.ngrid, tiles_x, ntiles, F.d.free_mask, x, y,
+      c->partials + kMaxBlocks * 8, c->counters + 4, skip);
   VTS_LAUNCHED(c);
   return 0;
 }

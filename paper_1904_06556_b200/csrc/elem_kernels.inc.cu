@@ -189,7 +189,7 @@ struct PhiElemArgs {
   double *q, *rho_hat, *mu_hat_lo, *mu_hat_up, *a, *b_lo, *b_up, *res_lo, *res_up, *w_out;
 };
 
-__global__ void __launch_bounds__(kThreads) k_phi_elem(PhiElemArgs A, double* partials, unsigned* flags) {
+__global__ void __launch_bounds__(kThreads, 2) k_phi_elem(PhiElemArgs A, double* partials, unsigned* flags) {
   __shared__ double scratch[7 * kThreads / 32];
   double acc[7] = {0, 0, 0, 0, 0, 0, 0};
   unsigned sat = 0;

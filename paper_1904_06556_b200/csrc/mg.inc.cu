@@ -295,41 +295,6 @@ __global__ void k_prolong_add(int fnx, int fny, const uint8_t* __restrict__ ffm,
 // ---------------------------------------------------------------------------
 // exact-order Gauss-Seidel sweep, v2: old-value pass + staged wavefront solve
 // ---------------------------------------------------------------------------
-VTS_DEVICE_INLINE unsigned long long ld_acquire(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-VTS_DEVICE_INLINE void st_release(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-VTS_DEVICE_INLINE uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
-VTS_DEVICE_INLINE void mbar_init(unsigned long long* m, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
-}
-VTS_DEVICE_INLINE void mbar_expect_tx(unsigned long long* m, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
-}
-VTS_DEVICE_INLINE bool mbar_try_wait(unsigned long long* m, unsigned parity) {
-  unsigned ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(smem_u32(m)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-VTS_DEVICE_INLINE void mbar_wait(unsigned long long* m, unsigned parity) {
-  while (!mbar_try_wait(m, parity)) {
-  }
-}
-// bulk global -> shared copy (TMA engine), completion counted on mbarrier m
-VTS_DEVICE_INLINE void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* m) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(m))
-               : "memory");
-}
 
 // Old-value pass of one sweep: P = b - border x_alpha - U x_old (forward) or
 // - L x_old (backward).  Sums follow the CSR column order of multigrid.py:41-47.
@@ -416,18 +381,6 @@ struct Smem {
 static_assert(sizeof(InSlot) % 128 == 0, "TMA destinations must stay 128-B aligned");
 static_assert(((W * kHalf * 8) / 16) % 2 == 1, "lane stride must be an odd multiple of 16 B");
 }  // namespace gs
-
-VTS_DEVICE_INLINE void mbar_arrive(unsigned long long* m) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(m)) : "memory");
-}
-// 3-D TMA tile load (box of the tensor map at {c0, c1, c2}) with mbarrier completion
-VTS_DEVICE_INLINE void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, unsigned long long* m) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-      "[%5];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(m))
-      : "memory");
-}
 
 // Wavefront lower-triangular solve (D_L + L) x = P in sweep order (forward:
 // lexicographic; backward: reversed, where the U half plays the role of L).
@@ -920,7 +873,6 @@ __global__ void __launch_bounds__(1024) k_coarse_solve(int N, int nfree, int ngr
 // host drivers
 // ---------------------------------------------------------------------------
 static bool g_gs_attr_set = false;
-static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
 static int gs_prepare() {
   if (g_gs_attr_set) return 0;
@@ -931,12 +883,7 @@ static int gs_prepare() {
   VTS_CUDA(cudaFuncSetAttribute(k_gs_tri<true, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   VTS_CUDA(cudaFuncSetAttribute(k_gs_tri<true, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   VTS_CUDA(cudaFuncSetAttribute(k_gs_tri<false, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  cudaDriverEntryPointQueryResult q;
-  VTS_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&g_encode), cudaEnableDefault, &q));
-  if (q != cudaDriverEntryPointSuccess || !g_encode) {
-    set_error(5, "cuTensorMapEncodeTiled unavailable");
-    return 5;
-  }
+  if (int rc = tma_encoder()) return rc;
   g_gs_attr_set = true;
   return 0;
 }

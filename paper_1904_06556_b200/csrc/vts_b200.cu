@@ -17,6 +17,7 @@
 
 #include "../../include/vts_b200.h"
 #include "context.cuh"
+#include "tma.cuh"
 
 #include "elem_kernels.inc.cu"
 #include "apply.inc.cu"
