@@ -450,7 +450,11 @@ __global__ void __launch_bounds__(32 * gs::kWarps, 1)
       for (int a = 0; a < NSA && a <= nwin; ++a) mbar_expect_tx(&S.full_above[a], above_bytes(a));
     }
   }
-  // every CTA's barriers exist before any remote st.async lands
+  if (!has_above) {  // band 0 (and padding CTAs): lane 0 reads a zero previous row
+    double2* ab = &S.above[0][0];
+    for (int i = threadIdx.x; i < NSA * W; i += blockDim.x) ab[i] = make_double2(0.0, 0.0);
+  }
+  // every CTA's barriers exist (and band 0's ring is zeroed) before any remote st.async lands
   asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
   // band row l -> grid row; box row of band row l; slot position of step st
   auto grid_row = [&](int l) {
@@ -594,7 +598,6 @@ __device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int b
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r_armed) : "r"(smem_u32(&S.armed)), "r"(crank - 1));
   }
   const int l = lane;
-  const bool act = l < rows_here;
   static_assert(SKEW == 2, "the step pipeline below assumes a two-column skew");
   const int lc = l < R ? l : R - 1;
   const int brow = FWD ? lc : R - 1 - lc;  // box row holding band row l
@@ -693,9 +696,7 @@ __device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int b
     StepData cur = prepare(0, win[0], win[1]);
 #pragma unroll
     for (int st = 0; st < W; ++st) {
-      const int j = W * w - SKEW * l + st;
       const int pos = FWD ? st : W - 1 - st;
-      const bool valid = act && j >= 0 && j < nx;
       // the recurrence of step st (xp: previous row, column j+1, shuffled in last step):
       //   x_d0 = r0 (q0 - E[d0].xp - W[d0].w),  x_d1 = r1 (q1 - E[d1].xp - W[d1].w - c x_d0)
       const double2 xp = win[2];
@@ -706,16 +707,18 @@ __device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int b
       // step st+1's independent part (previous-row columns j, j+1 are in win[1..2])
       StepData nxt;
       if (st + 1 < W) nxt = prepare(st + 1, win[1], win[2]);
-      const double2 calc = FWD ? make_double2(n0, n1) : make_double2(n1, n0);
-      const double2 nv = valid ? calc : make_double2(0.0, 0.0);
-      wprev = valid ? calc : wprev;
+      // no validity selects: positions outside the row (j < 0, j >= nx) and rows
+      // outside the grid compute finite values from real neighbouring or zero-padded
+      // slot data; they are never stored, and every coupling that reads them at a
+      // valid position is an exact zero (no neighbour / Dirichlet)
+      const double2 nv = FWD ? make_double2(n0, n1) : make_double2(n1, n0);
+      wprev = nv;
       if (l < R) S.out[s][l][pos] = nv;
       const double r0s = __shfl_up_sync(0xffffffffu, nv.x, 1);
       const double r1s = __shfl_up_sync(0xffffffffu, nv.y, 1);
-      const double2 av = S.above[sa][st];  // zeros for band 0 (never filled, never read as valid)
-      const bool from_above = l == 0 && has_above;
-      const double r0 = l == 0 ? (from_above ? av.x : 0.0) : r0s;
-      const double r1 = l == 0 ? (from_above ? av.y : 0.0) : r1s;
+      const double2 av = S.above[sa][st];  // band 0: a zero-filled ring
+      const double r0 = l == 0 ? av.x : r0s;
+      const double r1 = l == 0 ? av.y : r1s;
 #pragma unroll
       for (int i = 0; i < SKEW; ++i) win[i] = win[i + 1];
       win[SKEW] = make_double2(r0, r1);
