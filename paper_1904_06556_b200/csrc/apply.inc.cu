@@ -188,6 +188,52 @@ __global__ void __launch_bounds__(kBX* kBY, 3) k_newton_apply(const __grid_const
 // y = A_k x (+ border x_alpha) on a block stencil; with `b` given, computes
 // r = b - (A x + border x_alpha) instead.  Border dot partials for y_alpha.
 // Row sums follow the CSR column order SW S SE W C E NW N NE (linalg.py:58).
+// one node of A_k x + border x_alpha (or b - that); also its border.x term
+template <bool RESIDUAL>
+VTS_DEVICE_INLINE double2 level_apply_node(int nx, int ny, const double* __restrict__ stL,
+                                           const double* __restrict__ stU, const double* border, const double* x,
+                                           const double* b, double xa, int nd, double& acc) {
+  const int ix = nd % nx, iy = nd / nx;
+  const double* l = stL + (size_t)nd * kHalf;
+  const double* u = stU + (size_t)nd * kHalf;
+  double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+  for (int blk = 0; blk < 9; ++blk) {
+    const int dx = blk % 3 - 1, dy = blk / 3 - 1;
+    const int jx = ix + dx, jy = iy + dy;
+    double2 xv = make_double2(0.0, 0.0);
+    if (jx >= 0 && jx < nx && jy >= 0 && jy < ny) xv = *reinterpret_cast<const double2*>(x + 2 * (jx + nx * jy));
+    double2 c01, c23;
+    if (blk == kBlockCenter) {
+      c01 = make_double2(l[kHDiag], u[kHC]);
+      c23 = make_double2(l[kHC], u[kHDiag]);
+    } else {
+      const double* h = (blk < 4 ? l : u) + half_offset(blk);
+      c01 = *reinterpret_cast<const double2*>(h);
+      c23 = *reinterpret_cast<const double2*>(h + 2);
+    }
+    s0 = fma(c01.x, xv.x, s0);
+    s0 = fma(c01.y, xv.y, s0);
+    s1 = fma(c23.x, xv.x, s1);
+    s1 = fma(c23.y, xv.y, s1);
+  }
+  const double2 bd = *reinterpret_cast<const double2*>(border + 2 * nd);
+  s0 = fma(bd.x, xa, s0);
+  s1 = fma(bd.y, xa, s1);
+  const double2 xv = *reinterpret_cast<const double2*>(x + 2 * nd);
+  acc = fma(bd.x, xv.x, acc);
+  acc = fma(bd.y, xv.y, acc);
+  if (RESIDUAL) {
+    const double2 bv = *reinterpret_cast<const double2*>(b + 2 * nd);
+    s0 = bv.x - s0;
+    s1 = bv.y - s1;
+  }
+  return make_double2(s0, s1);
+}
+
+// y = A_k x (+ border x_alpha) on a block stencil; with `b` given, computes
+// r = b - (A x + border x_alpha) instead.  Border dot partials for y_alpha.
+// Row sums follow the CSR column order SW S SE W C E NW N NE (linalg.py:58).
 template <bool RESIDUAL>
 __global__ void __launch_bounds__(256) k_level_apply(int nx, int ny, int ngrid, const double* __restrict__ stL,
                                                    const double* __restrict__ stU,
@@ -201,44 +247,8 @@ __global__ void __launch_bounds__(256) k_level_apply(int nx, int ny, int ngrid, 
   const int nnodes = nx * ny;
   const double xa = x[ngrid];
   double acc[1] = {0.0};
-  for (int nd = blockIdx.x * blockDim.x + threadIdx.x; nd < nnodes; nd += gridDim.x * blockDim.x) {
-    const int ix = nd % nx, iy = nd / nx;
-    const double* l = stL + (size_t)nd * kHalf;
-    const double* u = stU + (size_t)nd * kHalf;
-    double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-    for (int blk = 0; blk < 9; ++blk) {
-      const int dx = blk % 3 - 1, dy = blk / 3 - 1;
-      const int jx = ix + dx, jy = iy + dy;
-      double2 xv = make_double2(0.0, 0.0);
-      if (jx >= 0 && jx < nx && jy >= 0 && jy < ny) xv = *reinterpret_cast<const double2*>(x + 2 * (jx + nx * jy));
-      double2 c01, c23;
-      if (blk == kBlockCenter) {
-        c01 = make_double2(l[kHDiag], u[kHC]);
-        c23 = make_double2(l[kHC], u[kHDiag]);
-      } else {
-        const double* h = (blk < 4 ? l : u) + half_offset(blk);
-        c01 = *reinterpret_cast<const double2*>(h);
-        c23 = *reinterpret_cast<const double2*>(h + 2);
-      }
-      s0 = fma(c01.x, xv.x, s0);
-      s0 = fma(c01.y, xv.y, s0);
-      s1 = fma(c23.x, xv.x, s1);
-      s1 = fma(c23.y, xv.y, s1);
-    }
-    const double2 bd = *reinterpret_cast<const double2*>(border + 2 * nd);
-    s0 = fma(bd.x, xa, s0);
-    s1 = fma(bd.y, xa, s1);
-    const double2 xv = *reinterpret_cast<const double2*>(x + 2 * nd);
-    acc[0] = fma(bd.x, xv.x, acc[0]);
-    acc[0] = fma(bd.y, xv.y, acc[0]);
-    if (RESIDUAL) {
-      const double2 bv = *reinterpret_cast<const double2*>(b + 2 * nd);
-      s0 = bv.x - s0;
-      s1 = bv.y - s1;
-    }
-    *reinterpret_cast<double2*>(y + 2 * nd) = make_double2(s0, s1);
-  }
+  for (int nd = blockIdx.x * blockDim.x + threadIdx.x; nd < nnodes; nd += gridDim.x * blockDim.x)
+    *reinterpret_cast<double2*>(y + 2 * nd) = level_apply_node<RESIDUAL>(nx, ny, stL, stU, border, x, b, xa, nd, acc[0]);
   double tot[1];
   if (last_block_reduce<1>(acc, scratch, partials, counter, tot) && threadIdx.x == 0) {
     const double ya = fma(*corner_ptr, xa, tot[0]);

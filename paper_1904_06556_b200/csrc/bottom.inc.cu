@@ -1,0 +1,419 @@
+// Fused bottom of the V-cycle (included by mg.inc.cu inside namespace vts).
+//
+// MgPreconditioner._cycle (multigrid.py:113-143) on the coarse levels 0..kb
+// in ONE single-CTA launch: on those levels every sweep is a few dozen
+// dependent wavefront steps, and as separate launches each level costs ~60 us
+// of fixed launch / barrier-init / TMA-descriptor latency per V-cycle.  Here
+// the level vectors live in shared memory, each sweep stages its half-stencil
+// into shared memory, the parallel passes (old values, residual, restriction,
+// prolongation) use all 1024 threads, the wavefront runs on one warp (lane =
+// grid row; kb is the largest level with <= 32 node rows), and the coarsest
+// bordered system is solved with the Cholesky factor from mg_setup.
+//
+// Arithmetic is the multi-launch path's, operation for operation
+// (gs_old_node, the wavefront step of k_gs_tri, level_apply_node with the
+// same fixed reduction tree, restrict_node, prolong_node, k_coarse_solve's
+// column order), so the fused and unfused V-cycles agree bit for bit up to
+// the sign of zeros.
+
+constexpr int kBotThreads = 1024;
+#ifdef VTS_BOT_PROBE
+__device__ long long g_bot_probe[64];
+__device__ int g_bot_n;
+#define BOT_MARK()                                                           \
+  do {                                                                       \
+    if (threadIdx.x == 0) {                                                  \
+      long long t_;                                                          \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                 \
+      if (g_bot_n < 64) g_bot_probe[g_bot_n++] = t_;                         \
+    }                                                                        \
+  } while (0)
+#else
+#define BOT_MARK() \
+  do {             \
+  } while (0)
+#endif
+constexpr int kBotMaxLevels = 8;
+
+struct BotLevel {
+  int nx, ny, nn, ngrid;
+  const uint8_t* fm;
+  const double* stL;
+  const double* stU;
+  const double* border;
+  int off_b, off_x, off_r;  // shared-memory offsets (doubles) of b, x, r/P (ngrid + 1 each)
+};
+
+struct BotArgs {
+  int kb;  // highest fused level (>= 1)
+  BotLevel lv[kBotMaxLevels];
+  const double* gb;  // level kb right-hand side (global, bordered grid vector)
+  double* gx;        // level kb result (global)
+  const double* corner;
+  // coarsest bordered Cholesky solve (k_coarse_solve)
+  int N0, nfree0;
+  const int32_t* f2g0;
+  const double* chol;
+  int off_chol;  // -1: factor read from global memory
+  int off_y;
+  int off_stage, off_q;  // staged half-stencil (nn * kHalf) and staged border (2 nn)
+  int off_red;           // reduction scratch: 32 virtual-block partials + 8 x 32 warp sums
+};
+
+// one Gauss-Seidel sweep of level L: x <- sweep(x; b) (zero_guess: x_old = 0)
+// (not inlined: one copy of each sweep's code, warm in the instruction cache
+// after its first use; inlined copies per call site ran 3.6x slower cold)
+template <bool FWD, bool ZERO>
+__device__ __noinline__ void bot_sweep(const BotLevel& L, double* sm, const BotArgs& A) {
+  double* sb = sm + L.off_b;
+  double* sx = sm + L.off_x;
+  double* sP = sm + L.off_r;
+  double* stage = sm + A.off_stage;
+  double* sq = sm + A.off_q;
+  const int tid = threadIdx.x;
+  const double* solve_half = FWD ? L.stL : L.stU;
+  // stage the half the wavefront solves with (+ the border for the zero-guess sweep);
+  // the old-value pass reads the other half straight from L2
+  {
+    const double2* src = reinterpret_cast<const double2*>(solve_half);
+    double2* dst = reinterpret_cast<double2*>(stage);
+    for (int i = tid; i < L.nn * kHalf / 2; i += blockDim.x) dst[i] = src[i];
+    if (ZERO)
+      for (int i = tid; i < L.nn; i += blockDim.x)
+        reinterpret_cast<double2*>(sq)[i] = reinterpret_cast<const double2*>(L.border)[i];
+  }
+  __syncthreads();
+  BOT_MARK();  // staged
+  if (!ZERO) {
+    const double xa = sx[L.ngrid];
+    for (int nd = tid; nd < L.nn; nd += blockDim.x)
+      *reinterpret_cast<double2*>(sP + 2 * nd) =
+          gs_old_node<FWD>(L.nx, L.ny, FWD ? L.stU : L.stL, sb, L.border, sx, xa, nd);
+  }
+  __syncthreads();
+  BOT_MARK();  // old pass
+  if (tid < 32) {
+    // the wavefront of k_gs_tri on a single band: lane l = sweep row, skew 2;
+    // software-pipelined like k_gs_tri (step t+1's loads and previous-row part
+    // while step t's own-row recurrence runs); out-of-range positions compute
+    // on clamped data and are neither stored nor passed on
+    const int l = tid;
+    const int iy = FWD ? l : L.ny - 1 - l;
+    const double xa = ZERO ? sx[L.ngrid] : 0.0;
+    constexpr int d0 = FWD ? 0 : 1;
+    constexpr int d1 = 1 - d0;
+    struct Raw {
+      double a[20];
+      double p0, p1;
+      int nd;
+      bool valid;
+    };
+    auto load = [&](int t, Raw& r) {
+      const int j = t - 2 * l;
+      r.valid = l < L.ny && j >= 0 && j < L.nx;
+      const int jc = j < 0 ? 0 : (j >= L.nx ? L.nx - 1 : j);
+      const int ix = FWD ? jc : L.nx - 1 - jc;
+      const int iyc = l < L.ny ? iy : 0;
+      r.nd = ix + L.nx * iyc;
+      const double2* a2 = reinterpret_cast<const double2*>(stage + (size_t)r.nd * kHalf);
+#pragma unroll
+      for (int i = 0; i < 10; ++i) {
+        const double2 v = a2[i];
+        r.a[2 * i] = v.x;
+        r.a[2 * i + 1] = v.y;
+      }
+      if (ZERO) {
+        const double2 bb = *reinterpret_cast<const double2*>(sb + 2 * r.nd);
+        const double2 qq = *reinterpret_cast<const double2*>(sq + 2 * r.nd);
+        r.p0 = __dsub_rn(bb.x, __dmul_rn(qq.x, xa));
+        r.p1 = __dsub_rn(bb.y, __dmul_rn(qq.y, xa));
+      } else {
+        const double2 pp = *reinterpret_cast<const double2*>(sP + 2 * r.nd);
+        r.p0 = pp.x;
+        r.p1 = pp.y;
+      }
+    };
+    struct StepData {
+      double q0, q1, e00, e01, e10, e11, w00, w01, w10, w11, c, r0, r1;
+      int nd;
+      bool valid;
+    };
+    auto prepare = [&](const Raw& r, const double2 xm, const double2 xz) {
+      auto pre = [&](int d, double p) {
+        const double t1 = fma(-r.a[0 + 2 * d], xm.x, -r.a[1 + 2 * d] * xm.y);
+        const double t2 = fma(-r.a[4 + 2 * d], xz.x, -r.a[5 + 2 * d] * xz.y);
+        return p + (t1 + t2);
+      };
+      StepData o;
+      o.q0 = pre(d0, d0 == 0 ? r.p0 : r.p1);
+      o.q1 = pre(d1, d1 == 0 ? r.p0 : r.p1);
+      o.e00 = r.a[8 + 2 * d0];
+      o.e01 = r.a[9 + 2 * d0];
+      o.e10 = r.a[8 + 2 * d1];
+      o.e11 = r.a[9 + 2 * d1];
+      o.w00 = r.a[12 + 2 * d0];
+      o.w01 = r.a[13 + 2 * d0];
+      o.w10 = r.a[12 + 2 * d1];
+      o.w11 = r.a[13 + 2 * d1];
+      o.c = r.a[kHC];
+      o.r0 = r.a[d0 == 0 ? kHRd0 : kHRd1];
+      o.r1 = r.a[d1 == 0 ? kHRd0 : kHRd1];
+      o.nd = r.nd;
+      o.valid = r.valid;
+      return o;
+    };
+    double2 win[3] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+    double2 wprev = make_double2(0.0, 0.0);
+    const int T = L.nx + 2 * (L.ny - 1);
+    Raw raw;
+    load(0, raw);
+    StepData cur = prepare(raw, win[0], win[1]);
+    for (int t = 0; t < T; ++t) {
+      load(t + 1 < T ? t + 1 : t, raw);
+      const double2 xp = win[2];
+      const double u0 = fma(-cur.e00, xp.x, fma(-cur.e01, xp.y, cur.q0));
+      const double u1 = fma(-cur.e10, xp.x, fma(-cur.e11, xp.y, cur.q1));
+      const double n0 = fma(-cur.w00, wprev.x, fma(-cur.w01, wprev.y, u0)) * cur.r0;
+      const double n1 = fma(-cur.c, n0, fma(-cur.w10, wprev.x, fma(-cur.w11, wprev.y, u1))) * cur.r1;
+      const double2 calc = FWD ? make_double2(n0, n1) : make_double2(n1, n0);
+      const double2 nv = cur.valid ? calc : make_double2(0.0, 0.0);
+      if (cur.valid) *reinterpret_cast<double2*>(sx + 2 * cur.nd) = nv;
+      const StepData nxt = prepare(raw, win[1], win[2]);
+      wprev = nv;
+      double2 up;
+      up.x = __shfl_up_sync(0xffffffffu, nv.x, 1);
+      up.y = __shfl_up_sync(0xffffffffu, nv.y, 1);
+      if (l == 0) up = make_double2(0.0, 0.0);  // a single band: no previous row
+      win[0] = win[1];
+      win[1] = win[2];
+      win[2] = up;
+      cur = nxt;
+    }
+  }
+  __syncthreads();
+  BOT_MARK();  // wavefront
+}
+
+// r = b - (A x + border x_alpha) with k_level_apply<true>'s reduction tree for
+// the border row (virtual blocks of 256 threads, last-block sum)
+__device__ __noinline__ void bot_residual(const BotLevel& L, double* sm, const BotArgs& A) {
+  double* sb = sm + L.off_b;
+  double* sx = sm + L.off_x;
+  double* sr = sm + L.off_r;
+  double* part = sm + A.off_red;         // [32] virtual-block partials
+  double* wsum = sm + A.off_red + 32;    // [32 blocks][8 warps]
+  const int tid = threadIdx.x, g = tid >> 8, t = tid & 255, w = t >> 5, lane = tid & 31;
+  const int nvb = (L.nn + 255) / 256;
+  const double xa = sx[L.ngrid];
+  for (int vb0 = 0; vb0 < nvb; vb0 += 4) {
+    const int vb = vb0 + g;
+    double acc = 0.0;
+    if (vb < nvb) {
+      const int nd = vb * 256 + t;
+      if (nd < L.nn)
+        *reinterpret_cast<double2*>(sr + 2 * nd) =
+            level_apply_node<true>(L.nx, L.ny, L.stL, L.stU, L.border, sx, sb, xa, nd, acc);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0 && vb < nvb) wsum[vb * 8 + w] = acc;
+  }
+  __syncthreads();
+  if (tid < nvb) {
+    double s = 0.0;
+    for (int i = 0; i < 8; ++i) s += wsum[tid * 8 + i];
+    part[tid] = s;
+  }
+  __syncthreads();
+  if (tid < 32) {
+    double v = tid < nvb ? part[tid] : 0.0;
+    v = warp_sum(v);
+    if (tid == 0) {
+      // block_sum's thread 0 adds the 8 warp totals of the finishing block (7 zeros)
+      double s = 0.0;
+      s += v;
+      for (int i = 1; i < 8; ++i) s += 0.0;
+      sr[L.ngrid] = sb[L.ngrid] - fma(*A.corner, xa, s);
+    }
+  }
+  __syncthreads();
+}
+
+// x0 = chol^-1 b0 (k_coarse_solve's column order)
+__device__ void bot_coarse(const BotLevel& C, double* sm, const BotArgs& A) {
+  double* sb = sm + C.off_b;
+  double* sx = sm + C.off_x;
+  double* y = sm + A.off_y;
+  const double* Lf = A.off_chol >= 0 ? sm + A.off_chol : A.chol;
+  const int N = A.N0, tid = threadIdx.x;
+  if (A.off_chol >= 0)
+    for (int i = tid; i < N * N; i += blockDim.x) sm[A.off_chol + i] = A.chol[i];
+  for (int i = tid; i < N; i += blockDim.x) y[i] = (i < A.nfree0) ? sb[A.f2g0[i]] : sb[C.ngrid];
+  __syncthreads();
+  if (N <= 32) {
+    // one warp, lane i owns y[i]; same column order and operations as below
+    if (tid < 32) {
+      double yi = tid < N ? y[tid] : 0.0;
+      for (int j = 0; j < N; ++j) {
+        if (tid == j) yi = yi / Lf[(size_t)j * N + j];
+        const double yj = __shfl_sync(0xffffffffu, yi, j);
+        if (tid > j && tid < N) yi = fma(-Lf[(size_t)tid * N + j], yj, yi);
+      }
+      for (int j = N - 1; j >= 0; --j) {
+        if (tid == j) yi = yi / Lf[(size_t)j * N + j];
+        const double yj = __shfl_sync(0xffffffffu, yi, j);
+        if (tid < j) yi = fma(-Lf[(size_t)j * N + tid], yj, yi);
+      }
+      if (tid < N) y[tid] = yi;
+    }
+    __syncthreads();
+  } else {
+  for (int j = 0; j < N; ++j) {
+    if (tid == 0) y[j] = y[j] / Lf[(size_t)j * N + j];
+    __syncthreads();
+    const double yj = y[j];
+    for (int i = j + 1 + tid; i < N; i += blockDim.x) y[i] = fma(-Lf[(size_t)i * N + j], yj, y[i]);
+    __syncthreads();
+  }
+  for (int j = N - 1; j >= 0; --j) {
+    if (tid == 0) y[j] = y[j] / Lf[(size_t)j * N + j];
+    __syncthreads();
+    const double yj = y[j];
+    for (int i = tid; i < j; i += blockDim.x) y[i] = fma(-Lf[(size_t)j * N + i], yj, y[i]);
+    __syncthreads();
+  }
+  }
+  for (int i = tid; i <= C.ngrid; i += blockDim.x) sx[i] = 0.0;
+  __syncthreads();
+  for (int i = tid; i < N; i += blockDim.x) {
+    if (i < A.nfree0) sx[A.f2g0[i]] = y[i];
+    else sx[C.ngrid] = y[i];
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kBotThreads, 1) k_vcycle_bottom(const __grid_constant__ BotArgs A, const int* skip) {
+  if (skip && *skip) return;
+  extern __shared__ __align__(16) double sm[];
+  const int tid = threadIdx.x;
+  {
+    const BotLevel& T = A.lv[A.kb];
+    for (int i = tid; i <= T.ngrid; i += blockDim.x) sm[T.off_b + i] = A.gb[i];
+  }
+  __syncthreads();
+  for (int k = A.kb; k >= 1; --k) {  // descent (multigrid.py:115-131)
+    const BotLevel& L = A.lv[k];
+    if (tid == 0) sm[L.off_x + L.ngrid] = 0.0;  // k_alpha_init on a coarse level
+    __syncthreads();
+    bot_sweep<true, true>(L, sm, A);
+    bot_sweep<true, false>(L, sm, A);
+    bot_residual(L, sm, A);
+    BOT_MARK();  // residual
+    const BotLevel& C = A.lv[k - 1];
+    for (int cn = tid; cn <= C.nn; cn += blockDim.x) {
+      if (cn == C.nn) sm[C.off_b + C.ngrid] = sm[L.off_r + L.ngrid];
+      else
+        *reinterpret_cast<double2*>(sm + C.off_b + 2 * cn) =
+            restrict_node(L.nx, L.ny, L.fm, sm + L.off_r, C.nx, C.fm, cn);
+    }
+    __syncthreads();
+  }
+  BOT_MARK();
+  bot_coarse(A.lv[0], sm, A);
+  BOT_MARK();
+  for (int k = 1; k <= A.kb; ++k) {  // ascent (multigrid.py:132-139)
+    const BotLevel& L = A.lv[k];
+    const BotLevel& C = A.lv[k - 1];
+    for (int fi = tid; fi <= L.nn; fi += blockDim.x) {
+      if (fi == L.nn) sm[L.off_x + L.ngrid] += sm[C.off_x + C.ngrid];
+      else
+        *reinterpret_cast<double2*>(sm + L.off_x + 2 * fi) =
+            prolong_node(L.nx, L.fm, sm + L.off_x, C.nx, C.fm, sm + C.off_x, fi);
+    }
+    __syncthreads();
+    bot_sweep<false, false>(L, sm, A);
+    bot_sweep<false, false>(L, sm, A);
+  }
+  {
+    const BotLevel& T = A.lv[A.kb];
+    for (int i = tid; i <= T.ngrid; i += blockDim.x) A.gx[i] = sm[T.off_x + i];
+  }
+}
+
+// Highest level the fused kernel can take (0 = none): below the top, <= 32
+// node rows, and its vectors + one staged half-stencil fit in shared memory.
+static int bottom_plan(Ctx* c, BotArgs* A, size_t* smem_bytes) {
+  const int top = c->L - 1;
+  int kb = 0;
+  for (int k = 1; k < top && k < kBotMaxLevels; ++k) {
+    if (c->lv[k].d.ny > 32) break;
+    kb = k;
+  }
+  while (kb >= 1) {
+    size_t off = 0;
+    for (int k = 0; k <= kb; ++k) {
+      const LevelDev& d = c->lv[k].d;
+      BotLevel& b = A->lv[k];
+      b.nx = d.nx;
+      b.ny = d.ny;
+      b.nn = d.nnodes;
+      b.ngrid = d.ngrid;
+      b.fm = d.free_mask;
+      b.stL = d.stL;
+      b.stU = d.stU;
+      b.border = d.border;
+      const size_t v = (size_t)d.ngrid + 2;  // ngrid + 1, kept even for double2 alignment
+      b.off_b = (int)off;
+      off += v;
+      b.off_x = (int)off;
+      off += v;
+      b.off_r = (int)off;
+      off += v;
+    }
+    A->off_stage = (int)off;
+    off += (size_t)c->lv[kb].d.nnodes * kHalf;
+    A->off_q = (int)off;
+    off += 2 * (size_t)c->lv[kb].d.nnodes;
+    A->off_red = (int)off;
+    off += 32 + 32 * 8;
+    A->off_y = (int)off;
+    off += (size_t)c->N0 + (c->N0 & 1);
+    const size_t base = off * 8;
+    const size_t chol = (size_t)c->N0 * c->N0 * 8;
+    A->off_chol = -1;
+    if (base + chol <= 200 * 1024) {
+      A->off_chol = (int)off;
+      off += (size_t)c->N0 * c->N0;
+    }
+    if (off * 8 <= 200 * 1024) {
+      *smem_bytes = off * 8;
+      A->kb = kb;
+      return kb;
+    }
+    --kb;  // too big: fuse one level less
+  }
+  return 0;
+}
+
+static bool g_bot_attr_set = false;
+
+// levels 0..kb of the V-cycle in one launch; L(kb).b must hold the restricted
+// right-hand side, L(kb).x receives the level's result
+static int vcycle_bottom(Ctx* c, const BotArgs& plan, size_t smem, const int* skip) {
+  if (!g_bot_attr_set) {
+    VTS_CUDA(cudaFuncSetAttribute(k_vcycle_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    g_bot_attr_set = true;
+  }
+  BotArgs A = plan;
+  LevelBuf& T = c->lv[A.kb];
+  A.gb = T.b;
+  A.gx = T.x;
+  A.corner = c->d_corner;
+  A.N0 = c->N0;
+  A.nfree0 = c->lv[0].d.nfree;
+  A.f2g0 = c->lv[0].d.free2grid;
+  A.chol = c->chol;
+  k_vcycle_bottom<<<1, kBotThreads, smem, c->stream>>>(A, skip);
+  VTS_LAUNCHED(c);
+  return 0;
+}
+

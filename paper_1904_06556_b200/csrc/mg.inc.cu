@@ -229,17 +229,9 @@ __global__ void k_symmetrize(int nx, int ny, const double* __restrict__ raw, con
 // ---------------------------------------------------------------------------
 // vc = P^T vf on free dofs (csc_matvec order: fine dofs in increasing index);
 // with `bordered` the border slot is copied (multigrid.py:128-130)
-__global__ void k_restrict(int fnx, int fny, const uint8_t* __restrict__ ffm, const double* __restrict__ vf,
-                           int cnx, int cny, const uint8_t* __restrict__ cfm, double* __restrict__ vc,
-                           int bordered, const int* skip) {
-  if (skip && *skip) return;
-  const int cn = blockIdx.x * blockDim.x + threadIdx.x;
-  const int cnn = cnx * cny;
-  if (cn > cnn) return;
-  if (cn == cnn) {
-    if (bordered) vc[2 * cnn] = vf[2 * fnx * fny];
-    return;
-  }
+// one coarse node of P^T vf (free dofs only)
+VTS_DEVICE_INLINE double2 restrict_node(int fnx, int fny, const uint8_t* __restrict__ ffm, const double* vf, int cnx,
+                                        const uint8_t* __restrict__ cfm, int cn) {
   const int cx = cn % cnx, cy = cn / cnx;
   const uchar2 fc = *reinterpret_cast<const uchar2*>(cfm + 2 * cn);
   double s0 = 0.0, s1 = 0.0;
@@ -255,21 +247,27 @@ __global__ void k_restrict(int fnx, int fny, const uint8_t* __restrict__ ffm, co
       if (ff.y) s1 += wv * v.y;
     }
   }
-  *reinterpret_cast<double2*>(vc + 2 * cn) = make_double2(fc.x ? s0 : 0.0, fc.y ? s1 : 0.0);
+  return make_double2(fc.x ? s0 : 0.0, fc.y ? s1 : 0.0);
+}
+
+__global__ void k_restrict(int fnx, int fny, const uint8_t* __restrict__ ffm, const double* __restrict__ vf,
+                           int cnx, int cny, const uint8_t* __restrict__ cfm, double* __restrict__ vc,
+                           int bordered, const int* skip) {
+  if (skip && *skip) return;
+  const int cn = blockIdx.x * blockDim.x + threadIdx.x;
+  const int cnn = cnx * cny;
+  if (cn > cnn) return;
+  if (cn == cnn) {
+    if (bordered) vc[2 * cnn] = vf[2 * fnx * fny];
+    return;
+  }
+  *reinterpret_cast<double2*>(vc + 2 * cn) = restrict_node(fnx, fny, ffm, vf, cnx, cfm, cn);
 }
 
 // xf += P xc (multigrid.py:134-136): parents in increasing coarse index
-__global__ void k_prolong_add(int fnx, int fny, const uint8_t* __restrict__ ffm, double* __restrict__ xf,
-                              int cnx, int cny, const uint8_t* __restrict__ cfm, const double* __restrict__ xc,
-                              const int* skip) {
-  if (skip && *skip) return;
-  const int fi = blockIdx.x * blockDim.x + threadIdx.x;
-  const int fnn = fnx * fny;
-  if (fi > fnn) return;
-  if (fi == fnn) {
-    xf[2 * fnn] += xc[2 * cnx * cny];
-    return;
-  }
+// fine node fi of xf + P xc
+VTS_DEVICE_INLINE double2 prolong_node(int fnx, const uint8_t* __restrict__ ffm, const double* xf, int cnx,
+                                       const uint8_t* __restrict__ cfm, const double* xc, int fi) {
   const int fx = fi % fnx, fy = fi / fnx;
   const uchar2 ff = *reinterpret_cast<const uchar2*>(ffm + 2 * fi);
   double s0 = 0.0, s1 = 0.0;
@@ -286,10 +284,24 @@ __global__ void k_prolong_add(int fnx, int fny, const uint8_t* __restrict__ ffm,
       if (fc.y) s1 += wv * v.y;
     }
   }
-  double2 o = *reinterpret_cast<double2*>(xf + 2 * fi);
+  double2 o = *reinterpret_cast<const double2*>(xf + 2 * fi);
   if (ff.x) o.x += s0;
   if (ff.y) o.y += s1;
-  *reinterpret_cast<double2*>(xf + 2 * fi) = o;
+  return o;
+}
+
+__global__ void k_prolong_add(int fnx, int fny, const uint8_t* __restrict__ ffm, double* __restrict__ xf,
+                              int cnx, int cny, const uint8_t* __restrict__ cfm, const double* __restrict__ xc,
+                              const int* skip) {
+  if (skip && *skip) return;
+  const int fi = blockIdx.x * blockDim.x + threadIdx.x;
+  const int fnn = fnx * fny;
+  if (fi > fnn) return;
+  if (fi == fnn) {
+    xf[2 * fnn] += xc[2 * cnx * cny];
+    return;
+  }
+  *reinterpret_cast<double2*>(xf + 2 * fi) = prolong_node(fnx, ffm, xf, cnx, cfm, xc, fi);
 }
 
 // ---------------------------------------------------------------------------
@@ -299,15 +311,9 @@ __global__ void k_prolong_add(int fnx, int fny, const uint8_t* __restrict__ ffm,
 // Old-value pass of one sweep: P = b - border x_alpha - U x_old (forward) or
 // - L x_old (backward).  Sums follow the CSR column order of multigrid.py:41-47.
 template <bool FWD>
-__global__ void __launch_bounds__(256) k_gs_old(int nx, int ny, int ngrid, const double* __restrict__ half,
-                                              const double* __restrict__ b, const double* __restrict__ bd,
-                                              const double* __restrict__ x, double* __restrict__ P,
-                                              const int* skip) {
-  if (skip && *skip) return;
-  const int nd = blockIdx.x * blockDim.x + threadIdx.x;
-  if (nd >= nx * ny) return;
+VTS_DEVICE_INLINE double2 gs_old_node(int nx, int ny, const double* __restrict__ half, const double* b,
+                                      const double* bd, const double* x, double xa, int nd) {
   const int ix = nd % nx, iy = nd / nx;
-  const double xa = x[ngrid];
   const double* a = half + (size_t)nd * kHalf;
   const double2 bv = *reinterpret_cast<const double2*>(b + 2 * nd);
   const double2 dv = *reinterpret_cast<const double2*>(bd + 2 * nd);
@@ -346,7 +352,20 @@ __global__ void __launch_bounds__(256) k_gs_old(int nx, int ny, int ngrid, const
     }
     p1 = fma(-a[kHC], xo.x, p1);
   }
-  *reinterpret_cast<double2*>(P + 2 * nd) = make_double2(p0, p1);
+  return make_double2(p0, p1);
+}
+
+// Old-value pass of one sweep: P = b - border x_alpha - U x_old (forward) or
+// - L x_old (backward).  Sums follow the CSR column order of multigrid.py:41-47.
+template <bool FWD>
+__global__ void __launch_bounds__(256) k_gs_old(int nx, int ny, int ngrid, const double* __restrict__ half,
+                                              const double* __restrict__ b, const double* __restrict__ bd,
+                                              const double* __restrict__ x, double* __restrict__ P,
+                                              const int* skip) {
+  if (skip && *skip) return;
+  const int nd = blockIdx.x * blockDim.x + threadIdx.x;
+  if (nd >= nx * ny) return;
+  *reinterpret_cast<double2*>(P + 2 * nd) = gs_old_node<FWD>(nx, ny, half, b, bd, x, x[ngrid], nd);
 }
 
 #ifdef VTS_GS_PROBE
@@ -450,11 +469,15 @@ __global__ void __launch_bounds__(32 * gs::kWarps, 1)
       for (int a = 0; a < NSA && a <= nwin; ++a) mbar_expect_tx(&S.full_above[a], above_bytes(a));
     }
   }
-  if (!has_above) {  // band 0 (and padding CTAs): lane 0 reads a zero previous row
+  {
+    // zero the previous-row ring in every CTA: band 0 reads it as its zero previous
+    // row, and in the other bands the entries for columns >= nx are never written
+    // by the handoff yet are read (times an exactly zero coupling) at the last
+    // column -- stale shared memory there could hold a NaN pattern
     double2* ab = &S.above[0][0];
     for (int i = threadIdx.x; i < NSA * W; i += blockDim.x) ab[i] = make_double2(0.0, 0.0);
   }
-  // every CTA's barriers exist (and band 0's ring is zeroed) before any remote st.async lands
+  // every CTA's barriers exist (and its ring is zeroed) before any remote st.async lands
   asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
   // band row l -> grid row; box row of band row l; slot position of step st
   auto grid_row = [&](int l) {
@@ -974,10 +997,25 @@ static int gs_sweep(Ctx* c, int k, const double* b, double* x, bool forward, boo
   return launch_tri<false, false>(c, L, mS, mP, mP, x, skip);
 }
 
+#include "bottom.inc.cu"
+
+// VTS_UNFUSED_BOTTOM=1 runs every level through the multi-launch path (A/B checks)
+static bool fused_bottom_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("VTS_UNFUSED_BOTTOM");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
 int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
   const int top = c->L - 1;
+  BotArgs plan{};
+  size_t bot_smem = 0;
+  const int kb = fused_bottom_enabled() ? bottom_plan(c, &plan, &bot_smem) : 0;
+  const int lo = kb >= 1 ? kb + 1 : 1;  // lowest level handled by separate launches
   // descent
-  for (int k = top; k >= 1; --k) {
+  for (int k = top; k >= lo; --k) {
     LevelBuf& L = c->lv[k];
     const double* b = (k == top) ? b_top : L.b;
     double* x = (k == top) ? z_top : L.x;
@@ -991,7 +1029,9 @@ int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
                                                                      C.d.ny, C.d.free_mask, C.b, 1, skip);
     VTS_LAUNCHED(c);
   }
-  {
+  if (kb >= 1) {
+    if (int rc = vcycle_bottom(c, plan, bot_smem, skip)) return rc;
+  } else {
     LevelBuf& C = c->lv[0];
     double* x0 = (top == 0) ? z_top : C.x;
     const double* b0 = (top == 0) ? b_top : C.b;
@@ -1000,7 +1040,7 @@ int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
     VTS_LAUNCHED(c);
   }
   // ascent
-  for (int k = 1; k <= top; ++k) {
+  for (int k = lo; k <= top; ++k) {
     LevelBuf& L = c->lv[k];
     LevelBuf& C = c->lv[k - 1];
     const double* b = (k == top) ? b_top : L.b;

@@ -1,0 +1,60 @@
+"""Run-to-run determinism of the CUDA path (bit for bit).
+
+Every reduction is a fixed tree, the wavefront has a fixed schedule and no
+atomics touch values, so repeated solves must agree exactly.  This also
+guards the wavefront's reliance on finite slot data at out-of-range
+positions: a stale-shared-memory NaN there shows up as a run-to-run
+difference or a MINRES breakdown (it did once).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU containers
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1904_06556_b200 as vts  # noqa: E402
+
+
+def _system(key: str, seed: int = 0):
+    prob = vts.build_config(key)
+    n, m = prob.n, prob.m
+    rng = np.random.default_rng(seed)
+    host = dict(u=rng.normal(0.0, 1e-2, n), alpha=1e-3, nu_lo=rng.uniform(0, 1e-2, m),
+                nu_up=rng.uniform(0, 1e-2, m), rho=rng.uniform(0.5, 2.0, m), mu_lo=np.ones(m), mu_up=np.ones(m),
+                p=np.full(m, 1e-2), q_lo=np.ones(m), q_up=np.ones(m))
+    st = vts.PbmState(**{k: (v if k == "alpha" else torch.as_tensor(v, device="cuda")) for k, v in host.items()})
+    ops = vts.ElementOps(prob.fine)
+    ev = vts.eval_lagrangian(st, ops, prob.f, vts.DensityBounds.for_problem(m, prob.volume, 0.0),
+                             vts.PenaltyBarrier())
+    mat, rhs = vts.schur_system(ev, ops)
+    return prob, mat, rhs
+
+
+@pytest.mark.parametrize("key", ["C1", "C2"])
+def test_vcycle_and_minres_bitwise_repeatable(key):
+    prob, mat, rhs = _system(key)
+    mg = vts.MgPreconditioner(mat, prob.transfers)
+    z0 = mg.apply(rhs).cpu().numpy()
+    for _ in range(100):
+        assert np.array_equal(mg.apply(rhs).cpu().numpy(), z0)
+    cfg = vts.MinresConfig(tol=1e-10, max_iters=500)
+    ref = vts.minres_solve(mat, rhs, cfg, mg.apply)
+    for _ in range(10):
+        res = vts.minres_solve(mat, rhs, cfg, mg.apply)
+        assert res.iterations == ref.iterations
+        assert np.array_equal(res.x.cpu().numpy(), ref.x.cpu().numpy())
+
+
+def test_full_pbm_bitwise_repeatable():
+    runs = [vts.solve_pbm(vts.build_config("C1")) for _ in range(4)]
+    for r in runs[1:]:
+        assert r.outer_iterations == runs[0].outer_iterations
+        assert list(r.extras["minres_per_newton"]) == list(runs[0].extras["minres_per_newton"])
+        assert r.objective == runs[0].objective
+        assert np.array_equal(r.rho.cpu().numpy(), runs[0].rho.cpu().numpy())

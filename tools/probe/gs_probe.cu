@@ -4,17 +4,19 @@
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o gs_probe gs_probe.cu
 #include "../../paper_1904_06556_b200/csrc/vts_b200.cu"
 #include <cstdio>
+#include <cstring>
 #include <random>
 #include <vector>
 
 int main(int argc, char** argv) {
   const int levels = argc > 1 ? atoi(argv[1]) : 9;
+  const int base = argc > 2 ? atoi(argv[2]) : 4;  // coarsest elements in x (y = base / 2)
   std::vector<int32_t> ex(levels), ey(levels);
   std::vector<std::vector<int64_t>> dofs(levels);
   std::vector<const int64_t*> ptrs(levels);
   for (int k = 0; k < levels; ++k) {
-    ex[k] = 4 << k;
-    ey[k] = 2 << k;
+    ex[k] = base << k;
+    ey[k] = (base / 2) << k;
     const int nx = ex[k] + 1, ny = ey[k] + 1;
     dofs[k].assign(2 * nx * ny, -1);
     int64_t n = 0;
@@ -96,6 +98,39 @@ int main(int argc, char** argv) {
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
   printf("V-cycle: %.1f us (%s)\n", ms * 1e3 / 5, cudaGetErrorString(err));
+#ifdef VTS_BOT_PROBE
+  {
+    int zero = 0;
+    cudaMemcpyToSymbol(vts::g_bot_n, &zero, 4);
+    vts::vcycle_grid(c, xin, yout, nullptr);
+    cudaDeviceSynchronize();
+    int n = 0;
+    long long pr[64];
+    cudaMemcpyFromSymbol(&n, vts::g_bot_n, 4);
+    cudaMemcpyFromSymbol(pr, vts::g_bot_probe, 64 * 8);
+    for (int i = 1; i < n; ++i) printf("bottom mark %2d: +%6.2f us\n", i, (pr[i] - pr[i - 1]) / 1e3);
+    printf("bottom total (first to last mark): %.1f us\n", (pr[n - 1] - pr[0]) / 1e3);
+  }
+#endif
+  {  // determinism: the V-cycle on fixed input, bitwise, many times
+    const size_t n = c->lv[levels - 1].d.ngrid + 1;
+    std::vector<double> r0(n), r1(n);
+    vts::vcycle_grid(c, xin, yout, nullptr);
+    cudaMemcpy(r0.data(), yout, n * 8, cudaMemcpyDeviceToHost);
+    int bad = 0;
+    const int nrep = getenv("VTS_DET_REPS") ? atoi(getenv("VTS_DET_REPS")) : 200;
+    for (int r = 0; r < nrep; ++r) {
+      vts::vcycle_grid(c, xin, yout, nullptr);
+      cudaMemcpy(r1.data(), yout, n * 8, cudaMemcpyDeviceToHost);
+      if (memcmp(r0.data(), r1.data(), n * 8) != 0) {
+        ++bad;
+        size_t first = 0;
+        while (first < n && r0[first] == r1[first]) ++first;
+        if (bad <= 3) printf("determinism: rep %d differs first at %zu (%.17g vs %.17g)\n", r, first, r0[first], r1[first]);
+      }
+    }
+    printf("determinism: %d of %d V-cycles differ\n", bad, nrep);
+  }
   vts_ctx_destroy(h);
   return 0;
 }
