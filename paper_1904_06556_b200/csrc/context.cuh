@@ -21,8 +21,13 @@ struct LevelBuf {
   double* b = nullptr;           // [ngrid + 1] V-cycle right-hand side
   double* x = nullptr;           // [ngrid + 1] V-cycle iterate
   double* r = nullptr;           // [ngrid + 1] residual / scratch
-  unsigned long long* gs_flags = nullptr;  // GS wavefront progress, one per row group
+  // GS wavefront progress counters, 3 x gs_groups: [0, G) band handoff (single
+  // sweeps and sweep A of a pair), [G, 2G) band handoff of sweep B, [2G, 3G)
+  // sweep A's stored windows (epoch-tagged, never reset)
+  unsigned long long* gs_flags = nullptr;
   int gs_groups = 0;
+  unsigned long long pair_epoch = 0;  // launches of the pipelined sweep pair on this level
+  double* x1 = nullptr;               // [ngrid + 1] sweep A's result inside a pair
   size_t pad_nodes = 0;  // zero nodes before/after stL, stU and every vector of this level
 };
 

@@ -308,55 +308,86 @@ __global__ void k_prolong_add(int fnx, int fny, const uint8_t* __restrict__ ffm,
 // exact-order Gauss-Seidel sweep, v2: old-value pass + staged wavefront solve
 // ---------------------------------------------------------------------------
 
-// Old-value pass of one sweep: P = b - border x_alpha - U x_old (forward) or
-// - L x_old (backward).  Sums follow the CSR column order of multigrid.py:41-47.
+// Old-value pass of one sweep, per node: P = b - border x_alpha - U x_old
+// (forward) or - L x_old (backward), sums in the CSR column order of
+// multigrid.py:41-47.  Split into loads and arithmetic so callers can issue the
+// loads early (and, in the pipelined pair, prefetch the static half-stencil).
+struct OldIn {
+  double a[18];  // the other half-stencil: 4 blocks + centre coupling (kHC)
+  double2 bv, dv, xo, v[4];
+};
+
+// the vector inputs of one node's old-value pass (b, border, own and later neighbours' old values)
 template <bool FWD>
-VTS_DEVICE_INLINE double2 gs_old_node(int nx, int ny, const double* __restrict__ half, const double* b,
-                                      const double* bd, const double* x, double xa, int nd) {
+VTS_DEVICE_INLINE void gs_old_load_vectors(int nx, int ny, const double* b, const double* bd, const double* x, int nd,
+                                           OldIn& in) {
   const int ix = nd % nx, iy = nd / nx;
-  const double* a = half + (size_t)nd * kHalf;
-  const double2 bv = *reinterpret_cast<const double2*>(b + 2 * nd);
-  const double2 dv = *reinterpret_cast<const double2*>(bd + 2 * nd);
-  const double2 xo = *reinterpret_cast<const double2*>(x + 2 * nd);
+  in.bv = *reinterpret_cast<const double2*>(b + 2 * nd);
+  in.dv = *reinterpret_cast<const double2*>(bd + 2 * nd);
+  in.xo = *reinterpret_cast<const double2*>(x + 2 * nd);
   // half slots q = 0..3: FWD (U) NE N NW E at (+1,+1) (0,+1) (-1,+1) (+1,0); BWD (L) mirrored
   const int sg = FWD ? 1 : -1;
-  double2 v[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int dx = sg * (q == 0 ? 1 : q == 1 ? 0 : q == 2 ? -1 : 1);
     const int dy = sg * (q == 3 ? 0 : 1);
     const int jx = ix + dx, jy = iy + dy;
-    v[q] = (jx >= 0 && jx < nx && jy >= 0 && jy < ny) ? *reinterpret_cast<const double2*>(x + 2 * (jx + nx * jy))
-                                                      : make_double2(0.0, 0.0);
+    in.v[q] = (jx >= 0 && jx < nx && jy >= 0 && jy < ny) ? *reinterpret_cast<const double2*>(x + 2 * (jx + nx * jy))
+                                                         : make_double2(0.0, 0.0);
   }
-  double p0 = __dsub_rn(bv.x, __dmul_rn(dv.x, xa));
-  double p1 = __dsub_rn(bv.y, __dmul_rn(dv.y, xa));
+}
+
+template <bool FWD>
+VTS_DEVICE_INLINE void gs_old_load(int nx, int ny, const double* __restrict__ half, const double* b, const double* bd,
+                                   const double* x, int nd, OldIn& in) {
+  const double2* a2 = reinterpret_cast<const double2*>(half + (size_t)nd * kHalf);
+#pragma unroll
+  for (int i = 0; i < 9; ++i) {
+    const double2 t = a2[i];
+    in.a[2 * i] = t.x;
+    in.a[2 * i + 1] = t.y;
+  }
+  gs_old_load_vectors<FWD>(nx, ny, b, bd, x, nd, in);
+}
+
+template <bool FWD>
+VTS_DEVICE_INLINE double2 gs_old_eval(const OldIn& in, double xa) {
+  const double* a = in.a;
+  double p0 = __dsub_rn(in.bv.x, __dmul_rn(in.dv.x, xa));
+  double p1 = __dsub_rn(in.bv.y, __dmul_rn(in.dv.y, xa));
   if (FWD) {
     // CSR order of the upper part: C(a01 x1), E, NW, N, NE  (slots 3, 2, 1, 0)
-    p0 = fma(-a[kHC], xo.y, p0);
+    p0 = fma(-a[kHC], in.xo.y, p0);
 #pragma unroll
     for (int q = 3; q >= 0; --q) {
-      p0 = fma(-a[4 * q + 0], v[q].x, p0);
-      p0 = fma(-a[4 * q + 1], v[q].y, p0);
-      p1 = fma(-a[4 * q + 2], v[q].x, p1);
-      p1 = fma(-a[4 * q + 3], v[q].y, p1);
+      p0 = fma(-a[4 * q + 0], in.v[q].x, p0);
+      p0 = fma(-a[4 * q + 1], in.v[q].y, p0);
+      p1 = fma(-a[4 * q + 2], in.v[q].x, p1);
+      p1 = fma(-a[4 * q + 3], in.v[q].y, p1);
     }
   } else {
     // CSR order of the lower part: SW, S, SE, W, C(a10 x0)  (slots 0..3)
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      p0 = fma(-a[4 * q + 0], v[q].x, p0);
-      p0 = fma(-a[4 * q + 1], v[q].y, p0);
-      p1 = fma(-a[4 * q + 2], v[q].x, p1);
-      p1 = fma(-a[4 * q + 3], v[q].y, p1);
+      p0 = fma(-a[4 * q + 0], in.v[q].x, p0);
+      p0 = fma(-a[4 * q + 1], in.v[q].y, p0);
+      p1 = fma(-a[4 * q + 2], in.v[q].x, p1);
+      p1 = fma(-a[4 * q + 3], in.v[q].y, p1);
     }
-    p1 = fma(-a[kHC], xo.x, p1);
+    p1 = fma(-a[kHC], in.xo.x, p1);
   }
   return make_double2(p0, p1);
 }
 
-// Old-value pass of one sweep: P = b - border x_alpha - U x_old (forward) or
-// - L x_old (backward).  Sums follow the CSR column order of multigrid.py:41-47.
+template <bool FWD>
+VTS_DEVICE_INLINE double2 gs_old_node(int nx, int ny, const double* __restrict__ half, const double* b,
+                                      const double* bd, const double* x, double xa, int nd) {
+  OldIn in;
+  gs_old_load<FWD>(nx, ny, half, b, bd, x, nd, in);
+  return gs_old_eval<FWD>(in, xa);
+}
+
+// Old-value pass of one sweep as its own kernel (single sweeps, sweep A of a pair).
 template <bool FWD>
 __global__ void __launch_bounds__(256) k_gs_old(int nx, int ny, int ngrid, const double* __restrict__ half,
                                               const double* __restrict__ b, const double* __restrict__ bd,
@@ -383,6 +414,8 @@ constexpr int NS = 3;      // window slots in flight (in and out rings)
 constexpr int NSA = 4;     // window slots of the previous band's row
 constexpr int SKEW = 2;    // columns between consecutive rows of the wavefront
 constexpr int kWarps = 5;  // compute, loader, storer, publisher, stager
+constexpr int kBuild = 9;  // pipelined pair, sweep B: builder warps (one node of a window's R x W box each)
+constexpr int kWarpsPair = kWarps + kBuild;
 // one window slot = three TMA boxes: R rows x W nodes x {22 stencil, 2 P, 2 border} doubles
 struct __align__(128) InSlot {
   double st[R][W][kHalf];
@@ -421,19 +454,40 @@ static_assert(((W * kHalf * 8) / 16) % 2 == 1, "lane stride must be an odd multi
 template <bool FWD, bool ZERO>
 __device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int band, int rows_here, bool has_above,
                                            bool dsm_in, unsigned crank, int nwin,
-                                           double* __restrict__ x);
+                                           const double* __restrict__ x);
 
-template <bool FWD, bool ZERO>
-__global__ void __launch_bounds__(32 * gs::kWarps, 1)
-    k_gs_tri(int nx, int ny, int ngrid, int pad_nodes, int bands, const __grid_constant__ CUtensorMap mapS,
-             const __grid_constant__ CUtensorMap mapP, const __grid_constant__ CUtensorMap mapQ,
-             double* __restrict__ x, unsigned long long* flags, const int* skip) {
+// One band of a wavefront sweep.  ROLE 0: a single sweep (P by TMA box).  In
+// the pipelined pair (k_gs_pair) of two consecutive sweeps, ROLE 1 is sweep A
+// (as ROLE 0, result into a scratch vector, plus the stored-window counters
+// sweep B waits on) and ROLE 2 is sweep B (its right-hand side
+// P = b - border x_alpha - U x_A is computed by builder warps from sweep A's
+// result as that becomes available, instead of a separate old-value pass).
+struct GsBand {
+  int nx, ny, ngrid, pad_nodes, bands, band;
+  const CUtensorMap* mapS;  // half-stencil the wavefront solves with
+  const CUtensorMap* mapP;  // P (ROLE 0/1), b (ZERO)
+  const CUtensorMap* mapQ;  // border (ZERO)
+  double* x;                // the sweep's result
+  const double* xa_src;     // bordered vector holding x_alpha (slot ngrid)
+  unsigned long long* flags;   // band-to-band handoff counters of this sweep
+  unsigned long long* stored;  // sweep A's stored-window counters (pair only)
+  unsigned long long epoch;    // pair launch tag of the stored counters
+  const double* b;             // ROLE 2 builders: right-hand side, border, old-value half-stencil,
+  const double* border;        //   sweep A's result
+  const double* half_old;
+  const double* x_in;
+};
+
+template <bool FWD, bool ZERO, int ROLE>
+__device__ __forceinline__ void gs_band(const GsBand& G) {
   using namespace gs;
-  if (skip && *skip) return;
+  const int nx = G.nx, ny = G.ny, ngrid = G.ngrid, pad_nodes = G.pad_nodes, bands = G.bands;
+  double* __restrict__ x = G.x;
+  unsigned long long* flags = G.flags;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int band = blockIdx.x;
+  const int band = G.band;
   const bool real = band < bands;  // grids are padded to whole clusters
   const int rows_here = real ? min(R, ny - band * R) : 0;
   const bool has_above = real && band > 0;
@@ -454,7 +508,7 @@ __global__ void __launch_bounds__(32 * gs::kWarps, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
-      mbar_init(&S.full_in[s], 1);
+      mbar_init(&S.full_in[s], ROLE == 2 ? 1 + kBuild : 1);  // sweep B: + one arrive per builder warp
       mbar_init(&S.empty_in[s], 1);
       mbar_init(&S.full_out[s], 1);
       mbar_init(&S.empty_out[s], 2);
@@ -498,10 +552,16 @@ __global__ void __launch_bounds__(32 * gs::kWarps, 1)
         // node index of box element (p = 0, box row 0)
         const int node0 = FWD ? iy0 * nx + W * w : (iyb - R + 2) * nx - W * (w + 1) + SKEW * (R - 1);
         const int c1 = node0 + pad_nodes;
-        mbar_expect_tx(&S.full_in[s], (unsigned)(sizeof(S.in[s].st) + sizeof(S.in[s].p) + (ZERO ? sizeof(S.in[s].q) : 0)));
-        tma_load_3d(&S.in[s].st[0][0][0], &mapS, 0, c1, 0, &S.full_in[s]);
-        tma_load_3d(&S.in[s].p[0][0][0], &mapP, 0, c1, 0, &S.full_in[s]);
-        if (ZERO) tma_load_3d(&S.in[s].q[0][0][0], &mapQ, 0, c1, 0, &S.full_in[s]);
+        if (ROLE == 2) {  // sweep B: the builders write P
+          mbar_expect_tx(&S.full_in[s], (unsigned)sizeof(S.in[s].st));
+          tma_load_3d(&S.in[s].st[0][0][0], G.mapS, 0, c1, 0, &S.full_in[s]);
+        } else {
+          mbar_expect_tx(&S.full_in[s],
+                         (unsigned)(sizeof(S.in[s].st) + sizeof(S.in[s].p) + (ZERO ? sizeof(S.in[s].q) : 0)));
+          tma_load_3d(&S.in[s].st[0][0][0], G.mapS, 0, c1, 0, &S.full_in[s]);
+          tma_load_3d(&S.in[s].p[0][0][0], G.mapP, 0, c1, 0, &S.full_in[s]);
+          if (ZERO) tma_load_3d(&S.in[s].q[0][0][0], G.mapQ, 0, c1, 0, &S.full_in[s]);
+        }
       }
     }
   } else if (warp == 2 || warp == 3) {  // ---------------- storer (rows 0..R-2) / publisher (row R-1)
@@ -517,13 +577,19 @@ __global__ void __launch_bounds__(32 * gs::kWarps, 1)
       const int s = w % NS;
       mbar_wait(&S.full_out[s], (w / NS) & 1);
       if (!pub) {
-        for (int i = lane; i < (R - 1) * W; i += 32) {
+        // sweep A of a pair also stores the last row, so its stored counter covers every row
+        for (int i = lane; i < (ROLE == 1 ? R : R - 1) * W; i += 32) {
           const int l = i / W, p = i - (i / W) * W;
           if (l >= rows_here) continue;
           const int ix = grid_ix(w, l, p);
           const int j = FWD ? ix : nx - 1 - ix;
           if (j < 0 || j >= nx || ix < 0 || ix >= nx) continue;
           *reinterpret_cast<double2*>(x + 2 * ((size_t)grid_row(l) * nx + ix)) = S.out[s][l][p];
+        }
+        if (ROLE == 1) {
+          __threadfence();
+          __syncwarp();
+          if (lane == 0) st_release(G.stored + band, (G.epoch << 32) | (unsigned long long)(w + 1));
         }
       } else if (R - 1 < rows_here) {
         const int l = R - 1;
@@ -596,18 +662,120 @@ __global__ void __launch_bounds__(32 * gs::kWarps, 1)
       }
       if (lane == 0) flags[band - 1] = 0ull;  // consumed by this band only
     }
-  } else {
-    gs_compute<FWD, ZERO>(S, nx, ngrid, band, rows_here, has_above, dsm_in, crank, nwin, x);
+  } else if (warp == 0) {
+    gs_compute<FWD, ZERO>(S, nx, ngrid, band, rows_here, has_above, dsm_in, crank, nwin, G.xa_src);
+  } else if (ROLE == 2) {  // ---------------- builders: sweep B's P from sweep A's result
+    // P = b - border x_alpha - U x_A (gs_old_eval, CSR order) for the nodes of each
+    // window's box (node index node0 + k (nx - SKEW) + p, like the TMA box; outside
+    // the grid: 0).  Sweep A's stored-window counters gate the reads of x_A: window w
+    // of band b needs A's band b through window w+1 (this row and the next, up to one
+    // column past the window) and A's band b+1 (its first row) through window w-1.
+    // The static half-stencil is prefetched two windows ahead.
+    const int tb = threadIdx.x - kWarps * 32;
+    const int nnodes = nx * ny;
+    const double xa = G.xa_src[ngrid];
+    const int iy0 = band * R, iyb = ny - 1 - band * R;
+    const bool has_item = tb < R * W;
+    const int k = tb / W, p = tb - (tb / W) * W;
+    auto node_of = [&](int w) {
+      const int node0 = FWD ? iy0 * nx + W * w : (iyb - R + 2) * nx - W * (w + 1) + SKEW * (R - 1);
+      return node0 + k * (nx - SKEW) + p;
+    };
+    auto load_half = [&](int w, double (&h)[18]) {
+      const int n = node_of(w);
+      if (has_item && n >= 0 && n < nnodes) {
+        const double2* a2 = reinterpret_cast<const double2*>(G.half_old + (size_t)n * kHalf);
+#pragma unroll
+        for (int i = 0; i < 9; ++i) {
+          const double2 t = a2[i];
+          h[2 * i] = t.x;
+          h[2 * i + 1] = t.y;
+        }
+      }
+    };
+    const unsigned long long tag = G.epoch << 32;
+    unsigned long long seen0 = 0, seen1 = 0;
+    double h0[18], h1[18];
+#pragma unroll
+    for (int i = 0; i < 18; ++i) h0[i] = h1[i] = 0.0;
+    load_half(0, h0);
+    if (nwin > 1) load_half(1, h1);
+    for (int w = 0; w < nwin; ++w) {
+      const int s = w % NS;
+      if (w >= NS) mbar_wait(&S.empty_in[s], ((w / NS) - 1) & 1);
+      if (lane == 0) {
+        const unsigned long long need0 = tag | (unsigned long long)min(w + 2, nwin);
+        while (seen0 < need0) seen0 = ld_acquire(G.stored + band);
+        if (band + 1 < bands) {
+          const unsigned long long need1 = tag | (unsigned long long)min(w, nwin);
+          while (seen1 < need1) seen1 = ld_acquire(G.stored + band + 1);
+        }
+      }
+      __syncwarp();
+      if (has_item) {
+        const int n = node_of(w);
+        double2 pv = make_double2(0.0, 0.0);
+        if (n >= 0 && n < nnodes) {
+          OldIn in;
+#pragma unroll
+          for (int i = 0; i < 18; ++i) in.a[i] = h0[i];
+          gs_old_load_vectors<FWD>(nx, ny, G.b, G.border, G.x_in, n, in);
+          pv = gs_old_eval<FWD>(in, xa);
+        }
+        *reinterpret_cast<double2*>(&S.in[s].p[k][p][0]) = pv;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.full_in[s]);
+#pragma unroll
+      for (int i = 0; i < 18; ++i) h0[i] = h1[i];
+      if (w + 2 < nwin) load_half(w + 2, h1);
+    }
   }
   // no CTA leaves while a cluster peer may still write into its shared memory
   asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
 }
 
+template <bool FWD, bool ZERO>
+__global__ void __launch_bounds__(32 * gs::kWarps, 1)
+    k_gs_tri(int nx, int ny, int ngrid, int pad_nodes, int bands, const __grid_constant__ CUtensorMap mapS,
+             const __grid_constant__ CUtensorMap mapP, const __grid_constant__ CUtensorMap mapQ,
+             double* __restrict__ x, unsigned long long* flags, const int* skip) {
+  if (skip && *skip) return;
+  GsBand G{nx, ny, ngrid, pad_nodes, bands, (int)blockIdx.x, &mapS, &mapP, &mapQ, x, x, flags,
+           nullptr, 0ull, nullptr, nullptr, nullptr, nullptr};
+  gs_band<FWD, ZERO, 0>(G);
+}
+
+// Two consecutive sweeps of one level, pipelined: the first half of the grid
+// (whole clusters) runs sweep A into x1, the second half sweep B into x, each
+// band of B trailing A's bands by about two band lags instead of a whole sweep.
+// flags: [0, G) A's band handoff, [G, 2G) B's, [2G, 3G) A's stored windows.
+template <bool FWD, bool ZERO_A>
+__global__ void __launch_bounds__(32 * gs::kWarpsPair, 1)
+    k_gs_pair(int nx, int ny, int ngrid, int pad_nodes, int bands, const __grid_constant__ CUtensorMap mapSA,
+              const __grid_constant__ CUtensorMap mapPA, const __grid_constant__ CUtensorMap mapQA,
+              const __grid_constant__ CUtensorMap mapSB, double* __restrict__ x1, double* __restrict__ x,
+              unsigned long long* flags, int groups, unsigned long long epoch, const double* __restrict__ b,
+              const double* __restrict__ border, const double* __restrict__ half_old, const int* skip) {
+  if (skip && *skip) return;
+  const int nA = (int)gridDim.x / 2;
+  if ((int)blockIdx.x < nA) {
+    GsBand G{nx, ny, ngrid, pad_nodes, bands, (int)blockIdx.x, &mapSA, &mapPA, &mapQA, x1, x, flags,
+             flags + 2 * groups, epoch, nullptr, nullptr, nullptr, nullptr};
+    gs_band<FWD, ZERO_A, 1>(G);
+  } else {
+    GsBand G{nx, ny, ngrid, pad_nodes, bands, (int)blockIdx.x - nA, &mapSB, &mapSB, &mapSB, x, x, flags + groups,
+             flags + 2 * groups, epoch, b, border, half_old, x1};
+    gs_band<FWD, false, 2>(G);
+  }
+}
+
+
 // warp 0 of k_gs_tri: the wavefront itself
 template <bool FWD, bool ZERO>
 __device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int band, int rows_here, bool has_above,
                                            bool dsm_in, unsigned crank, int nwin,
-                                           double* __restrict__ x) {
+                                           const double* __restrict__ x) {
   using namespace gs;
   const int lane = threadIdx.x & 31;
   auto above_bytes = [&](int a) -> unsigned {
@@ -909,6 +1077,12 @@ static int gs_prepare() {
   VTS_CUDA(cudaFuncSetAttribute(k_gs_tri<true, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   VTS_CUDA(cudaFuncSetAttribute(k_gs_tri<true, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   VTS_CUDA(cudaFuncSetAttribute(k_gs_tri<false, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  VTS_CUDA(cudaFuncSetAttribute(k_gs_pair<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  VTS_CUDA(cudaFuncSetAttribute(k_gs_pair<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  VTS_CUDA(cudaFuncSetAttribute(k_gs_pair<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  VTS_CUDA(cudaFuncSetAttribute(k_gs_pair<true, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  VTS_CUDA(cudaFuncSetAttribute(k_gs_pair<true, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  VTS_CUDA(cudaFuncSetAttribute(k_gs_pair<false, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   if (int rc = tma_encoder()) return rc;
   g_gs_attr_set = true;
   return 0;
@@ -997,6 +1171,95 @@ static int gs_sweep(Ctx* c, int k, const double* b, double* x, bool forward, boo
   return launch_tri<false, false>(c, L, mS, mP, mP, x, skip);
 }
 
+// Two consecutive sweeps of level k as one pipelined launch (k_gs_pair): x <- B(A(x)).
+// Forward pair: A may start from the zero guess (the V-cycle's first pre-smoothing
+// sweep).  Returns 1 (nothing launched) when the 2 x clusters of the grid cannot
+// all be resident at once -- sweep B spins on sweep A, so co-residency is required.
+static int gs_pair(Ctx* c, int k, const double* b, double* x, bool forward, bool zero_a, const int* skip,
+                   bool* launched) {
+  *launched = false;
+  if (int rc = gs_prepare()) return rc;
+  LevelBuf& L = c->lv[k];
+  const int bands = div_up(L.d.ny, gs::R);
+  const int ncl = div_up(bands, 16);
+  const int cs = div_up(bands, ncl);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * cs * ncl);
+  cfg.blockDim = dim3(32 * gs::kWarpsPair);
+  cfg.dynamicSmemBytes = sizeof(gs::Smem);
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  static int max_clusters[17] = {0};
+  if (max_clusters[cs] == 0) {
+    int n = 0;
+    const void* fn = forward ? (zero_a ? (const void*)k_gs_pair<true, true> : (const void*)k_gs_pair<true, false>)
+                             : (const void*)k_gs_pair<false, false>;
+    VTS_CUDA(cudaOccupancyMaxActiveClusters(&n, fn, &cfg));
+    max_clusters[cs] = n > 0 ? n : -1;
+  }
+  if (max_clusters[cs] < 2 * ncl) return 0;  // not all resident: caller runs two sweeps
+  CUtensorMap mSA, mPA, mQA, mSB;
+  const double* solve_half = forward ? L.d.stL : L.d.stU;
+  const double* old_half = forward ? L.d.stU : L.d.stL;
+  if (encode_skewed(&mSA, solve_half, kHalf, L)) return 5;
+  mSB = mSA;
+  const double* pa = b;  // sweep A's box: b (zero guess, with the border box) or P1
+  if (!zero_a) {
+    if (forward)
+      k_gs_old<true><<<div_up(L.d.nnodes, 256), 256, 0, c->stream>>>(L.d.nx, L.d.ny, L.d.ngrid, old_half, b,
+                                                                      L.d.border, x, L.r, skip);
+    else
+      k_gs_old<false><<<div_up(L.d.nnodes, 256), 256, 0, c->stream>>>(L.d.nx, L.d.ny, L.d.ngrid, old_half, b,
+                                                                       L.d.border, x, L.r, skip);
+    VTS_LAUNCHED(c);
+    pa = L.r;
+  }
+  if (encode_skewed(&mPA, pa, 2, L)) return 5;
+  if (encode_skewed(&mQA, zero_a ? L.d.border : pa, 2, L)) return 5;
+  const unsigned long long epoch = ++L.pair_epoch;
+  if (forward && zero_a)
+    VTS_CUDA(cudaLaunchKernelEx(&cfg, k_gs_pair<true, true>, L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, bands, mSA,
+                                mPA, mQA, mSB, L.x1, x, L.gs_flags, L.gs_groups, epoch, b,
+                                (const double*)L.d.border, old_half, skip));
+  else if (forward)
+    VTS_CUDA(cudaLaunchKernelEx(&cfg, k_gs_pair<true, false>, L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, bands, mSA,
+                                mPA, mQA, mSB, L.x1, x, L.gs_flags, L.gs_groups, epoch, b,
+                                (const double*)L.d.border, old_half, skip));
+  else
+    VTS_CUDA(cudaLaunchKernelEx(&cfg, k_gs_pair<false, false>, L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, bands,
+                                mSA, mPA, mQA, mSB, L.x1, x, L.gs_flags, L.gs_groups, epoch, b,
+                                (const double*)L.d.border, old_half, skip));
+  VTS_LAUNCHED(c);
+  *launched = true;
+  return 0;
+}
+
+// VTS_NO_PAIR=1 runs the two sweeps of each pair as separate launches (A/B checks)
+static bool pair_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("VTS_NO_PAIR");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
+// the two sweeps of a smoothing step: pipelined when possible
+static int gs_two_sweeps(Ctx* c, int k, const double* b, double* x, bool forward, bool zero_first, const int* skip) {
+  if (pair_enabled()) {
+    bool launched = false;
+    if (int rc = gs_pair(c, k, b, x, forward, zero_first, skip, &launched)) return rc;
+    if (launched) return 0;
+  }
+  if (int rc = gs_sweep(c, k, b, x, forward, zero_first, skip)) return rc;
+  return gs_sweep(c, k, b, x, forward, false, skip);
+}
+
 #include "bottom.inc.cu"
 
 // VTS_UNFUSED_BOTTOM=1 runs every level through the multi-launch path (A/B checks)
@@ -1021,8 +1284,7 @@ int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
     double* x = (k == top) ? z_top : L.x;
     k_alpha_init<<<1, 1, 0, c->stream>>>(L.d.ngrid, b, x, c->d_corner, k == top ? 1 : 0, skip);
     VTS_LAUNCHED(c);
-    if (int rc = gs_sweep(c, k, b, x, true, true, skip)) return rc;
-    if (int rc = gs_sweep(c, k, b, x, true, false, skip)) return rc;
+    if (int rc = gs_two_sweeps(c, k, b, x, true, true, skip)) return rc;
     if (int rc = level_residual_grid(c, k, x, b, L.r, skip)) return rc;
     LevelBuf& C = c->lv[k - 1];
     k_restrict<<<div_up(C.d.nnodes + 1, 256), 256, 0, c->stream>>>(L.d.nx, L.d.ny, L.d.free_mask, L.r, C.d.nx,
@@ -1048,8 +1310,7 @@ int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
     k_prolong_add<<<div_up(L.d.nnodes + 1, 256), 256, 0, c->stream>>>(L.d.nx, L.d.ny, L.d.free_mask, x, C.d.nx,
                                                                         C.d.ny, C.d.free_mask, C.x, skip);
     VTS_LAUNCHED(c);
-    for (int s = 0; s < 2; ++s)
-      if (int rc = gs_sweep(c, k, b, x, false, false, skip)) return rc;
+    if (int rc = gs_two_sweeps(c, k, b, x, false, false, skip)) return rc;
     if (k == top) {
       const int grid = (int)std::min<long long>(div_up(L.d.ngrid, 256), kReduceGridCap);
       k_alpha_relax<<<grid, 256, 0, c->stream>>>(L.d.ngrid, L.d.border, b, x, c->d_corner, c->partials,

@@ -170,14 +170,15 @@ static int create(Ctx** out, int levels, const int32_t* ex, const int32_t* ey, c
         dalloc_pad(c, &L.d.stL, (size_t)L.d.nnodes * kHalf, L.pad_nodes * kHalf) ||
         dalloc_pad(c, &L.d.stU, (size_t)L.d.nnodes * kHalf, L.pad_nodes * kHalf) ||
         dalloc_pad(c, &L.d.border, ng + 1, 2 * L.pad_nodes) || dalloc_pad(c, &L.b, ng + 1, 2 * L.pad_nodes) ||
-        dalloc_pad(c, &L.x, ng + 1, 2 * L.pad_nodes) || dalloc_pad(c, &L.r, ng + 1, 2 * L.pad_nodes))
+        dalloc_pad(c, &L.x, ng + 1, 2 * L.pad_nodes) || dalloc_pad(c, &L.r, ng + 1, 2 * L.pad_nodes) ||
+        dalloc_pad(c, &L.x1, ng + 1, 2 * L.pad_nodes))
       return fail(VTS_E_CUDA);
     L.gs_groups = div_up(L.d.ny, 8);  // >= bands of any GS row-band height used
-    if (dalloc(&L.gs_flags, L.gs_groups)) return fail(VTS_E_CUDA);
+    if (dalloc(&L.gs_flags, 3 * (size_t)L.gs_groups)) return fail(VTS_E_CUDA);
     if (cudaMemcpy(const_cast<uint8_t*>(L.d.free_mask), mask.data(), ng, cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy(const_cast<int32_t*>(L.d.free2grid), f2g.data(), sizeof(int32_t) * nfree, cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy(L.grid2free, g2f.data(), sizeof(int32_t) * ng, cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemset(L.gs_flags, 0, sizeof(unsigned long long) * L.gs_groups) != cudaSuccess) {
+        cudaMemset(L.gs_flags, 0, sizeof(unsigned long long) * 3 * L.gs_groups) != cudaSuccess) {
       set_error(VTS_E_CUDA, "vts_ctx_create: device upload failed");
       return fail(VTS_E_CUDA);
     }
