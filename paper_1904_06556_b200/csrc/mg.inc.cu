@@ -401,6 +401,7 @@ __global__ void __launch_bounds__(256) k_gs_old(int nx, int ny, int ngrid, const
 
 #ifdef VTS_GS_PROBE
 __device__ long long g_gs_probe[4 * 256];
+__device__ long long g_gs_probe2[2 * 256];
 VTS_DEVICE_INLINE long long gtimer() {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -410,27 +411,48 @@ VTS_DEVICE_INLINE long long gtimer() {
 namespace gs {
 constexpr int R = 16;      // grid rows (compute lanes) per band / CTA
 constexpr int W = 17;      // wavefront steps per window (odd: conflict-free lane stride)
-constexpr int NS = 3;      // window slots in flight (in and out rings)
+#ifndef VTS_GS_NS
+#define VTS_GS_NS 2
+#endif
+constexpr int NS = VTS_GS_NS;  // window slots in flight (in and out rings)
 constexpr int NSA = 4;     // window slots of the previous band's row
 constexpr int SKEW = 2;    // columns between consecutive rows of the wavefront
 constexpr int kWarps = 5;  // compute, loader, storer, publisher, stager
 constexpr int kBuild = 9;  // pipelined pair, sweep B: builder warps (one node of a window's R x W box each)
-constexpr int kWarpsPair = kWarps + kBuild;
+// Pair CTAs have 16 warps.  Warp w runs on SM sub-partition w % 4: the compute
+// warp (0) must keep its sub-partition's issue slots and fp64 pipe, so the
+// builders sit on warps with w % 4 != 0 (5 6 7 9 10 11 13 14 15); warp 8 loads
+// sweep B's x_A boxes (a slow acquire-poll loop), warps 4 and 12 stay light.
+constexpr int kWarpsPair = 16;
+constexpr int kXLoadWarp = 8;
+VTS_DEVICE_INLINE int builder_index(int warp) {  // -1: not a builder warp
+  return (warp < kWarps || (warp & 3) == 0) ? -1 : (warp - kWarps) - (warp - kWarps + 1) / 4;
+}
 // one window slot = three TMA boxes: R rows x W nodes x {22 stencil, 2 P, 2 border} doubles
 struct __align__(128) InSlot {
   double st[R][W][kHalf];
-  double p[R][W][2];
-  double q[R][W][2];
+  double p[R][W][2];   // P (TMA box, or written by sweep B's builders)
+  double q[R][W][2];   // border (zero-guess sweeps, sweep B)
+  double b[R][W][2];   // sweep B: right-hand side
+  double xb[R + 1][W + 3][2];  // sweep B: sweep A's result around the window (rows +1, columns +3)
+  double xb_pad[8];
+  double u[R][W][18];  // sweep B: the old-value half-stencil (18 of its 22 doubles)
 };
 struct Smem {
   InSlot in[NS];
   double2 out[NS][R][W];
   double2 above[NSA][W];
   unsigned long long full_in[NS], empty_in[NS], full_out[NS], empty_out[NS];
+  unsigned long long loaded[NS];     // sweep B: the slot's static TMA boxes have landed (builders wait)
+  unsigned long long xloaded[NS];    // sweep B: the slot's x_A box has landed (builders wait)
+  unsigned stored_cnt;                // sweep A: windows x {storer, publisher} whose stores are issued
   unsigned long long full_above[NSA], empty_above[NSA];
   int armed;  // (producer side) highest above-ring chunk the consumer has armed
 };
-static_assert(sizeof(InSlot) % 128 == 0, "TMA destinations must stay 128-B aligned");
+static_assert(sizeof(InSlot) % 128 == 0 && offsetof(InSlot, p) % 128 == 0 && offsetof(InSlot, q) % 128 == 0 &&
+                  offsetof(InSlot, b) % 128 == 0 && offsetof(InSlot, xb) % 128 == 0 &&
+                  offsetof(InSlot, u) % 128 == 0,
+              "TMA destinations must stay 128-B aligned");
 static_assert(((W * kHalf * 8) / 16) % 2 == 1, "lane stride must be an odd multiple of 16 B");
 }  // namespace gs
 
@@ -466,7 +488,10 @@ struct GsBand {
   int nx, ny, ngrid, pad_nodes, bands, band;
   const CUtensorMap* mapS;  // half-stencil the wavefront solves with
   const CUtensorMap* mapP;  // P (ROLE 0/1), b (ZERO)
-  const CUtensorMap* mapQ;  // border (ZERO)
+  const CUtensorMap* mapQ;  // border (ZERO, sweep B)
+  const CUtensorMap* mapB;  // sweep B: right-hand side b
+  const CUtensorMap* mapX;  // sweep B: sweep A's result, (R + 1) x (W + 3) box
+  const CUtensorMap* mapU;  // sweep B: old-value half-stencil, 18-double box
   double* x;                // the sweep's result
   const double* xa_src;     // bordered vector holding x_alpha (slot ngrid)
   unsigned long long* flags;   // band-to-band handoff counters of this sweep
@@ -508,8 +533,10 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
-      mbar_init(&S.full_in[s], ROLE == 2 ? 1 + kBuild : 1);  // sweep B: + one arrive per builder warp
+      mbar_init(&S.full_in[s], ROLE == 2 ? kBuild : 1);  // sweep B: one arrive per builder warp
       mbar_init(&S.empty_in[s], 1);
+      mbar_init(&S.loaded[s], 1);
+      mbar_init(&S.xloaded[s], 1);
       mbar_init(&S.full_out[s], 1);
       mbar_init(&S.empty_out[s], 2);
     }
@@ -518,6 +545,7 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
       mbar_init(&S.empty_above[s], 1);
     }
     S.armed = NSA - 1;  // the consumer arms above slots 0 .. NSA-1 before the first cluster barrier
+    S.stored_cnt = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (dsm_in) {
       for (int a = 0; a < NSA && a <= nwin; ++a) mbar_expect_tx(&S.full_above[a], above_bytes(a));
@@ -552,9 +580,15 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
         // node index of box element (p = 0, box row 0)
         const int node0 = FWD ? iy0 * nx + W * w : (iyb - R + 2) * nx - W * (w + 1) + SKEW * (R - 1);
         const int c1 = node0 + pad_nodes;
-        if (ROLE == 2) {  // sweep B: the builders write P
-          mbar_expect_tx(&S.full_in[s], (unsigned)sizeof(S.in[s].st));
-          tma_load_3d(&S.in[s].st[0][0][0], G.mapS, 0, c1, 0, &S.full_in[s]);
+        if (ROLE == 2) {
+          // sweep B: the static boxes (stencil, b, border) as soon as the slot is free;
+          // the x_A box comes from the x-loader warp once sweep A has stored it
+          mbar_expect_tx(&S.loaded[s], (unsigned)(sizeof(S.in[s].st) + sizeof(S.in[s].q) + sizeof(S.in[s].b) +
+                                                  sizeof(S.in[s].u)));
+          tma_load_3d(&S.in[s].st[0][0][0], G.mapS, 0, c1, 0, &S.loaded[s]);
+          tma_load_3d(&S.in[s].u[0][0][0], G.mapU, 0, c1, 0, &S.loaded[s]);
+          tma_load_3d(&S.in[s].q[0][0][0], G.mapQ, 0, c1, 0, &S.loaded[s]);
+          tma_load_3d(&S.in[s].b[0][0][0], G.mapB, 0, c1, 0, &S.loaded[s]);
         } else {
           mbar_expect_tx(&S.full_in[s],
                          (unsigned)(sizeof(S.in[s].st) + sizeof(S.in[s].p) + (ZERO ? sizeof(S.in[s].q) : 0)));
@@ -578,7 +612,7 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
       mbar_wait(&S.full_out[s], (w / NS) & 1);
       if (!pub) {
         // sweep A of a pair also stores the last row, so its stored counter covers every row
-        for (int i = lane; i < (ROLE == 1 ? R : R - 1) * W; i += 32) {
+        for (int i = lane; i < (R - 1) * W; i += 32) {
           const int l = i / W, p = i - (i / W) * W;
           if (l >= rows_here) continue;
           const int ix = grid_ix(w, l, p);
@@ -586,11 +620,7 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
           if (j < 0 || j >= nx || ix < 0 || ix >= nx) continue;
           *reinterpret_cast<double2*>(x + 2 * ((size_t)grid_row(l) * nx + ix)) = S.out[s][l][p];
         }
-        if (ROLE == 1) {
-          __threadfence();
-          __syncwarp();
-          if (lane == 0) st_release(G.stored + band, (G.epoch << 32) | (unsigned long long)(w + 1));
-        }
+
       } else if (R - 1 < rows_here) {
         const int l = R - 1;
         if (lane < W) {
@@ -633,7 +663,11 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&S.empty_out[s]);
+      if (lane == 0) {
+        if (ROLE == 1)  // this warp's part of window w is issued to global memory
+          asm volatile("red.release.cta.shared::cta.add.u32 [%0], 1;" ::"r"(smem_u32(&S.stored_cnt)) : "memory");
+        mbar_arrive(&S.empty_out[s]);
+      }
     }
   } else if (warp == 4) {  // ---------------- stager (previous band's last row -> above ring)
     if (has_above && rows_here > 0 && !dsm_in) {
@@ -663,15 +697,52 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
       if (lane == 0) flags[band - 1] = 0ull;  // consumed by this band only
     }
   } else if (warp == 0) {
-    gs_compute<FWD, ZERO>(S, nx, ngrid, band, rows_here, has_above, dsm_in, crank, nwin, G.xa_src);
-  } else if (ROLE == 2) {  // ---------------- builders: sweep B's P from sweep A's result
+    gs_compute<FWD, ZERO>(S, nx, ngrid, band + (ROLE == 2 ? 128 : 0), rows_here, has_above, dsm_in, crank, nwin,
+                          G.xa_src);  // (band only labels the probe timeline)
+  } else if (ROLE == 1 && warp == kWarps) {  // ---------------- sweep A: stored-window counter
+    // storer and publisher count their issued windows in stored_cnt (release, CTA
+    // scope; a counter, not an mbarrier: nothing gates them on this warp, so they can
+    // run a whole ring ahead); the release here (gpu scope, cumulative over what this
+    // warp acquired) publishes them to sweep B without stalling the storer on the drain
+    for (int w = 0; w < nwin; ++w) {
+      unsigned cnt = 0;
+      do {
+        asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(cnt) : "r"(smem_u32(&S.stored_cnt)) : "memory");
+      } while (cnt < 2u * (unsigned)(w + 1));
+      __threadfence();
+      if (lane == 0) st_release(G.stored + band, (G.epoch << 32) | (unsigned long long)(w + 1));
+    }
+  } else if (ROLE == 2 && warp == kXLoadWarp) {  // ---------------- sweep B: x_A box loader
+    // window w's box of sweep A's result (rows of the window and the next, up to 3
+    // columns past it) may be read once A's band stored through window w+1 and A's
+    // next band (its first row) through window w-1
+    if (lane == 0) {
+      const unsigned long long tag = G.epoch << 32;
+      const int iy0 = band * R, iyb = ny - 1 - band * R;
+      for (int w = 0; w < nwin; ++w) {
+        const int s = w % NS;
+        if (w >= NS) mbar_wait(&S.empty_in[s], ((w / NS) - 1) & 1);
+        while (ld_acquire(G.stored + band) < (tag | (unsigned long long)min(w + 2, nwin))) {
+        }
+        if (band + 1 < bands)
+          while (ld_acquire(G.stored + band + 1) < (tag | (unsigned long long)min(w, nwin))) {
+          }
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // A's generic stores -> this TMA read
+        const int node0 = FWD ? iy0 * nx + W * w : (iyb - R + 2) * nx - W * (w + 1) + SKEW * (R - 1);
+        const int c1 = node0 + pad_nodes;
+        const int cx = FWD ? c1 : c1 - (nx - SKEW) - 3;  // backward: one row and 3 nodes earlier
+        mbar_expect_tx(&S.xloaded[s], (unsigned)sizeof(S.in[s].xb));
+        tma_load_3d(&S.in[s].xb[0][0][0], G.mapX, 0, cx, 0, &S.xloaded[s]);
+      }
+    }
+  } else if (ROLE == 2 && builder_index(warp) >= 0) {  // ---------------- builders: sweep B's P from A's result
     // P = b - border x_alpha - U x_A (gs_old_eval, CSR order) for the nodes of each
-    // window's box (node index node0 + k (nx - SKEW) + p, like the TMA box; outside
-    // the grid: 0).  Sweep A's stored-window counters gate the reads of x_A: window w
-    // of band b needs A's band b through window w+1 (this row and the next, up to one
-    // column past the window) and A's band b+1 (its first row) through window w-1.
-    // The static half-stencil is prefetched two windows ahead.
-    const int tb = threadIdx.x - kWarps * 32;
+    // window's box, all from the slot's TMA boxes (U, b, border, x_A around the window):
+    // loads through the SM's LSU here would slow the compute warp's shared-memory
+    // loads and shuffles, which sit on its critical chain.
+    // Box neighbours outside the grid read real wrapped nodes or padding zeros where
+    // the multi-launch pass reads 0; their couplings are exact zeros either way.
+    const int tb = builder_index(warp) * 32 + lane;
     const int nnodes = nx * ny;
     const double xa = G.xa_src[ngrid];
     const int iy0 = band * R, iyb = ny - 1 - band * R;
@@ -681,55 +752,39 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
       const int node0 = FWD ? iy0 * nx + W * w : (iyb - R + 2) * nx - W * (w + 1) + SKEW * (R - 1);
       return node0 + k * (nx - SKEW) + p;
     };
-    auto load_half = [&](int w, double (&h)[18]) {
-      const int n = node_of(w);
-      if (has_item && n >= 0 && n < nnodes) {
-        const double2* a2 = reinterpret_cast<const double2*>(G.half_old + (size_t)n * kHalf);
-#pragma unroll
-        for (int i = 0; i < 9; ++i) {
-          const double2 t = a2[i];
-          h[2 * i] = t.x;
-          h[2 * i + 1] = t.y;
-        }
-      }
-    };
-    const unsigned long long tag = G.epoch << 32;
-    unsigned long long seen0 = 0, seen1 = 0;
-    double h0[18], h1[18];
-#pragma unroll
-    for (int i = 0; i < 18; ++i) h0[i] = h1[i] = 0.0;
-    load_half(0, h0);
-    if (nwin > 1) load_half(1, h1);
-    for (int w = 0; w < nwin; ++w) {
+    // box coordinates of the node (C) and of its later neighbours NE N NW E (slots 0..3)
+    const int ck = FWD ? k : k + 1, cp = FWD ? p : p + 3;
+    const int nk[4] = {FWD ? k + 1 : k, FWD ? k + 1 : k, FWD ? k + 1 : k, ck};
+    const int np[4] = {FWD ? p + 3 : p, FWD ? p + 2 : p + 1, FWD ? p + 1 : p + 2, FWD ? p + 1 : p + 2};
+    auto build = [&](int w) {
       const int s = w % NS;
-      if (w >= NS) mbar_wait(&S.empty_in[s], ((w / NS) - 1) & 1);
-      if (lane == 0) {
-        const unsigned long long need0 = tag | (unsigned long long)min(w + 2, nwin);
-        while (seen0 < need0) seen0 = ld_acquire(G.stored + band);
-        if (band + 1 < bands) {
-          const unsigned long long need1 = tag | (unsigned long long)min(w, nwin);
-          while (seen1 < need1) seen1 = ld_acquire(G.stored + band + 1);
-        }
-      }
-      __syncwarp();
+      mbar_wait(&S.loaded[s], (w / NS) & 1);
+      mbar_wait(&S.xloaded[s], (w / NS) & 1);
       if (has_item) {
         const int n = node_of(w);
         double2 pv = make_double2(0.0, 0.0);
         if (n >= 0 && n < nnodes) {
-          OldIn in;
+          const InSlot& in = S.in[s];
+          OldIn o;
 #pragma unroll
-          for (int i = 0; i < 18; ++i) in.a[i] = h0[i];
-          gs_old_load_vectors<FWD>(nx, ny, G.b, G.border, G.x_in, n, in);
-          pv = gs_old_eval<FWD>(in, xa);
+          for (int i = 0; i < 18; i += 2) {
+            const double2 t = *reinterpret_cast<const double2*>(&in.u[k][p][i]);
+            o.a[i] = t.x;
+            o.a[i + 1] = t.y;
+          }
+          o.bv = *reinterpret_cast<const double2*>(&in.b[k][p][0]);
+          o.dv = *reinterpret_cast<const double2*>(&in.q[k][p][0]);
+          o.xo = *reinterpret_cast<const double2*>(&in.xb[ck][cp][0]);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) o.v[q] = *reinterpret_cast<const double2*>(&in.xb[nk[q]][np[q]][0]);
+          pv = gs_old_eval<FWD>(o, xa);
         }
         *reinterpret_cast<double2*>(&S.in[s].p[k][p][0]) = pv;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.full_in[s]);
-#pragma unroll
-      for (int i = 0; i < 18; ++i) h0[i] = h1[i];
-      if (w + 2 < nwin) load_half(w + 2, h1);
-    }
+    };
+    for (int w = 0; w < nwin; ++w) build(w);
   }
   // no CTA leaves while a cluster peer may still write into its shared memory
   asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
@@ -741,7 +796,7 @@ __global__ void __launch_bounds__(32 * gs::kWarps, 1)
              const __grid_constant__ CUtensorMap mapP, const __grid_constant__ CUtensorMap mapQ,
              double* __restrict__ x, unsigned long long* flags, const int* skip) {
   if (skip && *skip) return;
-  GsBand G{nx, ny, ngrid, pad_nodes, bands, (int)blockIdx.x, &mapS, &mapP, &mapQ, x, x, flags,
+  GsBand G{nx, ny, ngrid, pad_nodes, bands, (int)blockIdx.x, &mapS, &mapP, &mapQ, &mapQ, &mapQ, &mapQ, x, x, flags,
            nullptr, 0ull, nullptr, nullptr, nullptr, nullptr};
   gs_band<FWD, ZERO, 0>(G);
 }
@@ -754,18 +809,25 @@ template <bool FWD, bool ZERO_A>
 __global__ void __launch_bounds__(32 * gs::kWarpsPair, 1)
     k_gs_pair(int nx, int ny, int ngrid, int pad_nodes, int bands, const __grid_constant__ CUtensorMap mapSA,
               const __grid_constant__ CUtensorMap mapPA, const __grid_constant__ CUtensorMap mapQA,
-              const __grid_constant__ CUtensorMap mapSB, double* __restrict__ x1, double* __restrict__ x,
+              const __grid_constant__ CUtensorMap mapSB, const __grid_constant__ CUtensorMap mapBB,
+              const __grid_constant__ CUtensorMap mapQB, const __grid_constant__ CUtensorMap mapXB,
+              const __grid_constant__ CUtensorMap mapUB,
+              double* __restrict__ x1, double* __restrict__ x,
               unsigned long long* flags, int groups, unsigned long long epoch, const double* __restrict__ b,
               const double* __restrict__ border, const double* __restrict__ half_old, const int* skip) {
   if (skip && *skip) return;
   const int nA = (int)gridDim.x / 2;
   if ((int)blockIdx.x < nA) {
-    GsBand G{nx, ny, ngrid, pad_nodes, bands, (int)blockIdx.x, &mapSA, &mapPA, &mapQA, x1, x, flags,
+    GsBand G{nx, ny, ngrid, pad_nodes, bands, (int)blockIdx.x, &mapSA, &mapPA, &mapQA, &mapQA, &mapQA, &mapQA, x1, x,
+             flags,
              flags + 2 * groups, epoch, nullptr, nullptr, nullptr, nullptr};
     gs_band<FWD, ZERO_A, 1>(G);
   } else {
-    GsBand G{nx, ny, ngrid, pad_nodes, bands, (int)blockIdx.x - nA, &mapSB, &mapSB, &mapSB, x, x, flags + groups,
-             flags + 2 * groups, epoch, b, border, half_old, x1};
+#ifdef VTS_PAIR_NO_B
+    return;  // probe builds only: time sweep A alone inside the pair launch
+#endif
+    GsBand G{nx, ny, ngrid, pad_nodes, bands, (int)blockIdx.x - nA, &mapSB, &mapSB, &mapQB, &mapBB, &mapXB, &mapUB, x, x,
+             flags + groups, flags + 2 * groups, epoch, b, border, half_old, x1};
     gs_band<FWD, false, 2>(G);
   }
 }
@@ -814,13 +876,24 @@ __device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int b
     }
   }
 #ifdef VTS_GS_PROBE
-  long long t_first = 0, t_wait_above = 0;
+  long long t_first = 0, t_wait_above = 0, t_wait_in = 0, t_wait_out = 0;
   if (l == 0) g_gs_probe[4 * band] = gtimer();
 #endif
   for (int w = 0; w < nwin; ++w) {
     const int s = w % NS;
+#ifdef VTS_GS_PROBE
+    {
+      const long long t0 = gtimer();
+      mbar_wait(&S.full_in[s], (w / NS) & 1);
+      const long long t1 = gtimer();
+      if (w >= NS) mbar_wait(&S.empty_out[s], ((w / NS) - 1) & 1);
+      t_wait_in += t1 - t0;
+      t_wait_out += gtimer() - t1;
+    }
+#else
     mbar_wait(&S.full_in[s], (w / NS) & 1);
     if (w >= NS) mbar_wait(&S.empty_out[s], ((w / NS) - 1) & 1);
+#endif
     const int sa = (w + 1) % NSA;
 #ifdef VTS_GS_PROBE
     const long long tw0 = gtimer();
@@ -933,6 +1006,8 @@ __device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int b
     g_gs_probe[4 * band + 1] = t_first;
     g_gs_probe[4 * band + 2] = gtimer();
     g_gs_probe[4 * band + 3] = t_wait_above;
+    g_gs_probe2[2 * band] = t_wait_in;
+    g_gs_probe2[2 * band + 1] = t_wait_out;
   }
 #endif
 }
@@ -1091,11 +1166,12 @@ static int gs_prepare() {
 // 3-D map over a padded node array of `width` doubles per node: dims {width,
 // nodes incl. padding, R rows}, strides {width, (nx - SKEW) * width} doubles,
 // box {width, W, R}.  `data` points at node 0 (pad_nodes nodes precede it).
-static int encode_skewed(CUtensorMap* map, const double* data, int width, const LevelBuf& L) {
+static int encode_skewed(CUtensorMap* map, const double* data, int width, const LevelBuf& L, int rows = gs::R,
+                         int cols = gs::W, int box_width = 0) {
   const cuuint64_t nodes = (cuuint64_t)(L.d.nnodes + 2 * L.pad_nodes);
-  const cuuint64_t dims[3] = {(cuuint64_t)width, nodes, (cuuint64_t)gs::R};
+  const cuuint64_t dims[3] = {(cuuint64_t)width, nodes, (cuuint64_t)rows};
   const cuuint64_t strides[2] = {(cuuint64_t)width * 8, (cuuint64_t)(L.d.nx - gs::SKEW) * width * 8};
-  const cuuint32_t box[3] = {(cuuint32_t)width, (cuuint32_t)gs::W, (cuuint32_t)gs::R};
+  const cuuint32_t box[3] = {(cuuint32_t)(box_width ? box_width : width), (cuuint32_t)cols, (cuuint32_t)rows};
   const cuuint32_t estr[3] = {1, 1, 1};
   void* base = const_cast<double*>(data - L.pad_nodes * width);
   const CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
@@ -1204,11 +1280,14 @@ static int gs_pair(Ctx* c, int k, const double* b, double* x, bool forward, bool
     max_clusters[cs] = n > 0 ? n : -1;
   }
   if (max_clusters[cs] < 2 * ncl) return 0;  // not all resident: caller runs two sweeps
-  CUtensorMap mSA, mPA, mQA, mSB;
+  CUtensorMap mSA, mPA, mQA, mSB, mBB, mQB, mXB, mUB;
   const double* solve_half = forward ? L.d.stL : L.d.stU;
   const double* old_half = forward ? L.d.stU : L.d.stL;
   if (encode_skewed(&mSA, solve_half, kHalf, L)) return 5;
   mSB = mSA;
+  if (encode_skewed(&mBB, b, 2, L) || encode_skewed(&mQB, L.d.border, 2, L) ||
+      encode_skewed(&mXB, L.x1, 2, L, gs::R + 1, gs::W + 3) || encode_skewed(&mUB, old_half, kHalf, L, gs::R, gs::W, 18))
+    return 5;
   const double* pa = b;  // sweep A's box: b (zero guess, with the border box) or P1
   if (!zero_a) {
     if (forward)
@@ -1225,15 +1304,15 @@ static int gs_pair(Ctx* c, int k, const double* b, double* x, bool forward, bool
   const unsigned long long epoch = ++L.pair_epoch;
   if (forward && zero_a)
     VTS_CUDA(cudaLaunchKernelEx(&cfg, k_gs_pair<true, true>, L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, bands, mSA,
-                                mPA, mQA, mSB, L.x1, x, L.gs_flags, L.gs_groups, epoch, b,
+                                mPA, mQA, mSB, mBB, mQB, mXB, mUB, L.x1, x, L.gs_flags, L.gs_groups, epoch, b,
                                 (const double*)L.d.border, old_half, skip));
   else if (forward)
     VTS_CUDA(cudaLaunchKernelEx(&cfg, k_gs_pair<true, false>, L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, bands, mSA,
-                                mPA, mQA, mSB, L.x1, x, L.gs_flags, L.gs_groups, epoch, b,
+                                mPA, mQA, mSB, mBB, mQB, mXB, mUB, L.x1, x, L.gs_flags, L.gs_groups, epoch, b,
                                 (const double*)L.d.border, old_half, skip));
   else
     VTS_CUDA(cudaLaunchKernelEx(&cfg, k_gs_pair<false, false>, L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, bands,
-                                mSA, mPA, mQA, mSB, L.x1, x, L.gs_flags, L.gs_groups, epoch, b,
+                                mSA, mPA, mQA, mSB, mBB, mQB, mXB, mUB, L.x1, x, L.gs_flags, L.gs_groups, epoch, b,
                                 (const double*)L.d.border, old_half, skip));
   VTS_LAUNCHED(c);
   *launched = true;

@@ -87,6 +87,27 @@ int main(int argc, char** argv) {
              (pr[4 * b] - t0) / 1e3, (pr[4 * b + 1] - t0) / 1e3, (pr[4 * b + 2] - t0) / 1e3,
              (pr[4 * b + 2] - pr[4 * b + 1]) / 1e3, pr[4 * b + 3] / 1e3);
   }
+  {  // pair timeline: sweep A bands (probe slots 0..) and sweep B bands (128..)
+    vts::LevelBuf& L = c->lv[levels - 1];
+    vts::gs_two_sweeps(c, levels - 1, L.b, L.x, false, false, nullptr);
+    cudaDeviceSynchronize();
+    std::vector<long long> pr(4 * 256);
+    cudaMemcpyFromSymbol(pr.data(), vts::g_gs_probe, pr.size() * 8);
+    std::vector<long long> pr2(2 * 256);
+    cudaMemcpyFromSymbol(pr2.data(), vts::g_gs_probe2, pr2.size() * 8);
+    const int bands = (L.d.ny + vts::gs::R - 1) / vts::gs::R;
+    long long t0 = pr[0];
+    printf("pair timeline (bwd pair, finest):\n");
+    for (int b : {0, 1, 2, 10, 11, 16, 22, 32}) {
+      if (b >= bands) continue;
+      for (int role = 0; role < 2; ++role) {
+        const int i = b + 128 * role;
+        printf("  %s band %2d: start %7.1f  first-window %7.1f  end %7.1f  (dur %6.1f, waiting-above %6.1f, in %6.1f, out %6.1f)\n",
+               role ? "B" : "A", b, (pr[4 * i] - t0) / 1e3, (pr[4 * i + 1] - t0) / 1e3, (pr[4 * i + 2] - t0) / 1e3,
+               (pr[4 * i + 2] - pr[4 * i + 1]) / 1e3, pr[4 * i + 3] / 1e3, pr2[2 * i] / 1e3, pr2[2 * i + 1] / 1e3);
+      }
+    }
+  }
 #endif
   double* xin = c->fvec[10];
   double* yout = c->fvec[11];
