@@ -69,14 +69,19 @@ def algorithmic_bytes(prob) -> dict:
     # half-stencil it solves with, the 2-double right-hand side P, the 2-double result
     fine = lv[-1]
     A_tri = fine.nx * fine.ny * 8 * (20 + 2 + 2)
-    return dict(phi=A_phi, apply=A_ap, vcycle=A_V, minres_iter=A_MR, gs_fine_sweep=A_gs, gs_tri_fine=A_tri)
+    # one finest-level sweep pair (k_gs_pair): sweep A as above; sweep B reads the
+    # 20-double half-stencil, 18 doubles of the other half, b, border and sweep A's
+    # result, and writes its own result
+    A_pair = A_tri + fine.nx * fine.ny * 8 * (20 + 18 + 2 + 2 + 2 + 2)
+    return dict(phi=A_phi, apply=A_ap, vcycle=A_V, minres_iter=A_MR, gs_fine_sweep=A_gs, gs_tri_fine=A_tri,
+                gs_pair_fine=A_pair)
 
 
-def ncu_traffic():
-    """dram bytes per finest-level k_gs_tri launch from the committed ncu --set full capture."""
+def ncu_traffic(kernel: str = "k_gs_tri"):
+    """dram bytes per finest-level launch of `kernel` from the committed ncu --set full capture."""
     import csv
 
-    path = os.path.join(REPO, "profiles", "r01_ncu_full_k_gs_tri_fine_raw_subset.csv")
+    path = os.path.join(REPO, "profiles", f"r01_ncu_full_{kernel}_fine_raw_subset.csv")
     try:
         with open(path) as fh:
             rows = list(csv.reader(fh))
@@ -300,7 +305,7 @@ def main() -> None:
     # --- profiling pass (not the timed value): the same K iterations with every
     # wavefront launch bracketed by CUDA events on the context stream, giving the
     # dominant kernel's average launch time and its share of the step
-    prof = (ctypes.c_double * 4)()
+    prof = (ctypes.c_double * 6)()
     p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     _lib.check(lib.vts_profile_begin(ops.handle), "vts_profile_begin")
     p0.record(stream)
@@ -308,7 +313,7 @@ def main() -> None:
     p1.record(stream)
     _lib.check(lib.vts_profile_end(ops.handle, prof), "vts_profile_end")
     prof_region_ms = p0.elapsed_time(p1)
-    tri_total_ms, tri_n, tri_fine_ms, tri_fine_n = list(prof)
+    gs_total_ms, gs_n, tri_fine_ms, tri_fine_n, pair_fine_ms, pair_fine_n = list(prof)
 
     # --- e2e through the C-ABI with host buffers (pinned), copies inside the timed region
     rhs_host = torch.as_tensor(rhs_h).pin_memory()
@@ -338,11 +343,16 @@ def main() -> None:
     def gbs(nbytes, ms):
         return nbytes / (ms * 1e-3) / 1e9
 
-    # dominant kernel of the MINRES iteration: the wavefront Gauss-Seidel kernel
-    # k_gs_tri (~75 % of the step); roofline unit = one finest-level launch
-    tri_fine_avg_ms = tri_fine_ms / max(tri_fine_n, 1.0)
-    achieved = gbs(bytes_["gs_tri_fine"], tri_fine_avg_ms)
-    traffic = ncu_traffic()
+    # dominant kernel of the MINRES iteration: the wavefront Gauss-Seidel kernel,
+    # k_gs_pair (both sweeps of a smoothing step) when the pipelined pairs ran,
+    # else k_gs_tri; roofline unit = one finest-level launch
+    if pair_fine_n > 0:
+        dom, dom_bytes, dom_ms, dom_n = "k_gs_pair", bytes_["gs_pair_fine"], pair_fine_ms, pair_fine_n
+    else:
+        dom, dom_bytes, dom_ms, dom_n = "k_gs_tri", bytes_["gs_tri_fine"], tri_fine_ms, tri_fine_n
+    dom_avg_ms = dom_ms / max(dom_n, 1.0)
+    achieved = gbs(dom_bytes, dom_avg_ms)
+    traffic = ncu_traffic(dom)
     pbm = None
     if not args.no_pbm and rank == 0:
         t_p = time.perf_counter()
@@ -370,12 +380,13 @@ def main() -> None:
                 "d2h_bytes_per_step": 8 * (n + 1) / args.steps,
                 "note": "one C-ABI vts_minres call of K iterations; RHS H2D and solution D2H once per call"},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "hbm", "kernel": "k_gs_tri, finest level (1025x513 wavefront sweep)",
+        "roofline": {"bound": "hbm", "kernel": f"{dom}, finest level (1025x513 wavefront"
+                                                 f"{' sweep pair' if dom == 'k_gs_pair' else ' sweep'})",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "frac_of_8TBs": achieved / 8000.0, "traffic": traffic, "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": bytes_["gs_tri_fine"], "launch_ms": tri_fine_avg_ms,
-                     "launches_in_profiled_region": int(tri_n), "finest_launches": int(tri_fine_n),
-                     "share_of_step": tri_total_ms / prof_region_ms,
+                     "algorithmic_bytes_per_launch": dom_bytes, "launch_ms": dom_avg_ms,
+                     "launches_in_profiled_region": int(gs_n), "finest_launches": int(dom_n),
+                     "share_of_step": gs_total_ms / prof_region_ms,
                      "note": "latency-bound: a sweep is a wavefront of nx + 2 ny dependent steps "
                              "(DESIGN.md, 'Gauss-Seidel depth'); traffic from profiles/ ncu --set full"},
         "kernels": {

@@ -195,12 +195,13 @@ int64_t vts_kernel_launches(const vts_ctx* ctx);
 
 /*
  * Profiling helper (no reference counterpart): between vts_profile_begin and
- * vts_profile_end every launch of the wavefront Gauss-Seidel kernel is
- * bracketed by a CUDA event pair on the context stream.  vts_profile_end
- * synchronises the stream and writes HOST out[4] = {total ms of those
- * launches, number of launches, ms of the finest-level launches, number of
- * finest-level launches}.  Used by bench.py for the dominant kernel's share
- * of a MINRES iteration; costs two event records per sweep while enabled.
+ * vts_profile_end every launch of a wavefront Gauss-Seidel kernel (a single
+ * sweep, or a pipelined pair of sweeps) is bracketed by a CUDA event pair on
+ * the context stream.  vts_profile_end synchronises the stream and writes
+ * HOST out[6] = {total ms of those launches, number of launches, ms and count
+ * of the finest-level single-sweep launches, ms and count of the finest-level
+ * pair launches}.  Used by bench.py for the dominant kernel's share of a
+ * MINRES iteration; costs two event records per launch while enabled.
  */
 int vts_profile_begin(vts_ctx* ctx);
 int vts_profile_end(vts_ctx* ctx, double* out);

@@ -1184,6 +1184,23 @@ static int encode_skewed(CUtensorMap* map, const double* data, int width, const 
   return 0;
 }
 
+// optional per-launch event pair around a wavefront launch (vts_profile_begin/end)
+static int prof_begin(Ctx* c, const LevelBuf& L, int pair, Ctx::ProfEv** pe) {
+  *pe = nullptr;
+  if (!c->prof) return 0;
+  if (c->prof_used == c->prof_ev.size()) {
+    Ctx::ProfEv e{};
+    VTS_CUDA(cudaEventCreate(&e.a));
+    VTS_CUDA(cudaEventCreate(&e.b));
+    c->prof_ev.push_back(e);
+  }
+  *pe = &c->prof_ev[c->prof_used++];
+  (*pe)->level = (int)(&L - c->lv.data());
+  (*pe)->pair = pair;
+  VTS_CUDA(cudaEventRecord((*pe)->a, c->stream));
+  return 0;
+}
+
 // launch the wavefront on `bands` row bands, grouped in clusters of <= 16 CTAs
 template <bool FWD, bool ZERO>
 static int launch_tri(Ctx* c, LevelBuf& L, const CUtensorMap& mS, const CUtensorMap& mP, const CUtensorMap& mQ,
@@ -1204,17 +1221,7 @@ static int launch_tri(Ctx* c, LevelBuf& L, const CUtensorMap& mS, const CUtensor
   cfg.attrs = at;
   cfg.numAttrs = 1;
   Ctx::ProfEv* pe = nullptr;
-  if (c->prof) {
-    if (c->prof_used == c->prof_ev.size()) {
-      Ctx::ProfEv e{};
-      VTS_CUDA(cudaEventCreate(&e.a));
-      VTS_CUDA(cudaEventCreate(&e.b));
-      c->prof_ev.push_back(e);
-    }
-    pe = &c->prof_ev[c->prof_used++];
-    pe->level = (int)(&L - c->lv.data());
-    VTS_CUDA(cudaEventRecord(pe->a, c->stream));
-  }
+  if (int rc = prof_begin(c, L, 0, &pe)) return rc;
   VTS_CUDA(cudaLaunchKernelEx(&cfg, k_gs_tri<FWD, ZERO>, L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, bands, mS, mP,
                               mQ, x, L.gs_flags, skip));
   VTS_LAUNCHED(c);
@@ -1302,6 +1309,8 @@ static int gs_pair(Ctx* c, int k, const double* b, double* x, bool forward, bool
   if (encode_skewed(&mPA, pa, 2, L)) return 5;
   if (encode_skewed(&mQA, zero_a ? L.d.border : pa, 2, L)) return 5;
   const unsigned long long epoch = ++L.pair_epoch;
+  Ctx::ProfEv* pe = nullptr;
+  if (int rc = prof_begin(c, L, 1, &pe)) return rc;
   if (forward && zero_a)
     VTS_CUDA(cudaLaunchKernelEx(&cfg, k_gs_pair<true, true>, L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, bands, mSA,
                                 mPA, mQA, mSB, mBB, mQB, mXB, mUB, L.x1, x, L.gs_flags, L.gs_groups, epoch, b,
@@ -1315,6 +1324,7 @@ static int gs_pair(Ctx* c, int k, const double* b, double* x, bool forward, bool
                                 mSA, mPA, mQA, mSB, mBB, mQB, mXB, mUB, L.x1, x, L.gs_flags, L.gs_groups, epoch, b,
                                 (const double*)L.d.border, old_half, skip));
   VTS_LAUNCHED(c);
+  if (pe) VTS_CUDA(cudaEventRecord(pe->b, c->stream));
   *launched = true;
   return 0;
 }
@@ -1468,8 +1478,9 @@ int mg_setup(Ctx* c, double shift_scale) {
 // ms[1] one V-cycle, ms[2] one forward GS sweep (old-value pass + wavefront)
 // on the finest level, ms[3] the same on the second-finest level, ms[4]
 // finest residual, ms[5] mg_setup (stencil + Galerkin chain + coarse factor).
-// per-launch timing of k_gs_tri between profile_begin and profile_end:
-// out = {total ms, launches, finest-level ms, finest-level launches}
+// per-launch timing of the wavefront kernels between profile_begin and
+// profile_end: out = {total ms, launches, finest-level k_gs_tri ms, its
+// launches, finest-level k_gs_pair ms, its launches}
 int profile_begin(Ctx* c) {
   c->prof = true;
   c->prof_used = 0;
@@ -1479,21 +1490,23 @@ int profile_begin(Ctx* c) {
 int profile_end(Ctx* c, double* out) {
   c->prof = false;
   VTS_CUDA(cudaStreamSynchronize(c->stream));
-  double tot = 0.0, fine = 0.0;
-  long long nf = 0;
+  double tot = 0.0, fine[2] = {0.0, 0.0};
+  long long nf[2] = {0, 0};
   for (size_t i = 0; i < c->prof_used; ++i) {
     float t = 0.f;
     VTS_CUDA(cudaEventElapsedTime(&t, c->prof_ev[i].a, c->prof_ev[i].b));
     tot += t;
     if (c->prof_ev[i].level == c->L - 1) {
-      fine += t;
-      ++nf;
+      fine[c->prof_ev[i].pair] += t;
+      ++nf[c->prof_ev[i].pair];
     }
   }
   out[0] = tot;
   out[1] = (double)c->prof_used;
-  out[2] = fine;
-  out[3] = (double)nf;
+  out[2] = fine[0];
+  out[3] = (double)nf[0];
+  out[4] = fine[1];
+  out[5] = (double)nf[1];
   c->prof_used = 0;
   return 0;
 }
