@@ -421,38 +421,47 @@ constexpr int kWarps = 5;  // compute, loader, storer, publisher, stager
 constexpr int kBuild = 9;  // pipelined pair, sweep B: builder warps (one node of a window's R x W box each)
 // Pair CTAs have 16 warps.  Warp w runs on SM sub-partition w % 4: the compute
 // warp (0) must keep its sub-partition's issue slots and fp64 pipe, so the
-// builders sit on warps with w % 4 != 0 (5 6 7 9 10 11 13 14 15); warp 8 loads
-// sweep B's x_A boxes (a slow acquire-poll loop), warps 4 and 12 stay light.
+// builders sit on warps with w % 4 != 0 (5 6 7 9 10 11 13 14 15); warps 8 and 12
+// issue sweep B's builder-input boxes (x_A after an acquire-poll, and U, b,
+// border), warp 4 is the (cross-cluster) stager: all light loops.
 constexpr int kWarpsPair = 16;
 constexpr int kXLoadWarp = 8;
+constexpr int kBLoadWarp = 12;
 VTS_DEVICE_INLINE int builder_index(int warp) {  // -1: not a builder warp
   return (warp < kWarps || (warp & 3) == 0) ? -1 : (warp - kWarps) - (warp - kWarps + 1) / 4;
 }
 // one window slot = three TMA boxes: R rows x W nodes x {22 stencil, 2 P, 2 border} doubles
-struct __align__(128) InSlot {
+struct __align__(128) InSlot {  // the compute warp's ring
   double st[R][W][kHalf];
   double p[R][W][2];   // P (TMA box, or written by sweep B's builders)
-  double q[R][W][2];   // border (zero-guess sweeps, sweep B)
-  double b[R][W][2];   // sweep B: right-hand side
-  double xb[R + 1][W + 3][2];  // sweep B: sweep A's result around the window (rows +1, columns +3)
+  double q[R][W][2];   // border (zero-guess sweeps)
+};
+constexpr int NSB = 2;  // sweep B: builder-input ring (refilled as soon as the builders are done)
+struct __align__(128) BSlot {  // sweep B's builder inputs
+  double u[R][W][18];  // the old-value half-stencil (18 of its 22 doubles)
+  double b[R][W][2];   // right-hand side
+  double qb[R][W][2];  // border
+  double xb[R + 1][W + 3][2];  // sweep A's result around the window (rows +1, columns +3)
   double xb_pad[8];
-  double u[R][W][18];  // sweep B: the old-value half-stencil (18 of its 22 doubles)
 };
 struct Smem {
   InSlot in[NS];
+  BSlot bin[NSB];
   double2 out[NS][R][W];
   double2 above[NSA][W];
   unsigned long long full_in[NS], empty_in[NS], full_out[NS], empty_out[NS];
-  unsigned long long loaded[NS];     // sweep B: the slot's static TMA boxes have landed (builders wait)
-  unsigned long long xloaded[NS];    // sweep B: the slot's x_A box has landed (builders wait)
+  unsigned long long loaded[NSB];    // sweep B: a builder slot's static TMA boxes have landed
+  unsigned long long xloaded[NSB];   // sweep B: a builder slot's x_A box has landed
+  unsigned long long bempty[NSB];    // sweep B: the builders are done with a builder slot
   unsigned stored_cnt;                // sweep A: windows x {storer, publisher} whose stores are issued
   unsigned long long full_above[NSA], empty_above[NSA];
   int armed;  // (producer side) highest above-ring chunk the consumer has armed
 };
 static_assert(sizeof(InSlot) % 128 == 0 && offsetof(InSlot, p) % 128 == 0 && offsetof(InSlot, q) % 128 == 0 &&
-                  offsetof(InSlot, b) % 128 == 0 && offsetof(InSlot, xb) % 128 == 0 &&
-                  offsetof(InSlot, u) % 128 == 0,
+                  sizeof(BSlot) % 128 == 0 && offsetof(BSlot, b) % 128 == 0 && offsetof(BSlot, qb) % 128 == 0 &&
+                  offsetof(BSlot, xb) % 128 == 0 && offsetof(Smem, bin) % 128 == 0,
               "TMA destinations must stay 128-B aligned");
+static_assert(sizeof(Smem) <= 232448, "exceeds the 227 KB of shared memory per block");
 static_assert(((W * kHalf * 8) / 16) % 2 == 1, "lane stride must be an odd multiple of 16 B");
 }  // namespace gs
 
@@ -533,12 +542,15 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
-      mbar_init(&S.full_in[s], ROLE == 2 ? kBuild : 1);  // sweep B: one arrive per builder warp
+      mbar_init(&S.full_in[s], ROLE == 2 ? 1 + kBuild : 1);  // sweep B: stencil box + one arrive per builder warp
       mbar_init(&S.empty_in[s], 1);
-      mbar_init(&S.loaded[s], 1);
-      mbar_init(&S.xloaded[s], 1);
       mbar_init(&S.full_out[s], 1);
       mbar_init(&S.empty_out[s], 2);
+    }
+    for (int s = 0; s < NSB; ++s) {
+      mbar_init(&S.loaded[s], 1);
+      mbar_init(&S.xloaded[s], 1);
+      mbar_init(&S.bempty[s], kBuild);
     }
     for (int s = 0; s < NSA; ++s) {
       mbar_init(&S.full_above[s], 1);
@@ -580,15 +592,9 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
         // node index of box element (p = 0, box row 0)
         const int node0 = FWD ? iy0 * nx + W * w : (iyb - R + 2) * nx - W * (w + 1) + SKEW * (R - 1);
         const int c1 = node0 + pad_nodes;
-        if (ROLE == 2) {
-          // sweep B: the static boxes (stencil, b, border) as soon as the slot is free;
-          // the x_A box comes from the x-loader warp once sweep A has stored it
-          mbar_expect_tx(&S.loaded[s], (unsigned)(sizeof(S.in[s].st) + sizeof(S.in[s].q) + sizeof(S.in[s].b) +
-                                                  sizeof(S.in[s].u)));
-          tma_load_3d(&S.in[s].st[0][0][0], G.mapS, 0, c1, 0, &S.loaded[s]);
-          tma_load_3d(&S.in[s].u[0][0][0], G.mapU, 0, c1, 0, &S.loaded[s]);
-          tma_load_3d(&S.in[s].q[0][0][0], G.mapQ, 0, c1, 0, &S.loaded[s]);
-          tma_load_3d(&S.in[s].b[0][0][0], G.mapB, 0, c1, 0, &S.loaded[s]);
+        if (ROLE == 2) {  // sweep B: the stencil box; the builders add P
+          mbar_expect_tx(&S.full_in[s], (unsigned)sizeof(S.in[s].st));
+          tma_load_3d(&S.in[s].st[0][0][0], G.mapS, 0, c1, 0, &S.full_in[s]);
         } else {
           mbar_expect_tx(&S.full_in[s],
                          (unsigned)(sizeof(S.in[s].st) + sizeof(S.in[s].p) + (ZERO ? sizeof(S.in[s].q) : 0)));
@@ -720,8 +726,8 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
       const unsigned long long tag = G.epoch << 32;
       const int iy0 = band * R, iyb = ny - 1 - band * R;
       for (int w = 0; w < nwin; ++w) {
-        const int s = w % NS;
-        if (w >= NS) mbar_wait(&S.empty_in[s], ((w / NS) - 1) & 1);
+        const int sb = w % NSB;
+        if (w >= NSB) mbar_wait(&S.bempty[sb], ((w / NSB) - 1) & 1);
         while (ld_acquire(G.stored + band) < (tag | (unsigned long long)min(w + 2, nwin))) {
         }
         if (band + 1 < bands)
@@ -731,8 +737,24 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
         const int node0 = FWD ? iy0 * nx + W * w : (iyb - R + 2) * nx - W * (w + 1) + SKEW * (R - 1);
         const int c1 = node0 + pad_nodes;
         const int cx = FWD ? c1 : c1 - (nx - SKEW) - 3;  // backward: one row and 3 nodes earlier
-        mbar_expect_tx(&S.xloaded[s], (unsigned)sizeof(S.in[s].xb));
-        tma_load_3d(&S.in[s].xb[0][0][0], G.mapX, 0, cx, 0, &S.xloaded[s]);
+        mbar_expect_tx(&S.xloaded[sb], (unsigned)sizeof(S.bin[sb].xb));
+        tma_load_3d(&S.bin[sb].xb[0][0][0], G.mapX, 0, cx, 0, &S.xloaded[sb]);
+      }
+    }
+  } else if (ROLE == 2 && warp == kBLoadWarp) {  // ---------------- sweep B: builder-input loader
+    // U, b and border of window w as soon as the builders are done with the slot's
+    // previous window -- ahead of the compute ring, which frees slots later
+    if (lane == 0) {
+      const int iy0 = band * R, iyb = ny - 1 - band * R;
+      for (int w = 0; w < nwin; ++w) {
+        const int sb = w % NSB;
+        if (w >= NSB) mbar_wait(&S.bempty[sb], ((w / NSB) - 1) & 1);
+        const int node0 = FWD ? iy0 * nx + W * w : (iyb - R + 2) * nx - W * (w + 1) + SKEW * (R - 1);
+        const int c1 = node0 + pad_nodes;
+        mbar_expect_tx(&S.loaded[sb], (unsigned)(sizeof(S.bin[sb].u) + sizeof(S.bin[sb].b) + sizeof(S.bin[sb].qb)));
+        tma_load_3d(&S.bin[sb].u[0][0][0], G.mapU, 0, c1, 0, &S.loaded[sb]);
+        tma_load_3d(&S.bin[sb].b[0][0][0], G.mapB, 0, c1, 0, &S.loaded[sb]);
+        tma_load_3d(&S.bin[sb].qb[0][0][0], G.mapQ, 0, c1, 0, &S.loaded[sb]);
       }
     }
   } else if (ROLE == 2 && builder_index(warp) >= 0) {  // ---------------- builders: sweep B's P from A's result
@@ -757,14 +779,14 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
     const int nk[4] = {FWD ? k + 1 : k, FWD ? k + 1 : k, FWD ? k + 1 : k, ck};
     const int np[4] = {FWD ? p + 3 : p, FWD ? p + 2 : p + 1, FWD ? p + 1 : p + 2, FWD ? p + 1 : p + 2};
     auto build = [&](int w) {
-      const int s = w % NS;
-      mbar_wait(&S.loaded[s], (w / NS) & 1);
-      mbar_wait(&S.xloaded[s], (w / NS) & 1);
+      const int s = w % NS, sb = w % NSB;
+      mbar_wait(&S.loaded[sb], (w / NSB) & 1);
+      mbar_wait(&S.xloaded[sb], (w / NSB) & 1);
+      double2 pv = make_double2(0.0, 0.0);
       if (has_item) {
         const int n = node_of(w);
-        double2 pv = make_double2(0.0, 0.0);
         if (n >= 0 && n < nnodes) {
-          const InSlot& in = S.in[s];
+          const BSlot& in = S.bin[sb];
           OldIn o;
 #pragma unroll
           for (int i = 0; i < 18; i += 2) {
@@ -773,14 +795,17 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
             o.a[i + 1] = t.y;
           }
           o.bv = *reinterpret_cast<const double2*>(&in.b[k][p][0]);
-          o.dv = *reinterpret_cast<const double2*>(&in.q[k][p][0]);
+          o.dv = *reinterpret_cast<const double2*>(&in.qb[k][p][0]);
           o.xo = *reinterpret_cast<const double2*>(&in.xb[ck][cp][0]);
 #pragma unroll
           for (int q = 0; q < 4; ++q) o.v[q] = *reinterpret_cast<const double2*>(&in.xb[nk[q]][np[q]][0]);
           pv = gs_old_eval<FWD>(o, xa);
         }
-        *reinterpret_cast<double2*>(&S.in[s].p[k][p][0]) = pv;
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.bempty[sb]);  // inputs consumed: the next window's may land
+      if (w >= NS) mbar_wait(&S.empty_in[s], ((w / NS) - 1) & 1);  // the compute slot is free
+      if (has_item) *reinterpret_cast<double2*>(&S.in[s].p[k][p][0]) = pv;
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.full_in[s]);
     };
