@@ -418,17 +418,18 @@ constexpr int NS = VTS_GS_NS;  // window slots in flight (in and out rings)
 constexpr int NSA = 4;     // window slots of the previous band's row
 constexpr int SKEW = 2;    // columns between consecutive rows of the wavefront
 constexpr int kWarps = 5;  // compute, loader, storer, publisher, stager
-constexpr int kBuild = 9;  // pipelined pair, sweep B: builder warps (one node of a window's R x W box each)
+constexpr int kBuild = 6;  // pipelined pair, sweep B: builder warps (<= 2 nodes of a window's R x W box each)
 // Pair CTAs have 16 warps.  Warp w runs on SM sub-partition w % 4: the compute
 // warp (0) must keep its sub-partition's issue slots and fp64 pipe, so the
-// builders sit on warps with w % 4 != 0 (5 6 7 9 10 11 13 14 15); warps 8 and 12
+// builders sit on warps with w % 4 in {1, 2} (5 6 9 10 13 14), away from the
+// compute warp's and the publisher's sub-partitions (0, 3); warps 8 and 12
 // issue sweep B's builder-input boxes (x_A after an acquire-poll, and U, b,
 // border), warp 4 is the (cross-cluster) stager: all light loops.
 constexpr int kWarpsPair = 16;
 constexpr int kXLoadWarp = 8;
 constexpr int kBLoadWarp = 12;
-VTS_DEVICE_INLINE int builder_index(int warp) {  // -1: not a builder warp
-  return (warp < kWarps || (warp & 3) == 0) ? -1 : (warp - kWarps) - (warp - kWarps + 1) / 4;
+VTS_DEVICE_INLINE int builder_index(int warp) {  // -1: not a builder warp (sub-partitions 1 and 2 only)
+  return (warp < kWarps || (warp & 3) == 0 || (warp & 3) == 3) ? -1 : 2 * ((warp - kWarps) / 4) + ((warp - kWarps) & 1);
 }
 // one window slot = three TMA boxes: R rows x W nodes x {22 stencil, 2 P, 2 border} doubles
 struct __align__(128) InSlot {  // the compute warp's ring
@@ -765,47 +766,52 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
     // Box neighbours outside the grid read real wrapped nodes or padding zeros where
     // the multi-launch pass reads 0; their couplings are exact zeros either way.
     const int tb = builder_index(warp) * 32 + lane;
+    constexpr int kItems = (R * W + 32 * kBuild - 1) / (32 * kBuild);  // box nodes per builder thread
+    static_assert(kItems <= 2, "builder registers sized for two nodes per thread");
     const int nnodes = nx * ny;
     const double xa = G.xa_src[ngrid];
     const int iy0 = band * R, iyb = ny - 1 - band * R;
-    const bool has_item = tb < R * W;
-    const int k = tb / W, p = tb - (tb / W) * W;
-    auto node_of = [&](int w) {
-      const int node0 = FWD ? iy0 * nx + W * w : (iyb - R + 2) * nx - W * (w + 1) + SKEW * (R - 1);
-      return node0 + k * (nx - SKEW) + p;
-    };
-    // box coordinates of the node (C) and of its later neighbours NE N NW E (slots 0..3)
-    const int ck = FWD ? k : k + 1, cp = FWD ? p : p + 3;
-    const int nk[4] = {FWD ? k + 1 : k, FWD ? k + 1 : k, FWD ? k + 1 : k, ck};
-    const int np[4] = {FWD ? p + 3 : p, FWD ? p + 2 : p + 1, FWD ? p + 1 : p + 2, FWD ? p + 1 : p + 2};
     auto build = [&](int w) {
       const int s = w % NS, sb = w % NSB;
       mbar_wait(&S.loaded[sb], (w / NSB) & 1);
       mbar_wait(&S.xloaded[sb], (w / NSB) & 1);
-      double2 pv = make_double2(0.0, 0.0);
-      if (has_item) {
-        const int n = node_of(w);
-        if (n >= 0 && n < nnodes) {
-          const BSlot& in = S.bin[sb];
-          OldIn o;
+      const int node0 = FWD ? iy0 * nx + W * w : (iyb - R + 2) * nx - W * (w + 1) + SKEW * (R - 1);
+      double2 pv[kItems];
 #pragma unroll
-          for (int i = 0; i < 18; i += 2) {
-            const double2 t = *reinterpret_cast<const double2*>(&in.u[k][p][i]);
-            o.a[i] = t.x;
-            o.a[i + 1] = t.y;
-          }
-          o.bv = *reinterpret_cast<const double2*>(&in.b[k][p][0]);
-          o.dv = *reinterpret_cast<const double2*>(&in.qb[k][p][0]);
-          o.xo = *reinterpret_cast<const double2*>(&in.xb[ck][cp][0]);
+      for (int it = 0; it < kItems; ++it) {
+        pv[it] = make_double2(0.0, 0.0);
+        const int i = tb + it * 32 * kBuild;
+        if (i >= R * W) continue;
+        const int k = i / W, p = i - (i / W) * W;
+        const int n = node0 + k * (nx - SKEW) + p;
+        if (n < 0 || n >= nnodes) continue;
+        // box coordinates of the node (C) and of its later neighbours NE N NW E (slots 0..3)
+        const int ck = FWD ? k : k + 1, cp = FWD ? p : p + 3;
+        const int nk[4] = {FWD ? k + 1 : k, FWD ? k + 1 : k, FWD ? k + 1 : k, ck};
+        const int np[4] = {FWD ? p + 3 : p, FWD ? p + 2 : p + 1, FWD ? p + 1 : p + 2, FWD ? p + 1 : p + 2};
+        const BSlot& in = S.bin[sb];
+        OldIn o;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) o.v[q] = *reinterpret_cast<const double2*>(&in.xb[nk[q]][np[q]][0]);
-          pv = gs_old_eval<FWD>(o, xa);
+        for (int j = 0; j < 18; j += 2) {
+          const double2 t = *reinterpret_cast<const double2*>(&in.u[k][p][j]);
+          o.a[j] = t.x;
+          o.a[j + 1] = t.y;
         }
+        o.bv = *reinterpret_cast<const double2*>(&in.b[k][p][0]);
+        o.dv = *reinterpret_cast<const double2*>(&in.qb[k][p][0]);
+        o.xo = *reinterpret_cast<const double2*>(&in.xb[ck][cp][0]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) o.v[q] = *reinterpret_cast<const double2*>(&in.xb[nk[q]][np[q]][0]);
+        pv[it] = gs_old_eval<FWD>(o, xa);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.bempty[sb]);  // inputs consumed: the next window's may land
       if (w >= NS) mbar_wait(&S.empty_in[s], ((w / NS) - 1) & 1);  // the compute slot is free
-      if (has_item) *reinterpret_cast<double2*>(&S.in[s].p[k][p][0]) = pv;
+#pragma unroll
+      for (int it = 0; it < kItems; ++it) {
+        const int i = tb + it * 32 * kBuild;
+        if (i < R * W) *reinterpret_cast<double2*>(&S.in[s].p[i / W][i - (i / W) * W][0]) = pv[it];
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.full_in[s]);
     };
