@@ -56,129 +56,120 @@ struct BotArgs {
   const double* chol;
   int off_chol;  // -1: factor read from global memory
   int off_y;
-  int off_stage, off_q;  // staged half-stencil (nn * kHalf) and staged border (2 nn)
+  int off_stage, off_q;  // staged half-stencil and right-hand side, padded ((nn + 2 kBotPad) nodes)
   int off_red;           // reduction scratch: 32 virtual-block partials + 8 x 32 warp sums
 };
 
 // one Gauss-Seidel sweep of level L: x <- sweep(x; b) (zero_guess: x_old = 0)
 // (not inlined: one copy of each sweep's code, warm in the instruction cache
 // after its first use; inlined copies per call site ran 3.6x slower cold)
+constexpr int kBotPad = 64;  // zero nodes before/after the staged level (>= 2 x 31, the largest skew)
 template <bool FWD, bool ZERO>
 __device__ __noinline__ void bot_sweep(const BotLevel& L, double* sm, const BotArgs& A) {
   double* sb = sm + L.off_b;
   double* sx = sm + L.off_x;
-  double* sP = sm + L.off_r;
-  double* stage = sm + A.off_stage;
-  double* sq = sm + A.off_q;
+  double* stage = sm + A.off_stage;  // [(nn + 2 pad) * kHalf] the half the wavefront solves with
+  double* pst = sm + A.off_q;        // [(nn + 2 pad) * 2] its right-hand side P
   const int tid = threadIdx.x;
+  const int nn = L.nn;
   const double* solve_half = FWD ? L.stL : L.stU;
-  // stage the half the wavefront solves with (+ the border for the zero-guess sweep);
-  // the old-value pass reads the other half straight from L2
+  // stage the solve half and P = b - border x_alpha [- U x_old / - L x_old] (the
+  // old-value pass, gs_old_node) in padded node order; the pads are zeros
   {
     const double2* src = reinterpret_cast<const double2*>(solve_half);
     double2* dst = reinterpret_cast<double2*>(stage);
-    for (int i = tid; i < L.nn * kHalf / 2; i += blockDim.x) dst[i] = src[i];
-    if (ZERO)
-      for (int i = tid; i < L.nn; i += blockDim.x)
-        reinterpret_cast<double2*>(sq)[i] = reinterpret_cast<const double2*>(L.border)[i];
+    const int lo = kBotPad * kHalf / 2, hi = (kBotPad + nn) * kHalf / 2, end = (2 * kBotPad + nn) * kHalf / 2;
+    for (int i = tid; i < end; i += blockDim.x) dst[i] = (i >= lo && i < hi) ? src[i - lo] : make_double2(0.0, 0.0);
+    const double xa = sx[L.ngrid];
+    double2* pd = reinterpret_cast<double2*>(pst);
+    for (int i = tid; i < nn + 2 * kBotPad; i += blockDim.x) {
+      const int nd = i - kBotPad;
+      double2 pv = make_double2(0.0, 0.0);
+      if (nd >= 0 && nd < nn) {
+        if (ZERO) {
+          const double2 bb = *reinterpret_cast<const double2*>(sb + 2 * nd);
+          const double2 qq = *reinterpret_cast<const double2*>(L.border + 2 * nd);
+          pv = make_double2(__dsub_rn(bb.x, __dmul_rn(qq.x, xa)), __dsub_rn(bb.y, __dmul_rn(qq.y, xa)));
+        } else {
+          pv = gs_old_node<FWD>(L.nx, L.ny, FWD ? L.stU : L.stL, sb, L.border, sx, xa, nd);
+        }
+      }
+      pd[i] = pv;
+    }
   }
   __syncthreads();
   BOT_MARK();  // staged
-  if (!ZERO) {
-    const double xa = sx[L.ngrid];
-    for (int nd = tid; nd < L.nn; nd += blockDim.x)
-      *reinterpret_cast<double2*>(sP + 2 * nd) =
-          gs_old_node<FWD>(L.nx, L.ny, FWD ? L.stU : L.stL, sb, L.border, sx, xa, nd);
-  }
-  __syncthreads();
-  BOT_MARK();  // old pass
+  BOT_MARK();  // (old pass: part of staging)
   if (tid < 32) {
-    // the wavefront of k_gs_tri on a single band: lane l = sweep row, skew 2;
-    // software-pipelined like k_gs_tri (step t+1's loads and previous-row part
-    // while step t's own-row recurrence runs); out-of-range positions compute
-    // on clamped data and are neither stored nor passed on
+    // the wavefront of k_gs_tri on a single band: lane l = sweep row, skew 2,
+    // software-pipelined, branch-free like k_gs_tri: every lane streams its row
+    // through the padded stage with a pointer that moves one node per step;
+    // positions off the row (and lanes below the grid, clamped to the last row)
+    // compute on finite real-neighbour or zero-pad data and are never stored;
+    // every coupling that reads them at a valid position is an exact zero
     const int l = tid;
-    const int iy = FWD ? l : L.ny - 1 - l;
-    const double xa = ZERO ? sx[L.ngrid] : 0.0;
+    const int nx = L.nx, ny = L.ny;  // registers: the loop must not re-read L through a generic pointer
+    const int lc = l < ny ? l : ny - 1;
     constexpr int d0 = FWD ? 0 : 1;
     constexpr int d1 = 1 - d0;
-    struct Raw {
-      double a[20];
-      double p0, p1;
-      int nd;
-      bool valid;
-    };
-    auto load = [&](int t, Raw& r) {
-      const int j = t - 2 * l;
-      r.valid = l < L.ny && j >= 0 && j < L.nx;
-      const int jc = j < 0 ? 0 : (j >= L.nx ? L.nx - 1 : j);
-      const int ix = FWD ? jc : L.nx - 1 - jc;
-      const int iyc = l < L.ny ? iy : 0;
-      r.nd = ix + L.nx * iyc;
-      const double2* a2 = reinterpret_cast<const double2*>(stage + (size_t)r.nd * kHalf);
-#pragma unroll
-      for (int i = 0; i < 10; ++i) {
-        const double2 v = a2[i];
-        r.a[2 * i] = v.x;
-        r.a[2 * i + 1] = v.y;
-      }
-      if (ZERO) {
-        const double2 bb = *reinterpret_cast<const double2*>(sb + 2 * r.nd);
-        const double2 qq = *reinterpret_cast<const double2*>(sq + 2 * r.nd);
-        r.p0 = __dsub_rn(bb.x, __dmul_rn(qq.x, xa));
-        r.p1 = __dsub_rn(bb.y, __dmul_rn(qq.y, xa));
-      } else {
-        const double2 pp = *reinterpret_cast<const double2*>(sP + 2 * r.nd);
-        r.p0 = pp.x;
-        r.p1 = pp.y;
-      }
-    };
+    constexpr int dir = FWD ? 1 : -1;
+    // node of (row lc, sweep column t - 2 l) at t = 0, in padded stage order
+    const int n0 = FWD ? lc * nx - 2 * l : (ny - 1 - lc) * nx + nx - 1 + 2 * l;
+    const double* ap = stage + (size_t)(kBotPad + n0) * kHalf;
+    const double* pp = pst + (size_t)(kBotPad + n0) * 2;
+    double* xp_out = sx + 2 * (ptrdiff_t)n0;
     struct StepData {
       double q0, q1, e00, e01, e10, e11, w00, w01, w10, w11, c, r0, r1;
-      int nd;
-      bool valid;
     };
-    auto prepare = [&](const Raw& r, const double2 xm, const double2 xz) {
+    auto prepare = [&](const double* a, const double* pv, const double2 xm, const double2 xz) {
+      double r[20];
+#pragma unroll
+      for (int i = 0; i < 10; ++i) {
+        const double2 v = reinterpret_cast<const double2*>(a)[i];
+        r[2 * i] = v.x;
+        r[2 * i + 1] = v.y;
+      }
+      const double2 pq = *reinterpret_cast<const double2*>(pv);
       auto pre = [&](int d, double p) {
-        const double t1 = fma(-r.a[0 + 2 * d], xm.x, -r.a[1 + 2 * d] * xm.y);
-        const double t2 = fma(-r.a[4 + 2 * d], xz.x, -r.a[5 + 2 * d] * xz.y);
+        const double t1 = fma(-r[0 + 2 * d], xm.x, -r[1 + 2 * d] * xm.y);
+        const double t2 = fma(-r[4 + 2 * d], xz.x, -r[5 + 2 * d] * xz.y);
         return p + (t1 + t2);
       };
       StepData o;
-      o.q0 = pre(d0, d0 == 0 ? r.p0 : r.p1);
-      o.q1 = pre(d1, d1 == 0 ? r.p0 : r.p1);
-      o.e00 = r.a[8 + 2 * d0];
-      o.e01 = r.a[9 + 2 * d0];
-      o.e10 = r.a[8 + 2 * d1];
-      o.e11 = r.a[9 + 2 * d1];
-      o.w00 = r.a[12 + 2 * d0];
-      o.w01 = r.a[13 + 2 * d0];
-      o.w10 = r.a[12 + 2 * d1];
-      o.w11 = r.a[13 + 2 * d1];
-      o.c = r.a[kHC];
-      o.r0 = r.a[d0 == 0 ? kHRd0 : kHRd1];
-      o.r1 = r.a[d1 == 0 ? kHRd0 : kHRd1];
-      o.nd = r.nd;
-      o.valid = r.valid;
+      o.q0 = pre(d0, d0 == 0 ? pq.x : pq.y);
+      o.q1 = pre(d1, d1 == 0 ? pq.x : pq.y);
+      o.e00 = r[8 + 2 * d0];
+      o.e01 = r[9 + 2 * d0];
+      o.e10 = r[8 + 2 * d1];
+      o.e11 = r[9 + 2 * d1];
+      o.w00 = r[12 + 2 * d0];
+      o.w01 = r[13 + 2 * d0];
+      o.w10 = r[12 + 2 * d1];
+      o.w11 = r[13 + 2 * d1];
+      o.c = r[kHC];
+      o.r0 = r[d0 == 0 ? kHRd0 : kHRd1];
+      o.r1 = r[d1 == 0 ? kHRd0 : kHRd1];
       return o;
     };
     double2 win[3] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
     double2 wprev = make_double2(0.0, 0.0);
-    const int T = L.nx + 2 * (L.ny - 1);
-    Raw raw;
-    load(0, raw);
-    StepData cur = prepare(raw, win[0], win[1]);
+    const int T = nx + 2 * (ny - 1);
+    StepData cur = prepare(ap, pp, win[0], win[1]);
+    const bool row_ok = l < ny;
+    double* const trash = sm + A.off_red;  // stores of off-row positions land here (unused during sweeps)
+#pragma unroll 4
     for (int t = 0; t < T; ++t) {
-      load(t + 1 < T ? t + 1 : t, raw);
+      const int j = t - 2 * l;
       const double2 xp = win[2];
       const double u0 = fma(-cur.e00, xp.x, fma(-cur.e01, xp.y, cur.q0));
       const double u1 = fma(-cur.e10, xp.x, fma(-cur.e11, xp.y, cur.q1));
-      const double n0 = fma(-cur.w00, wprev.x, fma(-cur.w01, wprev.y, u0)) * cur.r0;
-      const double n1 = fma(-cur.c, n0, fma(-cur.w10, wprev.x, fma(-cur.w11, wprev.y, u1))) * cur.r1;
-      const double2 calc = FWD ? make_double2(n0, n1) : make_double2(n1, n0);
-      const double2 nv = cur.valid ? calc : make_double2(0.0, 0.0);
-      if (cur.valid) *reinterpret_cast<double2*>(sx + 2 * cur.nd) = nv;
-      const StepData nxt = prepare(raw, win[1], win[2]);
+      const double n0v = fma(-cur.w00, wprev.x, fma(-cur.w01, wprev.y, u0)) * cur.r0;
+      const double n1v = fma(-cur.c, n0v, fma(-cur.w10, wprev.x, fma(-cur.w11, wprev.y, u1))) * cur.r1;
+      const double2 nv = FWD ? make_double2(n0v, n1v) : make_double2(n1v, n0v);
+      // branch-free store: off-row positions write the scratch slot instead
+      double* dst = (row_ok && j >= 0 && j < nx) ? xp_out + 2 * dir * t : trash;
+      *reinterpret_cast<double2*>(dst) = nv;
+      const StepData nxt = prepare(ap + (size_t)((t + 1) * dir * kHalf), pp + 2 * dir * (t + 1), win[1], win[2]);
       wprev = nv;
       double2 up;
       up.x = __shfl_up_sync(0xffffffffu, nv.x, 1);
@@ -370,9 +361,9 @@ static int bottom_plan(Ctx* c, BotArgs* A, size_t* smem_bytes) {
       off += v;
     }
     A->off_stage = (int)off;
-    off += (size_t)c->lv[kb].d.nnodes * kHalf;
+    off += ((size_t)c->lv[kb].d.nnodes + 2 * kBotPad) * kHalf;
     A->off_q = (int)off;
-    off += 2 * (size_t)c->lv[kb].d.nnodes;
+    off += 2 * ((size_t)c->lv[kb].d.nnodes + 2 * kBotPad);
     A->off_red = (int)off;
     off += 32 + 32 * 8;
     A->off_y = (int)off;
