@@ -58,3 +58,25 @@ def test_full_pbm_bitwise_repeatable():
         assert list(r.extras["minres_per_newton"]) == list(runs[0].extras["minres_per_newton"])
         assert r.objective == runs[0].objective
         assert np.array_equal(r.rho.cpu().numpy(), runs[0].rho.cpu().numpy())
+
+
+def _run_ab(tmp_path, name, env_extra):
+    import os
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = tmp_path / f"{name}.npy"
+    env = dict(os.environ, **env_extra)
+    subprocess.run([sys.executable, os.path.join(repo, "tools", "checks", "ab_vcycle.py"), str(out), "C2"],
+                   cwd=repo, env=env, check=True, capture_output=True, timeout=600)
+    return np.load(out)
+
+
+@pytest.mark.parametrize("switch", ["VTS_NO_PAIR", "VTS_UNFUSED_BOTTOM"])
+def test_fast_paths_are_bitwise_identical_to_the_plain_path(tmp_path, switch):
+    """The pipelined sweep pairs and the fused V-cycle bottom compute exactly what
+    the one-sweep-per-launch path computes (V-cycle output and a MINRES solution)."""
+    fast = _run_ab(tmp_path, "fast", {})
+    plain = _run_ab(tmp_path, "plain", {switch: "1"})
+    assert np.array_equal(fast, plain)
