@@ -1295,29 +1295,41 @@ static int gs_pair(Ctx* c, int k, const double* b, double* x, bool forward, bool
   if (int rc = gs_prepare()) return rc;
   LevelBuf& L = c->lv[k];
   const int bands = div_up(L.d.ny, gs::R);
-  const int ncl = div_up(bands, 16);
-  const int cs = div_up(bands, ncl);
+  const void* fn = forward ? (zero_a ? (const void*)k_gs_pair<true, true> : (const void*)k_gs_pair<true, false>)
+                           : (const void*)k_gs_pair<false, false>;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(2 * cs * ncl);
   cfg.blockDim = dim3(32 * gs::kWarpsPair);
   cfg.dynamicSmemBytes = sizeof(gs::Smem);
   cfg.stream = c->stream;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = cs;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  // the largest clusters (fewest cross-cluster handoffs) with which both halves of
+  // the grid can be resident at once; none -> two single sweeps
   static int max_clusters[17] = {0};
-  if (max_clusters[cs] == 0) {
-    int n = 0;
-    const void* fn = forward ? (zero_a ? (const void*)k_gs_pair<true, true> : (const void*)k_gs_pair<true, false>)
-                             : (const void*)k_gs_pair<false, false>;
-    VTS_CUDA(cudaOccupancyMaxActiveClusters(&n, fn, &cfg));
-    max_clusters[cs] = n > 0 ? n : -1;
+  int cs = 0, ncl = 0;
+  for (int n = div_up(bands, 16); n <= bands; ++n) {
+    const int size = div_up(bands, n);
+    if (div_up(bands, size) != n) continue;  // same cluster size as a smaller n
+    if (max_clusters[size] == 0) {
+      at[0].val.clusterDim.x = size;
+      cfg.gridDim = dim3(2 * size * n);
+      int m = 0;
+      VTS_CUDA(cudaOccupancyMaxActiveClusters(&m, fn, &cfg));
+      max_clusters[size] = m > 0 ? m : -1;
+    }
+    if (max_clusters[size] >= 2 * n) {
+      cs = size;
+      ncl = n;
+      break;
+    }
   }
-  if (max_clusters[cs] < 2 * ncl) return 0;  // not all resident: caller runs two sweeps
+  if (cs == 0) return 0;  // not all resident: caller runs two sweeps
+  at[0].val.clusterDim.x = cs;
+  cfg.gridDim = dim3(2 * cs * ncl);
   CUtensorMap mSA, mPA, mQA, mSB, mBB, mQB, mXB, mUB;
   const double* solve_half = forward ? L.d.stL : L.d.stU;
   const double* old_half = forward ? L.d.stU : L.d.stL;
