@@ -427,6 +427,7 @@ constexpr int kBuild = 6;  // pipelined pair, sweep B: builder warps (<= 2 nodes
 // border), warp 4 is the (cross-cluster) stager: all light loops.
 constexpr int kWarpsPair = 16;
 constexpr int kXLoadWarp = 8;
+constexpr int kReleaseWarp = 7;  // sweep A: publishes the stored-window counters (backs off while waiting)
 constexpr int kBLoadWarp = 12;
 VTS_DEVICE_INLINE int builder_index(int warp) {  // -1: not a builder warp (sub-partitions 1 and 2 only)
   return (warp < kWarps || (warp & 3) == 0 || (warp & 3) == 3) ? -1 : 2 * ((warp - kWarps) / 4) + ((warp - kWarps) & 1);
@@ -516,6 +517,11 @@ struct GsBand {
 template <bool FWD, bool ZERO, int ROLE>
 __device__ __forceinline__ void gs_band(const GsBand& G) {
   using namespace gs;
+  // P by builder warps: always for sweep B (from sweep A's result, gated by A's stored
+  // counters); for sweep A of a pair unless it starts from the zero guess (from x_old,
+  // no gating) -- this replaces the old-value pass kernel in front of the pair
+  constexpr bool kBuilt = ROLE == 2 || (ROLE == 1 && !ZERO);
+  constexpr bool kGated = ROLE == 2;
   const int nx = G.nx, ny = G.ny, ngrid = G.ngrid, pad_nodes = G.pad_nodes, bands = G.bands;
   double* __restrict__ x = G.x;
   unsigned long long* flags = G.flags;
@@ -543,7 +549,7 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
-      mbar_init(&S.full_in[s], ROLE == 2 ? 1 + kBuild : 1);  // sweep B: stencil box + one arrive per builder warp
+      mbar_init(&S.full_in[s], kBuilt ? 1 + kBuild : 1);  // built P: stencil box + one arrive per builder warp
       mbar_init(&S.empty_in[s], 1);
       mbar_init(&S.full_out[s], 1);
       mbar_init(&S.empty_out[s], 2);
@@ -593,7 +599,7 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
         // node index of box element (p = 0, box row 0)
         const int node0 = FWD ? iy0 * nx + W * w : (iyb - R + 2) * nx - W * (w + 1) + SKEW * (R - 1);
         const int c1 = node0 + pad_nodes;
-        if (ROLE == 2) {  // sweep B: the stencil box; the builders add P
+        if (kBuilt) {  // the stencil box; the builders add P
           mbar_expect_tx(&S.full_in[s], (unsigned)sizeof(S.in[s].st));
           tma_load_3d(&S.in[s].st[0][0][0], G.mapS, 0, c1, 0, &S.full_in[s]);
         } else {
@@ -706,20 +712,22 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
   } else if (warp == 0) {
     gs_compute<FWD, ZERO>(S, nx, ngrid, band + (ROLE == 2 ? 128 : 0), rows_here, has_above, dsm_in, crank, nwin,
                           G.xa_src);  // (band only labels the probe timeline)
-  } else if (ROLE == 1 && warp == kWarps) {  // ---------------- sweep A: stored-window counter
+  } else if (ROLE == 1 && warp == kReleaseWarp) {  // ---------------- sweep A: stored-window counter
     // storer and publisher count their issued windows in stored_cnt (release, CTA
     // scope; a counter, not an mbarrier: nothing gates them on this warp, so they can
     // run a whole ring ahead); the release here (gpu scope, cumulative over what this
     // warp acquired) publishes them to sweep B without stalling the storer on the drain
     for (int w = 0; w < nwin; ++w) {
       unsigned cnt = 0;
-      do {
+      while (true) {
         asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(cnt) : "r"(smem_u32(&S.stored_cnt)) : "memory");
-      } while (cnt < 2u * (unsigned)(w + 1));
+        if (cnt >= 2u * (unsigned)(w + 1)) break;
+        __nanosleep(64);  // shares a sub-partition with the publisher
+      }
       __threadfence();
       if (lane == 0) st_release(G.stored + band, (G.epoch << 32) | (unsigned long long)(w + 1));
     }
-  } else if (ROLE == 2 && warp == kXLoadWarp) {  // ---------------- sweep B: x_A box loader
+  } else if (kBuilt && warp == kXLoadWarp) {  // ---------------- built P: x box loader
     // window w's box of sweep A's result (rows of the window and the next, up to 3
     // columns past it) may be read once A's band stored through window w+1 and A's
     // next band (its first row) through window w-1
@@ -729,12 +737,14 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
       for (int w = 0; w < nwin; ++w) {
         const int sb = w % NSB;
         if (w >= NSB) mbar_wait(&S.bempty[sb], ((w / NSB) - 1) & 1);
-        while (ld_acquire(G.stored + band) < (tag | (unsigned long long)min(w + 2, nwin))) {
-        }
-        if (band + 1 < bands)
-          while (ld_acquire(G.stored + band + 1) < (tag | (unsigned long long)min(w, nwin))) {
+        if (kGated) {
+          while (ld_acquire(G.stored + band) < (tag | (unsigned long long)min(w + 2, nwin))) {
           }
-        asm volatile("fence.proxy.async.global;" ::: "memory");  // A's generic stores -> this TMA read
+          if (band + 1 < bands)
+            while (ld_acquire(G.stored + band + 1) < (tag | (unsigned long long)min(w, nwin))) {
+            }
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // A's generic stores -> this TMA read
+        }
         const int node0 = FWD ? iy0 * nx + W * w : (iyb - R + 2) * nx - W * (w + 1) + SKEW * (R - 1);
         const int c1 = node0 + pad_nodes;
         const int cx = FWD ? c1 : c1 - (nx - SKEW) - 3;  // backward: one row and 3 nodes earlier
@@ -742,7 +752,7 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
         tma_load_3d(&S.bin[sb].xb[0][0][0], G.mapX, 0, cx, 0, &S.xloaded[sb]);
       }
     }
-  } else if (ROLE == 2 && warp == kBLoadWarp) {  // ---------------- sweep B: builder-input loader
+  } else if (kBuilt && warp == kBLoadWarp) {  // ---------------- built P: builder-input loader
     // U, b and border of window w as soon as the builders are done with the slot's
     // previous window -- ahead of the compute ring, which frees slots later
     if (lane == 0) {
@@ -758,7 +768,7 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
         tma_load_3d(&S.bin[sb].qb[0][0][0], G.mapQ, 0, c1, 0, &S.loaded[sb]);
       }
     }
-  } else if (ROLE == 2 && builder_index(warp) >= 0) {  // ---------------- builders: sweep B's P from A's result
+  } else if (kBuilt && builder_index(warp) >= 0) {  // ---------------- builders: P from x_old (A) or A's result (B)
     // P = b - border x_alpha - U x_A (gs_old_eval, CSR order) for the nodes of each
     // window's box, all from the slot's TMA boxes (U, b, border, x_A around the window):
     // loads through the SM's LSU here would slow the compute warp's shared-memory
@@ -842,16 +852,17 @@ __global__ void __launch_bounds__(32 * gs::kWarpsPair, 1)
               const __grid_constant__ CUtensorMap mapPA, const __grid_constant__ CUtensorMap mapQA,
               const __grid_constant__ CUtensorMap mapSB, const __grid_constant__ CUtensorMap mapBB,
               const __grid_constant__ CUtensorMap mapQB, const __grid_constant__ CUtensorMap mapXB,
-              const __grid_constant__ CUtensorMap mapUB,
+              const __grid_constant__ CUtensorMap mapUB, const __grid_constant__ CUtensorMap mapXA,
               double* __restrict__ x1, double* __restrict__ x,
               unsigned long long* flags, int groups, unsigned long long epoch, const double* __restrict__ b,
               const double* __restrict__ border, const double* __restrict__ half_old, const int* skip) {
   if (skip && *skip) return;
   const int nA = (int)gridDim.x / 2;
   if ((int)blockIdx.x < nA) {
-    GsBand G{nx, ny, ngrid, pad_nodes, bands, (int)blockIdx.x, &mapSA, &mapPA, &mapQA, &mapQA, &mapQA, &mapQA, x1, x,
-             flags,
-             flags + 2 * groups, epoch, nullptr, nullptr, nullptr, nullptr};
+    // sweep A: with the zero guess P = b - border x_alpha from TMA boxes (mapPA, mapQA);
+    // otherwise built from x (mapXA), the old-value half (mapUB), b and border
+    GsBand G{nx, ny, ngrid, pad_nodes, bands, (int)blockIdx.x, &mapSA, &mapPA, ZERO_A ? &mapQA : &mapQB, &mapBB,
+             &mapXA, &mapUB, x1, x, flags, flags + 2 * groups, epoch, b, border, half_old, x};
     gs_band<FWD, ZERO_A, 1>(G);
   } else {
 #ifdef VTS_PAIR_NO_B
@@ -1330,7 +1341,7 @@ static int gs_pair(Ctx* c, int k, const double* b, double* x, bool forward, bool
   if (cs == 0) return 0;  // not all resident: caller runs two sweeps
   at[0].val.clusterDim.x = cs;
   cfg.gridDim = dim3(2 * cs * ncl);
-  CUtensorMap mSA, mPA, mQA, mSB, mBB, mQB, mXB, mUB;
+  CUtensorMap mSA, mPA, mQA, mSB, mBB, mQB, mXB, mUB, mXA;
   const double* solve_half = forward ? L.d.stL : L.d.stU;
   const double* old_half = forward ? L.d.stU : L.d.stL;
   if (encode_skewed(&mSA, solve_half, kHalf, L)) return 5;
@@ -1338,33 +1349,24 @@ static int gs_pair(Ctx* c, int k, const double* b, double* x, bool forward, bool
   if (encode_skewed(&mBB, b, 2, L) || encode_skewed(&mQB, L.d.border, 2, L) ||
       encode_skewed(&mXB, L.x1, 2, L, gs::R + 1, gs::W + 3) || encode_skewed(&mUB, old_half, kHalf, L, gs::R, gs::W, 18))
     return 5;
-  const double* pa = b;  // sweep A's box: b (zero guess, with the border box) or P1
-  if (!zero_a) {
-    if (forward)
-      k_gs_old<true><<<div_up(L.d.nnodes, 256), 256, 0, c->stream>>>(L.d.nx, L.d.ny, L.d.ngrid, old_half, b,
-                                                                      L.d.border, x, L.r, skip);
-    else
-      k_gs_old<false><<<div_up(L.d.nnodes, 256), 256, 0, c->stream>>>(L.d.nx, L.d.ny, L.d.ngrid, old_half, b,
-                                                                       L.d.border, x, L.r, skip);
-    VTS_LAUNCHED(c);
-    pa = L.r;
-  }
-  if (encode_skewed(&mPA, pa, 2, L)) return 5;
-  if (encode_skewed(&mQA, zero_a ? L.d.border : pa, 2, L)) return 5;
+  // sweep A's boxes: b and border (zero guess), or x_old around each window (built P)
+  if (encode_skewed(&mPA, b, 2, L) || encode_skewed(&mQA, L.d.border, 2, L) ||
+      encode_skewed(&mXA, x, 2, L, gs::R + 1, gs::W + 3))
+    return 5;
   const unsigned long long epoch = ++L.pair_epoch;
   Ctx::ProfEv* pe = nullptr;
   if (int rc = prof_begin(c, L, 1, &pe)) return rc;
   if (forward && zero_a)
     VTS_CUDA(cudaLaunchKernelEx(&cfg, k_gs_pair<true, true>, L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, bands, mSA,
-                                mPA, mQA, mSB, mBB, mQB, mXB, mUB, L.x1, x, L.gs_flags, L.gs_groups, epoch, b,
+                                mPA, mQA, mSB, mBB, mQB, mXB, mUB, mXA, L.x1, x, L.gs_flags, L.gs_groups, epoch, b,
                                 (const double*)L.d.border, old_half, skip));
   else if (forward)
     VTS_CUDA(cudaLaunchKernelEx(&cfg, k_gs_pair<true, false>, L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, bands, mSA,
-                                mPA, mQA, mSB, mBB, mQB, mXB, mUB, L.x1, x, L.gs_flags, L.gs_groups, epoch, b,
+                                mPA, mQA, mSB, mBB, mQB, mXB, mUB, mXA, L.x1, x, L.gs_flags, L.gs_groups, epoch, b,
                                 (const double*)L.d.border, old_half, skip));
   else
     VTS_CUDA(cudaLaunchKernelEx(&cfg, k_gs_pair<false, false>, L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, bands,
-                                mSA, mPA, mQA, mSB, mBB, mQB, mXB, mUB, L.x1, x, L.gs_flags, L.gs_groups, epoch, b,
+                                mSA, mPA, mQA, mSB, mBB, mQB, mXB, mUB, mXA, L.x1, x, L.gs_flags, L.gs_groups, epoch, b,
                                 (const double*)L.d.border, old_half, skip));
   VTS_LAUNCHED(c);
   if (pe) VTS_CUDA(cudaEventRecord(pe->b, c->stream));
