@@ -865,9 +865,6 @@ __global__ void __launch_bounds__(32 * gs::kWarpsPair, 1)
              &mapXA, &mapUB, x1, x, flags, flags + 2 * groups, epoch, b, border, half_old, x};
     gs_band<FWD, ZERO_A, 1>(G);
   } else {
-#ifdef VTS_PAIR_NO_B
-    return;  // probe builds only: time sweep A alone inside the pair launch
-#endif
     GsBand G{nx, ny, ngrid, pad_nodes, bands, (int)blockIdx.x - nA, &mapSB, &mapSB, &mapQB, &mapBB, &mapXB, &mapUB, x, x,
              flags + groups, flags + 2 * groups, epoch, b, border, half_old, x1};
     gs_band<FWD, false, 2>(G);
