@@ -69,12 +69,16 @@ def algorithmic_bytes(prob) -> dict:
     # half-stencil it solves with, the 2-double right-hand side P, the 2-double result
     fine = lv[-1]
     A_tri = fine.nx * fine.ny * 8 * (20 + 2 + 2)
-    # one finest-level sweep pair (k_gs_pair): sweep A as above; sweep B reads the
-    # 20-double half-stencil, 18 doubles of the other half, b, border and sweep A's
-    # result, and writes its own result
-    A_pair = A_tri + fine.nx * fine.ny * 8 * (20 + 18 + 2 + 2 + 2 + 2)
+    # one finest-level sweep pair (k_gs_pair), per node: sweep B reads the 20-double
+    # solve half, 18 doubles of the other half, b, border and sweep A's result and
+    # writes its own (46 doubles); descent sweep A (zero guess) reads the solve half,
+    # b, border and writes its result (26); ascent sweep A builds its P like B (46)
+    nodes = fine.nx * fine.ny
+    B_side = 20 + 18 + 2 + 2 + 2 + 2
+    A_pair = nodes * 8 * ((20 + 2 + 2 + 2) + B_side)
+    A_pair_asc = nodes * 8 * (B_side + B_side)
     return dict(phi=A_phi, apply=A_ap, vcycle=A_V, minres_iter=A_MR, gs_fine_sweep=A_gs, gs_tri_fine=A_tri,
-                gs_pair_fine=A_pair)
+                gs_pair_fine=A_pair, gs_pair_asc_fine=A_pair_asc)
 
 
 def ncu_traffic(kernel: str = "k_gs_tri"):
@@ -305,7 +309,7 @@ def main() -> None:
     # --- profiling pass (not the timed value): the same K iterations with every
     # wavefront launch bracketed by CUDA events on the context stream, giving the
     # dominant kernel's average launch time and its share of the step
-    prof = (ctypes.c_double * 6)()
+    prof = (ctypes.c_double * 8)()
     p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     _lib.check(lib.vts_profile_begin(ops.handle), "vts_profile_begin")
     p0.record(stream)
@@ -313,7 +317,8 @@ def main() -> None:
     p1.record(stream)
     _lib.check(lib.vts_profile_end(ops.handle, prof), "vts_profile_end")
     prof_region_ms = p0.elapsed_time(p1)
-    gs_total_ms, gs_n, tri_fine_ms, tri_fine_n, pair_fine_ms, pair_fine_n = list(prof)
+    (gs_total_ms, gs_n, tri_fine_ms, tri_fine_n, pair_fine_ms, pair_fine_n, asc_fine_ms,
+     asc_fine_n) = list(prof)
 
     # --- e2e through the C-ABI with host buffers (pinned), copies inside the timed region
     rhs_host = torch.as_tensor(rhs_h).pin_memory()
@@ -345,7 +350,9 @@ def main() -> None:
 
     # dominant kernel of the MINRES iteration: the wavefront Gauss-Seidel kernel,
     # k_gs_pair (both sweeps of a smoothing step) when the pipelined pairs ran,
-    # else k_gs_tri; roofline unit = one finest-level launch
+    # else k_gs_tri; roofline unit = one finest-level launch (for the pair: the
+    # descent pair, the launch the committed ncu capture is of; the ascent pair's
+    # time and bytes are reported beside it)
     if pair_fine_n > 0:
         dom, dom_bytes, dom_ms, dom_n = "k_gs_pair", bytes_["gs_pair_fine"], pair_fine_ms, pair_fine_n
     else:
@@ -387,6 +394,10 @@ def main() -> None:
                      "algorithmic_bytes_per_launch": dom_bytes, "launch_ms": dom_avg_ms,
                      "launches_in_profiled_region": int(gs_n), "finest_launches": int(dom_n),
                      "share_of_step": gs_total_ms / prof_region_ms,
+                     "ascent_pair": ({"launch_ms": asc_fine_ms / asc_fine_n,
+                                      "algorithmic_bytes_per_launch": bytes_["gs_pair_asc_fine"],
+                                      "achieved": gbs(bytes_["gs_pair_asc_fine"], asc_fine_ms / asc_fine_n)}
+                                     if asc_fine_n > 0 else None),
                      "note": "latency-bound: a sweep is a wavefront of nx + 2 ny dependent steps "
                              "(DESIGN.md, 'Gauss-Seidel depth'); traffic from profiles/ ncu --set full"},
         "kernels": {

@@ -198,9 +198,9 @@ int64_t vts_kernel_launches(const vts_ctx* ctx);
  * vts_profile_end every launch of a wavefront Gauss-Seidel kernel (a single
  * sweep, or a pipelined pair of sweeps) is bracketed by a CUDA event pair on
  * the context stream.  vts_profile_end synchronises the stream and writes
- * HOST out[6] = {total ms of those launches, number of launches, ms and count
- * of the finest-level single-sweep launches, ms and count of the finest-level
- * pair launches}.  Used by bench.py for the dominant kernel's share of a
+ * HOST out[8] = {total ms of those launches, number of launches, then ms and
+ * count of the finest-level single-sweep launches, descent pairs (zero guess
+ * + forward) and ascent pairs (backward + backward)}.  Used by bench.py for the dominant kernel's share of a
  * MINRES iteration; costs two event records per launch while enabled.
  */
 int vts_profile_begin(vts_ctx* ctx);

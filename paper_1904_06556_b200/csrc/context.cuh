@@ -84,7 +84,7 @@ struct Ctx {
   struct ProfEv {
     cudaEvent_t a, b;
     int level;
-    int pair;  // 1: k_gs_pair (two sweeps), 0: k_gs_tri
+    int pair;  // 0: k_gs_tri, 1: k_gs_pair descent (zero guess + forward), 2: k_gs_pair ascent
   };
   std::vector<ProfEv> prof_ev;
   size_t prof_used = 0;  // padded device arrays owned by the context

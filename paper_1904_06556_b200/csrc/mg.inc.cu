@@ -1352,7 +1352,7 @@ static int gs_pair(Ctx* c, int k, const double* b, double* x, bool forward, bool
     return 5;
   const unsigned long long epoch = ++L.pair_epoch;
   Ctx::ProfEv* pe = nullptr;
-  if (int rc = prof_begin(c, L, 1, &pe)) return rc;
+  if (int rc = prof_begin(c, L, zero_a ? 1 : 2, &pe)) return rc;  // 1: descent pair, 2: ascent pair
   if (forward && zero_a)
     VTS_CUDA(cudaLaunchKernelEx(&cfg, k_gs_pair<true, true>, L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, bands, mSA,
                                 mPA, mQA, mSB, mBB, mQB, mXB, mUB, mXA, L.x1, x, L.gs_flags, L.gs_groups, epoch, b,
@@ -1521,8 +1521,9 @@ int mg_setup(Ctx* c, double shift_scale) {
 // on the finest level, ms[3] the same on the second-finest level, ms[4]
 // finest residual, ms[5] mg_setup (stencil + Galerkin chain + coarse factor).
 // per-launch timing of the wavefront kernels between profile_begin and
-// profile_end: out = {total ms, launches, finest-level k_gs_tri ms, its
-// launches, finest-level k_gs_pair ms, its launches}
+// profile_end: out = {total ms, launches, then ms and launches on the finest
+// level of: k_gs_tri, k_gs_pair descent pairs (zero guess + forward),
+// k_gs_pair ascent pairs (backward + backward)}
 int profile_begin(Ctx* c) {
   c->prof = true;
   c->prof_used = 0;
@@ -1532,8 +1533,8 @@ int profile_begin(Ctx* c) {
 int profile_end(Ctx* c, double* out) {
   c->prof = false;
   VTS_CUDA(cudaStreamSynchronize(c->stream));
-  double tot = 0.0, fine[2] = {0.0, 0.0};
-  long long nf[2] = {0, 0};
+  double tot = 0.0, fine[3] = {0.0, 0.0, 0.0};
+  long long nf[3] = {0, 0, 0};
   for (size_t i = 0; i < c->prof_used; ++i) {
     float t = 0.f;
     VTS_CUDA(cudaEventElapsedTime(&t, c->prof_ev[i].a, c->prof_ev[i].b));
@@ -1549,6 +1550,8 @@ int profile_end(Ctx* c, double* out) {
   out[3] = (double)nf[0];
   out[4] = fine[1];
   out[5] = (double)nf[1];
+  out[6] = fine[2];
+  out[7] = (double)nf[2];
   c->prof_used = 0;
   return 0;
 }
