@@ -77,7 +77,7 @@ struct Ctx {
   MinresDev* hmst = nullptr;    // pinned host mirror
 
   long long launches = 0;
-  std::vector<void*> allocs;  // padded device arrays owned by the context
+  std::vector<void*> allocs;  // the device arena holding every array of the context
 
   // optional per-launch timing of the wavefront kernel (vts_profile_begin/end)
   bool prof = false;

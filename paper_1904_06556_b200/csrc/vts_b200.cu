@@ -10,6 +10,8 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <type_traits>
+#include <utility>
 #include <vector>
 
 #include <cuda.h>
@@ -50,50 +52,82 @@ static int ensure_ke(Ctx* c) {
   return 0;
 }
 
+// Every device array of a context lives in ONE allocation (cudaMalloc and
+// cudaFree cost tens to hundreds of microseconds each, and a context has ~130
+// arrays).  Creation records requests, then `Arena::commit` allocates, zeroes
+// the whole block once and hands out 256-byte aligned pointers.
+// Pinned host scalars ([64] doubles, then the MINRES state mirror) come from a
+// process-wide pool: cudaMallocHost costs milliseconds, and solvers create a
+// context per problem.  free_ctx releases a block only after cudaFree has
+// synchronised the device, so no copy into it can still be in flight.
+constexpr size_t kPinnedBytes = ((64 * sizeof(double) + sizeof(MinresDev)) + 255) & ~size_t(255);
+static std::mutex g_pinned_mutex;
+static std::vector<void*> g_pinned_free;
+
+static void* pinned_acquire() {
+  {
+    std::lock_guard<std::mutex> lock(g_pinned_mutex);
+    if (!g_pinned_free.empty()) {
+      void* p = g_pinned_free.back();
+      g_pinned_free.pop_back();
+      return p;
+    }
+  }
+  void* p = nullptr;
+  return cudaMallocHost(&p, kPinnedBytes) == cudaSuccess ? p : nullptr;
+}
+
+static void pinned_release(void* p) {
+  std::lock_guard<std::mutex> lock(g_pinned_mutex);
+  g_pinned_free.push_back(p);
+}
+
+#ifndef VTS_CREATE_MARK
+#define VTS_CREATE_MARK(s)
+#endif
+
+struct Arena {
+  struct Req {
+    void** slot;
+    size_t offset;  // bytes from the arena base to the handed-out pointer
+  };
+  std::vector<Req> reqs;
+  size_t used = 0;
+
+  size_t take(void** slot, size_t bytes, size_t pad_bytes) {
+    const size_t start = (used + 255) & ~size_t(255);
+    used = start + std::max<size_t>(bytes + 2 * pad_bytes, 1);
+    reqs.push_back({slot, start + pad_bytes});
+    return start + pad_bytes;
+  }
+  int commit(Ctx* c) {
+    char* base = nullptr;
+    VTS_CUDA(cudaMalloc(reinterpret_cast<void**>(&base), std::max<size_t>(used, 256)));
+    c->allocs.push_back(base);
+    VTS_CUDA(cudaMemset(base, 0, used));
+    for (const Req& r : reqs) *r.slot = base + r.offset;
+    return 0;
+  }
+};
+
 template <typename T>
-static int dalloc(T** p, size_t count) {
-  VTS_CUDA(cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T)));
-  return 0;
+static size_t dalloc(Arena& a, T** p, size_t count) {
+  return a.take(reinterpret_cast<void**>(p), count * sizeof(T), 0);
 }
 
 // zeroed array of `count` doubles with `pad` zero doubles before and after
 // (the skewed TMA boxes of the Gauss-Seidel wavefront read into the padding)
-static int dalloc_pad(Ctx* c, double** p, size_t count, size_t pad) {
-  double* base = nullptr;
-  const size_t total = count + 2 * pad;
-  VTS_CUDA(cudaMalloc(reinterpret_cast<void**>(&base), total * sizeof(double)));
-  VTS_CUDA(cudaMemset(base, 0, total * sizeof(double)));
-  c->allocs.push_back(base);
-  *p = base + pad;
-  return 0;
+static void dalloc_pad(Arena& a, double** p, size_t count, size_t pad) {
+  a.take(reinterpret_cast<void**>(p), count * sizeof(double), pad * sizeof(double));
 }
 
 static void free_ctx(Ctx* c) {
-  for (auto& L : c->lv) {
-    cudaFree(const_cast<uint8_t*>(L.d.free_mask));
-    cudaFree(const_cast<int32_t*>(L.d.free2grid));
-    cudaFree(L.grid2free);
-    cudaFree(L.gs_flags);
-  }
   for (void* p : c->allocs) cudaFree(p);
   for (auto& e : c->prof_ev) {
     cudaEventDestroy(e.a);
     cudaEventDestroy(e.b);
   }
-  cudaFree(c->u_grid);
-  cudaFree(c->rho_hat);
-  cudaFree(c->chat);
-  cudaFree(c->d_corner);
-  cudaFree(c->chol);
-  cudaFree(c->chol_status);
-  cudaFree(c->rap_tmp);
-  cudaFree(c->partials);
-  cudaFree(c->counters);
-  cudaFree(c->dscal);
-  cudaFree(c->dflags);
-  cudaFree(c->mst);
-  if (c->hscal) cudaFreeHost(c->hscal);
-  if (c->hmst) cudaFreeHost(c->hmst);
+  if (c->hscal) pinned_release(c->hscal);
   {
     std::lock_guard<std::mutex> lock(g_ke_mutex);
     if (g_ke_owner == c) g_ke_owner = nullptr;
@@ -126,6 +160,12 @@ static int create(Ctx** out, int levels, const int32_t* ex, const int32_t* ey, c
     free_ctx(c);
     return rc;
   };
+  Arena arena;
+  // the per-level index maps (free mask, free->grid, grid->free) are placed
+  // first in the arena; they are written into one host image and uploaded
+  // with one copy after the allocation (free->grid is sized by ng, an upper
+  // bound of the free count)
+  std::vector<size_t> map_off(3 * levels);
   for (int k = 0; k < levels; ++k) {
     LevelBuf& L = c->lv[k];
     L.d.ex = ex[k];
@@ -134,22 +174,30 @@ static int create(Ctx** out, int levels, const int32_t* ex, const int32_t* ey, c
     L.d.ny = ey[k] + 1;
     L.d.nnodes = L.d.nx * L.d.ny;
     L.d.ngrid = 2 * L.d.nnodes;
+    const size_t ng = L.d.ngrid;
+    map_off[3 * k] = dalloc(arena, const_cast<uint8_t**>(&L.d.free_mask), ng);
+    map_off[3 * k + 1] = dalloc(arena, const_cast<int32_t**>(&L.d.free2grid), ng);
+    map_off[3 * k + 2] = dalloc(arena, &L.grid2free, ng);
+  }
+  std::vector<char> image(arena.used);
+  for (int k = 0; k < levels; ++k) {
+    LevelBuf& L = c->lv[k];
     const int ng = L.d.ngrid;
-    std::vector<uint8_t> mask(ng);
-    std::vector<int32_t> g2f(ng);
-    std::vector<int32_t> f2g;
-    f2g.reserve(ng);
+    uint8_t* mask = reinterpret_cast<uint8_t*>(image.data() + map_off[3 * k]);
+    int32_t* f2g = reinterpret_cast<int32_t*>(image.data() + map_off[3 * k + 1]);
+    int32_t* g2f = reinterpret_cast<int32_t*>(image.data() + map_off[3 * k + 2]);
+    const int64_t* dm = dof_maps[k];
     int nfree = 0;
     for (int i = 0; i < ng; ++i) {
-      const int64_t d = dof_maps[k][i];
+      const int64_t d = dm[i];
       if (d >= 0) {
         if (d != nfree) {
           set_error(VTS_E_ARGUMENT, "vts_ctx_create: dof map must number free dofs node-major in order");
           return fail(VTS_E_ARGUMENT);
         }
         mask[i] = 1;
-        g2f[i] = nfree++;
-        f2g.push_back(i);
+        g2f[i] = nfree;
+        f2g[nfree++] = i;
       } else {
         mask[i] = 0;
         g2f[i] = -1;
@@ -160,53 +208,60 @@ static int create(Ctx** out, int levels, const int32_t* ex, const int32_t* ey, c
       return fail(VTS_E_ARGUMENT);
     }
     L.d.nfree = nfree;
-    uint8_t* fm_d = nullptr;
-    int32_t* f2g_d = nullptr;
-    const int arc = dalloc(&fm_d, ng) || dalloc(&f2g_d, nfree);
-    L.d.free_mask = fm_d;
-    L.d.free2grid = f2g_d;
+  }
+  VTS_CREATE_MARK("maps");
+  const size_t upload_end = arena.used;
+  for (int k = 0; k < levels; ++k) {
+    LevelBuf& L = c->lv[k];
+    const size_t ng = L.d.ngrid;
     L.pad_nodes = (size_t)kPadRows * L.d.nx;
-    if (arc || dalloc(&L.grid2free, ng) ||
-        dalloc_pad(c, &L.d.stL, (size_t)L.d.nnodes * kHalf, L.pad_nodes * kHalf) ||
-        dalloc_pad(c, &L.d.stU, (size_t)L.d.nnodes * kHalf, L.pad_nodes * kHalf) ||
-        dalloc_pad(c, &L.d.border, ng + 1, 2 * L.pad_nodes) || dalloc_pad(c, &L.b, ng + 1, 2 * L.pad_nodes) ||
-        dalloc_pad(c, &L.x, ng + 1, 2 * L.pad_nodes) || dalloc_pad(c, &L.r, ng + 1, 2 * L.pad_nodes) ||
-        dalloc_pad(c, &L.x1, ng + 1, 2 * L.pad_nodes))
-      return fail(VTS_E_CUDA);
+    dalloc_pad(arena, &L.d.stL, (size_t)L.d.nnodes * kHalf, L.pad_nodes * kHalf);
+    dalloc_pad(arena, &L.d.stU, (size_t)L.d.nnodes * kHalf, L.pad_nodes * kHalf);
+    dalloc_pad(arena, &L.d.border, ng + 1, 2 * L.pad_nodes);
+    dalloc_pad(arena, &L.b, ng + 1, 2 * L.pad_nodes);
+    dalloc_pad(arena, &L.x, ng + 1, 2 * L.pad_nodes);
+    dalloc_pad(arena, &L.r, ng + 1, 2 * L.pad_nodes);
+    dalloc_pad(arena, &L.x1, ng + 1, 2 * L.pad_nodes);
     L.gs_groups = div_up(L.d.ny, 8);  // >= bands of any GS row-band height used
-    if (dalloc(&L.gs_flags, 3 * (size_t)L.gs_groups)) return fail(VTS_E_CUDA);
-    if (cudaMemcpy(const_cast<uint8_t*>(L.d.free_mask), mask.data(), ng, cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(const_cast<int32_t*>(L.d.free2grid), f2g.data(), sizeof(int32_t) * nfree, cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(L.grid2free, g2f.data(), sizeof(int32_t) * ng, cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemset(L.gs_flags, 0, sizeof(unsigned long long) * 3 * L.gs_groups) != cudaSuccess) {
-      set_error(VTS_E_CUDA, "vts_ctx_create: device upload failed");
-      return fail(VTS_E_CUDA);
-    }
+    dalloc(arena, &L.gs_flags, 3 * (size_t)L.gs_groups);
   }
   const LevelBuf& F = c->lv[levels - 1];
   c->n = F.d.nfree;
   c->m = F.d.ex * F.d.ey;
   const int len = F.d.ngrid + 1;
   c->fvec.assign(kNumFineVecs, nullptr);
-  for (int i = 0; i < kNumFineVecs; ++i) {
-    if (dalloc_pad(c, &c->fvec[i], std::max(len, c->m + 1), 2 * F.pad_nodes)) return fail(VTS_E_CUDA);
-  }
-  if (dalloc(&c->u_grid, len) || dalloc(&c->rho_hat, c->m) || dalloc(&c->chat, c->m) || dalloc(&c->d_corner, 1))
-    return fail(VTS_E_CUDA);
+  for (int i = 0; i < kNumFineVecs; ++i) dalloc_pad(arena, &c->fvec[i], std::max(len, c->m + 1), 2 * F.pad_nodes);
+  dalloc(arena, &c->u_grid, len);
+  dalloc(arena, &c->rho_hat, c->m);
+  dalloc(arena, &c->chat, c->m);
+  dalloc(arena, &c->d_corner, 1);
   c->N0 = c->lv[0].d.nfree + 1;
-  if (dalloc(&c->chol, (size_t)c->N0 * c->N0) || dalloc(&c->chol_status, 1)) return fail(VTS_E_CUDA);
+  dalloc(arena, &c->chol, (size_t)c->N0 * c->N0);
+  dalloc(arena, &c->chol_status, 1);
   const size_t rap = levels > 1 ? (size_t)c->lv[levels - 2].d.nnodes * kStencilStride : 1;
-  if (dalloc(&c->rap_tmp, rap)) return fail(VTS_E_CUDA);
-  if (dalloc(&c->partials, (size_t)kMaxBlocks * kMaxPartials) || dalloc(&c->counters, 64) ||
-      dalloc(&c->dscal, 64) || dalloc(&c->dflags, 4) || dalloc(&c->mst, 1))
-    return fail(VTS_E_CUDA);
-  cudaMemset(c->counters, 0, sizeof(unsigned) * 64);
-  cudaMemset(c->dscal, 0, sizeof(double) * 64);
-  if (cudaMallocHost(reinterpret_cast<void**>(&c->hscal), sizeof(double) * 64) != cudaSuccess ||
-      cudaMallocHost(reinterpret_cast<void**>(&c->hmst), sizeof(MinresDev)) != cudaSuccess) {
+  dalloc(arena, &c->rap_tmp, rap);
+  dalloc(arena, &c->partials, (size_t)kMaxBlocks * kMaxPartials);
+  dalloc(arena, &c->counters, 64);
+  dalloc(arena, &c->dscal, 64);
+  dalloc(arena, &c->dflags, 4);
+  dalloc(arena, &c->mst, 1);
+  VTS_CREATE_MARK("plan");
+  if (arena.commit(c)) return fail(VTS_E_CUDA);
+  VTS_CREATE_MARK("commit");
+  {
+    char* base = static_cast<char*>(c->allocs.back());
+    if (cudaMemcpy(base, image.data(), upload_end, cudaMemcpyHostToDevice) != cudaSuccess) {
+      set_error(VTS_E_CUDA, "vts_ctx_create: device upload failed");
+      return fail(VTS_E_CUDA);
+    }
+  }
+  VTS_CREATE_MARK("upload");
+  if (!(c->hscal = static_cast<double*>(pinned_acquire()))) {
     set_error(VTS_E_CUDA, "vts_ctx_create: pinned allocation failed");
     return fail(VTS_E_CUDA);
   }
+  c->hmst = reinterpret_cast<MinresDev*>(c->hscal + 64);
+  VTS_CREATE_MARK("pinned");
   if (cudaDeviceSynchronize() != cudaSuccess) {
     set_error(VTS_E_CUDA, "vts_ctx_create: device synchronisation failed");
     return fail(VTS_E_CUDA);
