@@ -14,7 +14,8 @@ import os
 import subprocess
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_build", "libvts_b200.so")
+# VTS_LIB overrides the library path (A/B comparisons of two builds; tools/checks)
+LIB_PATH = os.environ.get("VTS_LIB") or os.path.join(_HERE, "_build", "libvts_b200.so")
 
 VTS_OK = 0
 VTS_E_INDEFINITE = 1

@@ -88,17 +88,25 @@ __global__ void __launch_bounds__(128) k_fine_stencil(int nx, int ny, int ex, in
   const int nd = blockIdx.x * blockDim.x + threadIdx.x;
   if (nd >= nx * ny) return;
   const int ix = nd % nx, iy = nd / nx;
-  const NodeElems ne = node_elems(ix, iy, ex, ey);
   // corner offsets of the element's local nodes relative to its node 0
-  const int cdx[4] = {0, 1, 1, 0}, cdy[4] = {0, 0, 1, 1};
+  constexpr int cdx[4] = {0, 1, 1, 0}, cdy[4] = {0, 0, 1, 1};
   double blk[36];
 #pragma unroll
   for (int i = 0; i < 36; ++i) blk[i] = 0.0;
   bool seen[36];
 #pragma unroll
   for (int i = 0; i < 36; ++i) seen[i] = false;
-  for (int k = 0; k < ne.cnt; ++k) {
-    const int e = ne.e[k], li = ne.li[k];
+  // the four elements around the node in increasing element index (node_elems
+  // order), unrolled so the node's local corner li, and with it every block
+  // slot, is a compile-time constant (blk stays in registers); an element off
+  // the mesh reads element 0 and contributes nothing
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    constexpr int kli[4] = {2, 3, 1, 0};
+    const int li = kli[k];
+    const int exi = ix - 1 + (k & 1), eyi = iy - 1 + (k >> 1);
+    const bool ve = exi >= 0 && exi < ex && eyi >= 0 && eyi < ey;
+    const int e = ve ? exi + ex * eyi : 0;
     int n4[4];
     elem_nodes(e, ex, nx, n4);
     double ue[8], w[8];
@@ -117,8 +125,8 @@ __global__ void __launch_bounds__(128) k_fine_stencil(int nx, int ny, int ex, in
           const double v = __dadd_rn(__dmul_rn(rh, c_ke[(2 * li + r) * 8 + 2 * lj + cc]),
                                      __dmul_rn(ch, __dmul_rn(w[2 * li + r], w[2 * lj + cc])));
           const int slot = 4 * b + 2 * r + cc;
-          blk[slot] = seen[slot] ? __dadd_rn(blk[slot], v) : v;
-          seen[slot] = true;
+          blk[slot] = ve ? (seen[slot] ? __dadd_rn(blk[slot], v) : v) : blk[slot];
+          seen[slot] = seen[slot] || ve;
         }
     }
   }
@@ -140,58 +148,87 @@ __global__ void __launch_bounds__(128) k_fine_stencil(int nx, int ny, int ex, in
 }
 
 // ---------------------------------------------------------------------------
-// coarse operator P^T A P (unsymmetrised) on coarse node I
+// coarse operator P^T A P (unsymmetrised): block D of coarse node I
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_rap(int fnx, int fny, const double* __restrict__ fL,
-                                           const double* __restrict__ fU,
-                                           const uint8_t* __restrict__ ffm, int cnx, int cny,
-                                           const uint8_t* __restrict__ cfm, double* __restrict__ out) {
-  const int cn = blockIdx.x * blockDim.x + threadIdx.x;
-  if (cn >= cnx * cny) return;
-  const int cx = cn % cnx, cy = cn / cnx;
-  double acc[36];
+// One thread per (I, D), D = the 3x3 position of the coarse neighbour J = I + D.
+// Entry (r, c) of the block is sum_{fine i near I} sum_{fine j = i + b}
+// P(i, I)_r A(i, j)_{rc} P(j, J)_c, accumulated with one fma per (i, b) in the
+// order fine row, fine column, b; at most one parent of j is J, so each entry
+// sees exactly the chain a whole-node loop over (i, b, parents of j) gives it.
+// A block is 9 warps over the same 32 coarse nodes, warp w computing D = w, so
+// D is warp-uniform and, per D, the (i, b) pairs that can reach J and both
+// prolongation weights are compile-time: only grid edges and Dirichlet masks
+// remain, as selects over loads from clamped (always valid) addresses.
+template <int DX, int DY>
+VTS_DEVICE_INLINE void rap_block(int fnx, int fny, const double* __restrict__ fL, const double* __restrict__ fU,
+                                 const uint8_t* __restrict__ ffm, int cx, int cy, uchar2 fI, uchar2 fJ,
+                                 double (&acc)[4]) {
 #pragma unroll
-  for (int i = 0; i < 36; ++i) acc[i] = 0.0;
-  const uchar2 fI = *reinterpret_cast<const uchar2*>(cfm + 2 * cn);
-  for (int fy = 2 * cy - 1; fy <= 2 * cy + 1; ++fy) {
-    if (fy < 0 || fy >= fny) continue;
-    for (int fx = 2 * cx - 1; fx <= 2 * cx + 1; ++fx) {
-      if (fx < 0 || fx >= fnx) continue;
-      const int fi = fx + fnx * fy;
+  for (int oy = -1; oy <= 1; ++oy) {
+#pragma unroll
+    for (int ox = -1; ox <= 1; ++ox) {
+      const int fx = 2 * cx + ox, fy = 2 * cy + oy;
+      const bool vi = fy >= 0 && fy < fny && fx >= 0 && fx < fnx;
+      const int fi = vi ? fx + fnx * fy : 0;
       const uchar2 ff = *reinterpret_cast<const uchar2*>(ffm + 2 * fi);
-      const double wI = pweight(fx, fy, cx, cy);
+      const double wI = (ox == 0 ? 1.0 : 0.5) * (oy == 0 ? 1.0 : 0.5);
       const double pr0 = (ff.x && fI.x) ? wI : 0.0, pr1 = (ff.y && fI.y) ? wI : 0.0;
-      if (pr0 == 0.0 && pr1 == 0.0) continue;
+      const bool use_i = vi && !(pr0 == 0.0 && pr1 == 0.0);
+#pragma unroll
       for (int b = 0; b < 9; ++b) {
-        const int jx = fx + b % 3 - 1, jy = fy + b / 3 - 1;
-        if (jx < 0 || jx >= fnx || jy < 0 || jy >= fny) continue;
+        const int bx = b % 3 - 1, by = b / 3 - 1;
+        // j - 2J per axis; J is a parent of j iff both lie in [-1, 1]
+        const int djx = ox + bx - 2 * DX, djy = oy + by - 2 * DY;
+        if (djx < -1 || djx > 1 || djy < -1 || djy > 1) continue;  // compile-time
+        const int jx = fx + bx, jy = fy + by;
+        const bool v = use_i && jx >= 0 && jx < fnx && jy >= 0 && jy < fny;
+        const int fj_i = v ? jx + fnx * jy : 0;
         const double a00 = stencil_entry(fL, fU, fi, b, 0, 0), a01 = stencil_entry(fL, fU, fi, b, 0, 1);
         const double a10 = stencil_entry(fL, fU, fi, b, 1, 0), a11 = stencil_entry(fL, fU, fi, b, 1, 1);
-        const uchar2 fj = *reinterpret_cast<const uchar2*>(ffm + 2 * (jx + fnx * jy));
-        // coarse parents of fine node j (one per even, two per odd coordinate)
-        int qxs[2], qys[2];
-        const int nqx = parents(jx, qxs), nqy = parents(jy, qys);
-        for (int iqy = 0; iqy < nqy; ++iqy) {
-          for (int iqx = 0; iqx < nqx; ++iqx) {
-            const int qx = qxs[iqx], qy = qys[iqy];
-            const int Dx = qx - cx, Dy = qy - cy;
-            if (Dx < -1 || Dx > 1 || Dy < -1 || Dy > 1) continue;
-            const double wJ = pweight(jx, jy, qx, qy);
-            const uchar2 fJ = *reinterpret_cast<const uchar2*>(cfm + 2 * (qx + cnx * qy));
-            const double pc0 = (fj.x && fJ.x) ? wJ : 0.0, pc1 = (fj.y && fJ.y) ? wJ : 0.0;
-            const int D = (Dy + 1) * 3 + (Dx + 1);
-            acc[4 * D + 0] = fma(pr0 * a00, pc0, acc[4 * D + 0]);
-            acc[4 * D + 1] = fma(pr0 * a01, pc1, acc[4 * D + 1]);
-            acc[4 * D + 2] = fma(pr1 * a10, pc0, acc[4 * D + 2]);
-            acc[4 * D + 3] = fma(pr1 * a11, pc1, acc[4 * D + 3]);
-          }
-        }
+        const uchar2 fj = *reinterpret_cast<const uchar2*>(ffm + 2 * fj_i);
+        const double wJ = (djx == 0 ? 1.0 : 0.5) * (djy == 0 ? 1.0 : 0.5);
+        // an invalid pair adds an exact zero (finite operands, zero weight),
+        // which keeps the loop branch-free so every load can issue up front
+        const double pc0 = (v && fj.x && fJ.x) ? wJ : 0.0, pc1 = (v && fj.y && fJ.y) ? wJ : 0.0;
+        acc[0] = fma(pr0 * a00, pc0, acc[0]);
+        acc[1] = fma(pr0 * a01, pc1, acc[1]);
+        acc[2] = fma(pr1 * a10, pc0, acc[2]);
+        acc[3] = fma(pr1 * a11, pc1, acc[3]);
       }
     }
   }
-  double* o = out + (size_t)cn * kStencilStride;
-#pragma unroll
-  for (int i = 0; i < 36; i += 2) *reinterpret_cast<double2*>(o + i) = make_double2(acc[i], acc[i + 1]);
+}
+
+constexpr int kRapNodes = 32;  // coarse nodes per block (one per lane)
+
+__global__ void __launch_bounds__(9 * kRapNodes) k_rap(int fnx, int fny, const double* __restrict__ fL,
+                                                      const double* __restrict__ fU,
+                                                      const uint8_t* __restrict__ ffm, int cnx, int cny,
+                                                      const uint8_t* __restrict__ cfm, double* __restrict__ out) {
+  const int D = threadIdx.x / kRapNodes;
+  const int cn = blockIdx.x * kRapNodes + threadIdx.x % kRapNodes;
+  if (cn >= cnx * cny) return;
+  const int cx = cn % cnx, cy = cn / cnx;
+  const int qx = cx + D % 3 - 1, qy = cy + D / 3 - 1;  // coarse neighbour J
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  if (qx >= 0 && qx < cnx && qy >= 0 && qy < cny) {
+    const uchar2 fI = *reinterpret_cast<const uchar2*>(cfm + 2 * cn);
+    const uchar2 fJ = *reinterpret_cast<const uchar2*>(cfm + 2 * (qx + cnx * qy));
+    switch (D) {
+      case 0: rap_block<-1, -1>(fnx, fny, fL, fU, ffm, cx, cy, fI, fJ, acc); break;
+      case 1: rap_block<0, -1>(fnx, fny, fL, fU, ffm, cx, cy, fI, fJ, acc); break;
+      case 2: rap_block<1, -1>(fnx, fny, fL, fU, ffm, cx, cy, fI, fJ, acc); break;
+      case 3: rap_block<-1, 0>(fnx, fny, fL, fU, ffm, cx, cy, fI, fJ, acc); break;
+      case 4: rap_block<0, 0>(fnx, fny, fL, fU, ffm, cx, cy, fI, fJ, acc); break;
+      case 5: rap_block<1, 0>(fnx, fny, fL, fU, ffm, cx, cy, fI, fJ, acc); break;
+      case 6: rap_block<-1, 1>(fnx, fny, fL, fU, ffm, cx, cy, fI, fJ, acc); break;
+      case 7: rap_block<0, 1>(fnx, fny, fL, fU, ffm, cx, cy, fI, fJ, acc); break;
+      default: rap_block<1, 1>(fnx, fny, fL, fU, ffm, cx, cy, fI, fJ, acc); break;
+    }
+  }
+  double* o = out + (size_t)cn * kStencilStride + 4 * D;
+  *reinterpret_cast<double2*>(o) = make_double2(acc[0], acc[1]);
+  *reinterpret_cast<double2*>(o + 2) = make_double2(acc[2], acc[3]);
 }
 
 // (C + C^T)/2 (linalg.py:79) and reciprocal diagonals, written as halves
@@ -1469,7 +1506,7 @@ int mg_setup(Ctx* c, double shift_scale) {
     LevelBuf& F = c->lv[k];
     LevelBuf& C = c->lv[k - 1];
     double* tmp = c->rap_tmp;
-    k_rap<<<div_up(C.d.nnodes, 128), 128, 0, c->stream>>>(F.d.nx, F.d.ny, F.d.stL, F.d.stU, F.d.free_mask, C.d.nx,
+    k_rap<<<div_up(C.d.nnodes, kRapNodes), 9 * kRapNodes, 0, c->stream>>>(F.d.nx, F.d.ny, F.d.stL, F.d.stU, F.d.free_mask, C.d.nx,
                                                            C.d.ny, C.d.free_mask, tmp);
     VTS_LAUNCHED(c);
     k_symmetrize<<<div_up(C.d.nnodes, 128), 128, 0, c->stream>>>(C.d.nx, C.d.ny, tmp, C.d.free_mask, C.d.stL,
