@@ -28,6 +28,10 @@ struct LevelBuf {
   int gs_groups = 0;
   unsigned long long pair_epoch = 0;  // launches of the pipelined sweep pair on this level
   double* x1 = nullptr;               // [ngrid + 1] sweep A's result inside a pair
+  // cross-cluster band handoff rows, 2 x gs_groups x nx nodes (sweep A / single
+  // sweeps, sweep B): each value is its own ready flag (kXferEmpty until the
+  // producing band writes it; the consuming band resets it after reading)
+  double* gs_xfer = nullptr;
   size_t pad_nodes = 0;  // zero nodes before/after stL, stU and every vector of this level
 };
 

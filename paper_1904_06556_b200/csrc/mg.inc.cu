@@ -439,6 +439,7 @@ __global__ void __launch_bounds__(256) k_gs_old(int nx, int ny, int ngrid, const
 #ifdef VTS_GS_PROBE
 __device__ long long g_gs_probe[4 * 256];
 __device__ long long g_gs_probe2[2 * 256];
+__device__ long long g_gs_probe3[2 * 256];  // time inside the step loops, time in the end-of-window handoff
 VTS_DEVICE_INLINE long long gtimer() {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -447,7 +448,10 @@ VTS_DEVICE_INLINE long long gtimer() {
 #endif
 namespace gs {
 constexpr int R = 16;      // grid rows (compute lanes) per band / CTA
-constexpr int W = 17;      // wavefront steps per window (odd: conflict-free lane stride)
+#ifndef VTS_GS_W
+#define VTS_GS_W 17
+#endif
+constexpr int W = VTS_GS_W;  // wavefront steps per window (odd: conflict-free lane stride)
 #ifndef VTS_GS_NS
 #define VTS_GS_NS 2
 #endif
@@ -480,7 +484,7 @@ struct __align__(128) BSlot {  // sweep B's builder inputs
   double u[R][W][18];  // the old-value half-stencil (18 of its 22 doubles)
   double b[R][W][2];   // right-hand side
   double qb[R][W][2];  // border
-  double xb[R + 1][W + 3][2];  // sweep A's result around the window (rows +1, columns +3)
+  double xb[R + 1][W + SKEW + 1][2];  // sweep A's result around the window (rows +1, columns +SKEW+1)
   double xb_pad[8];
 };
 struct Smem {
@@ -542,7 +546,8 @@ struct GsBand {
   const CUtensorMap* mapU;  // sweep B: old-value half-stencil, 18-double box
   double* x;                // the sweep's result
   const double* xa_src;     // bordered vector holding x_alpha (slot ngrid)
-  unsigned long long* flags;   // band-to-band handoff counters of this sweep
+  unsigned long long* flags;   // (unused since the handoff rows) band-to-band handoff counters
+  double* xfer;                // cross-cluster handoff rows of this sweep, [bands][nx] nodes
   unsigned long long* stored;  // sweep A's stored-window counters (pair only)
   unsigned long long epoch;    // pair launch tag of the stored counters
   const double* b;             // ROLE 2 builders: right-hand side, border, old-value half-stencil,
@@ -656,7 +661,6 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
       asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r_above) : "r"(smem_u32(&S.above[0][0])), "r"(crank + 1));
       asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r_mbar) : "r"(smem_u32(&S.full_above[0])), "r"(crank + 1));
     }
-    unsigned long long published = 0;
     for (int w = 0; w < nwin; ++w) {
       const int s = w % NS;
       mbar_wait(&S.full_out[s], (w / NS) & 1);
@@ -675,8 +679,15 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
         const int l = R - 1;
         if (lane < W) {
           const int ix = grid_ix(w, l, lane);
-          if (ix >= 0 && ix < nx)
-            *reinterpret_cast<double2*>(x + 2 * ((size_t)grid_row(l) * nx + ix)) = S.out[s][l][lane];
+          if (ix >= 0 && ix < nx) {
+            const double2 v = S.out[s][l][lane];
+            *reinterpret_cast<double2*>(x + 2 * ((size_t)grid_row(l) * nx + ix)) = v;
+            // the next band is in another cluster: each value is its own ready flag,
+            // no fence or counter (the consumer polls the value slots)
+            if (publish)
+              st_relaxed_v2(G.xfer + 2 * ((size_t)band * nx + (FWD ? ix : nx - 1 - ix)),
+                            make_double2(xfer_canon(v.x), xfer_canon(v.y)));
+          }
         }
         if (dsm_out) {
           // hand the row to the next band of the cluster: one st.async per column into
@@ -700,17 +711,6 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
                          : "memory");
           }
         }
-        if (publish) {
-          __threadfence();
-          __syncwarp();
-          // sweep columns < W*(w+1) - SKEW*(R-1) of the last row are final
-          const long long c = (long long)W * (w + 1) - SKEW * (R - 1);
-          const unsigned long long done = (unsigned long long)(c < 0 ? 0 : (c > nx ? nx : c));
-          if (lane == 0 && done > published) {
-            st_release(flags + band, done);
-            published = done;
-          }
-        }
       }
       __syncwarp();
       if (lane == 0) {
@@ -721,30 +721,28 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
     }
   } else if (warp == 4) {  // ---------------- stager (previous band's last row -> above ring)
     if (has_above && rows_here > 0 && !dsm_in) {
-      const int prev_y = FWD ? grid_row(0) - 1 : grid_row(0) + 1;
-      unsigned long long seen = 0;
+      double* row = G.xfer + 2 * (size_t)(band - 1) * nx;  // the previous band's last row
       // above slot a = w + 1 holds sweep columns W*w + SKEW + [0, W); a = 0 is the preload
       for (int a = 0; a <= nwin; ++a) {
         const int s = a % NSA;
         if (a >= NSA) mbar_wait(&S.empty_above[s], ((a / NSA) - 1) & 1);
         const int c0 = W * (a - 1) + SKEW;
-        const unsigned long long need = (unsigned long long)max(0, min(nx, c0 + W));
-        if (lane == 0)
-          while (seen < need) seen = ld_acquire(flags + band - 1);
-        __syncwarp();
         if (lane < W) {
           const int j = c0 + lane;
           double2 v = make_double2(0.0, 0.0);
           if (j >= 0 && j < nx) {
-            const int ix = FWD ? j : nx - 1 - j;
-            v = __ldcg(reinterpret_cast<const double2*>(x + 2 * ((size_t)prev_y * nx + ix)));
+            do {
+              v = ld_relaxed_v2(row + 2 * j);
+            } while (xfer_empty(v));
+            // empty again for the next launch (each slot is written once per launch)
+            st_relaxed_v2(row + 2 * j, make_double2(__longlong_as_double((long long)kXferEmpty),
+                                                    __longlong_as_double((long long)kXferEmpty)));
           }
           S.above[s][lane] = v;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&S.full_above[s]);
       }
-      if (lane == 0) flags[band - 1] = 0ull;  // consumed by this band only
     }
   } else if (warp == 0) {
     gs_compute<FWD, ZERO>(S, nx, ngrid, band + (ROLE == 2 ? 128 : 0), rows_here, has_above, dsm_in, crank, nwin,
@@ -784,7 +782,7 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
         }
         const int node0 = FWD ? iy0 * nx + W * w : (iyb - R + 2) * nx - W * (w + 1) + SKEW * (R - 1);
         const int c1 = node0 + pad_nodes;
-        const int cx = FWD ? c1 : c1 - (nx - SKEW) - 3;  // backward: one row and 3 nodes earlier
+        const int cx = FWD ? c1 : c1 - (nx - SKEW) - (SKEW + 1);  // backward: one row and SKEW+1 nodes earlier
         mbar_expect_tx(&S.xloaded[sb], (unsigned)sizeof(S.bin[sb].xb));
         tma_load_3d(&S.bin[sb].xb[0][0][0], G.mapX, 0, cx, 0, &S.xloaded[sb]);
       }
@@ -833,9 +831,10 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
         const int n = node0 + k * (nx - SKEW) + p;
         if (n < 0 || n >= nnodes) continue;
         // box coordinates of the node (C) and of its later neighbours NE N NW E (slots 0..3)
-        const int ck = FWD ? k : k + 1, cp = FWD ? p : p + 3;
+        const int ck = FWD ? k : k + 1, cp = FWD ? p : p + SKEW + 1;
         const int nk[4] = {FWD ? k + 1 : k, FWD ? k + 1 : k, FWD ? k + 1 : k, ck};
-        const int np[4] = {FWD ? p + 3 : p, FWD ? p + 2 : p + 1, FWD ? p + 1 : p + 2, FWD ? p + 1 : p + 2};
+        const int np[4] = {FWD ? p + SKEW + 1 : p, FWD ? p + SKEW : p + 1, FWD ? p + SKEW - 1 : p + 2,
+                           FWD ? p + 1 : p + SKEW};
         const BSlot& in = S.bin[sb];
         OldIn o;
 #pragma unroll
@@ -872,10 +871,10 @@ template <bool FWD, bool ZERO>
 __global__ void __launch_bounds__(32 * gs::kWarps, 1)
     k_gs_tri(int nx, int ny, int ngrid, int pad_nodes, int bands, const __grid_constant__ CUtensorMap mapS,
              const __grid_constant__ CUtensorMap mapP, const __grid_constant__ CUtensorMap mapQ,
-             double* __restrict__ x, unsigned long long* flags, const int* skip) {
+             double* __restrict__ x, unsigned long long* flags, double* xfer, const int* skip) {
   if (skip && *skip) return;
   GsBand G{nx, ny, ngrid, pad_nodes, bands, (int)blockIdx.x, &mapS, &mapP, &mapQ, &mapQ, &mapQ, &mapQ, x, x, flags,
-           nullptr, 0ull, nullptr, nullptr, nullptr, nullptr};
+           xfer, nullptr, 0ull, nullptr, nullptr, nullptr, nullptr};
   gs_band<FWD, ZERO, 0>(G);
 }
 
@@ -891,7 +890,8 @@ __global__ void __launch_bounds__(32 * gs::kWarpsPair, 1)
               const __grid_constant__ CUtensorMap mapQB, const __grid_constant__ CUtensorMap mapXB,
               const __grid_constant__ CUtensorMap mapUB, const __grid_constant__ CUtensorMap mapXA,
               double* __restrict__ x1, double* __restrict__ x,
-              unsigned long long* flags, int groups, unsigned long long epoch, const double* __restrict__ b,
+              unsigned long long* flags, double* xfer, int groups, unsigned long long epoch,
+              const double* __restrict__ b,
               const double* __restrict__ border, const double* __restrict__ half_old, const int* skip) {
   if (skip && *skip) return;
   const int nA = (int)gridDim.x / 2;
@@ -899,11 +899,11 @@ __global__ void __launch_bounds__(32 * gs::kWarpsPair, 1)
     // sweep A: with the zero guess P = b - border x_alpha from TMA boxes (mapPA, mapQA);
     // otherwise built from x (mapXA), the old-value half (mapUB), b and border
     GsBand G{nx, ny, ngrid, pad_nodes, bands, (int)blockIdx.x, &mapSA, &mapPA, ZERO_A ? &mapQA : &mapQB, &mapBB,
-             &mapXA, &mapUB, x1, x, flags, flags + 2 * groups, epoch, b, border, half_old, x};
+             &mapXA, &mapUB, x1, x, flags, xfer, flags + 2 * groups, epoch, b, border, half_old, x};
     gs_band<FWD, ZERO_A, 1>(G);
   } else {
     GsBand G{nx, ny, ngrid, pad_nodes, bands, (int)blockIdx.x - nA, &mapSB, &mapSB, &mapQB, &mapBB, &mapXB, &mapUB, x, x,
-             flags + groups, flags + 2 * groups, epoch, b, border, half_old, x1};
+             flags + groups, xfer + 2 * (size_t)groups * nx, flags + 2 * groups, epoch, b, border, half_old, x1};
     gs_band<FWD, false, 2>(G);
   }
 }
@@ -952,7 +952,7 @@ __device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int b
     }
   }
 #ifdef VTS_GS_PROBE
-  long long t_first = 0, t_wait_above = 0, t_wait_in = 0, t_wait_out = 0;
+  long long t_first = 0, t_wait_above = 0, t_wait_in = 0, t_wait_out = 0, t_loop = 0, t_end = 0;
   if (l == 0) g_gs_probe[4 * band] = gtimer();
 #endif
   for (int w = 0; w < nwin; ++w) {
@@ -979,6 +979,9 @@ __device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int b
 #endif
     if (has_above) mbar_wait(&S.full_above[sa], ((w + 1) / NSA) & 1);
     const InSlot& in = S.in[s];
+#ifdef VTS_GS_PROBE
+    const long long tl0 = gtimer();
+#endif
     // branch-free, software-pipelined steps: while step st runs its 5-op
     // recurrence, step st+1's coefficients are loaded and its
     // recurrence-independent partial sums are formed from the window (all
@@ -1064,6 +1067,10 @@ __device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int b
       win[SKEW] = make_double2(r0, r1);
       if (st + 1 < W) cur = nxt;
     }
+#ifdef VTS_GS_PROBE
+    const long long tl1 = gtimer();
+    t_loop += tl1 - tl0;
+#endif
     __syncwarp();
     if (l == 0) {
       mbar_arrive(&S.empty_in[s]);
@@ -1076,6 +1083,10 @@ __device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int b
         mbar_arrive(&S.empty_above[sa]);
       }
     }
+#ifdef VTS_GS_PROBE
+    __syncwarp();
+    t_end += gtimer() - tl1;
+#endif
   }
 #ifdef VTS_GS_PROBE
   if (l == 0) {
@@ -1084,6 +1095,8 @@ __device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int b
     g_gs_probe[4 * band + 3] = t_wait_above;
     g_gs_probe2[2 * band] = t_wait_in;
     g_gs_probe2[2 * band + 1] = t_wait_out;
+    g_gs_probe3[2 * band] = t_loop;
+    g_gs_probe3[2 * band + 1] = t_end;
   }
 #endif
 }
@@ -1299,7 +1312,7 @@ static int launch_tri(Ctx* c, LevelBuf& L, const CUtensorMap& mS, const CUtensor
   Ctx::ProfEv* pe = nullptr;
   if (int rc = prof_begin(c, L, 0, &pe)) return rc;
   VTS_CUDA(cudaLaunchKernelEx(&cfg, k_gs_tri<FWD, ZERO>, L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, bands, mS, mP,
-                              mQ, x, L.gs_flags, skip));
+                              mQ, x, L.gs_flags, L.gs_xfer, skip));
   VTS_LAUNCHED(c);
   if (pe) VTS_CUDA(cudaEventRecord(pe->b, c->stream));
   return 0;
@@ -1381,26 +1394,26 @@ static int gs_pair(Ctx* c, int k, const double* b, double* x, bool forward, bool
   if (encode_skewed(&mSA, solve_half, kHalf, L)) return 5;
   mSB = mSA;
   if (encode_skewed(&mBB, b, 2, L) || encode_skewed(&mQB, L.d.border, 2, L) ||
-      encode_skewed(&mXB, L.x1, 2, L, gs::R + 1, gs::W + 3) || encode_skewed(&mUB, old_half, kHalf, L, gs::R, gs::W, 18))
+      encode_skewed(&mXB, L.x1, 2, L, gs::R + 1, gs::W + gs::SKEW + 1) || encode_skewed(&mUB, old_half, kHalf, L, gs::R, gs::W, 18))
     return 5;
   // sweep A's boxes: b and border (zero guess), or x_old around each window (built P)
   if (encode_skewed(&mPA, b, 2, L) || encode_skewed(&mQA, L.d.border, 2, L) ||
-      encode_skewed(&mXA, x, 2, L, gs::R + 1, gs::W + 3))
+      encode_skewed(&mXA, x, 2, L, gs::R + 1, gs::W + gs::SKEW + 1))
     return 5;
   const unsigned long long epoch = ++L.pair_epoch;
   Ctx::ProfEv* pe = nullptr;
   if (int rc = prof_begin(c, L, zero_a ? 1 : 2, &pe)) return rc;  // 1: descent pair, 2: ascent pair
   if (forward && zero_a)
     VTS_CUDA(cudaLaunchKernelEx(&cfg, k_gs_pair<true, true>, L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, bands, mSA,
-                                mPA, mQA, mSB, mBB, mQB, mXB, mUB, mXA, L.x1, x, L.gs_flags, L.gs_groups, epoch, b,
+                                mPA, mQA, mSB, mBB, mQB, mXB, mUB, mXA, L.x1, x, L.gs_flags, L.gs_xfer, L.gs_groups, epoch, b,
                                 (const double*)L.d.border, old_half, skip));
   else if (forward)
     VTS_CUDA(cudaLaunchKernelEx(&cfg, k_gs_pair<true, false>, L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, bands, mSA,
-                                mPA, mQA, mSB, mBB, mQB, mXB, mUB, mXA, L.x1, x, L.gs_flags, L.gs_groups, epoch, b,
+                                mPA, mQA, mSB, mBB, mQB, mXB, mUB, mXA, L.x1, x, L.gs_flags, L.gs_xfer, L.gs_groups, epoch, b,
                                 (const double*)L.d.border, old_half, skip));
   else
     VTS_CUDA(cudaLaunchKernelEx(&cfg, k_gs_pair<false, false>, L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, bands,
-                                mSA, mPA, mQA, mSB, mBB, mQB, mXB, mUB, mXA, L.x1, x, L.gs_flags, L.gs_groups, epoch, b,
+                                mSA, mPA, mQA, mSB, mBB, mQB, mXB, mUB, mXA, L.x1, x, L.gs_flags, L.gs_xfer, L.gs_groups, epoch, b,
                                 (const double*)L.d.border, old_half, skip));
   VTS_LAUNCHED(c);
   if (pe) VTS_CUDA(cudaEventRecord(pe->b, c->stream));

@@ -14,6 +14,25 @@ VTS_DEVICE_INLINE unsigned long long ld_acquire(const unsigned long long* p) {
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+// cross-cluster handoff rows: a value slot is empty while either half holds
+// this NaN pattern (arithmetic never produces it: the producer maps it to the
+// default quiet NaN), so every 8-byte half is its own ready flag
+constexpr unsigned long long kXferEmpty = 0xFFFFFFFFFFFFFFFFull;
+VTS_DEVICE_INLINE void st_relaxed_v2(double* p, double2 v) {
+  asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+VTS_DEVICE_INLINE double2 ld_relaxed_v2(const double* p) {
+  double2 v;
+  asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+  return v;
+}
+VTS_DEVICE_INLINE bool xfer_empty(double2 v) {
+  return (unsigned long long)__double_as_longlong(v.x) == kXferEmpty ||
+         (unsigned long long)__double_as_longlong(v.y) == kXferEmpty;
+}
+VTS_DEVICE_INLINE double xfer_canon(double v) {
+  return (unsigned long long)__double_as_longlong(v) == kXferEmpty ? __longlong_as_double(0x7FF8000000000000ll) : v;
+}
 VTS_DEVICE_INLINE void st_release(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }

@@ -224,6 +224,7 @@ static int create(Ctx** out, int levels, const int32_t* ex, const int32_t* ey, c
     dalloc_pad(arena, &L.x1, ng + 1, 2 * L.pad_nodes);
     L.gs_groups = div_up(L.d.ny, 8);  // >= bands of any GS row-band height used
     dalloc(arena, &L.gs_flags, 3 * (size_t)L.gs_groups);
+    dalloc(arena, &L.gs_xfer, 2 * 2 * (size_t)L.gs_groups * L.d.nx);
   }
   const LevelBuf& F = c->lv[levels - 1];
   c->n = F.d.nfree;
@@ -252,6 +253,13 @@ static int create(Ctx** out, int levels, const int32_t* ex, const int32_t* ey, c
     char* base = static_cast<char*>(c->allocs.back());
     if (cudaMemcpy(base, image.data(), upload_end, cudaMemcpyHostToDevice) != cudaSuccess) {
       set_error(VTS_E_CUDA, "vts_ctx_create: device upload failed");
+      return fail(VTS_E_CUDA);
+    }
+  }
+  for (int k = 0; k < levels; ++k) {  // handoff rows start empty (kXferEmpty: all bits set)
+    const LevelBuf& L = c->lv[k];
+    if (cudaMemset(L.gs_xfer, 0xFF, 2 * 2 * (size_t)L.gs_groups * L.d.nx * sizeof(double)) != cudaSuccess) {
+      set_error(VTS_E_CUDA, "vts_ctx_create: device memset failed");
       return fail(VTS_E_CUDA);
     }
   }

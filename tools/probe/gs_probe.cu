@@ -81,11 +81,18 @@ int main(int argc, char** argv) {
     std::vector<long long> pr(4 * 256);
     cudaMemcpyFromSymbol(pr.data(), vts::g_gs_probe, pr.size() * 8);
     const int bands = (L.d.ny + vts::gs::R - 1) / vts::gs::R;
+    std::vector<long long> p2(2 * 256), p3(2 * 256);
+    cudaMemcpyFromSymbol(p2.data(), vts::g_gs_probe2, p2.size() * 8);
+    cudaMemcpyFromSymbol(p3.data(), vts::g_gs_probe3, p3.size() * 8);
     long long t0 = pr[0];
+    const int nwin = (L.d.nx + vts::gs::SKEW * (vts::gs::R - 1) + vts::gs::W - 1) / vts::gs::W;
+    printf("W %d, %d windows per band\n", vts::gs::W, nwin);
     for (int b = 0; b < bands; ++b)
-      printf("band %2d: start %7.1f us  first-window %7.1f  end %7.1f  (dur %6.1f, waiting-above %6.1f us)\n", b,
+      printf("band %2d: start %7.1f us  first-window %7.1f  end %7.1f  (dur %6.1f, above %6.1f, in %5.1f, out %5.1f, "
+             "loops %6.1f = %4.0f ns/step, end-of-window %5.1f us)\n", b,
              (pr[4 * b] - t0) / 1e3, (pr[4 * b + 1] - t0) / 1e3, (pr[4 * b + 2] - t0) / 1e3,
-             (pr[4 * b + 2] - pr[4 * b + 1]) / 1e3, pr[4 * b + 3] / 1e3);
+             (pr[4 * b + 2] - pr[4 * b + 1]) / 1e3, pr[4 * b + 3] / 1e3, p2[2 * b] / 1e3, p2[2 * b + 1] / 1e3,
+             p3[2 * b] / 1e3, p3[2 * b] / double(nwin * vts::gs::W), p3[2 * b + 1] / 1e3);
   }
   {  // pair timeline: sweep A bands (probe slots 0..) and sweep B bands (128..)
     vts::LevelBuf& L = c->lv[levels - 1];
@@ -95,6 +102,8 @@ int main(int argc, char** argv) {
     cudaMemcpyFromSymbol(pr.data(), vts::g_gs_probe, pr.size() * 8);
     std::vector<long long> pr2(2 * 256);
     cudaMemcpyFromSymbol(pr2.data(), vts::g_gs_probe2, pr2.size() * 8);
+    std::vector<long long> pr3(2 * 256);
+    cudaMemcpyFromSymbol(pr3.data(), vts::g_gs_probe3, pr3.size() * 8);
     const int bands = (L.d.ny + vts::gs::R - 1) / vts::gs::R;
     long long t0 = pr[0];
     printf("pair timeline (bwd pair, finest):\n");
@@ -102,9 +111,11 @@ int main(int argc, char** argv) {
       if (b >= bands) continue;
       for (int role = 0; role < 2; ++role) {
         const int i = b + 128 * role;
-        printf("  %s band %2d: start %7.1f  first-window %7.1f  end %7.1f  (dur %6.1f, waiting-above %6.1f, in %6.1f, out %6.1f)\n",
+        printf("  %s band %2d: start %7.1f  first-window %7.1f  end %7.1f  (dur %6.1f, waiting-above %6.1f, in %6.1f, out %6.1f, "
+               "loops %6.1f, end-of-window %5.1f)\n",
                role ? "B" : "A", b, (pr[4 * i] - t0) / 1e3, (pr[4 * i + 1] - t0) / 1e3, (pr[4 * i + 2] - t0) / 1e3,
-               (pr[4 * i + 2] - pr[4 * i + 1]) / 1e3, pr[4 * i + 3] / 1e3, pr2[2 * i] / 1e3, pr2[2 * i + 1] / 1e3);
+               (pr[4 * i + 2] - pr[4 * i + 1]) / 1e3, pr[4 * i + 3] / 1e3, pr2[2 * i] / 1e3, pr2[2 * i + 1] / 1e3,
+               pr3[2 * i] / 1e3, pr3[2 * i + 1] / 1e3);
       }
     }
   }
