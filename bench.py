@@ -287,7 +287,15 @@ def main() -> None:
     # --- per-kernel device times (roofline) and the 100-apply / 100-V-cycle figures
     kms = (ctypes.c_double * 6)()
     _lib.check(lib.vts_time_kernels(ops.handle, 100, kms), "vts_time_kernels")
-    apply_ms, vcycle_ms, gs_fine_ms, gs_l2_ms, resid_ms, setup_ms = list(kms)
+    apply_warm_ms, vcycle_ms, gs_fine_ms, gs_l2_ms, resid_warm_ms, setup_ms = list(kms)
+    # the apply's and the residual's inputs (34 / 118 MB) fit in the 126 MB L2, so
+    # back-to-back launches would read L2: time them cold (L2 overwritten before
+    # each launch), as they run inside a MINRES iteration
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    cold = (ctypes.c_double * 2)()
+    _lib.check(lib.vts_time_cold(ops.handle, 50, flush.data_ptr(), flush.numel(), cold), "vts_time_cold")
+    apply_ms, resid_ms = list(cold)
+    del flush
 
     # --- warm-up then the timed region: K MINRES iterations, device resident
     minres_dev(args.warmup)
@@ -403,6 +411,10 @@ def main() -> None:
         "kernels": {
             "phi_pass_ms": phi_ms, "phi_pass_GBs": gbs(bytes_["phi"], phi_ms),
             "apply_ms": apply_ms, "apply_GBs": gbs(bytes_["apply"], apply_ms), "applies_per_s": 1e3 / apply_ms,
+            "apply_frac": gbs(bytes_["apply"], apply_ms) / peak,
+            "apply_l2_warm_ms": apply_warm_ms, "residual_l2_warm_ms": resid_warm_ms,
+            "note": "apply and residual timed cold (256 MB written between launches); phi pass: 10 back-to-back "
+                    "calls (100 MB of inputs, partly L2-resident)",
             "vcycle_ms": vcycle_ms, "vcycles_per_s": 1e3 / vcycle_ms,
             "gs_fine_sweep_ms": gs_fine_ms, "gs_fine_sweep_GBs": gbs(bytes_["gs_fine_sweep"], gs_fine_ms),
             "gs_level8_sweep_ms": gs_l2_ms, "residual_fine_ms": resid_ms, "mg_setup_ms": setup_ms,

@@ -190,6 +190,15 @@ int vts_penalty_eval(vts_ctx* ctx, int64_t n, const double* tau, double branch, 
  */
 int vts_time_kernels(vts_ctx* ctx, int32_t reps, double* ms);
 
+/*
+ * Benchmark helper (no reference counterpart): cold-L2 device time in ms of
+ * {Newton apply, finest residual}, averaged over `reps` launches; before each
+ * launch the DEVICE buffer `flush` (flush_bytes, larger than the 126 MB L2) is
+ * overwritten on the context stream, and each launch has its own event pair.
+ * HOST `ms` (2 doubles).  Same preconditions as vts_time_kernels.
+ */
+int vts_time_cold(vts_ctx* ctx, int32_t reps, void* flush, int64_t flush_bytes, double* ms);
+
 /* Number of kernels this context launched since creation (evidence counter). */
 int64_t vts_kernel_launches(const vts_ctx* ctx);
 

@@ -58,6 +58,7 @@ SIGNATURES = {
     "vts_gap": (ctypes.c_int, [_P, _P, _D] + [_P] * 6 + [_D, _P, _PD, _PD, _PD, _PD]),
     "vts_penalty_eval": (ctypes.c_int, [_P, _I64, _P, _D, _P, _P, _P, _PU32]),
     "vts_time_kernels": (ctypes.c_int, [_P, _I32, _PD]),
+    "vts_time_cold": (ctypes.c_int, [_P, _I32, _P, ctypes.c_int64, _PD]),
     "vts_kernel_launches": (ctypes.c_int64, [_P]),
     "vts_profile_begin": (ctypes.c_int, [_P]),
     "vts_profile_end": (ctypes.c_int, [_P, _PD]),

@@ -24,6 +24,13 @@ constexpr int kTX = kBX - 1, kTY = kBY - 1;  // owned nodes
 constexpr int kHX = kTX + 2, kHY = kTY + 2;  // halo nodes (33 x 9)
 constexpr int kEX = kBX, kEY = kBY;
 constexpr int kES = kEX * kEY;               // elements per tile
+#ifndef VTS_APPLY_STAGES
+#define VTS_APPLY_STAGES 2
+#endif
+constexpr int kApplyStages = VTS_APPLY_STAGES;  // halo boxes in flight per CTA
+#ifndef VTS_APPLY_MINB
+#define VTS_APPLY_MINB 3
+#endif
 
 // TMA boxes of the tile's halo nodes (x, u).  The element arrays are read
 // directly: a 2-D box starting at element column x0 - 1 has an inner start
@@ -34,9 +41,9 @@ struct __align__(128) ApplyStage {
   double2 us[kHY * kHX];
 };
 struct ApplySmem {
-  ApplyStage st[2];
+  ApplyStage st[kApplyStages];
   double contrib[8 * kES];  // structure of arrays: conflict-free
-  unsigned long long full[2];
+  unsigned long long full[kApplyStages];
   double scratch[kES / 32];
 };
 static_assert(offsetof(ApplyStage, us) % 128 == 0, "TMA alignment");
@@ -90,10 +97,90 @@ VTS_DEVICE_INLINE double apply_element(const ApplyStage& G, double* contrib, int
   return theta;
 }
 
+// The same element phase in the corner-mode basis (modal_form, vts_b200.cu):
+// u~ = T^T u_e and x~ = T^T x_e by differences, w~ = K' u~ (K' = T^T K_e T / 16,
+// 8 coefficients), theta = w~ . x~ - x_alpha (= w_e . x_e - x_alpha since
+// w_e = T w~), and contrib = K_e (rho_hat x_e + chat theta u_e) = T K' z~ with
+// z~ = rho_hat x~ + chat theta u~ -- one modal product instead of two dense ones.
+struct Modes {
+  double xi_x, eta_x, h_x, xi_y, eta_y, h_y;
+};
+VTS_DEVICE_INLINE Modes to_modes(const double2 (&v)[4]) {
+  Modes m;
+  {
+    const double d10 = v[1].x - v[0].x, d23 = v[2].x - v[3].x, d30 = v[3].x - v[0].x, d21 = v[2].x - v[1].x;
+    m.xi_x = d10 + d23;
+    m.eta_x = d30 + d21;
+    m.h_x = d21 - d30;
+  }
+  {
+    const double d10 = v[1].y - v[0].y, d23 = v[2].y - v[3].y, d30 = v[3].y - v[0].y, d21 = v[2].y - v[1].y;
+    m.xi_y = d10 + d23;
+    m.eta_y = d30 + d21;
+    m.h_y = d21 - d30;
+  }
+  return m;
+}
+VTS_DEVICE_INLINE Modes modal_k(const Modes& a, const double* __restrict__ km) {
+  Modes y;
+  y.xi_x = fma(km[2], a.eta_y, km[0] * a.xi_x);
+  y.eta_y = fma(km[2], a.xi_x, km[1] * a.eta_y);
+  y.xi_y = fma(km[5], a.eta_x, km[3] * a.xi_y);
+  y.eta_x = fma(km[5], a.xi_y, km[4] * a.eta_x);
+  y.h_x = km[6] * a.h_x;
+  y.h_y = km[7] * a.h_y;
+  return y;
+}
+VTS_DEVICE_INLINE double apply_element_modal(const ApplyStage& G, double* contrib, int tid, int h0, double xa,
+                                             double rh, double ch, const double* __restrict__ km) {
+  const int hn[4] = {h0, h0 + 1, h0 + kHX + 1, h0 + kHX};
+  double2 uv[4], xv[4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    uv[a] = G.us[hn[a]];
+    xv[a] = G.xs[hn[a]];
+  }
+  const Modes ut = to_modes(uv), xt = to_modes(xv);
+  const Modes wt = modal_k(ut, km);
+  double wx = wt.xi_x * xt.xi_x;
+  wx = fma(wt.eta_x, xt.eta_x, wx);
+  wx = fma(wt.h_x, xt.h_x, wx);
+  wx = fma(wt.xi_y, xt.xi_y, wx);
+  wx = fma(wt.eta_y, xt.eta_y, wx);
+  wx = fma(wt.h_y, xt.h_y, wx);
+  const double theta = wx - xa;
+  const double ct = ch * theta;
+  Modes z;
+  z.xi_x = fma(ct, ut.xi_x, rh * xt.xi_x);
+  z.eta_x = fma(ct, ut.eta_x, rh * xt.eta_x);
+  z.h_x = fma(ct, ut.h_x, rh * xt.h_x);
+  z.xi_y = fma(ct, ut.xi_y, rh * xt.xi_y);
+  z.eta_y = fma(ct, ut.eta_y, rh * xt.eta_y);
+  z.h_y = fma(ct, ut.h_y, rh * xt.h_y);
+  const Modes y = modal_k(z, km);
+  // back to the corners: node (sign of xi, eta, h) = 0 (-,-,+), 1 (+,-,-), 2 (+,+,+), 3 (-,+,-)
+  {
+    const double a = y.xi_x + y.eta_x, b = y.xi_x - y.eta_x;
+    contrib[0 * kES + tid] = y.h_x - a;
+    contrib[2 * kES + tid] = b - y.h_x;
+    contrib[4 * kES + tid] = a + y.h_x;
+    contrib[6 * kES + tid] = -b - y.h_x;
+  }
+  {
+    const double a = y.xi_y + y.eta_y, b = y.xi_y - y.eta_y;
+    contrib[1 * kES + tid] = y.h_y - a;
+    contrib[3 * kES + tid] = b - y.h_y;
+    contrib[5 * kES + tid] = a + y.h_y;
+    contrib[7 * kES + tid] = -b - y.h_y;
+  }
+  return theta;
+}
+
 // Persistent: CTA b takes tiles b, b + grid, ...; the halo boxes (TMA, OOB
 // zero fill) and element coefficients of the next tile are in flight while
 // the current tile computes (2 stages).
-__global__ void __launch_bounds__(kBX* kBY, 3) k_newton_apply(const __grid_constant__ CUtensorMap mapX,
+template <bool MODAL>
+__global__ void __launch_bounds__(kBX* kBY, VTS_APPLY_MINB) k_newton_apply(const __grid_constant__ CUtensorMap mapX,
                                                              const __grid_constant__ CUtensorMap mapU,
                                                              const double* __restrict__ rho_hat,
                                                              const double* __restrict__ chat, int nx, int ny,
@@ -123,11 +210,10 @@ __global__ void __launch_bounds__(kBX* kBY, 3) k_newton_apply(const __grid_const
     }
   };
   if (tid == 0) {
-    mbar_init(&S.full[0], 1);
-    mbar_init(&S.full[1], 1);
+    for (int i = 0; i < kApplyStages; ++i) mbar_init(&S.full[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if ((int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
-    if ((int)blockIdx.x + (int)gridDim.x < ntiles) issue(blockIdx.x + gridDim.x, 1);
+    for (int i = 0; i < kApplyStages; ++i)
+      if ((int)blockIdx.x + i * (int)gridDim.x < ntiles) issue(blockIdx.x + i * gridDim.x, i);
   }
   const double xa = x[ngrid];
   double rh, ch;
@@ -137,15 +223,16 @@ __global__ void __launch_bounds__(kBX* kBY, 3) k_newton_apply(const __grid_const
   double acc = 0.0;
   int k = 0;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
-    const int s = k & 1;
+    const int s = k % kApplyStages;
     const int x0 = (t % tiles_x) * kTX, y0 = (t / tiles_x) * kTY;
     double rh_n, ch_n;
     coeffs(t + gridDim.x, rh_n, ch_n);  // next tile's coefficients, in flight during this one
-    mbar_wait(&S.full[s], (k >> 1) & 1);
+    mbar_wait(&S.full[s], (k / kApplyStages) & 1);
     int z;
     asm volatile("mov.u32 %0, 0;" : "=r"(z));
     double* contrib = S.contrib;
-    const double theta = apply_element(S.st[s], contrib, tid, h0, xa, rh, ch, c_ke + z);
+    const double theta = MODAL ? apply_element_modal(S.st[s], contrib, tid, h0, xa, rh, ch, c_modal + z)
+                               : apply_element(S.st[s], contrib, tid, h0, xa, rh, ch, c_ke + z);
     // y_alpha sums the elements this tile owns (ch = 0 outside the mesh)
     {
       const int gx = x0 - 1 + lx, gy = y0 - 1 + ly;
@@ -154,7 +241,7 @@ __global__ void __launch_bounds__(kBX* kBY, 3) k_newton_apply(const __grid_const
     rh = rh_n;
     ch = ch_n;
     __syncthreads();  // stage s consumed, contrib complete
-    if (tid == 0 && t + 2 * (int)gridDim.x < ntiles) issue(t + 2 * gridDim.x, s);
+    if (tid == 0 && t + kApplyStages * (int)gridDim.x < ntiles) issue(t + kApplyStages * gridDim.x, s);
     const int ix = x0 + lx, iy = y0 + ly;
     if (lx < kTX && ly < kTY && ix < nx && iy < ny) {
       // elements (ix-1,iy-1) c2, (ix,iy-1) c3, (ix-1,iy) c1, (ix,iy) c0: the reference's scatter order
@@ -258,18 +345,32 @@ __global__ void __launch_bounds__(256) k_level_apply(int nx, int ny, int ngrid, 
 
 static bool g_apply_attr_set = false;
 
+// VTS_DENSE_APPLY=1 keeps the dense K_e products even when the modal form exists (A/B checks)
+static bool modal_apply_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("VTS_DENSE_APPLY");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
 int newton_apply_grid(Ctx* c, const double* x, double* y, const int* skip) {
   const LevelBuf& F = c->lv[c->L - 1];
   if (!g_apply_attr_set) {
-    VTS_CUDA(cudaFuncSetAttribute(k_newton_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ApplySmem)));
+    VTS_CUDA(cudaFuncSetAttribute(k_newton_apply<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sizeof(ApplySmem)));
+    VTS_CUDA(cudaFuncSetAttribute(k_newton_apply<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sizeof(ApplySmem)));
     g_apply_attr_set = true;
   }
+  const bool modal = c->modal_ok && modal_apply_enabled();
+  const auto kern = modal ? k_newton_apply<true> : k_newton_apply<false>;
   const int tiles_x = div_up(F.d.nx, kTX), tiles_y = div_up(F.d.ny, kTY);
   const int ntiles = tiles_x * tiles_y;
   int dev = 0, sms = 148, per_sm = 2;
   VTS_CUDA(cudaGetDevice(&dev));
   VTS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  VTS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_newton_apply, kBX * kBY, sizeof(ApplySmem)));
+  VTS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBX * kBY, sizeof(ApplySmem)));
   const int grid = std::max(1, std::min(ntiles, sms * std::max(per_sm, 1)));
   if (grid > kMaxBlocks * 8) {
     set_error(4, "apply grid exceeds the partial buffer");
@@ -281,7 +382,7 @@ int newton_apply_grid(Ctx* c, const double* x, double* y, const int* skip) {
   const cuuint32_t nb3[3] = {2, kHX, kHY};
   if (int rc = encode_tiled(&mX, x, 3, nd3, ns3, nb3)) return rc;
   if (int rc = encode_tiled(&mU, c->u_grid, 3, nd3, ns3, nb3)) return rc;
-  k_newton_apply<<<grid, kBX * kBY, sizeof(ApplySmem), c->stream>>>(
+  kern<<<grid, kBX * kBY, sizeof(ApplySmem), c->stream>>>(
       mX, mU, c->rho_hat, c->chat, F.d.nx, F.d.ny, F.d.ex, F.d.ey, F.d.ngrid, tiles_x, ntiles, F.d.free_mask, x, y,
       c->partials + kMaxBlocks * 8, c->counters + 4, skip);
   VTS_LAUNCHED(c);

@@ -50,6 +50,8 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   int n = 0, m = 0;             // finest free dofs, elements
   double ke[64];
+  double modal[8];         // K_e in the corner-mode basis / 16 (c_modal); valid when modal_ok
+  bool modal_ok = false;   // K_e has the rectangular-Q1 mode structure: modal Newton apply
 
   // bound Newton matrix (finest level)
   double* u_grid = nullptr;     // [ngrid]

@@ -48,6 +48,7 @@ static int ensure_ke(Ctx* c) {
   std::lock_guard<std::mutex> lock(g_ke_mutex);
   if (g_ke_owner == c) return 0;
   VTS_CUDA(cudaMemcpyToSymbolAsync(c_ke, c->ke, sizeof(double) * 64, 0, cudaMemcpyHostToDevice, c->stream));
+  VTS_CUDA(cudaMemcpyToSymbolAsync(c_modal, c->modal, sizeof(double) * 8, 0, cudaMemcpyHostToDevice, c->stream));
   g_ke_owner = c;
   return 0;
 }
@@ -135,6 +136,45 @@ static void free_ctx(Ctx* c) {
   delete c;
 }
 
+// K_e in the basis of corner modes.  Per displacement component the four nodal
+// values (corners (0,0) (1,0) (1,1) (0,1)) map to the modes 1 = (1 1 1 1),
+// xi = (-1 1 1 -1), eta = (-1 -1 1 1) and h = (1 -1 1 -1); T (8 x 8) holds them
+// as columns and T^T T = 4 I, so K u = T (T^T K T / 16) (T^T u).  For the
+// bilinear rectangle (any E, nu, aspect) T^T K T vanishes on the translations
+// and couples only {xi_x, eta_y} (normal strains), {xi_y, eta_x} (shear) and
+// each hourglass mode with itself: 8 numbers instead of 64, and the Newton
+// apply does ~80 instead of ~150 fp64 operations per element.  Any other K_e
+// keeps the dense apply (modal_ok = false).
+static void modal_form(Ctx* c) {
+  static const double e[4][4] = {{1, 1, 1, 1}, {-1, 1, 1, -1}, {-1, -1, 1, 1}, {1, -1, 1, -1}};
+  double t[8][8] = {};  // column 2k + comp: mode k of component comp
+  for (int k = 0; k < 4; ++k)
+    for (int a = 0; a < 4; ++a)
+      for (int comp = 0; comp < 2; ++comp) t[2 * a + comp][2 * k + comp] = e[k][a];
+  double km[8][8];
+  double kmax = 0.0;
+  for (int i = 0; i < 8; ++i)
+    for (int j = 0; j < 8; ++j) {
+      double sum = 0.0;
+      for (int p = 0; p < 8; ++p)
+        for (int q = 0; q < 8; ++q) sum += t[p][i] * c->ke[8 * p + q] * t[q][j];
+      km[i][j] = sum / 16.0;
+      kmax = std::max(kmax, std::fabs(km[i][j]));
+    }
+  // modes: 0 1x, 1 1y, 2 xi_x, 3 xi_y, 4 eta_x, 5 eta_y, 6 h_x, 7 h_y
+  const int keep[8][2] = {{2, 2}, {5, 5}, {2, 5}, {3, 3}, {4, 4}, {3, 4}, {6, 6}, {7, 7}};
+  bool ok = kmax > 0.0;
+  for (int i = 0; i < 8 && ok; ++i)
+    for (int j = 0; j < 8 && ok; ++j) {
+      bool kept = false;
+      for (const auto& kv : keep) kept |= (kv[0] == i && kv[1] == j) || (kv[0] == j && kv[1] == i);
+      if (!kept && std::fabs(km[i][j]) > 1e-13 * kmax) ok = false;
+      if (std::fabs(km[i][j] - km[j][i]) > 1e-13 * kmax) ok = false;
+    }
+  for (int i = 0; i < 8; ++i) c->modal[i] = km[keep[i][0]][keep[i][1]];
+  c->modal_ok = ok;
+}
+
 static int create(Ctx** out, int levels, const int32_t* ex, const int32_t* ey, const int64_t* const* dof_maps,
                   const double* ke, int64_t stream) {
   if (levels < 1 || !ex || !ey || !dof_maps || !ke || !out) {
@@ -155,6 +195,7 @@ static int create(Ctx** out, int levels, const int32_t* ex, const int32_t* ey, c
   c->L = levels;
   c->stream = reinterpret_cast<cudaStream_t>(stream);
   std::memcpy(c->ke, ke, sizeof(double) * 64);
+  modal_form(c);
   c->lv.resize(levels);
   auto fail = [&](int rc) {
     free_ctx(c);
@@ -475,6 +516,15 @@ int vts_penalty_eval(vts_ctx* ctx, int64_t n, const double* tau, double branch, 
 int vts_time_kernels(vts_ctx* ctx, int32_t reps, double* ms) {
   VTS_REQUIRE_CTX(ctx);
   return vts::time_kernels(C(ctx), reps, ms);
+}
+
+int vts_time_cold(vts_ctx* ctx, int32_t reps, void* flush, int64_t flush_bytes, double* ms) {
+  VTS_REQUIRE_CTX(ctx);
+  if (reps < 1 || !flush || flush_bytes <= 0 || !ms) {
+    vts::set_error(4, "vts_time_cold: bad arguments");
+    return 4;
+  }
+  return vts::time_cold(C(ctx), reps, flush, (size_t)flush_bytes, ms);
 }
 
 int64_t vts_kernel_launches(const vts_ctx* ctx) { return ctx ? C(ctx)->launches : 0; }

@@ -57,6 +57,10 @@ VTS_DEVICE_INLINE double stencil_entry(const double* __restrict__ L, const doubl
 // Element stiffness of the unit Q1 square, row-major 8x8 (set by the context).
 // Defined here: the library is one translation unit (csrc/vts_b200.cu).
 __constant__ double c_ke[64];
+// K_e in the corner-mode basis (see modal_form in vts_b200.cu), divided by 16:
+// {A1 (xi_x xi_x), A2 (eta_y eta_y), B (xi_x eta_y), S1 (xi_y xi_y), S2 (eta_x eta_x),
+//  S12 (xi_y eta_x), H1 (h_x h_x), H2 (h_y h_y)}
+__constant__ double c_modal[8];
 
 struct LevelDev {
   int ex, ey;         // elements per axis
