@@ -6,7 +6,7 @@
 // of fixed launch / barrier-init / TMA-descriptor latency per V-cycle.  Here
 // the level vectors live in shared memory, each sweep stages its half-stencil
 // into shared memory, the parallel passes (old values, residual, restriction,
-// prolongation) use all 1024 threads, the wavefront runs on one warp (lane =
+// prolongation) use all 512 threads, the wavefront runs on one warp (lane =
 // grid row; kb is the largest level with <= 32 node rows), and the coarsest
 // bordered system is solved with the Cholesky factor from mg_setup.
 //
@@ -16,7 +16,7 @@
 // column order), so the fused and unfused V-cycles agree bit for bit up to
 // the sign of zeros.
 
-constexpr int kBotThreads = 1024;
+constexpr int kBotThreads = 512;  // 128 registers: the wavefront warp keeps two steps of operands live
 #ifdef VTS_BOT_PROBE
 __device__ long long g_bot_probe[64];
 __device__ int g_bot_n;
@@ -121,23 +121,19 @@ __device__ __noinline__ void bot_sweep(const BotLevel& L, double* sm, const BotA
     struct StepData {
       double q0, q1, e00, e01, e10, e11, w00, w01, w10, w11, c, r0, r1;
     };
+    // gs_pre / gs_rec2 of k_gs_tri's skew-2 steps, so both paths compute the same bits
     auto prepare = [&](const double* a, const double* pv, const double2 xm, const double2 xz) {
-      double r[20];
+      double r[19];
 #pragma unroll
-      for (int i = 0; i < 10; ++i) {
+      for (int i = 0; i < 9; ++i) {
         const double2 v = reinterpret_cast<const double2*>(a)[i];
         r[2 * i] = v.x;
         r[2 * i + 1] = v.y;
       }
+      r[18] = a[18];
       const double2 pq = *reinterpret_cast<const double2*>(pv);
-      auto pre = [&](int d, double p) {
-        const double t1 = fma(-r[0 + 2 * d], xm.x, -r[1 + 2 * d] * xm.y);
-        const double t2 = fma(-r[4 + 2 * d], xz.x, -r[5 + 2 * d] * xz.y);
-        return p + (t1 + t2);
-      };
       StepData o;
-      o.q0 = pre(d0, d0 == 0 ? pq.x : pq.y);
-      o.q1 = pre(d1, d1 == 0 ? pq.x : pq.y);
+      gs_pre<d0>(r, pq.x, pq.y, xm, xz, o.q0, o.q1);
       o.e00 = r[8 + 2 * d0];
       o.e01 = r[9 + 2 * d0];
       o.e10 = r[8 + 2 * d1];
@@ -160,16 +156,14 @@ __device__ __noinline__ void bot_sweep(const BotLevel& L, double* sm, const BotA
 #pragma unroll 4
     for (int t = 0; t < T; ++t) {
       const int j = t - 2 * l;
-      const double2 xp = win[2];
-      const double u0 = fma(-cur.e00, xp.x, fma(-cur.e01, xp.y, cur.q0));
-      const double u1 = fma(-cur.e10, xp.x, fma(-cur.e11, xp.y, cur.q1));
-      const double n0v = fma(-cur.w00, wprev.x, fma(-cur.w01, wprev.y, u0)) * cur.r0;
-      const double n1v = fma(-cur.c, n0v, fma(-cur.w10, wprev.x, fma(-cur.w11, wprev.y, u1))) * cur.r1;
-      const double2 nv = FWD ? make_double2(n0v, n1v) : make_double2(n1v, n0v);
+      const double2 nv = gs_rec2<d0>(cur.q0, cur.q1, cur.w00, cur.w01, cur.w10, cur.w11, cur.e00, cur.e01, cur.e10,
+                                     cur.e11, cur.c, cur.r0, cur.r1, wprev, win[2]);
+      // the next step's loads before this step's store (shared memory: the store
+      // would otherwise order them behind it)
+      const StepData nxt = prepare(ap + (size_t)((t + 1) * dir * kHalf), pp + 2 * dir * (t + 1), win[1], win[2]);
       // branch-free store: off-row positions write the scratch slot instead
       double* dst = (row_ok && j >= 0 && j < nx) ? xp_out + 2 * dir * t : trash;
       *reinterpret_cast<double2*>(dst) = nv;
-      const StepData nxt = prepare(ap + (size_t)((t + 1) * dir * kHalf), pp + 2 * dir * (t + 1), win[1], win[2]);
       wprev = nv;
       double2 up;
       up.x = __shfl_up_sync(0xffffffffu, nv.x, 1);
@@ -196,7 +190,7 @@ __device__ __noinline__ void bot_residual(const BotLevel& L, double* sm, const B
   const int tid = threadIdx.x, g = tid >> 8, t = tid & 255, w = t >> 5, lane = tid & 31;
   const int nvb = (L.nn + 255) / 256;
   const double xa = sx[L.ngrid];
-  for (int vb0 = 0; vb0 < nvb; vb0 += 4) {
+  for (int vb0 = 0; vb0 < nvb; vb0 += kBotThreads / 256) {
     const int vb = vb0 + g;
     double acc = 0.0;
     if (vb < nvb) {

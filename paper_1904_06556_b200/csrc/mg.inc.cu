@@ -387,6 +387,69 @@ VTS_DEVICE_INLINE void gs_old_load(int nx, int ny, const double* __restrict__ ha
   gs_old_load_vectors<FWD>(nx, ny, b, bd, x, nd, in);
 }
 
+// One node of the wavefront solve (D_L + L) x = P, shared by k_gs_tri / k_gs_pair
+// and the fused bottom so that every path computes the same bits.  `a` is the
+// node's solve half-stencil (blocks SW S SE W, kHC, reciprocals); d0 is the dof
+// solved first (x forward, y backward).  Each dof's sum subtracts its lower
+// couplings as one fma chain in the CSR column order of multigrid.py:41-47
+// (SW, S, SE, W, then the centre coupling), then multiplies by the reciprocal
+// diagonal:
+//   gs_pre  P - SW.xm - S.xz            (previous row, final long before)
+//   gs_se   ... - SE.xq                 (previous row, column j+1)
+//   gs_rec  ... - W.wp, x_d0 = r0 (...), x_d1 = r1 (... - c x_d0)
+// The own-row value solved last (wp's d1 component) enters last, so the
+// loop-carried chain is four dependent operations.
+template <int d0>
+VTS_DEVICE_INLINE void gs_pre(const double* a, double p0, double p1, const double2 xm, const double2 xz, double& q0,
+                              double& q1) {
+  constexpr int d1 = 1 - d0;
+  auto chain = [&](int d, double p) {
+    double q = fma(-a[0 + 2 * d], xm.x, p);
+    q = fma(-a[1 + 2 * d], xm.y, q);
+    q = fma(-a[4 + 2 * d], xz.x, q);
+    return fma(-a[5 + 2 * d], xz.y, q);
+  };
+  q0 = chain(d0, d0 == 0 ? p0 : p1);
+  q1 = chain(d1, d1 == 0 ? p0 : p1);
+}
+// e_dc: SE block, row d0 / d1 (solve order), storage column c
+VTS_DEVICE_INLINE void gs_se(double e00, double e01, double e10, double e11, const double2 xq, double& q0,
+                             double& q1) {
+  q0 = fma(-e01, xq.y, fma(-e00, xq.x, q0));
+  q1 = fma(-e11, xq.y, fma(-e10, xq.x, q1));
+}
+// Skew-2 form of the rest of the step: the previous row's column j+1 (xq) was
+// shuffled in at the end of the step before, so it enters after the own-row
+// neighbour: ... - W.wp - SE.xq, then the reciprocal; the loop-carried chain is
+// shuffle + four dependent operations.
+template <int d0>
+VTS_DEVICE_INLINE double2 gs_rec2(double q0, double q1, double w00, double w01, double w10, double w11, double e00,
+                                  double e01, double e10, double e11, double c, double r0, double r1, const double2 wp,
+                                  const double2 xq) {
+  const double wf = d0 == 0 ? wp.x : wp.y, wl = d0 == 0 ? wp.y : wp.x;
+  const double f0 = d0 == 0 ? w00 : w01, l0 = d0 == 0 ? w01 : w00;
+  const double f1 = d0 == 0 ? w10 : w11, l1 = d0 == 0 ? w11 : w10;
+  const double u0 = fma(-l0, wl, fma(-f0, wf, q0));
+  const double u1 = fma(-l1, wl, fma(-f1, wf, q1));
+  const double n0 = fma(-e01, xq.y, fma(-e00, xq.x, u0)) * r0;
+  const double n1 = fma(-c, n0, fma(-e11, xq.y, fma(-e10, xq.x, u1))) * r1;
+  return d0 == 0 ? make_double2(n0, n1) : make_double2(n1, n0);
+}
+
+// wp: the own row's previous node in sweep order, (x, y) storage order
+template <int d0>
+VTS_DEVICE_INLINE double2 gs_rec(double q0, double q1, double w00, double w01, double w10, double w11, double c,
+                                 double r0, double r1, const double2 wp) {
+  // w_d0c / w_d1c couple dof d0 / d1 to wp's storage component c (x, y); the
+  // component solved last (forward y, backward x) enters last
+  const double wf = d0 == 0 ? wp.x : wp.y, wl = d0 == 0 ? wp.y : wp.x;
+  const double f0 = d0 == 0 ? w00 : w01, l0 = d0 == 0 ? w01 : w00;
+  const double f1 = d0 == 0 ? w10 : w11, l1 = d0 == 0 ? w11 : w10;
+  const double n0 = fma(-l0, wl, fma(-f0, wf, q0)) * r0;
+  const double n1 = fma(-c, n0, fma(-l1, wl, fma(-f1, wf, q1))) * r1;
+  return d0 == 0 ? make_double2(n0, n1) : make_double2(n1, n0);
+}
+
 template <bool FWD>
 VTS_DEVICE_INLINE double2 gs_old_eval(const OldIn& in, double xa) {
   const double* a = in.a;
@@ -460,7 +523,8 @@ constexpr int NSA = 4;     // window slots of the previous band's row
 #ifndef VTS_GS_SKEW
 #define VTS_GS_SKEW 2
 #endif
-constexpr int SKEW = VTS_GS_SKEW;  // columns between consecutive rows of the wavefront (2 or 3)
+constexpr int SKEW = VTS_GS_SKEW;  // columns between consecutive rows of the wavefront (2, or 3: the
+                                   // previous row's newest value is needed a step after it arrives)
 constexpr int kWarps = 5;  // compute, loader, storer, publisher, stager
 constexpr int kBuild = 6;  // pipelined pair, sweep B: builder warps (<= 2 nodes of a window's R x W box each)
 // Pair CTAs have 16 warps.  Warp w runs on SM sub-partition w % 4: the compute
@@ -994,82 +1058,82 @@ __device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int b
     constexpr int d0 = FWD ? 0 : 1;
     constexpr int d1 = 1 - d0;
     struct StepData {
-      double q0, q1;        // partial sums without the own-row and the newest previous-row neighbour
-      double e00, e01, e10, e11;  // coupling to the previous row's column j+1 (arrives by shuffle)
-      double w00, w01, w10, w11, c, r0, r1;  // own-row block rows d0/d1, centre coupling, reciprocals
+      double q0, q1;                         // partial sums before the recurrence's terms
+      double w00, w01, w10, w11, c, r0, r1;  // own-row block rows d0/d1 (solve order), centre coupling, reciprocals
+      double e00, e01, e10, e11;             // skew 2: the previous row's column j+1 (shuffled in last step)
     };
-    auto prepare = [&](int st, const double2 xm, const double2 xz, const double2 xq) {
+    // shared-memory operands of one step, loaded two steps ahead (the loads of
+    // step st+2 are issued before step st's store, so they are not ordered
+    // behind it, and the arithmetic that consumes them runs a step later)
+    struct Raw {
+      double a[19];  // the node's half-stencil (blocks SW S SE W, centre coupling, reciprocals)
+      double2 p, q;  // P (or b) and, from the zero guess, the border column
+    };
+    auto load_raw = [&](int st, Raw& r) {
       const int pos = FWD ? st : W - 1 - st;
       const double2* a2 = reinterpret_cast<const double2*>(in.st[brow][pos]);
-      double a[20];
 #pragma unroll
-      for (int i = 0; i < 10; ++i) {
+      for (int i = 0; i < 9; ++i) {
         const double2 v = a2[i];
-        a[2 * i] = v.x;
-        a[2 * i + 1] = v.y;
+        r.a[2 * i] = v.x;
+        r.a[2 * i + 1] = v.y;
       }
+      r.a[18] = in.st[brow][pos][18];
+      r.p = *reinterpret_cast<const double2*>(in.p[brow][pos]);
+      if (ZERO) r.q = *reinterpret_cast<const double2*>(in.q[brow][pos]);
+    };
+    // the recurrence-independent part of a step: everything up to the own-row neighbour
+    auto prepare = [&](const Raw& r, const double2 xm, const double2 xz, const double2 xq) {
       double p0, p1;
-      const double2 pp = *reinterpret_cast<const double2*>(in.p[brow][pos]);
       if (ZERO) {
-        const double2 qq = *reinterpret_cast<const double2*>(in.q[brow][pos]);
-        p0 = __dsub_rn(pp.x, __dmul_rn(qq.x, xa));
-        p1 = __dsub_rn(pp.y, __dmul_rn(qq.y, xa));
+        p0 = __dsub_rn(r.p.x, __dmul_rn(r.q.x, xa));
+        p1 = __dsub_rn(r.p.y, __dmul_rn(r.q.y, xa));
       } else {
-        p0 = pp.x;
-        p1 = pp.y;
+        p0 = r.p.x;
+        p1 = r.p.y;
       }
-      auto pre = [&](int d, double p) {
-        const double t1 = fma(-a[0 + 2 * d], xm.x, -a[1 + 2 * d] * xm.y);
-        const double t2 = fma(-a[4 + 2 * d], xz.x, -a[5 + 2 * d] * xz.y);
-        return p + (t1 + t2);
-      };
       StepData o;
-      o.e00 = a[8 + 2 * d0];
-      o.e01 = a[9 + 2 * d0];
-      o.e10 = a[8 + 2 * d1];
-      o.e11 = a[9 + 2 * d1];
-      o.q0 = pre(d0, d0 == 0 ? p0 : p1);
-      o.q1 = pre(d1, d1 == 0 ? p0 : p1);
-      if constexpr (SKEW == 3) {  // column j+1 is final one step early: same operations, off the recurrence
-        o.q0 = fma(-o.e00, xq.x, fma(-o.e01, xq.y, o.q0));
-        o.q1 = fma(-o.e10, xq.x, fma(-o.e11, xq.y, o.q1));
-      }
-      o.w00 = a[12 + 2 * d0];
-      o.w01 = a[13 + 2 * d0];
-      o.w10 = a[12 + 2 * d1];
-      o.w11 = a[13 + 2 * d1];
-      o.c = a[kHC];
-      o.r0 = a[d0 == 0 ? kHRd0 : kHRd1];
-      o.r1 = a[d1 == 0 ? kHRd0 : kHRd1];
+      gs_pre<d0>(r.a, p0, p1, xm, xz, o.q0, o.q1);
+      o.e00 = r.a[8 + 2 * d0];
+      o.e01 = r.a[9 + 2 * d0];
+      o.e10 = r.a[8 + 2 * d1];
+      o.e11 = r.a[9 + 2 * d1];
+      if constexpr (SKEW == 3) gs_se(o.e00, o.e01, o.e10, o.e11, xq, o.q0, o.q1);
+      o.w00 = r.a[12 + 2 * d0];
+      o.w01 = r.a[13 + 2 * d0];
+      o.w10 = r.a[12 + 2 * d1];
+      o.w11 = r.a[13 + 2 * d1];
+      o.c = r.a[kHC];
+      o.r0 = r.a[d0 == 0 ? kHRd0 : kHRd1];
+      o.r1 = r.a[d1 == 0 ? kHRd0 : kHRd1];
       return o;
     };
-    StepData cur = prepare(0, win[0], win[1], win[2]);
+    Raw ra;
+    load_raw(0, ra);
+    StepData cur = prepare(ra, win[0], win[1], win[2]);
+    load_raw(1, ra);
 #pragma unroll
     for (int st = 0; st < W; ++st) {
       const int pos = FWD ? st : W - 1 - st;
-      // the recurrence of step st (xp: previous row, column j+1, shuffled in last step):
-      //   x_d0 = r0 (q0 - E[d0].xp - W[d0].w),  x_d1 = r1 (q1 - E[d1].xp - W[d1].w - c x_d0)
-      double u0 = cur.q0, u1 = cur.q1;
-      if constexpr (SKEW == 2) {
-        const double2 xp = win[2];
-        u0 = fma(-cur.e00, xp.x, fma(-cur.e01, xp.y, cur.q0));
-        u1 = fma(-cur.e10, xp.x, fma(-cur.e11, xp.y, cur.q1));
-      }
-      const double n0 = fma(-cur.w00, wprev.x, fma(-cur.w01, wprev.y, u0)) * cur.r0;
-      const double n1 = fma(-cur.c, n0, fma(-cur.w10, wprev.x, fma(-cur.w11, wprev.y, u1))) * cur.r1;
-      // step st+1's independent part (previous-row columns j, j+1 are in win[1..2])
+      const double2 av = S.above[sa][st];  // band 0: a zero-filled ring
+      double2 nv;
+      if constexpr (SKEW == 3)
+        nv = gs_rec<d0>(cur.q0, cur.q1, cur.w00, cur.w01, cur.w10, cur.w11, cur.c, cur.r0, cur.r1, wprev);
+      else
+        nv = gs_rec2<d0>(cur.q0, cur.q1, cur.w00, cur.w01, cur.w10, cur.w11, cur.e00, cur.e01, cur.e10, cur.e11, cur.c,
+                         cur.r0, cur.r1, wprev, win[2]);
+      // step st+1's independent part: previous-row columns j, j+1 (, j+2) (win[1..])
       StepData nxt;
-      if (st + 1 < W) nxt = prepare(st + 1, win[1], win[2], win[SKEW == 3 ? 3 : 2]);
+      if (st + 1 < W) nxt = prepare(ra, win[1], win[2], win[SKEW]);
+      if (st + 2 < W) load_raw(st + 2, ra);
       // no validity selects: positions outside the row (j < 0, j >= nx) and rows
       // outside the grid compute finite values from real neighbouring or zero-padded
       // slot data; they are never stored, and every coupling that reads them at a
       // valid position is an exact zero (no neighbour / Dirichlet)
-      const double2 nv = FWD ? make_double2(n0, n1) : make_double2(n1, n0);
       wprev = nv;
       if (l < R) S.out[s][l][pos] = nv;
       const double r0s = __shfl_up_sync(0xffffffffu, nv.x, 1);
       const double r1s = __shfl_up_sync(0xffffffffu, nv.y, 1);
-      const double2 av = S.above[sa][st];  // band 0: a zero-filled ring
       const double r0 = l == 0 ? av.x : r0s;
       const double r1 = l == 0 ? av.y : r1s;
 #pragma unroll
