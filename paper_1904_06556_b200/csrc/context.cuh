@@ -80,7 +80,8 @@ struct Ctx {
   double* hscal = nullptr;      // pinned host scalars [64]
   unsigned* dflags = nullptr;   // device warning flags
   MinresDev* mst = nullptr;     // device MINRES state
-  MinresDev* hmst = nullptr;    // pinned host mirror
+  MinresDev* hmst = nullptr;    // pinned host mirror, [2]: the two iterations in flight
+  cudaEvent_t mr_ev[2] = {nullptr, nullptr};  // their state copies have landed
 
   long long launches = 0;
   std::vector<void*> allocs;  // the device arena holding every array of the context

@@ -283,10 +283,11 @@ int minres(Ctx* c, const double* b_free, double* x_free, double tol, int max_ite
   std::vector<double*> freeb = {pool[3], pool[4], pool[5], pool[6], pool[7]};
   const int* stopped = &c->mst->stopped;
   const int* nover = &c->mst->no_verify;
-  std::vector<double> hist_host;
   double* dhist = c->dscal + 32;  // latest history entry, read back every iteration
-  int status = kRunning;
-  for (int it = 0; it < cap; ++it) {
+  // one iteration's launches; its update reads x_in and writes x_out
+  double* x_in[2] = {nullptr, nullptr};
+  double* x_out[2] = {nullptr, nullptr};
+  auto enqueue = [&](int it) -> int {
     k_mr_scale<<<grid, kThreads, 0, c->stream>>>(len, y, v, c->mst);
     VTS_LAUNCHED(c);
     if (int rc = newton_apply_grid(c, v, y, stopped)) return rc;
@@ -325,14 +326,39 @@ int minres(Ctx* c, const double* b_free, double* x_free, double tol, int max_ite
     if (int rc = newton_apply_grid(c, xalt, T, nover)) return rc;
     k_mr_verify<<<grid, kThreads, 0, c->stream>>>(len, B, T, c->mst, c->partials, c->counters + 12);
     VTS_LAUNCHED(c);
-    if (int rc = read_state(c)) return rc;
-    const MinresDev& s = *c->hmst;
+    // assume the update succeeds (the next iteration reads x_out); a failed or
+    // stopped iteration makes every later launch a no-op on the device
+    x_in[it & 1] = x;
+    x_out[it & 1] = xalt;
+    std::swap(x, xalt);
+    VTS_CUDA(cudaMemcpyAsync(c->hmst + (it & 1), c->mst, sizeof(MinresDev), cudaMemcpyDeviceToHost, c->stream));
+    VTS_CUDA(cudaEventRecord(c->mr_ev[it & 1], c->stream));
+    return 0;
+  };
+  if (!c->mr_ev[0]) {
+    VTS_CUDA(cudaEventCreateWithFlags(&c->mr_ev[0], cudaEventDisableTiming));
+    VTS_CUDA(cudaEventCreateWithFlags(&c->mr_ev[1], cudaEventDisableTiming));
+  }
+  // Iteration it+1 is enqueued before iteration it's state is read back, so the
+  // host's launch latency hides behind the device's work (the history hook
+  // reads back every iteration and stays synchronous).
+  int status = kRunning;
+  double* xfinal = x;
+  int last = -1;
+  if (cap > 0)
+    if (int rc = enqueue(0)) return rc;
+  for (int it = 0; it < cap; ++it) {
+    if (!history && it + 1 < cap)
+      if (int rc = enqueue(it + 1)) return rc;
+    VTS_CUDA(cudaEventSynchronize(c->mr_ev[it & 1]));
+    const MinresDev s = c->hmst[it & 1];
+    last = it;
     if (s.status == kIndefinite || s.status == kBreakdown || s.status == kNonfinite) {
       status = s.status;
+      xfinal = x_in[it & 1];  // the last sound iterate
       break;
     }
-    // the update succeeded: x <- x_new
-    std::swap(x, xalt);
+    xfinal = x_out[it & 1];
     if (history) {
       double hv;
       VTS_CUDA(cudaMemcpy(&hv, dhist, sizeof(double), cudaMemcpyDeviceToHost));
@@ -342,7 +368,13 @@ int minres(Ctx* c, const double* b_free, double* x_free, double tol, int max_ite
       status = s.status;
       break;
     }
+    if (history && it + 1 < cap)
+      if (int rc = enqueue(it + 1)) return rc;
   }
+  // a look-ahead iteration behind the one that stopped ran as device no-ops
+  VTS_CUDA(cudaStreamSynchronize(c->stream));
+  x = xfinal;
+  if (last >= 0) *c->hmst = c->hmst[last & 1];
   if (status == kRunning) status = kCap;
   const MinresDev& s = *c->hmst;
   double relres = s.relres;

@@ -61,7 +61,7 @@ static int ensure_ke(Ctx* c) {
 // process-wide pool: cudaMallocHost costs milliseconds, and solvers create a
 // context per problem.  free_ctx releases a block only after cudaFree has
 // synchronised the device, so no copy into it can still be in flight.
-constexpr size_t kPinnedBytes = ((64 * sizeof(double) + sizeof(MinresDev)) + 255) & ~size_t(255);
+constexpr size_t kPinnedBytes = ((64 * sizeof(double) + 2 * sizeof(MinresDev)) + 255) & ~size_t(255);
 static std::mutex g_pinned_mutex;
 static std::vector<void*> g_pinned_free;
 
@@ -124,6 +124,8 @@ static void dalloc_pad(Arena& a, double** p, size_t count, size_t pad) {
 
 static void free_ctx(Ctx* c) {
   for (void* p : c->allocs) cudaFree(p);
+  for (cudaEvent_t e : c->mr_ev)
+    if (e) cudaEventDestroy(e);
   for (auto& e : c->prof_ev) {
     cudaEventDestroy(e.a);
     cudaEventDestroy(e.b);
