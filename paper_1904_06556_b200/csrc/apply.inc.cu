@@ -188,6 +188,7 @@ __global__ void __launch_bounds__(kBX* kBY, VTS_APPLY_MINB) k_newton_apply(const
                                                              const uint8_t* __restrict__ fmask,
                                                              const double* __restrict__ x, double* __restrict__ y,
                                                              double* partials, unsigned* counter, const int* skip) {
+  pdl_enter();
   if (skip && *skip) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   ApplySmem& S = *reinterpret_cast<ApplySmem*>(smem_raw);
@@ -329,6 +330,7 @@ __global__ void __launch_bounds__(256) k_level_apply(int nx, int ny, int ngrid, 
                                                    const double* __restrict__ x,
                                                    const double* __restrict__ b, double* __restrict__ y,
                                                    double* partials, unsigned* counter, const int* skip) {
+  pdl_enter();
   if (skip && *skip) return;
   __shared__ double scratch[256 / 32];
   const int nnodes = nx * ny;
@@ -382,9 +384,9 @@ int newton_apply_grid(Ctx* c, const double* x, double* y, const int* skip) {
   const cuuint32_t nb3[3] = {2, kHX, kHY};
   if (int rc = encode_tiled(&mX, x, 3, nd3, ns3, nb3)) return rc;
   if (int rc = encode_tiled(&mU, c->u_grid, 3, nd3, ns3, nb3)) return rc;
-  kern<<<grid, kBX * kBY, sizeof(ApplySmem), c->stream>>>(
+  VTS_CUDA(launch_pdl(kern, dim3(grid), dim3(kBX * kBY), sizeof(ApplySmem), c->stream, 
       mX, mU, c->rho_hat, c->chat, F.d.nx, F.d.ny, F.d.ex, F.d.ey, F.d.ngrid, tiles_x, ntiles, F.d.free_mask, x, y,
-      c->partials + kMaxBlocks * 8, c->counters + 4, skip);
+      c->partials + kMaxBlocks * 8, c->counters + 4, skip));
   VTS_LAUNCHED(c);
   return 0;
 }
@@ -392,9 +394,9 @@ int newton_apply_grid(Ctx* c, const double* x, double* y, const int* skip) {
 int level_apply_grid(Ctx* c, int k, const double* x, double* y, const int* skip) {
   const LevelBuf& L = c->lv[k];
   const int grid = (int)std::min<long long>(div_up(L.d.nnodes, 256), kReduceGridCap);
-  k_level_apply<false><<<grid, 256, 0, c->stream>>>(L.d.nx, L.d.ny, L.d.ngrid, L.d.stL, L.d.stU, L.d.border,
+  VTS_CUDA(launch_pdl(k_level_apply<false>, dim3(grid), dim3(256), 0, c->stream, L.d.nx, L.d.ny, L.d.ngrid, L.d.stL, L.d.stU, L.d.border,
                                                      c->d_corner, x, nullptr, y, c->partials, c->counters + 5,
-                                                     skip);
+                                                     skip));
   VTS_LAUNCHED(c);
   return 0;
 }
@@ -402,8 +404,8 @@ int level_apply_grid(Ctx* c, int k, const double* x, double* y, const int* skip)
 int level_residual_grid(Ctx* c, int k, const double* x, const double* b, double* r, const int* skip) {
   const LevelBuf& L = c->lv[k];
   const int grid = (int)std::min<long long>(div_up(L.d.nnodes, 256), kReduceGridCap);
-  k_level_apply<true><<<grid, 256, 0, c->stream>>>(L.d.nx, L.d.ny, L.d.ngrid, L.d.stL, L.d.stU, L.d.border,
-                                                    c->d_corner, x, b, r, c->partials, c->counters + 5, skip);
+  VTS_CUDA(launch_pdl(k_level_apply<true>, dim3(grid), dim3(256), 0, c->stream, L.d.nx, L.d.ny, L.d.ngrid, L.d.stL, L.d.stU, L.d.border,
+                                                    c->d_corner, x, b, r, c->partials, c->counters + 5, skip));
   VTS_LAUNCHED(c);
   return 0;
 }

@@ -277,6 +277,7 @@ __device__ void bot_coarse(const BotLevel& C, double* sm, const BotArgs& A) {
 }
 
 __global__ void __launch_bounds__(kBotThreads, 1) k_vcycle_bottom(const __grid_constant__ BotArgs A, const int* skip) {
+  pdl_enter();
   if (skip && *skip) return;
   extern __shared__ __align__(16) double sm[];
   const int tid = threadIdx.x;
@@ -397,7 +398,7 @@ static int vcycle_bottom(Ctx* c, const BotArgs& plan, size_t smem, const int* sk
   A.nfree0 = c->lv[0].d.nfree;
   A.f2g0 = c->lv[0].d.free2grid;
   A.chol = c->chol;
-  k_vcycle_bottom<<<1, kBotThreads, smem, c->stream>>>(A, skip);
+  VTS_CUDA(launch_pdl(k_vcycle_bottom, dim3(1), dim3(kBotThreads), smem, c->stream, A, skip));
   VTS_LAUNCHED(c);
   return 0;
 }

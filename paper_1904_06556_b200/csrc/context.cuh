@@ -4,6 +4,7 @@
 
 #include <cstdio>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "vts_common.cuh"
@@ -115,6 +116,40 @@ int cuda_check(cudaError_t e, const char* what);
     cudaError_t _e = cudaGetLastError();                      \
     if (_e != cudaSuccess) return cuda_check(_e, "launch");   \
   } while (0)
+
+// Programmatic dependent launch.  Kernels of the V-cycle / MINRES chain are
+// launched with the programmatic stream-serialization attribute, so the next
+// launch's CTAs are scheduled and run their prologue while the previous kernel
+// drains; every such kernel starts with pdl_enter(): wait until the previous
+// grid has completed and its memory is visible, then allow the next launch.
+// (A kernel launched without the attribute passes both instructions at once.)
+// VTS_NO_PDL=1 launches everything plainly (A/B checks).
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("VTS_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 inline int div_up(long long a, long long b) { return (int)((a + b - 1) / b); }
 

@@ -290,6 +290,7 @@ VTS_DEVICE_INLINE double2 restrict_node(int fnx, int fny, const uint8_t* __restr
 __global__ void k_restrict(int fnx, int fny, const uint8_t* __restrict__ ffm, const double* __restrict__ vf,
                            int cnx, int cny, const uint8_t* __restrict__ cfm, double* __restrict__ vc,
                            int bordered, const int* skip) {
+  pdl_enter();
   if (skip && *skip) return;
   const int cn = blockIdx.x * blockDim.x + threadIdx.x;
   const int cnn = cnx * cny;
@@ -330,6 +331,7 @@ VTS_DEVICE_INLINE double2 prolong_node(int fnx, const uint8_t* __restrict__ ffm,
 __global__ void k_prolong_add(int fnx, int fny, const uint8_t* __restrict__ ffm, double* __restrict__ xf,
                               int cnx, int cny, const uint8_t* __restrict__ cfm, const double* __restrict__ xc,
                               const int* skip) {
+  pdl_enter();
   if (skip && *skip) return;
   const int fi = blockIdx.x * blockDim.x + threadIdx.x;
   const int fnn = fnx * fny;
@@ -493,6 +495,7 @@ __global__ void __launch_bounds__(256) k_gs_old(int nx, int ny, int ngrid, const
                                               const double* __restrict__ b, const double* __restrict__ bd,
                                               const double* __restrict__ x, double* __restrict__ P,
                                               const int* skip) {
+  pdl_enter();
   if (skip && *skip) return;
   const int nd = blockIdx.x * blockDim.x + threadIdx.x;
   if (nd >= nx * ny) return;
@@ -939,6 +942,7 @@ __global__ void __launch_bounds__(32 * gs::kWarps, 1)
     k_gs_tri(int nx, int ny, int ngrid, int pad_nodes, int bands, const __grid_constant__ CUtensorMap mapS,
              const __grid_constant__ CUtensorMap mapP, const __grid_constant__ CUtensorMap mapQ,
              double* __restrict__ x, unsigned long long* flags, double* xfer, const int* skip) {
+  pdl_enter();
   if (skip && *skip) return;
   GsBand G{nx, ny, ngrid, pad_nodes, bands, (int)blockIdx.x, &mapS, &mapP, &mapQ, &mapQ, &mapQ, &mapQ, x, x, flags,
            xfer, nullptr, 0ull, nullptr, nullptr, nullptr, nullptr};
@@ -960,6 +964,7 @@ __global__ void __launch_bounds__(32 * gs::kWarpsPair, 1)
               unsigned long long* flags, double* xfer, int groups, unsigned long long epoch,
               const double* __restrict__ b,
               const double* __restrict__ border, const double* __restrict__ half_old, const int* skip) {
+  pdl_enter();
   if (skip && *skip) return;
   const int nA = (int)gridDim.x / 2;
   if ((int)blockIdx.x < nA) {
@@ -1180,12 +1185,14 @@ __device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int b
 // ---------------------------------------------------------------------------
 // top level: x_alpha = b_alpha / corner (multigrid.py:121-122); coarse levels start at 0
 __global__ void k_alpha_init(int ngrid, const double* b, double* x, const double* corner, int top, const int* skip) {
+  pdl_enter();
   if (skip && *skip) return;
   x[ngrid] = top ? b[ngrid] / *corner : 0.0;
 }
 
 __global__ void k_alpha_relax(int ngrid, const double* __restrict__ border, const double* b, double* x,
                               const double* corner, double* partials, unsigned* counter, const int* skip) {
+  pdl_enter();
   if (skip && *skip) return;
   __shared__ double scratch[256 / 32];
   double acc[1] = {0.0};
@@ -1275,6 +1282,7 @@ __global__ void __launch_bounds__(1024) k_cholesky(int N, double* A, int* status
 __global__ void __launch_bounds__(1024) k_coarse_solve(int N, int nfree, int ngrid, const double* __restrict__ Lf,
                                                      const int32_t* __restrict__ f2g, const double* __restrict__ b,
                                                      double* __restrict__ x, const int* skip) {
+  pdl_enter();
   if (skip && *skip) return;
   extern __shared__ double y[];
   for (int i = threadIdx.x; i < N; i += blockDim.x) y[i] = (i < nfree) ? b[f2g[i]] : b[ngrid];
@@ -1376,13 +1384,15 @@ static int launch_tri(Ctx* c, LevelBuf& L, const CUtensorMap& mS, const CUtensor
   cfg.blockDim = dim3(32 * gs::kWarps);
   cfg.dynamicSmemBytes = sizeof(gs::Smem);
   cfg.stream = c->stream;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = cs;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   Ctx::ProfEv* pe = nullptr;
   if (int rc = prof_begin(c, L, 0, &pe)) return rc;
   VTS_CUDA(cudaLaunchKernelEx(&cfg, k_gs_tri<FWD, ZERO>, L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, bands, mS, mP,
@@ -1404,14 +1414,14 @@ static int gs_sweep(Ctx* c, int k, const double* b, double* x, bool forward, boo
     return launch_tri<true, true>(c, L, mS, mP, mQ, x, skip);
   }
   if (forward) {
-    k_gs_old<true><<<div_up(L.d.nnodes, 256), 256, 0, c->stream>>>(L.d.nx, L.d.ny, L.d.ngrid, L.d.stU, b,
-                                                                    L.d.border, x, P, skip);
+    VTS_CUDA(launch_pdl(k_gs_old<true>, dim3(div_up(L.d.nnodes, 256)), dim3(256), 0, c->stream, L.d.nx, L.d.ny, L.d.ngrid, L.d.stU, b,
+                                                                    L.d.border, x, P, skip));
     VTS_LAUNCHED(c);
     if (encode_skewed(&mS, L.d.stL, kHalf, L) || encode_skewed(&mP, P, 2, L)) return 5;
     return launch_tri<true, false>(c, L, mS, mP, mP, x, skip);
   }
-  k_gs_old<false><<<div_up(L.d.nnodes, 256), 256, 0, c->stream>>>(L.d.nx, L.d.ny, L.d.ngrid, L.d.stL, b,
-                                                                   L.d.border, x, P, skip);
+  VTS_CUDA(launch_pdl(k_gs_old<false>, dim3(div_up(L.d.nnodes, 256)), dim3(256), 0, c->stream, L.d.nx, L.d.ny, L.d.ngrid, L.d.stL, b,
+                                                                   L.d.border, x, P, skip));
   VTS_LAUNCHED(c);
   if (encode_skewed(&mS, L.d.stU, kHalf, L) || encode_skewed(&mP, P, 2, L)) return 5;
   return launch_tri<false, false>(c, L, mS, mP, mP, x, skip);
@@ -1433,12 +1443,12 @@ static int gs_pair(Ctx* c, int k, const double* b, double* x, bool forward, bool
   cfg.blockDim = dim3(32 * gs::kWarpsPair);
   cfg.dynamicSmemBytes = sizeof(gs::Smem);
   cfg.stream = c->stream;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 1;  // the occupancy query below sees the cluster shape only
   // the largest clusters (fewest cross-cluster handoffs) with which both halves of
   // the grid can be resident at once; none -> two single sweeps
   static int max_clusters[17] = {0};
@@ -1461,6 +1471,9 @@ static int gs_pair(Ctx* c, int k, const double* b, double* x, bool forward, bool
   }
   if (cs == 0) return 0;  // not all resident: caller runs two sweeps
   at[0].val.clusterDim.x = cs;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = 2;
   cfg.gridDim = dim3(2 * cs * ncl);
   CUtensorMap mSA, mPA, mQA, mSB, mBB, mQB, mXB, mUB, mXA;
   const double* solve_half = forward ? L.d.stL : L.d.stU;
@@ -1537,13 +1550,13 @@ int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
     LevelBuf& L = c->lv[k];
     const double* b = (k == top) ? b_top : L.b;
     double* x = (k == top) ? z_top : L.x;
-    k_alpha_init<<<1, 1, 0, c->stream>>>(L.d.ngrid, b, x, c->d_corner, k == top ? 1 : 0, skip);
+    VTS_CUDA(launch_pdl(k_alpha_init, dim3(1), dim3(1), 0, c->stream, L.d.ngrid, b, x, c->d_corner, k == top ? 1 : 0, skip));
     VTS_LAUNCHED(c);
     if (int rc = gs_two_sweeps(c, k, b, x, true, true, skip)) return rc;
     if (int rc = level_residual_grid(c, k, x, b, L.r, skip)) return rc;
     LevelBuf& C = c->lv[k - 1];
-    k_restrict<<<div_up(C.d.nnodes + 1, 256), 256, 0, c->stream>>>(L.d.nx, L.d.ny, L.d.free_mask, L.r, C.d.nx,
-                                                                     C.d.ny, C.d.free_mask, C.b, 1, skip);
+    VTS_CUDA(launch_pdl(k_restrict, dim3(div_up(C.d.nnodes + 1, 256)), dim3(256), 0, c->stream, L.d.nx, L.d.ny, L.d.free_mask, L.r, C.d.nx,
+                                                                     C.d.ny, C.d.free_mask, C.b, 1, skip));
     VTS_LAUNCHED(c);
   }
   if (kb >= 1) {
@@ -1552,8 +1565,8 @@ int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
     LevelBuf& C = c->lv[0];
     double* x0 = (top == 0) ? z_top : C.x;
     const double* b0 = (top == 0) ? b_top : C.b;
-    k_coarse_solve<<<1, 1024, sizeof(double) * c->N0, c->stream>>>(c->N0, C.d.nfree, C.d.ngrid, c->chol,
-                                                                    C.d.free2grid, b0, x0, skip);
+    VTS_CUDA(launch_pdl(k_coarse_solve, dim3(1), dim3(1024), sizeof(double) * c->N0, c->stream, c->N0, C.d.nfree, C.d.ngrid, c->chol,
+                                                                    C.d.free2grid, b0, x0, skip));
     VTS_LAUNCHED(c);
   }
   // ascent
@@ -1562,14 +1575,14 @@ int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
     LevelBuf& C = c->lv[k - 1];
     const double* b = (k == top) ? b_top : L.b;
     double* x = (k == top) ? z_top : L.x;
-    k_prolong_add<<<div_up(L.d.nnodes + 1, 256), 256, 0, c->stream>>>(L.d.nx, L.d.ny, L.d.free_mask, x, C.d.nx,
-                                                                        C.d.ny, C.d.free_mask, C.x, skip);
+    VTS_CUDA(launch_pdl(k_prolong_add, dim3(div_up(L.d.nnodes + 1, 256)), dim3(256), 0, c->stream, L.d.nx, L.d.ny, L.d.free_mask, x, C.d.nx,
+                                                                        C.d.ny, C.d.free_mask, C.x, skip));
     VTS_LAUNCHED(c);
     if (int rc = gs_two_sweeps(c, k, b, x, false, false, skip)) return rc;
     if (k == top) {
       const int grid = (int)std::min<long long>(div_up(L.d.ngrid, 256), kReduceGridCap);
-      k_alpha_relax<<<grid, 256, 0, c->stream>>>(L.d.ngrid, L.d.border, b, x, c->d_corner, c->partials,
-                                                  c->counters + 6, skip);
+      VTS_CUDA(launch_pdl(k_alpha_relax, dim3(grid), dim3(256), 0, c->stream, L.d.ngrid, L.d.border, b, x, c->d_corner, c->partials,
+                                                  c->counters + 6, skip));
       VTS_LAUNCHED(c);
     }
   }
@@ -1599,9 +1612,9 @@ int mg_setup(Ctx* c, double shift_scale) {
     k_symmetrize<<<div_up(C.d.nnodes, 128), 128, 0, c->stream>>>(C.d.nx, C.d.ny, tmp, C.d.free_mask, C.d.stL,
                                                                   C.d.stU);
     VTS_LAUNCHED(c);
-    k_restrict<<<div_up(C.d.nnodes + 1, 256), 256, 0, c->stream>>>(F.d.nx, F.d.ny, F.d.free_mask, F.d.border,
+    VTS_CUDA(launch_pdl(k_restrict, dim3(div_up(C.d.nnodes + 1, 256)), dim3(256), 0, c->stream, F.d.nx, F.d.ny, F.d.free_mask, F.d.border,
                                                                      C.d.nx, C.d.ny, C.d.free_mask, C.d.border, 0,
-                                                                     nullptr);
+                                                                     nullptr));
     VTS_LAUNCHED(c);
   }
   // coarsest dense factor

@@ -13,6 +13,7 @@
 namespace vts {
 
 __global__ void k_mr_scale(int len, const double* __restrict__ y, double* __restrict__ v, const MinresDev* st) {
+  pdl_enter();
   if (st->stopped) return;
   const double s = 1.0 / st->beta;  // linalg.py:193-194
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x) v[i] = s * y[i];
@@ -21,6 +22,7 @@ __global__ void k_mr_scale(int len, const double* __restrict__ y, double* __rest
 // y = y - (beta/oldb) r1 (iteration >= 2), alfa = v.y   (linalg.py:196-198)
 __global__ void k_mr_lanczos(int len, double* __restrict__ y, const double* __restrict__ r1,
                              const double* __restrict__ v, MinresDev* st, double* partials, unsigned* counter) {
+  pdl_enter();
   if (st->stopped) return;
   __shared__ double scratch[kThreads / 32];
   const bool second = st->iters >= 1;  // st->iters counts completed iterations
@@ -38,6 +40,7 @@ __global__ void k_mr_lanczos(int len, double* __restrict__ y, const double* __re
 
 // y = y - (alfa/beta) r2   (linalg.py:199)
 __global__ void k_mr_axpy2(int len, double* __restrict__ y, const double* __restrict__ r2, const MinresDev* st) {
+  pdl_enter();
   if (st->stopped) return;
   const double f = st->alfa / st->beta;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x)
@@ -47,6 +50,7 @@ __global__ void k_mr_axpy2(int len, double* __restrict__ y, const double* __rest
 // beta = r2.y, then the Givens update of linalg.py:203-221 (last block)
 __global__ void k_mr_givens(int len, const double* __restrict__ r2, const double* __restrict__ y, MinresDev* st,
                             double* partials, unsigned* counter) {
+  pdl_enter();
   if (st->stopped) return;
   __shared__ double scratch[kThreads / 32];
   double acc[1] = {0.0};
@@ -90,6 +94,7 @@ __global__ void k_mr_givens(int len, const double* __restrict__ r2, const double
 __global__ void k_mr_update(int len, const double* __restrict__ v, const double* __restrict__ w1,
                             const double* __restrict__ w2, double* __restrict__ wn, const double* __restrict__ x,
                             double* __restrict__ xn, MinresDev* st, double* partials, unsigned* counter) {
+  pdl_enter();
   if (st->stopped) return;
   __shared__ double scratch[kThreads / 32];
   const double oldeps = st->oldeps, delta = st->delta, gamma = st->gamma, phi = st->phi;
@@ -123,6 +128,7 @@ __global__ void k_mr_update(int len, const double* __restrict__ v, const double*
 // true residual after a verify apply: relres = ||b - Ax|| / ||b||  (linalg.py:231-239)
 __global__ void k_mr_verify(int len, const double* __restrict__ b, const double* __restrict__ ax, MinresDev* st,
                             double* partials, unsigned* counter) {
+  pdl_enter();
   if (st->no_verify) return;
   __shared__ double scratch[kThreads / 32];
   double acc[1] = {0.0};
@@ -151,6 +157,7 @@ __global__ void k_mr_verify(int len, const double* __restrict__ b, const double*
 // history hook: ||b - A x|| / ||b|| after every iteration (tests only)
 __global__ void k_mr_history(int len, const double* __restrict__ b, const double* __restrict__ ax,
                              const MinresDev* st, double* hist, double* partials, unsigned* counter) {
+  pdl_enter();
   __shared__ double scratch[kThreads / 32];
   double acc[1] = {0.0};
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x) {
@@ -288,12 +295,12 @@ int minres(Ctx* c, const double* b_free, double* x_free, double tol, int max_ite
   double* x_in[2] = {nullptr, nullptr};
   double* x_out[2] = {nullptr, nullptr};
   auto enqueue = [&](int it) -> int {
-    k_mr_scale<<<grid, kThreads, 0, c->stream>>>(len, y, v, c->mst);
+    VTS_CUDA(launch_pdl(k_mr_scale, dim3(grid), dim3(kThreads), 0, c->stream, len, y, v, c->mst));
     VTS_LAUNCHED(c);
     if (int rc = newton_apply_grid(c, v, y, stopped)) return rc;
-    k_mr_lanczos<<<grid, kThreads, 0, c->stream>>>(len, y, r1, v, c->mst, c->partials, c->counters + 8);
+    VTS_CUDA(launch_pdl(k_mr_lanczos, dim3(grid), dim3(kThreads), 0, c->stream, len, y, r1, v, c->mst, c->partials, c->counters + 8));
     VTS_LAUNCHED(c);
-    k_mr_axpy2<<<grid, kThreads, 0, c->stream>>>(len, y, r2, c->mst);
+    VTS_CUDA(launch_pdl(k_mr_axpy2, dim3(grid), dim3(kThreads), 0, c->stream, len, y, r2, c->mst));
     VTS_LAUNCHED(c);
     // r1 = r2 ; r2 = y ; new y buffer
     double* dead = (r1 == r2) ? nullptr : r1;
@@ -307,24 +314,24 @@ int minres(Ctx* c, const double* b_free, double* x_free, double tol, int max_ite
     } else {
       VTS_CUDA(cudaMemcpyAsync(y, r2, sizeof(double) * len, cudaMemcpyDeviceToDevice, c->stream));
     }
-    k_mr_givens<<<grid, kThreads, 0, c->stream>>>(len, r2, y, c->mst, c->partials, c->counters + 9);
+    VTS_CUDA(launch_pdl(k_mr_givens, dim3(grid), dim3(kThreads), 0, c->stream, len, r2, y, c->mst, c->partials, c->counters + 9));
     VTS_LAUNCHED(c);
     // w1 = w2 ; w2 = w ; w = new (into the dead w1 buffer)
     double* w1 = w2;
     w2 = w;
     double* wn = wfree;
-    k_mr_update<<<grid, kThreads, 0, c->stream>>>(len, v, w1, w2, wn, x, xalt, c->mst, c->partials,
-                                                  c->counters + 10);
+    VTS_CUDA(launch_pdl(k_mr_update, dim3(grid), dim3(kThreads), 0, c->stream, len, v, w1, w2, wn, x, xalt, c->mst, c->partials,
+                                                  c->counters + 10));
     VTS_LAUNCHED(c);
     wfree = w1;
     w = wn;
     if (history) {
       if (int rc = newton_apply_grid(c, xalt, T, nullptr)) return rc;
-      k_mr_history<<<grid, kThreads, 0, c->stream>>>(len, B, T, c->mst, dhist, c->partials, c->counters + 11);
+      VTS_CUDA(launch_pdl(k_mr_history, dim3(grid), dim3(kThreads), 0, c->stream, len, B, T, c->mst, dhist, c->partials, c->counters + 11));
       VTS_LAUNCHED(c);
     }
     if (int rc = newton_apply_grid(c, xalt, T, nover)) return rc;
-    k_mr_verify<<<grid, kThreads, 0, c->stream>>>(len, B, T, c->mst, c->partials, c->counters + 12);
+    VTS_CUDA(launch_pdl(k_mr_verify, dim3(grid), dim3(kThreads), 0, c->stream, len, B, T, c->mst, c->partials, c->counters + 12));
     VTS_LAUNCHED(c);
     // assume the update succeeds (the next iteration reads x_out); a failed or
     // stopped iteration makes every later launch a no-op on the device
