@@ -86,6 +86,7 @@ struct Ctx {
 
   long long launches = 0;
   std::vector<void*> allocs;  // the device arena holding every array of the context
+  std::vector<size_t> alloc_bytes;  // sizes of `allocs` (returned to the device pool)
 
   // optional per-launch timing of the wavefront kernel (vts_profile_begin/end)
   bool prof = false;

@@ -59,11 +59,48 @@ static int ensure_ke(Ctx* c) {
 // the whole block once and hands out 256-byte aligned pointers.
 // Pinned host scalars ([64] doubles, then the MINRES state mirror) come from a
 // process-wide pool: cudaMallocHost costs milliseconds, and solvers create a
-// context per problem.  free_ctx releases a block only after cudaFree has
-// synchronised the device, so no copy into it can still be in flight.
+// context per problem.  free_ctx releases a block only after a device
+// synchronisation, so no copy into it can still be in flight.
 constexpr size_t kPinnedBytes = ((64 * sizeof(double) + 2 * sizeof(MinresDev)) + 255) & ~size_t(255);
 static std::mutex g_pinned_mutex;
 static std::vector<void*> g_pinned_free;
+
+// Device arenas are recycled the same way: a context's single allocation goes
+// back to a small process-wide pool (at most kDevPool blocks) and the next
+// context of a similar size takes it, so a solver that creates one context per
+// problem pays cudaMalloc once (tens of milliseconds for a 0.5 GB arena).
+constexpr size_t kDevPool = 2;
+static std::mutex g_dev_mutex;
+static std::vector<std::pair<void*, size_t>> g_dev_free;
+
+static cudaError_t device_acquire(void** p, size_t* bytes) {
+  {
+    std::lock_guard<std::mutex> lock(g_dev_mutex);
+    for (size_t i = 0; i < g_dev_free.size(); ++i) {
+      const size_t have = g_dev_free[i].second;
+      if (have >= *bytes && have <= 2 * *bytes) {
+        *p = g_dev_free[i].first;
+        *bytes = have;
+        g_dev_free.erase(g_dev_free.begin() + (ptrdiff_t)i);
+        return cudaSuccess;
+      }
+    }
+  }
+  return cudaMalloc(p, *bytes);
+}
+
+static void device_release(void* p, size_t bytes) {
+  void* evict = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(g_dev_mutex);
+    g_dev_free.emplace_back(p, bytes);
+    if (g_dev_free.size() > kDevPool) {
+      evict = g_dev_free.front().first;
+      g_dev_free.erase(g_dev_free.begin());
+    }
+  }
+  if (evict) cudaFree(evict);
+}
 
 static void* pinned_acquire() {
   {
@@ -103,8 +140,10 @@ struct Arena {
   }
   int commit(Ctx* c) {
     char* base = nullptr;
-    VTS_CUDA(cudaMalloc(reinterpret_cast<void**>(&base), std::max<size_t>(used, 256)));
+    size_t bytes = std::max<size_t>(used, 256);
+    VTS_CUDA(device_acquire(reinterpret_cast<void**>(&base), &bytes));
     c->allocs.push_back(base);
+    c->alloc_bytes.push_back(bytes);
     VTS_CUDA(cudaMemset(base, 0, used));
     for (const Req& r : reqs) *r.slot = base + r.offset;
     return 0;
@@ -123,7 +162,8 @@ static void dalloc_pad(Arena& a, double** p, size_t count, size_t pad) {
 }
 
 static void free_ctx(Ctx* c) {
-  for (void* p : c->allocs) cudaFree(p);
+  cudaDeviceSynchronize();  // nothing may still write into the blocks handed back below
+  for (size_t i = 0; i < c->allocs.size(); ++i) device_release(c->allocs[i], c->alloc_bytes[i]);
   for (cudaEvent_t e : c->mr_ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : c->prof_ev) {

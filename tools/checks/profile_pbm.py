@@ -28,4 +28,4 @@ rep = vts.solve_pbm(prob)
 torch.cuda.synchronize()
 pr.disable()
 st = pstats.Stats(pr)
-st.sort_stats("cumulative").print_stats(12)
+st.sort_stats("tottime").print_stats(25)
