@@ -1,0 +1,171 @@
+"""Size-independent properties of the CUDA path, at the BASELINE sizes too.
+
+The reference pins its linear algebra with properties as well as with dense
+oracles: the bordered Newton matrix is symmetric positive
+definite, the V(2,2) cycle is a symmetric positive definite operator that maps
+zero to zero and contracts in the energy norm (test_linalg_multigrid.py:
+217-258), and minres_solve stops on the true residual, honours its cap and
+returns zero for a zero right-hand side (test_linalg_multigrid.py:94-139).
+The same properties are checked here on the device operators, on the small
+configs and on the 1024x512 microbench system (C3), where no CPU oracle
+finishes in test time.  The A/B switches of the library (modal vs dense
+Newton apply, programmatic dependent launch) are checked against each other.
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU containers
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1904_06556_b200 as vts  # noqa: E402
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _system(key: str, seed: int = 0, stiffness: bool = False):
+    """A seeded Newton system; with `stiffness`, rho = 1 and a huge penalty p make the
+    Schur matrix the plain stiffness K (rank-one terms ~1e-6), the operator the
+    reference's contraction test uses (test_linalg_multigrid.py:223-228)."""
+    prob = vts.build_config(key)
+    n, m = prob.n, prob.m
+    rng = np.random.default_rng(seed)
+    host = dict(u=rng.normal(0.0, 1e-2, n), alpha=1e-3, nu_lo=rng.uniform(0, 1e-2, m),
+                nu_up=rng.uniform(0, 1e-2, m), rho=rng.uniform(0.5, 2.0, m), mu_lo=np.ones(m), mu_up=np.ones(m),
+                p=np.full(m, 1e-2), q_lo=np.ones(m), q_up=np.ones(m))
+    if stiffness:
+        host.update(rho=np.ones(m), p=np.full(m, 1e6), nu_lo=np.zeros(m), nu_up=np.zeros(m))
+    st = vts.PbmState(**{k: (v if k == "alpha" else torch.as_tensor(v, device="cuda")) for k, v in host.items()})
+    ops = vts.ElementOps(prob.fine)
+    ev = vts.eval_lagrangian(st, ops, prob.f, vts.DensityBounds.for_problem(m, prob.volume, 0.0),
+                             vts.PenaltyBarrier())
+    mat, rhs = vts.schur_system(ev, ops)
+    mg = vts.MgPreconditioner(mat, prob.transfers)
+    return prob, ops, mat, rhs, mg
+
+
+@pytest.fixture(scope="module", params=["C1", "C2", "C3"])
+def system(request):
+    return _system(request.param)
+
+
+def _rand(n, seed):
+    return torch.as_tensor(np.random.default_rng(seed).normal(size=n), device="cuda")
+
+
+def test_newton_matrix_is_symmetric_positive_definite(system):
+    _, _, mat, rhs, _ = system
+    a, b = _rand(rhs.numel(), 1), _rand(rhs.numel(), 2)
+    sa, sb = mat.matvec(a), mat.matvec(b)
+    lhs, rhs_ = float(torch.dot(sa, b)), float(torch.dot(a, sb))
+    scale = float(sa.norm() * b.norm() + a.norm() * sb.norm())
+    assert abs(lhs - rhs_) <= 1e-13 * scale
+    assert float(torch.dot(sa, a)) > 0.0 and float(torch.dot(sb, b)) > 0.0
+
+
+def test_vcycle_is_symmetric_positive_definite_and_maps_zero_to_zero(system):
+    _, _, _, rhs, mg = system
+    n = rhs.numel()
+    zero = torch.zeros(n, dtype=torch.float64, device="cuda")
+    assert torch.count_nonzero(mg.apply(zero)).item() == 0
+    a, b = _rand(n, 3), _rand(n, 4)
+    ma, mb = mg.apply(a), mg.apply(b)
+    lhs, rhs_ = float(torch.dot(ma, b)), float(torch.dot(a, mb))
+    scale = float(ma.norm() * b.norm() + a.norm() * mb.norm())
+    assert abs(lhs - rhs_) <= 1e-10 * scale
+    assert float(torch.dot(ma, a)) > 0.0
+
+
+def _contraction(apply_s, apply_m, dot, e, iters=15):
+    rate = 0.0
+    for _ in range(iters):
+        e_new = e - apply_m(apply_s(e))
+        rate = (dot(e_new, apply_s(e_new)) / dot(e, apply_s(e))) ** 0.5
+        e = e_new / dot(e_new, e_new) ** 0.5
+    return rate
+
+
+@pytest.mark.parametrize("key", ["C1", "C2", "C3"])
+def test_vcycle_contraction_matches_the_oracle(key):
+    """Energy-norm contraction ||I - M K||_K of the V-cycle by power iteration on
+    the stiffness operator (oracles.py:282-304), against the oracle's V-cycle on
+    the same inputs.  The reference bounds it by 0.5 on its cantilever
+    (test_linalg_multigrid.py:223-228); the MBB half-beam, held by one roller
+    and a symmetry line, contracts at 0.82 in both implementations."""
+    import oracle
+
+    _, _, mat, rhs, mg = _system(key, stiffness=True)
+    e0 = np.random.default_rng(5).normal(size=rhs.numel())
+    gpu = _contraction(mat.matvec, mg.apply, lambda a, b: float(torch.dot(a, b)),
+                       torch.as_tensor(e0, device="cuda"))
+    oprob = oracle.build_config(key)
+    n, m = oprob.n, oprob.m
+    rng = np.random.default_rng(0)
+    host = dict(u=rng.normal(0.0, 1e-2, n), alpha=1e-3, nu_lo=np.zeros(m), nu_up=np.zeros(m), rho=np.ones(m),
+                mu_lo=np.ones(m), mu_up=np.ones(m), p=np.full(m, 1e6), q_lo=np.ones(m), q_up=np.ones(m))
+    oev = oracle.eval_lagrangian(oracle.PbmState(**host), oracle.ElementOps2D(oprob.fine), oprob.f,
+                                 oracle.DensityBounds.for_problem(m, oprob.volume, 0.0), oracle.PenaltyBarrier())
+    omat, _ = oracle.schur_system(oev, oracle.ElementOps2D(oprob.fine))
+    omg = oracle.MgPreconditioner(omat, oprob.transfers)
+    ref = _contraction(omat.matvec, omg.apply, lambda a, b: float(a @ b), e0)
+    assert abs(gpu - ref) <= 1e-6 * ref
+    if key in ("C1", "C3"):  # cantilevers
+        assert gpu < 0.5
+
+
+def test_minres_contracts(system):
+    _, _, mat, rhs, mg = system
+    # stops on the true residual
+    res = vts.minres_solve(mat, rhs, vts.MinresConfig(tol=1e-8, max_iters=1000), mg.apply)
+    assert res.converged
+    true = float((rhs - mat.matvec(res.x)).norm() / rhs.norm())
+    assert true <= 1e-8 and abs(true - res.relres) <= 1e-3 * true
+    # honours the cap
+    capped = vts.minres_solve(mat, rhs, vts.MinresConfig(tol=1e-14, max_iters=3), mg.apply)
+    assert capped.iterations == 3 and not capped.converged
+    # zero right-hand side: zero solution, no iterations
+    zero = vts.minres_solve(mat, torch.zeros_like(rhs), vts.MinresConfig(tol=1e-8, max_iters=10), mg.apply)
+    assert zero.iterations == 0 and torch.count_nonzero(zero.x).item() == 0
+
+
+def test_minres_rejects_a_non_finite_right_hand_side():
+    _, _, mat, rhs, mg = _system("C1")
+    bad = rhs.clone()
+    bad[7] = float("nan")
+    with pytest.raises((vts.MinresError, ValueError)):
+        vts.minres_solve(mat, bad, vts.MinresConfig(tol=1e-8, max_iters=50), mg.apply)
+
+
+def _ab(tmp_path, name, key, env_extra):
+    out = tmp_path / f"{name}.npy"
+    env = dict(os.environ, **env_extra)
+    subprocess.run([sys.executable, os.path.join(REPO, "tools", "checks", "ab_vcycle.py"), str(out), key],
+                   cwd=REPO, env=env, check=True, capture_output=True, timeout=600)
+    return np.load(out)
+
+
+@pytest.mark.parametrize("key", ["C2", "C3"])
+def test_pdl_launches_are_bitwise_identical_to_plain_launches(tmp_path, key):
+    assert np.array_equal(_ab(tmp_path, "pdl", key, {}), _ab(tmp_path, "plain", key, {"VTS_NO_PDL": "1"}))
+
+
+@pytest.mark.parametrize("key", ["C2", "C3"])
+def test_modal_apply_matches_the_dense_products(tmp_path, key):
+    """V-cycle output and a MINRES solution with the modal Newton apply against the
+    dense K_e products: same iteration count, solutions within MINRES' own accuracy."""
+    modal = _ab(tmp_path, "modal", key, {})
+    dense = _ab(tmp_path, "dense", key, {"VTS_DENSE_APPLY": "1"})
+    assert modal[-1] == dense[-1]  # MINRES iterations
+    nz = (modal.size - 1) // 2
+    np.testing.assert_array_equal(modal[:nz], dense[:nz])  # the V-cycle does not use the apply
+    x_m, x_d = modal[nz:-1], dense[nz:-1]
+    assert np.abs(x_m - x_d).max() <= 1e-8 * np.abs(x_d).max()
