@@ -182,6 +182,50 @@ int vts_penalty_eval(vts_ctx* ctx, int64_t n, const double* tau, double branch, 
                      double* d2, uint32_t* warn_flags);
 
 /*
+ * Interior-point Newton step (ip.py:114-222) on the same operators.  All
+ * arrays are DEVICE pointers (u, du, res_u: n free dofs; element arrays: m).
+ *
+ * vts_ip_residual: `kkt_residual` (ip.py:114-134): writes q, res_c, res_lo,
+ * res_up (m) and res_u = K(rho) u - f (n); HOST `scalars` (9) = {res_alpha,
+ * tau_res, f.u, sum rho, nu_lo.(rho-lower), nu_up.(upper-rho), comp_max
+ * (ip.py:285-288), min_slack (ip.py:311-313), min(nu_lo, nu_up)}.
+ */
+int vts_ip_residual(vts_ctx* ctx, const double* u, double alpha, const double* rho, const double* nu_lo,
+                    const double* nu_up, double r, double s, const double* lower, const double* upper, double volume,
+                    const double* f, double norm_f, double* q, double* res_c, double* res_lo, double* res_up,
+                    double* res_u, double* scalars);
+
+/*
+ * vts_ip_schur_system: `schur_system` (ip.py:137-158) bound into the context.
+ * The reference's S+ has border +sum (1/D) w (`assemble(..., border_sign=+1)`,
+ * fem.py:188-209); with E = diag(I, -1) the context holds S- = E S+ E (the
+ * PBM operator's sign) and flips the border entry of every bordered vector at
+ * the API edge, so vts_newton_apply / vts_vcycle / vts_minres act as S+ and
+ * its preconditioner on vectors in the reference's convention.  Writes D
+ * (`dcoef`), g (m) and `rhs` (n+1, ip.py:155-157); HOST `corner` = sum 1/D.
+ */
+int vts_ip_schur_system(vts_ctx* ctx, const double* u, const double* rho, const double* nu_lo, const double* nu_up,
+                        const double* lower, const double* upper, const double* res_c, const double* res_lo,
+                        const double* res_up, const double* res_u, double res_alpha, double* dcoef, double* g,
+                        double* rhs, double* corner);
+
+/* vts_ip_reconstruct: `reconstruct` (ip.py:161-186); dalpha in the reference's sign. */
+int vts_ip_reconstruct(vts_ctx* ctx, const double* u, const double* du, double dalpha, const double* dcoef,
+                       const double* g, const double* res_c, const double* res_lo, const double* res_up,
+                       const double* rho, const double* nu_lo, const double* nu_up, const double* lower,
+                       const double* upper, double* drho, double* dnu_up, double* dnu_lo);
+
+/*
+ * vts_ip_step_bounds: the minima behind `step_lengths` (ip.py:189-222), HOST
+ * `mins` (4) = {min (upper-rho)/drho over drho > 0, min (lower-rho)/drho over
+ * drho < 0, min -nu_lo/dnu_lo over dnu_lo < 0, min -nu_up/dnu_up over
+ * dnu_up < 0}, +inf for an empty set.
+ */
+int vts_ip_step_bounds(vts_ctx* ctx, const double* rho, const double* drho, const double* nu_lo,
+                       const double* dnu_lo, const double* nu_up, const double* dnu_up, const double* lower,
+                       const double* upper, double* mins);
+
+/*
  * Benchmark helper (no reference counterpart): average device time in ms of
  * {Newton apply, one V-cycle, finest forward GS sweep, second-finest forward
  * GS sweep, finest residual, mg_setup} over `reps` back-to-back launches,

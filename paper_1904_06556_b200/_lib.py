@@ -59,6 +59,10 @@ SIGNATURES = {
     "vts_penalty_eval": (ctypes.c_int, [_P, _I64, _P, _D, _P, _P, _P, _PU32]),
     "vts_time_kernels": (ctypes.c_int, [_P, _I32, _PD]),
     "vts_time_cold": (ctypes.c_int, [_P, _I32, _P, ctypes.c_int64, _PD]),
+    "vts_ip_residual": (ctypes.c_int, [_P, _P, _D, _P, _P, _P, _D, _D, _P, _P, _D, _P, _D, _P, _P, _P, _P, _P, _PD]),
+    "vts_ip_schur_system": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _D, _P, _P, _P, _PD]),
+    "vts_ip_reconstruct": (ctypes.c_int, [_P, _P, _P, _D, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "vts_ip_step_bounds": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _PD]),
     "vts_kernel_launches": (ctypes.c_int64, [_P]),
     "vts_profile_begin": (ctypes.c_int, [_P]),
     "vts_profile_end": (ctypes.c_int, [_P, _PD]),

@@ -61,6 +61,7 @@ struct Ctx {
   double corner = 0.0;
   double* d_corner = nullptr;   // device copy of corner
   bool system_bound = false;
+  bool border_flip = false;    // the bound system is E S+ E (an IP system, ip.inc.cu): flip x_alpha at the API edge
   bool mg_ready = false;
   int shifted = 0;
 

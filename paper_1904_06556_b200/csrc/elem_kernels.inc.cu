@@ -127,7 +127,7 @@ __global__ void k_free_to_grid(int ngrid, int nfree, const int32_t* __restrict__
     const int f = g2f[i];
     dst[i] = f >= 0 ? src[f] : 0.0;
   } else if (i == ngrid && bordered) {
-    dst[ngrid] = src[nfree];
+    dst[ngrid] = bordered < 0 ? -src[nfree] : src[nfree];  // -1: the bound system is E S+ E (ip.inc.cu)
   }
 }
 
@@ -136,7 +136,7 @@ __global__ void k_grid_to_free(int nfree, int ngrid, const int32_t* __restrict__
                                int bordered) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < nfree) dst[i] = src[f2g[i]];
-  else if (i == nfree && bordered) dst[nfree] = src[ngrid];
+  else if (i == nfree && bordered) dst[nfree] = bordered < 0 ? -src[ngrid] : src[ngrid];
 }
 
 // trial displacement u + kappa du on the grid, with f . (u + kappa du)
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(kThreads) k_schur_node(int nnodes, int nx, int
   }
 }
 
-__global__ void k_schur_finish(int nb, const double* __restrict__ pe, double res_alpha, int n,
+__global__ void k_schur_finish(int nb, const double* __restrict__ pe, double res_alpha, double sign, int n,
                                double* rhs, double* d_corner, double* out) {
   __shared__ double scratch[2 * kThreads / 32];
   double t[2] = {0, 0};
@@ -393,7 +393,7 @@ __global__ void k_schur_finish(int nb, const double* __restrict__ pe, double res
   }
   block_sum<2>(t, scratch);
   if (threadIdx.x == 0) {
-    rhs[n] = -res_alpha - t[0];
+    rhs[n] = sign * (-res_alpha - t[0]);
     *d_corner = t[1];
     out[0] = t[1];
     out[1] = t[0];
@@ -570,7 +570,7 @@ int free_to_grid(Ctx* c, int level, const double* src, double* dst, bool bordere
   const LevelBuf& L = c->lv[level];
   const int total = L.d.ngrid + 1;
   k_free_to_grid<<<div_up(total, kThreads), kThreads, 0, c->stream>>>(L.d.ngrid, L.d.nfree, L.grid2free,
-                                                                      src, dst, bordered ? 1 : 0);
+                                                                      src, dst, bordered ? (c->border_flip ? -1 : 1) : 0);
   VTS_LAUNCHED(c);
   return 0;
 }
@@ -579,7 +579,7 @@ int grid_to_free(Ctx* c, int level, const double* src, double* dst, bool bordere
   const LevelBuf& L = c->lv[level];
   const int total = L.d.nfree + 1;
   k_grid_to_free<<<div_up(total, kThreads), kThreads, 0, c->stream>>>(L.d.nfree, L.d.ngrid, L.d.free2grid,
-                                                                      src, dst, bordered ? 1 : 0);
+                                                                      src, dst, bordered ? (c->border_flip ? -1 : 1) : 0);
   VTS_LAUNCHED(c);
   return 0;
 }
@@ -641,12 +641,13 @@ int schur_system(Ctx* c, const double* u, const double* res_u, double res_alpha,
                                                                    tcoef, c->chat, res_u, c->lv[F].grid2free,
                                                                    rhs, border, c->lv[F].d.border);
   VTS_LAUNCHED(c);
-  k_schur_finish<<<1, kThreads, 0, c->stream>>>(ge, c->partials, res_alpha, c->n, rhs, c->d_corner, c->dscal);
+  k_schur_finish<<<1, kThreads, 0, c->stream>>>(ge, c->partials, res_alpha, 1.0, c->n, rhs, c->d_corner, c->dscal);
   VTS_LAUNCHED(c);
   if (int rc = sync_scalars(c, 2)) return rc;
   c->corner = c->hscal[0];
   if (corner) *corner = c->corner;
   c->system_bound = true;
+  c->border_flip = false;
   c->mg_ready = false;
   return 0;
 }

@@ -25,6 +25,7 @@
 #include "apply.inc.cu"
 #include "mg.inc.cu"
 #include "minres.inc.cu"
+#include "ip.inc.cu"
 
 namespace vts {
 
@@ -567,6 +568,59 @@ int vts_time_cold(vts_ctx* ctx, int32_t reps, void* flush, int64_t flush_bytes, 
     return 4;
   }
   return vts::time_cold(C(ctx), reps, flush, (size_t)flush_bytes, ms);
+}
+
+int vts_ip_residual(vts_ctx* ctx, const double* u, double alpha, const double* rho, const double* nu_lo,
+                    const double* nu_up, double r, double s, const double* lower, const double* upper, double volume,
+                    const double* f, double norm_f, double* q, double* res_c, double* res_lo, double* res_up,
+                    double* res_u, double* scalars) {
+  VTS_REQUIRE_CTX(ctx);
+  if (!u || !rho || !nu_lo || !nu_up || !lower || !upper || !f || !q || !res_c || !res_lo || !res_up || !res_u ||
+      !scalars) {
+    vts::set_error(VTS_E_ARGUMENT, "vts_ip_residual: NULL argument");
+    return VTS_E_ARGUMENT;
+  }
+  return vts::ip_residual(C(ctx), u, alpha, rho, nu_lo, nu_up, r, s, lower, upper, volume, f, norm_f, q, res_c,
+                          res_lo, res_up, res_u, scalars);
+}
+
+int vts_ip_schur_system(vts_ctx* ctx, const double* u, const double* rho, const double* nu_lo, const double* nu_up,
+                        const double* lower, const double* upper, const double* res_c, const double* res_lo,
+                        const double* res_up, const double* res_u, double res_alpha, double* dcoef, double* g,
+                        double* rhs, double* corner) {
+  VTS_REQUIRE_CTX(ctx);
+  if (!u || !rho || !nu_lo || !nu_up || !lower || !upper || !res_c || !res_lo || !res_up || !res_u || !dcoef || !g ||
+      !rhs) {
+    vts::set_error(VTS_E_ARGUMENT, "vts_ip_schur_system: NULL argument");
+    return VTS_E_ARGUMENT;
+  }
+  return vts::ip_schur_system(C(ctx), u, rho, nu_lo, nu_up, lower, upper, res_c, res_lo, res_up, res_u, res_alpha,
+                              dcoef, g, rhs, corner);
+}
+
+int vts_ip_reconstruct(vts_ctx* ctx, const double* u, const double* du, double dalpha, const double* dcoef,
+                       const double* g, const double* res_c, const double* res_lo, const double* res_up,
+                       const double* rho, const double* nu_lo, const double* nu_up, const double* lower,
+                       const double* upper, double* drho, double* dnu_up, double* dnu_lo) {
+  VTS_REQUIRE_CTX(ctx);
+  if (!u || !du || !dcoef || !g || !res_c || !res_lo || !res_up || !rho || !nu_lo || !nu_up || !lower || !upper ||
+      !drho || !dnu_up || !dnu_lo) {
+    vts::set_error(VTS_E_ARGUMENT, "vts_ip_reconstruct: NULL argument");
+    return VTS_E_ARGUMENT;
+  }
+  return vts::ip_reconstruct(C(ctx), u, du, dalpha, dcoef, g, res_c, res_lo, res_up, rho, nu_lo, nu_up, lower, upper,
+                             drho, dnu_up, dnu_lo);
+}
+
+int vts_ip_step_bounds(vts_ctx* ctx, const double* rho, const double* drho, const double* nu_lo,
+                       const double* dnu_lo, const double* nu_up, const double* dnu_up, const double* lower,
+                       const double* upper, double* mins) {
+  VTS_REQUIRE_CTX(ctx);
+  if (!rho || !drho || !nu_lo || !dnu_lo || !nu_up || !dnu_up || !lower || !upper || !mins) {
+    vts::set_error(VTS_E_ARGUMENT, "vts_ip_step_bounds: NULL argument");
+    return VTS_E_ARGUMENT;
+  }
+  return vts::ip_step_bounds(C(ctx), rho, drho, nu_lo, dnu_lo, nu_up, dnu_up, lower, upper, mins);
 }
 
 int64_t vts_kernel_launches(const vts_ctx* ctx) { return ctx ? C(ctx)->launches : 0; }

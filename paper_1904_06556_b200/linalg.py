@@ -130,6 +130,24 @@ def minres_solve(a, b: torch.Tensor, config: MinresConfig, precond=None, x0=None
 
 
 @dataclass
+class ComplementarityTolerance:
+    """MINRES tolerance tied to the largest complementarity product (linalg.py:289-309):
+    the monotone running minimum of max(scale * comp_max, floor)."""
+
+    tol: float = 1e-2
+    floor: float = 1e-9
+    scale: float = 100.0
+
+    def current(self) -> float:
+        return self.tol
+
+    def observe(self, comp_max: float) -> None:
+        cand = max(self.scale * comp_max, self.floor)
+        if cand < self.tol:
+            self.tol = cand
+
+
+@dataclass
 class StagnationTolerance:
     """Tenfold shrink of the inner tolerance on stagnating Newton residuals."""
 
