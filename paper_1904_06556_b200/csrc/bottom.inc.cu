@@ -54,6 +54,7 @@ struct BotArgs {
   int N0, nfree0;
   const int32_t* f2g0;
   const double* chol;
+  const double* rdiag;  // reciprocals of the factor's diagonal (div_by)
   int off_chol;  // -1: factor read from global memory
   int off_y;
   int off_stage, off_q;  // staged half-stencil and right-hand side, padded ((nn + 2 kBotPad) nodes)
@@ -234,33 +235,40 @@ __device__ void bot_coarse(const BotLevel& C, double* sm, const BotArgs& A) {
     for (int i = tid; i < N * N; i += blockDim.x) sm[A.off_chol + i] = A.chol[i];
   for (int i = tid; i < N; i += blockDim.x) y[i] = (i < A.nfree0) ? sb[A.f2g0[i]] : sb[C.ngrid];
   __syncthreads();
+  BOT_MARK();  // coarse: factor staged, y gathered
   if (N <= 32) {
     // one warp, lane i owns y[i]; same column order and operations as below
     if (tid < 32) {
+      // every lane forms the quotient (div_by, as k_coarse_solve), lane j keeps its own
       double yi = tid < N ? y[tid] : 0.0;
       for (int j = 0; j < N; ++j) {
-        if (tid == j) yi = yi / Lf[(size_t)j * N + j];
+        const double q = div_by(yi, Lf[(size_t)j * N + j], A.rdiag[j]);
+        yi = tid == j ? q : yi;
         const double yj = __shfl_sync(0xffffffffu, yi, j);
-        if (tid > j && tid < N) yi = fma(-Lf[(size_t)tid * N + j], yj, yi);
+        const double lij = (tid > j && tid < N) ? Lf[(size_t)tid * N + j] : 0.0;
+        yi = (tid > j && tid < N) ? fma(-lij, yj, yi) : yi;
       }
       for (int j = N - 1; j >= 0; --j) {
-        if (tid == j) yi = yi / Lf[(size_t)j * N + j];
+        const double q = div_by(yi, Lf[(size_t)j * N + j], A.rdiag[j]);
+        yi = tid == j ? q : yi;
         const double yj = __shfl_sync(0xffffffffu, yi, j);
-        if (tid < j) yi = fma(-Lf[(size_t)j * N + tid], yj, yi);
+        const double lji = tid < j ? Lf[(size_t)j * N + tid] : 0.0;
+        yi = tid < j ? fma(-lji, yj, yi) : yi;
       }
       if (tid < N) y[tid] = yi;
     }
     __syncthreads();
+    BOT_MARK();  // coarse: both substitutions
   } else {
   for (int j = 0; j < N; ++j) {
-    if (tid == 0) y[j] = y[j] / Lf[(size_t)j * N + j];
+    if (tid == 0) y[j] = div_by(y[j], Lf[(size_t)j * N + j], A.rdiag[j]);
     __syncthreads();
     const double yj = y[j];
     for (int i = j + 1 + tid; i < N; i += blockDim.x) y[i] = fma(-Lf[(size_t)i * N + j], yj, y[i]);
     __syncthreads();
   }
   for (int j = N - 1; j >= 0; --j) {
-    if (tid == 0) y[j] = y[j] / Lf[(size_t)j * N + j];
+    if (tid == 0) y[j] = div_by(y[j], Lf[(size_t)j * N + j], A.rdiag[j]);
     __syncthreads();
     const double yj = y[j];
     for (int i = tid; i < j; i += blockDim.x) y[i] = fma(-Lf[(size_t)j * N + i], yj, y[i]);
@@ -398,6 +406,7 @@ static int vcycle_bottom(Ctx* c, const BotArgs& plan, size_t smem, const int* sk
   A.nfree0 = c->lv[0].d.nfree;
   A.f2g0 = c->lv[0].d.free2grid;
   A.chol = c->chol;
+  A.rdiag = c->chol_rdiag;
   VTS_CUDA(launch_pdl(k_vcycle_bottom, dim3(1), dim3(kBotThreads), smem, c->stream, A, skip));
   VTS_LAUNCHED(c);
   return 0;

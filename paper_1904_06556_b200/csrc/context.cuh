@@ -68,6 +68,7 @@ struct Ctx {
   // coarsest dense Cholesky (free order + border)
   int N0 = 0;
   double* chol = nullptr;       // [N0 * N0] lower factor (row-major)
+  double* chol_rdiag = nullptr; // [N0] correctly rounded reciprocals of its diagonal
   int* chol_status = nullptr;   // device status
 
   double* rap_tmp = nullptr;    // unsymmetrised coarse stencil of the largest coarse level

@@ -1279,7 +1279,21 @@ __global__ void __launch_bounds__(1024) k_cholesky(int N, double* A, int* status
   if (threadIdx.x == 0) *status = s_fail;
 }
 
+// y / d from the correctly rounded reciprocal r = 1/d (__drcp_rn, precomputed per
+// column): q = y r, then one fma correction with the exact remainder y - q d
+// (Markstein's quotient refinement) -- three dependent operations where the
+// division routine takes ~15; the A/B checks compare it bit for bit with '/'.
+VTS_DEVICE_INLINE double div_by(double y, double d, double r) {
+  const double q = y * r;
+  return fma(fma(-q, d, y), r, q);
+}
+
+__global__ void k_chol_rdiag(int N, const double* __restrict__ Lf, double* __restrict__ rdiag) {
+  for (int j = threadIdx.x; j < N; j += blockDim.x) rdiag[j] = __drcp_rn(Lf[(size_t)j * N + j]);
+}
+
 __global__ void __launch_bounds__(1024) k_coarse_solve(int N, int nfree, int ngrid, const double* __restrict__ Lf,
+                                                     const double* __restrict__ rdiag,
                                                      const int32_t* __restrict__ f2g, const double* __restrict__ b,
                                                      double* __restrict__ x, const int* skip) {
   pdl_enter();
@@ -1288,14 +1302,14 @@ __global__ void __launch_bounds__(1024) k_coarse_solve(int N, int nfree, int ngr
   for (int i = threadIdx.x; i < N; i += blockDim.x) y[i] = (i < nfree) ? b[f2g[i]] : b[ngrid];
   __syncthreads();
   for (int j = 0; j < N; ++j) {  // L y = b
-    if (threadIdx.x == 0) y[j] = y[j] / Lf[(size_t)j * N + j];
+    if (threadIdx.x == 0) y[j] = div_by(y[j], Lf[(size_t)j * N + j], rdiag[j]);
     __syncthreads();
     const double yj = y[j];
     for (int i = j + 1 + threadIdx.x; i < N; i += blockDim.x) y[i] = fma(-Lf[(size_t)i * N + j], yj, y[i]);
     __syncthreads();
   }
   for (int j = N - 1; j >= 0; --j) {  // L^T x = y
-    if (threadIdx.x == 0) y[j] = y[j] / Lf[(size_t)j * N + j];
+    if (threadIdx.x == 0) y[j] = div_by(y[j], Lf[(size_t)j * N + j], rdiag[j]);
     __syncthreads();
     const double yj = y[j];
     for (int i = threadIdx.x; i < j; i += blockDim.x) y[i] = fma(-Lf[(size_t)j * N + i], yj, y[i]);
@@ -1565,7 +1579,7 @@ int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
     LevelBuf& C = c->lv[0];
     double* x0 = (top == 0) ? z_top : C.x;
     const double* b0 = (top == 0) ? b_top : C.b;
-    VTS_CUDA(launch_pdl(k_coarse_solve, dim3(1), dim3(1024), sizeof(double) * c->N0, c->stream, c->N0, C.d.nfree, C.d.ngrid, c->chol,
+    VTS_CUDA(launch_pdl(k_coarse_solve, dim3(1), dim3(1024), sizeof(double) * c->N0, c->stream, c->N0, C.d.nfree, C.d.ngrid, c->chol, (const double*)c->chol_rdiag,
                                                                     C.d.free2grid, b0, x0, skip));
     VTS_LAUNCHED(c);
   }
@@ -1648,6 +1662,8 @@ int mg_setup(Ctx* c, double shift_scale) {
     }
     c->shifted = 1;
   }
+  k_chol_rdiag<<<1, 256, 0, c->stream>>>(c->N0, c->chol, c->chol_rdiag);
+  VTS_LAUNCHED(c);
   c->mg_ready = true;
   return 0;
 }

@@ -322,6 +322,7 @@ static int create(Ctx** out, int levels, const int32_t* ex, const int32_t* ey, c
   dalloc(arena, &c->d_corner, 1);
   c->N0 = c->lv[0].d.nfree + 1;
   dalloc(arena, &c->chol, (size_t)c->N0 * c->N0);
+  dalloc(arena, &c->chol_rdiag, (size_t)c->N0);
   dalloc(arena, &c->chol_status, 1);
   const size_t rap = levels > 1 ? (size_t)c->lv[levels - 2].d.nnodes * kStencilStride : 1;
   dalloc(arena, &c->rap_tmp, rap);
