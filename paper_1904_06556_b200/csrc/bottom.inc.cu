@@ -66,7 +66,7 @@ struct BotArgs {
 // after its first use; inlined copies per call site ran 3.6x slower cold)
 constexpr int kBotPad = 64;  // zero nodes before/after the staged level (>= 2 x 31, the largest skew)
 template <bool FWD, bool ZERO>
-__device__ __noinline__ void bot_sweep(const BotLevel& L, double* sm, const BotArgs& A) {
+__device__ __noinline__ void bot_sweep(const BotLevel& L, double* sm, const BotArgs& A, bool restage) {
   double* sb = sm + L.off_b;
   double* sx = sm + L.off_x;
   double* stage = sm + A.off_stage;  // [(nn + 2 pad) * kHalf] the half the wavefront solves with
@@ -80,7 +80,8 @@ __device__ __noinline__ void bot_sweep(const BotLevel& L, double* sm, const BotA
     const double2* src = reinterpret_cast<const double2*>(solve_half);
     double2* dst = reinterpret_cast<double2*>(stage);
     const int lo = kBotPad * kHalf / 2, hi = (kBotPad + nn) * kHalf / 2, end = (2 * kBotPad + nn) * kHalf / 2;
-    for (int i = tid; i < end; i += blockDim.x) dst[i] = (i >= lo && i < hi) ? src[i - lo] : make_double2(0.0, 0.0);
+    if (restage)  // the second sweep of a smoothing step solves with the same half: still staged
+      for (int i = tid; i < end; i += blockDim.x) dst[i] = (i >= lo && i < hi) ? src[i - lo] : make_double2(0.0, 0.0);
     const double xa = sx[L.ngrid];
     double2* pd = reinterpret_cast<double2*>(pst);
     for (int i = tid; i < nn + 2 * kBotPad; i += blockDim.x) {
@@ -298,8 +299,8 @@ __global__ void __launch_bounds__(kBotThreads, 1) k_vcycle_bottom(const __grid_c
     const BotLevel& L = A.lv[k];
     if (tid == 0) sm[L.off_x + L.ngrid] = 0.0;  // k_alpha_init on a coarse level
     __syncthreads();
-    bot_sweep<true, true>(L, sm, A);
-    bot_sweep<true, false>(L, sm, A);
+    bot_sweep<true, true>(L, sm, A, true);
+    bot_sweep<true, false>(L, sm, A, false);
     bot_residual(L, sm, A);
     BOT_MARK();  // residual
     const BotLevel& C = A.lv[k - 1];
@@ -324,8 +325,8 @@ __global__ void __launch_bounds__(kBotThreads, 1) k_vcycle_bottom(const __grid_c
             prolong_node(L.nx, L.fm, sm + L.off_x, C.nx, C.fm, sm + C.off_x, fi);
     }
     __syncthreads();
-    bot_sweep<false, false>(L, sm, A);
-    bot_sweep<false, false>(L, sm, A);
+    bot_sweep<false, false>(L, sm, A, true);
+    bot_sweep<false, false>(L, sm, A, false);
   }
   {
     const BotLevel& T = A.lv[A.kb];
