@@ -22,9 +22,9 @@ struct LevelBuf {
   double* b = nullptr;           // [ngrid + 1] V-cycle right-hand side
   double* x = nullptr;           // [ngrid + 1] V-cycle iterate
   double* r = nullptr;           // [ngrid + 1] residual / scratch
-  // GS wavefront progress counters, 3 x gs_groups: [0, G) band handoff (single
-  // sweeps and sweep A of a pair), [G, 2G) band handoff of sweep B, [2G, 3G)
-  // sweep A's stored windows (epoch-tagged, never reset)
+  // GS wavefront progress counters, 3 x gs_groups: [2G, 3G) sweep A's stored
+  // windows (epoch-tagged, never reset); [0, 2G) unused since the band handoff
+  // moved to the value-flag rows gs_xfer
   unsigned long long* gs_flags = nullptr;
   int gs_groups = 0;
   unsigned long long pair_epoch = 0;  // launches of the pipelined sweep pair on this level

@@ -616,7 +616,6 @@ struct GsBand {
   const CUtensorMap* mapU;  // sweep B: old-value half-stencil, 18-double box
   double* x;                // the sweep's result
   const double* xa_src;     // bordered vector holding x_alpha (slot ngrid)
-  unsigned long long* flags;   // (unused since the handoff rows) band-to-band handoff counters
   double* xfer;                // cross-cluster handoff rows of this sweep, [bands][nx] nodes
   unsigned long long* stored;  // sweep A's stored-window counters (pair only)
   unsigned long long epoch;    // pair launch tag of the stored counters
@@ -636,7 +635,6 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
   constexpr bool kGated = ROLE == 2;
   const int nx = G.nx, ny = G.ny, ngrid = G.ngrid, pad_nodes = G.pad_nodes, bands = G.bands;
   double* __restrict__ x = G.x;
-  unsigned long long* flags = G.flags;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -941,10 +939,10 @@ template <bool FWD, bool ZERO>
 __global__ void __launch_bounds__(32 * gs::kWarps, 1)
     k_gs_tri(int nx, int ny, int ngrid, int pad_nodes, int bands, const __grid_constant__ CUtensorMap mapS,
              const __grid_constant__ CUtensorMap mapP, const __grid_constant__ CUtensorMap mapQ,
-             double* __restrict__ x, unsigned long long* flags, double* xfer, const int* skip) {
+             double* __restrict__ x, double* xfer, const int* skip) {
   pdl_enter();
   if (skip && *skip) return;
-  GsBand G{nx, ny, ngrid, pad_nodes, bands, (int)blockIdx.x, &mapS, &mapP, &mapQ, &mapQ, &mapQ, &mapQ, x, x, flags,
+  GsBand G{nx, ny, ngrid, pad_nodes, bands, (int)blockIdx.x, &mapS, &mapP, &mapQ, &mapQ, &mapQ, &mapQ, x, x,
            xfer, nullptr, 0ull, nullptr, nullptr, nullptr, nullptr};
   gs_band<FWD, ZERO, 0>(G);
 }
@@ -971,11 +969,11 @@ __global__ void __launch_bounds__(32 * gs::kWarpsPair, 1)
     // sweep A: with the zero guess P = b - border x_alpha from TMA boxes (mapPA, mapQA);
     // otherwise built from x (mapXA), the old-value half (mapUB), b and border
     GsBand G{nx, ny, ngrid, pad_nodes, bands, (int)blockIdx.x, &mapSA, &mapPA, ZERO_A ? &mapQA : &mapQB, &mapBB,
-             &mapXA, &mapUB, x1, x, flags, xfer, flags + 2 * groups, epoch, b, border, half_old, x};
+             &mapXA, &mapUB, x1, x, xfer, flags + 2 * groups, epoch, b, border, half_old, x};
     gs_band<FWD, ZERO_A, 1>(G);
   } else {
     GsBand G{nx, ny, ngrid, pad_nodes, bands, (int)blockIdx.x - nA, &mapSB, &mapSB, &mapQB, &mapBB, &mapXB, &mapUB, x, x,
-             flags + groups, xfer + 2 * (size_t)groups * nx, flags + 2 * groups, epoch, b, border, half_old, x1};
+             xfer + 2 * (size_t)groups * nx, flags + 2 * groups, epoch, b, border, half_old, x1};
     gs_band<FWD, false, 2>(G);
   }
 }
@@ -1410,7 +1408,7 @@ static int launch_tri(Ctx* c, LevelBuf& L, const CUtensorMap& mS, const CUtensor
   Ctx::ProfEv* pe = nullptr;
   if (int rc = prof_begin(c, L, 0, &pe)) return rc;
   VTS_CUDA(cudaLaunchKernelEx(&cfg, k_gs_tri<FWD, ZERO>, L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, bands, mS, mP,
-                              mQ, x, L.gs_flags, L.gs_xfer, skip));
+                              mQ, x, L.gs_xfer, skip));
   VTS_LAUNCHED(c);
   if (pe) VTS_CUDA(cudaEventRecord(pe->b, c->stream));
   return 0;

@@ -190,12 +190,6 @@ __global__ void k_resnorm(int len, const double* __restrict__ b, const double* _
   if (last_block_reduce<1>(acc, scratch, partials, counter, tot) && threadIdx.x == 0) *out = tot[0];
 }
 
-static int read_state(Ctx* c) {
-  VTS_CUDA(cudaMemcpyAsync(c->hmst, c->mst, sizeof(MinresDev), cudaMemcpyDeviceToHost, c->stream));
-  VTS_CUDA(cudaStreamSynchronize(c->stream));
-  return 0;
-}
-
 int minres(Ctx* c, const double* b_free, double* x_free, double tol, int max_iters, double floor_tol,
            int precondition, int* iters_out, double* relres_out, int* conv_out, double* history) {
   (void)floor_tol;  // only used with a warm start, which this entry point does not take
