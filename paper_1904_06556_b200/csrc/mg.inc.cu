@@ -304,6 +304,8 @@ __global__ void k_restrict(int fnx, int fny, const uint8_t* __restrict__ ffm, co
 
 // xf += P xc (multigrid.py:134-136): parents in increasing coarse index
 // fine node fi of xf + P xc
+// (CG: coarse values through L2 only -- k_prolong_rows reads them while they are written)
+template <bool CG = false>
 VTS_DEVICE_INLINE double2 prolong_node(int fnx, const uint8_t* __restrict__ ffm, const double* xf, int cnx,
                                        const uint8_t* __restrict__ cfm, const double* xc, int fi) {
   const int fx = fi % fnx, fy = fi / fnx;
@@ -317,7 +319,7 @@ VTS_DEVICE_INLINE double2 prolong_node(int fnx, const uint8_t* __restrict__ ffm,
       const double wv = pweight(fx, fy, qx, qy);
       const int cn = qx + cnx * qy;
       const uchar2 fc = *reinterpret_cast<const uchar2*>(cfm + 2 * cn);
-      const double2 v = *reinterpret_cast<const double2*>(xc + 2 * cn);
+      const double2 v = CG ? __ldcg(reinterpret_cast<const double2*>(xc + 2 * cn)) : *reinterpret_cast<const double2*>(xc + 2 * cn);
       if (fc.x) s0 += wv * v.x;
       if (fc.y) s1 += wv * v.y;
     }
@@ -341,6 +343,45 @@ __global__ void k_prolong_add(int fnx, int fny, const uint8_t* __restrict__ ffm,
     return;
   }
   *reinterpret_cast<double2*>(xf + 2 * fi) = prolong_node(fnx, ffm, xf, cnx, cfm, xc, fi);
+}
+
+// Ascent overlap (VTS_NO_OVERLAP=1 turns it off): xf += P xc for one fine row band
+// per block, in the backward sweep's band order, each band as soon as the coarser
+// level's ascent pair has finished the coarse bands it reads (cdone >= ctag), then
+// ready[band] = tag for the finer level's pair, which is already resident and
+// waits on it.  Launched with PDL behind the coarser pair and never waits for it
+// as a grid.  Same arithmetic per node as k_prolong_add.
+__global__ void __launch_bounds__(512) k_prolong_rows(int fnx, int fny, const uint8_t* __restrict__ ffm, double* xf,
+                                                      int cnx, int cny, const uint8_t* __restrict__ cfm, const double* xc,
+                                                      const unsigned long long* cdone, unsigned long long ctag,
+                                                      const unsigned long long* cready, unsigned long long cready_tag,
+                                                      unsigned long long* ready, unsigned long long tag, const int* skip) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (skip && ld_relaxed_i32(skip)) return;
+  constexpr int R = 16;  // gs::R (row band height of the sweeps)
+  const int fb = blockIdx.x;
+  const int yhi = fny - 1 - fb * R, ylo = max(0, yhi - R + 1);
+  if (threadIdx.x == 0) {
+    // coarse rows ylo/2 .. (yhi+1)/2, in the coarse backward bands (cny-1-row)/R
+    const int cb_first = (cny - 1 - (yhi + 1) / 2) / R, cb_last = (cny - 1 - ylo / 2) / R;
+    for (int cb = cb_first; cb <= cb_last; ++cb)
+      while (ld_acquire(cdone + cb) < ctag) {
+      }
+    // the coarse x_alpha, added by the coarser prolongation's band-0 block
+    if (fb == 0 && cready)
+      while (ld_acquire(cready) < cready_tag) {
+      }
+  }
+  __syncthreads();
+  const int n0 = ylo * fnx, n1 = (yhi + 1) * fnx;
+  for (int fi = n0 + (int)threadIdx.x; fi < n1; fi += blockDim.x)
+    *reinterpret_cast<double2*>(xf + 2 * fi) = prolong_node<true>(fnx, ffm, xf, cnx, cfm, xc, fi);
+  if (fb == 0 && threadIdx.x == 0) xf[2 * fnx * fny] += __ldcg(xc + 2 * cnx * cny);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    st_release(ready + fb, tag);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -567,6 +608,7 @@ struct Smem {
   unsigned long long xloaded[NSB];   // sweep B: a builder slot's x_A box has landed
   unsigned long long bempty[NSB];    // sweep B: the builders are done with a builder slot
   unsigned stored_cnt;                // sweep A: windows x {storer, publisher} whose stores are issued
+  unsigned done_cnt;                  // sweep B (ascent overlap): storer and publisher finished the band
   unsigned long long full_above[NSA], empty_above[NSA];
   int armed;  // (producer side) highest above-ring chunk the consumer has armed
 };
@@ -617,6 +659,9 @@ struct GsBand {
   double* x;                // the sweep's result
   const double* xa_src;     // bordered vector holding x_alpha (slot ngrid)
   double* xfer;                // cross-cluster handoff rows of this sweep, [bands][nx] nodes
+  unsigned long long* bdone;   // ascent overlap, sweep B: band finished (epoch-tagged), or null
+  const unsigned long long* ready;  // ascent overlap, sweep A: band's x_old prolongated (tagged), or null
+  unsigned long long ready_tag;
   unsigned long long* stored;  // sweep A's stored-window counters (pair only)
   unsigned long long epoch;    // pair launch tag of the stored counters
   const double* b;             // ROLE 2 builders: right-hand side, border, old-value half-stencil,
@@ -675,6 +720,7 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
     }
     S.armed = NSA - 1;  // the consumer arms above slots 0 .. NSA-1 before the first cluster barrier
     S.stored_cnt = 0;
+    S.done_cnt = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (dsm_in) {
       for (int a = 0; a < NSA && a <= nwin; ++a) mbar_expect_tx(&S.full_above[a], above_bytes(a));
@@ -787,6 +833,20 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
         mbar_arrive(&S.empty_out[s]);
       }
     }
+    if (ROLE == 2 && G.bdone) {
+      // the band's rows are final: the second of the two warps to get here
+      // publishes it (the finer level's prolongation waits on it)
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) {
+        unsigned prev;
+        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(prev) : "r"(smem_u32(&S.done_cnt)) : "memory");
+        if (prev == 1u) {
+          __threadfence();
+          st_release(G.bdone + band, G.epoch);
+        }
+      }
+    }
   } else if (warp == 4) {  // ---------------- stager (previous band's last row -> above ring)
     if (has_above && rows_here > 0 && !dsm_in) {
       double* row = G.xfer + 2 * (size_t)(band - 1) * nx;  // the previous band's last row
@@ -837,6 +897,18 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
     if (lane == 0) {
       const unsigned long long tag = G.epoch << 32;
       const int iy0 = band * R, iyb = ny - 1 - band * R;
+      if (!kGated && G.ready) {
+        // ascent overlap: x_old of this band and of the next band's first row is
+        // prolongated by k_prolong_rows while the coarser level still sweeps
+        // (band - 1: the box's skewed rows wrap into its last row, read times exact zeros)
+        for (int b2 = max(band - 1, 0); b2 <= band; ++b2)
+          while (ld_acquire(G.ready + b2) < G.ready_tag) {
+          }
+        if (band + 1 < bands)
+          while (ld_acquire(G.ready + band + 1) < G.ready_tag) {
+          }
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores -> this warp's TMA reads
+      }
       for (int w = 0; w < nwin; ++w) {
         const int sb = w % NSB;
         if (w >= NSB) mbar_wait(&S.bempty[sb], ((w / NSB) - 1) & 1);
@@ -882,7 +954,14 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
     constexpr int kItems = (R * W + 32 * kBuild - 1) / (32 * kBuild);  // box nodes per builder thread
     static_assert(kItems <= 2, "builder registers sized for two nodes per thread");
     const int nnodes = nx * ny;
-    const double xa = G.xa_src[ngrid];
+    if (G.ready) {
+      // ascent overlap: x_alpha is added by the prolongation's band-0 block
+      if (lane == 0)
+        while (ld_acquire(G.ready) < G.ready_tag) {
+        }
+      __syncwarp();
+    }
+    const double xa = G.ready ? __ldcg(G.xa_src + ngrid) : G.xa_src[ngrid];
     const int iy0 = band * R, iyb = ny - 1 - band * R;
     auto build = [&](int w) {
       const int s = w % NS, sb = w % NSB;
@@ -943,7 +1022,7 @@ __global__ void __launch_bounds__(32 * gs::kWarps, 1)
   pdl_enter();
   if (skip && *skip) return;
   GsBand G{nx, ny, ngrid, pad_nodes, bands, (int)blockIdx.x, &mapS, &mapP, &mapQ, &mapQ, &mapQ, &mapQ, x, x,
-           xfer, nullptr, 0ull, nullptr, nullptr, nullptr, nullptr};
+           xfer, nullptr, nullptr, 0ull, nullptr, 0ull, nullptr, nullptr, nullptr, nullptr};
   gs_band<FWD, ZERO, 0>(G);
 }
 
@@ -961,19 +1040,30 @@ __global__ void __launch_bounds__(32 * gs::kWarpsPair, 1)
               double* __restrict__ x1, double* __restrict__ x,
               unsigned long long* flags, double* xfer, int groups, unsigned long long epoch,
               const double* __restrict__ b,
-              const double* __restrict__ border, const double* __restrict__ half_old, const int* skip) {
-  pdl_enter();
-  if (skip && *skip) return;
+              const double* __restrict__ border, const double* __restrict__ half_old,
+              const unsigned long long* ready, unsigned long long ready_tag, int mode, const int* skip) {
+  // mode bit 0 (ascent overlap): this launch runs beside the coarser level's pair and
+  // the prolongation (k_prolong_rows), ordered by the ready flags only, so it must
+  // not wait for the previous grid; bit 1: publish sweep B's band-done flags
+  if (mode & 1) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (skip && ld_relaxed_i32(skip)) return;
+  } else {
+    pdl_enter();
+    if (skip && *skip) return;
+    ready = nullptr;
+  }
   const int nA = (int)gridDim.x / 2;
   if ((int)blockIdx.x < nA) {
     // sweep A: with the zero guess P = b - border x_alpha from TMA boxes (mapPA, mapQA);
     // otherwise built from x (mapXA), the old-value half (mapUB), b and border
     GsBand G{nx, ny, ngrid, pad_nodes, bands, (int)blockIdx.x, &mapSA, &mapPA, ZERO_A ? &mapQA : &mapQB, &mapBB,
-             &mapXA, &mapUB, x1, x, xfer, flags + 2 * groups, epoch, b, border, half_old, x};
+             &mapXA, &mapUB, x1, x, xfer, nullptr, ready, ready_tag, flags + 2 * groups, epoch, b, border, half_old, x};
     gs_band<FWD, ZERO_A, 1>(G);
   } else {
     GsBand G{nx, ny, ngrid, pad_nodes, bands, (int)blockIdx.x - nA, &mapSB, &mapSB, &mapQB, &mapBB, &mapXB, &mapUB, x, x,
-             xfer + 2 * (size_t)groups * nx, flags + 2 * groups, epoch, b, border, half_old, x1};
+             xfer + 2 * (size_t)groups * nx, (mode & 2) ? flags : nullptr, ready, ready_tag, flags + 2 * groups, epoch, b,
+             border, half_old, x1};
     gs_band<FWD, false, 2>(G);
   }
 }
@@ -1443,14 +1533,59 @@ static int gs_sweep(Ctx* c, int k, const double* b, double* x, bool forward, boo
 // Forward pair: A may start from the zero guess (the V-cycle's first pre-smoothing
 // sweep).  Returns 1 (nothing launched) when the 2 x clusters of the grid cannot
 // all be resident at once -- sweep B spins on sweep A, so co-residency is required.
-static int gs_pair(Ctx* c, int k, const double* b, double* x, bool forward, bool zero_a, const int* skip,
-                   bool* launched) {
-  *launched = false;
-  if (int rc = gs_prepare()) return rc;
+// the largest clusters (fewest cross-cluster handoffs) with which both halves of
+// level k's grid can be resident at once, or cs = 0 (none: two single sweeps)
+static int pair_shape(Ctx* c, int k, bool forward, bool zero_a, int* cs_out, int* ncl_out) {
   LevelBuf& L = c->lv[k];
   const int bands = div_up(L.d.ny, gs::R);
   const void* fn = forward ? (zero_a ? (const void*)k_gs_pair<true, true> : (const void*)k_gs_pair<true, false>)
                            : (const void*)k_gs_pair<false, false>;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(32 * gs::kWarpsPair);
+  cfg.dynamicSmemBytes = sizeof(gs::Smem);
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  static int max_clusters[3][17] = {};
+  const int kind = forward ? (zero_a ? 0 : 1) : 2;
+  *cs_out = *ncl_out = 0;
+  for (int n = div_up(bands, 16); n <= bands; ++n) {
+    const int size = div_up(bands, n);
+    if (div_up(bands, size) != n) continue;  // same cluster size as a smaller n
+    if (max_clusters[kind][size] == 0) {
+      at[0].val.clusterDim.x = size;
+      cfg.gridDim = dim3(2 * size * n);
+      int m = 0;
+      VTS_CUDA(cudaOccupancyMaxActiveClusters(&m, fn, &cfg));
+      max_clusters[kind][size] = m > 0 ? m : -1;
+    }
+    if (max_clusters[kind][size] >= 2 * n) {
+      *cs_out = size;
+      *ncl_out = n;
+      return 0;
+    }
+  }
+  return 0;
+}
+
+// Two consecutive sweeps of level k as one pipelined launch (k_gs_pair): x <- B(A(x)).
+// Forward pair: A may start from the zero guess (the V-cycle's first pre-smoothing
+// sweep).  Sets *launched = false (nothing launched) when the 2 x clusters of the grid
+// cannot all be resident at once -- sweep B spins on sweep A, so co-residency is required.
+// mode / ready / ready_tag: the ascent overlap (k_gs_pair's mode bits).
+static int gs_pair(Ctx* c, int k, const double* b, double* x, bool forward, bool zero_a, const int* skip,
+                   bool* launched, int mode = 0, const unsigned long long* ready = nullptr,
+                   unsigned long long ready_tag = 0) {
+  *launched = false;
+  if (int rc = gs_prepare()) return rc;
+  LevelBuf& L = c->lv[k];
+  const int bands = div_up(L.d.ny, gs::R);
+  int cs = 0, ncl = 0;
+  if (int rc = pair_shape(c, k, forward, zero_a, &cs, &ncl)) return rc;
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(32 * gs::kWarpsPair);
   cfg.dynamicSmemBytes = sizeof(gs::Smem);
@@ -1460,27 +1595,6 @@ static int gs_pair(Ctx* c, int k, const double* b, double* x, bool forward, bool
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;  // the occupancy query below sees the cluster shape only
-  // the largest clusters (fewest cross-cluster handoffs) with which both halves of
-  // the grid can be resident at once; none -> two single sweeps
-  static int max_clusters[17] = {0};
-  int cs = 0, ncl = 0;
-  for (int n = div_up(bands, 16); n <= bands; ++n) {
-    const int size = div_up(bands, n);
-    if (div_up(bands, size) != n) continue;  // same cluster size as a smaller n
-    if (max_clusters[size] == 0) {
-      at[0].val.clusterDim.x = size;
-      cfg.gridDim = dim3(2 * size * n);
-      int m = 0;
-      VTS_CUDA(cudaOccupancyMaxActiveClusters(&m, fn, &cfg));
-      max_clusters[size] = m > 0 ? m : -1;
-    }
-    if (max_clusters[size] >= 2 * n) {
-      cs = size;
-      ncl = n;
-      break;
-    }
-  }
   if (cs == 0) return 0;  // not all resident: caller runs two sweeps
   at[0].val.clusterDim.x = cs;
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1505,15 +1619,15 @@ static int gs_pair(Ctx* c, int k, const double* b, double* x, bool forward, bool
   if (forward && zero_a)
     VTS_CUDA(cudaLaunchKernelEx(&cfg, k_gs_pair<true, true>, L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, bands, mSA,
                                 mPA, mQA, mSB, mBB, mQB, mXB, mUB, mXA, L.x1, x, L.gs_flags, L.gs_xfer, L.gs_groups, epoch, b,
-                                (const double*)L.d.border, old_half, skip));
+                                (const double*)L.d.border, old_half, ready, ready_tag, mode, skip));
   else if (forward)
     VTS_CUDA(cudaLaunchKernelEx(&cfg, k_gs_pair<true, false>, L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, bands, mSA,
                                 mPA, mQA, mSB, mBB, mQB, mXB, mUB, mXA, L.x1, x, L.gs_flags, L.gs_xfer, L.gs_groups, epoch, b,
-                                (const double*)L.d.border, old_half, skip));
+                                (const double*)L.d.border, old_half, ready, ready_tag, mode, skip));
   else
     VTS_CUDA(cudaLaunchKernelEx(&cfg, k_gs_pair<false, false>, L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, bands,
                                 mSA, mPA, mQA, mSB, mBB, mQB, mXB, mUB, mXA, L.x1, x, L.gs_flags, L.gs_xfer, L.gs_groups, epoch, b,
-                                (const double*)L.d.border, old_half, skip));
+                                (const double*)L.d.border, old_half, ready, ready_tag, mode, skip));
   VTS_LAUNCHED(c);
   if (pe) VTS_CUDA(cudaEventRecord(pe->b, c->stream));
   *launched = true;
@@ -1524,6 +1638,15 @@ static int gs_pair(Ctx* c, int k, const double* b, double* x, bool forward, bool
 static bool pair_enabled() {
   static const bool on = [] {
     const char* e = getenv("VTS_NO_PAIR");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
+// VTS_NO_OVERLAP=1 runs the ascent level by level (A/B checks)
+static bool overlap_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("VTS_NO_OVERLAP");
     return !(e && e[0] == '1');
   }();
   return on;
@@ -1581,16 +1704,63 @@ int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
                                                                     C.d.free2grid, b0, x0, skip));
     VTS_LAUNCHED(c);
   }
-  // ascent
+  // ascent; with the overlap, level k's prolongation (k_prolong_rows) and pair start
+  // while level k-1's pair still sweeps, gated band by band on flags
+  auto pairs = [&](int k) {
+    int cs = 0, ncl = 0;
+    pair_shape(c, k, false, false, &cs, &ncl);
+    return cs > 0;
+  };
+  const bool ovl = overlap_enabled() && pdl_enabled() && pair_enabled() && !c->prof;
+  bool prev_pub = false, prev_ovl = false;
   for (int k = lo; k <= top; ++k) {
     LevelBuf& L = c->lv[k];
     LevelBuf& C = c->lv[k - 1];
     const double* b = (k == top) ? b_top : L.b;
     double* x = (k == top) ? z_top : L.x;
-    VTS_CUDA(launch_pdl(k_prolong_add, dim3(div_up(L.d.nnodes + 1, 256)), dim3(256), 0, c->stream, L.d.nx, L.d.ny, L.d.free_mask, x, C.d.nx,
-                                                                        C.d.ny, C.d.free_mask, C.x, skip));
-    VTS_LAUNCHED(c);
-    if (int rc = gs_two_sweeps(c, k, b, x, false, false, skip)) return rc;
+    const bool pub = ovl && k < top && pairs(k) && pairs(k + 1);  // level k+1 overlaps this pair
+    const int mode = pub ? 2 : 0;
+    if (prev_pub) {
+      const unsigned long long tag = ++L.ready_epoch;
+      unsigned long long* ready = L.gs_flags + 3 * L.gs_groups;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(div_up(L.d.ny, gs::R));
+      cfg.blockDim = dim3(512);
+      cfg.stream = c->stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      VTS_CUDA(cudaLaunchKernelEx(&cfg, k_prolong_rows, L.d.nx, L.d.ny, (const uint8_t*)L.d.free_mask, x, C.d.nx, C.d.ny,
+                                  (const uint8_t*)C.d.free_mask, (const double*)C.x,
+                                  (const unsigned long long*)C.gs_flags, C.pair_epoch,
+                                  prev_ovl ? (const unsigned long long*)(C.gs_flags + 3 * C.gs_groups) : nullptr,
+                                  C.ready_epoch, ready, tag, skip));
+      VTS_LAUNCHED(c);
+      bool launched = false;
+      if (int rc = gs_pair(c, k, b, x, false, false, skip, &launched, 1 | mode, ready, tag)) return rc;
+      if (!launched) {
+        set_error(5, "vcycle: overlapped ascent pair did not launch");
+        return 5;
+      }
+    } else {
+      VTS_CUDA(launch_pdl(k_prolong_add, dim3(div_up(L.d.nnodes + 1, 256)), dim3(256), 0, c->stream, L.d.nx, L.d.ny, L.d.free_mask, x, C.d.nx,
+                                                                          C.d.ny, C.d.free_mask, C.x, skip));
+      VTS_LAUNCHED(c);
+      if (pub) {
+        bool launched = false;
+        if (int rc = gs_pair(c, k, b, x, false, false, skip, &launched, mode)) return rc;
+        if (!launched) {
+          set_error(5, "vcycle: ascent pair did not launch");
+          return 5;
+        }
+      } else if (int rc = gs_two_sweeps(c, k, b, x, false, false, skip)) {
+        return rc;
+      }
+    }
+    prev_ovl = prev_pub;
+    prev_pub = pub;
     if (k == top) {
       const int grid = (int)std::min<long long>(div_up(L.d.ngrid, 256), kReduceGridCap);
       VTS_CUDA(launch_pdl(k_alpha_relax, dim3(grid), dim3(256), 0, c->stream, L.d.ngrid, L.d.border, b, x, c->d_corner, c->partials,

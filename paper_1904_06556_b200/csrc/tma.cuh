@@ -14,6 +14,11 @@ VTS_DEVICE_INLINE unsigned long long ld_acquire(const unsigned long long* p) {
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+VTS_DEVICE_INLINE int ld_relaxed_i32(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 // cross-cluster handoff rows: a value slot is empty while either half holds
 // this NaN pattern (arithmetic never produces it: the producer maps it to the
 // default quiet NaN), so every 8-byte half is its own ready flag
