@@ -313,8 +313,11 @@ VTS_DEVICE_INLINE double2 prolong_node(int fnx, const uint8_t* __restrict__ ffm,
   double s0 = 0.0, s1 = 0.0;
   int qxs[2], qys[2];
   const int nqx = parents(fx, qxs), nqy = parents(fy, qys);
-  for (int iqy = 0; iqy < nqy; ++iqy) {
-    for (int iqx = 0; iqx < nqx; ++iqx) {
+#pragma unroll
+  for (int iqy = 0; iqy < 2; ++iqy) {
+#pragma unroll
+    for (int iqx = 0; iqx < 2; ++iqx) {
+      if (iqy >= nqy || iqx >= nqx) continue;  // (fixed trip counts: the loads issue together)
       const int qx = qxs[iqx], qy = qys[iqy];
       const double wv = pweight(fx, fy, qx, qy);
       const int cn = qx + cnx * qy;
@@ -350,8 +353,9 @@ __global__ void k_prolong_add(int fnx, int fny, const uint8_t* __restrict__ ffm,
 // level's ascent pair has finished the coarse bands it reads (cdone >= ctag), then
 // ready[band] = tag for the finer level's pair, which is already resident and
 // waits on it.  Launched with PDL behind the coarser pair and never waits for it
-// as a grid.  Same arithmetic per node as k_prolong_add.
-__global__ void __launch_bounds__(512) k_prolong_rows(int fnx, int fny, const uint8_t* __restrict__ ffm, double* xf,
+// as a grid.  Same arithmetic per node as k_prolong_add.  A few blocks take the
+// bands round robin: every block holds an SM the pair of this level may need.
+__global__ void __launch_bounds__(1024) k_prolong_rows(int fnx, int fny, const uint8_t* __restrict__ ffm, double* xf,
                                                       int cnx, int cny, const uint8_t* __restrict__ cfm, const double* xc,
                                                       const unsigned long long* cdone, unsigned long long ctag,
                                                       const unsigned long long* cready, unsigned long long cready_tag,
@@ -359,28 +363,43 @@ __global__ void __launch_bounds__(512) k_prolong_rows(int fnx, int fny, const ui
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (skip && ld_relaxed_i32(skip)) return;
   constexpr int R = 16;  // gs::R (row band height of the sweeps)
-  const int fb = blockIdx.x;
-  const int yhi = fny - 1 - fb * R, ylo = max(0, yhi - R + 1);
-  if (threadIdx.x == 0) {
-    // coarse rows ylo/2 .. (yhi+1)/2, in the coarse backward bands (cny-1-row)/R
-    const int cb_first = (cny - 1 - (yhi + 1) / 2) / R, cb_last = (cny - 1 - ylo / 2) / R;
-    for (int cb = cb_first; cb <= cb_last; ++cb)
-      while (ld_acquire(cdone + cb) < ctag) {
+  const int fbands = (fny + R - 1) / R;
+  for (int fb = blockIdx.x; fb < fbands; fb += gridDim.x) {
+    const int yhi = fny - 1 - fb * R, ylo = max(0, yhi - R + 1);
+    if (threadIdx.x == 0) {
+      // coarse rows ylo/2 .. (yhi+1)/2, in the coarse backward bands (cny-1-row)/R
+      const int cb_first = (cny - 1 - (yhi + 1) / 2) / R, cb_last = (cny - 1 - ylo / 2) / R;
+      for (int cb = cb_first; cb <= cb_last; ++cb)
+        while (ld_acquire(cdone + cb) < ctag) {
+        }
+      // the coarse x_alpha, added by the coarser prolongation's band-0 block
+      if (fb == 0 && cready)
+        while (ld_acquire(cready) < cready_tag) {
+        }
+    }
+    __syncthreads();
+    // latency-bound (L2 loads of x_c): kU nodes per thread in flight
+    constexpr int kU = 4;
+    const int n0 = ylo * fnx, n1 = (yhi + 1) * fnx;
+    for (int base = n0 + (int)threadIdx.x; base < n1; base += kU * blockDim.x) {
+      double2 o[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int fi = base + u * blockDim.x;
+        if (fi < n1) o[u] = prolong_node<true>(fnx, ffm, xf, cnx, cfm, xc, fi);
       }
-    // the coarse x_alpha, added by the coarser prolongation's band-0 block
-    if (fb == 0 && cready)
-      while (ld_acquire(cready) < cready_tag) {
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int fi = base + u * blockDim.x;
+        if (fi < n1) *reinterpret_cast<double2*>(xf + 2 * fi) = o[u];
       }
-  }
-  __syncthreads();
-  const int n0 = ylo * fnx, n1 = (yhi + 1) * fnx;
-  for (int fi = n0 + (int)threadIdx.x; fi < n1; fi += blockDim.x)
-    *reinterpret_cast<double2*>(xf + 2 * fi) = prolong_node<true>(fnx, ffm, xf, cnx, cfm, xc, fi);
-  if (fb == 0 && threadIdx.x == 0) xf[2 * fnx * fny] += __ldcg(xc + 2 * cnx * cny);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    st_release(ready + fb, tag);
+    }
+    if (fb == 0 && threadIdx.x == 0) xf[2 * fnx * fny] += __ldcg(xc + 2 * cnx * cny);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      st_release(ready + fb, tag);
+    }
   }
 }
 
@@ -1652,6 +1671,15 @@ static bool overlap_enabled() {
   return on;
 }
 
+// blocks of k_prolong_rows (VTS_OVL_WORKERS, A/B timing)
+static int ovl_workers() {
+  static const int n = [] {
+    const char* e = getenv("VTS_OVL_WORKERS");
+    return e ? std::max(1, atoi(e)) : 8;
+  }();
+  return n;
+}
+
 // the two sweeps of a smoothing step: pipelined when possible
 static int gs_two_sweeps(Ctx* c, int k, const double* b, double* x, bool forward, bool zero_first, const int* skip) {
   if (pair_enabled()) {
@@ -1724,8 +1752,8 @@ int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
       const unsigned long long tag = ++L.ready_epoch;
       unsigned long long* ready = L.gs_flags + 3 * L.gs_groups;
       cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(div_up(L.d.ny, gs::R));
-      cfg.blockDim = dim3(512);
+      cfg.gridDim = dim3(std::min(div_up(L.d.ny, gs::R), ovl_workers()));
+      cfg.blockDim = dim3(1024);
       cfg.stream = c->stream;
       cudaLaunchAttribute at[1];
       at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
