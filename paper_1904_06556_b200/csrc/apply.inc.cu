@@ -277,7 +277,8 @@ __global__ void __launch_bounds__(kBX* kBY, VTS_APPLY_MINB) k_newton_apply(const
 // r = b - (A x + border x_alpha) instead.  Border dot partials for y_alpha.
 // Row sums follow the CSR column order SW S SE W C E NW N NE (linalg.py:58).
 // one node of A_k x + border x_alpha (or b - that); also its border.x term
-template <bool RESIDUAL>
+// (CG: x and b through L2 only -- k_residual_restrict_rows reads them while they are written)
+template <bool RESIDUAL, bool CG = false>
 VTS_DEVICE_INLINE double2 level_apply_node(int nx, int ny, const double* __restrict__ stL,
                                            const double* __restrict__ stU, const double* border, const double* x,
                                            const double* b, double xa, int nd, double& acc) {
@@ -290,7 +291,7 @@ VTS_DEVICE_INLINE double2 level_apply_node(int nx, int ny, const double* __restr
     const int dx = blk % 3 - 1, dy = blk / 3 - 1;
     const int jx = ix + dx, jy = iy + dy;
     double2 xv = make_double2(0.0, 0.0);
-    if (jx >= 0 && jx < nx && jy >= 0 && jy < ny) xv = *reinterpret_cast<const double2*>(x + 2 * (jx + nx * jy));
+    if (jx >= 0 && jx < nx && jy >= 0 && jy < ny) xv = ld2<CG>(x + 2 * (jx + nx * jy));
     double2 c01, c23;
     if (blk == kBlockCenter) {
       c01 = make_double2(l[kHDiag], u[kHC]);
@@ -308,11 +309,11 @@ VTS_DEVICE_INLINE double2 level_apply_node(int nx, int ny, const double* __restr
   const double2 bd = *reinterpret_cast<const double2*>(border + 2 * nd);
   s0 = fma(bd.x, xa, s0);
   s1 = fma(bd.y, xa, s1);
-  const double2 xv = *reinterpret_cast<const double2*>(x + 2 * nd);
+  const double2 xv = ld2<CG>(x + 2 * nd);
   acc = fma(bd.x, xv.x, acc);
   acc = fma(bd.y, xv.y, acc);
   if (RESIDUAL) {
-    const double2 bv = *reinterpret_cast<const double2*>(b + 2 * nd);
+    const double2 bv = ld2<CG>(b + 2 * nd);
     s0 = bv.x - s0;
     s1 = bv.y - s1;
   }

@@ -23,13 +23,18 @@ struct LevelBuf {
   double* x = nullptr;           // [ngrid + 1] V-cycle iterate
   double* r = nullptr;           // [ngrid + 1] residual / scratch
   // GS wavefront progress flags, 4 x gs_groups, all tagged and never reset:
-  // [0, G) sweep B's band done (pair epoch, ascent overlap), [G, 2G) unused,
+  // [0, G) sweep B's band done (pair epoch, overlap), [G, 2G) unused,
   // [2G, 3G) sweep A's stored windows, [3G, 4G) x_old of the band prolongated
   // (k_prolong_rows, ready_epoch)
   unsigned long long* gs_flags = nullptr;
   int gs_groups = 0;
   unsigned long long pair_epoch = 0;   // launches of the pipelined sweep pair on this level
   unsigned long long ready_epoch = 0;  // launches of k_prolong_rows into this level
+  // descent overlap, [gs_groups x kSeg] (row band x column segment), tagged:
+  unsigned long long* ovl_bready = nullptr;  // b restricted into this level (bready_epoch)
+  unsigned long long* ovl_rdone = nullptr;   // residual of this level computed (rdone_epoch)
+  unsigned long long bready_epoch = 0;
+  unsigned long long rdone_epoch = 0;
   double* x1 = nullptr;               // [ngrid + 1] sweep A's result inside a pair
   // cross-cluster band handoff rows, 2 x gs_groups x nx nodes (sweep A / single
   // sweeps, sweep B): each value is its own ready flag (kXferEmpty until the

@@ -267,6 +267,7 @@ __global__ void k_symmetrize(int nx, int ny, const double* __restrict__ raw, con
 // vc = P^T vf on free dofs (csc_matvec order: fine dofs in increasing index);
 // with `bordered` the border slot is copied (multigrid.py:128-130)
 // one coarse node of P^T vf (free dofs only)
+template <bool CG = false>
 VTS_DEVICE_INLINE double2 restrict_node(int fnx, int fny, const uint8_t* __restrict__ ffm, const double* vf, int cnx,
                                         const uint8_t* __restrict__ cfm, int cn) {
   const int cx = cn % cnx, cy = cn / cnx;
@@ -279,7 +280,7 @@ VTS_DEVICE_INLINE double2 restrict_node(int fnx, int fny, const uint8_t* __restr
       const int fi = fx + fnx * fy;
       const double wv = pweight(fx, fy, cx, cy);
       const uchar2 ff = *reinterpret_cast<const uchar2*>(ffm + 2 * fi);
-      const double2 v = *reinterpret_cast<const double2*>(vf + 2 * fi);
+      const double2 v = ld2<CG>(vf + 2 * fi);
       if (ff.x) s0 += wv * v.x;
       if (ff.y) s1 += wv * v.y;
     }
@@ -401,6 +402,122 @@ __global__ void __launch_bounds__(1024) k_prolong_rows(int fnx, int fny, const u
       st_release(ready + fb, tag);
     }
   }
+}
+
+// Descent overlap: level k's residual r = b - A x and its restriction into the
+// coarser level's b, band by band behind level k's descent pair (forward sweep
+// order), in kSeg column segments per band:
+//   R(fb, s): r on fine band fb once the pair's sweep B finished bands fb-1..fb+1
+//             (and, below the top, b on the band is restricted) -> rdone[fb][s]
+//   P(cb, s): the coarse band's rows of b_c = R r once r on the fine bands
+//             2cb-1 .. 2cb+1 is done -> cready[cb][s]; the coarser pair waits on it
+// Items run in dependency order, round robin over the blocks.  x_alpha's part of
+// the residual is a reduction over the whole level: k_alpha_residual, after the
+// overlapped levels.  Same arithmetic per node as k_level_apply<true> / k_restrict.
+constexpr int kSeg = 8;
+VTS_DEVICE_INLINE void seg_cols(int n, int s, int& c0, int& c1) {
+  c0 = (int)((long long)n * s / kSeg);
+  c1 = (int)((long long)n * (s + 1) / kSeg);
+}
+__global__ void __launch_bounds__(1024) k_residual_restrict_rows(
+    int nx, int ny, const double* __restrict__ stL, const double* __restrict__ stU, const double* __restrict__ border,
+    const uint8_t* __restrict__ ffm, const double* x, const double* b, double* r, int cnx, int cny,
+    const uint8_t* __restrict__ cfm, double* bc, const unsigned long long* bdone, unsigned long long btag,
+    const unsigned long long* bready, unsigned long long bready_tag, unsigned long long* rdone, unsigned long long rtag,
+    unsigned long long* cready, unsigned long long ctag, int ngrid, const int* skip) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (skip && ld_relaxed_i32(skip)) return;
+  constexpr int R = 16;
+  const int fbands = (ny + R - 1) / R, cbands = (cny + R - 1) / R;
+  const int items = cbands * 3 * kSeg;
+  const double xa = __ldcg(x + ngrid);
+  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+    const int cb = it / (3 * kSeg), j = (it / kSeg) % 3, s = it % kSeg;
+    if (j < 2) {
+      const int fb = 2 * cb + j;
+      if (fb >= fbands) continue;
+      if (threadIdx.x == 0) {
+        for (int bb = max(fb - 1, 0); bb <= min(fb + 1, fbands - 1); ++bb)
+          while (ld_acquire(bdone + bb) < btag) {
+          }
+        if (bready)
+          while (ld_acquire(bready + (size_t)fb * kSeg + s) < bready_tag) {
+          }
+      }
+      __syncthreads();
+      int c0, c1;
+      seg_cols(nx, s, c0, c1);
+      const int w = c1 - c0, y0 = fb * R, nr = min(R, ny - y0);
+      double acc = 0.0;
+      for (int i = threadIdx.x; i < w * nr; i += blockDim.x) {
+        const int nd = (y0 + i / w) * nx + c0 + i % w;
+        *reinterpret_cast<double2*>(r + 2 * nd) = level_apply_node<true, true>(nx, ny, stL, stU, border, x, b, xa, nd, acc);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        st_release(rdone + (size_t)fb * kSeg + s, rtag);
+      }
+    } else {
+      if (threadIdx.x == 0) {
+        for (int fb = max(2 * cb - 1, 0); fb <= min(2 * cb + 1, fbands - 1); ++fb)
+          for (int q = 0; q < kSeg; ++q)
+            while (ld_acquire(rdone + (size_t)fb * kSeg + q) < rtag) {
+            }
+      }
+      __syncthreads();
+      int c0, c1;
+      seg_cols(cnx, s, c0, c1);
+      const int w = c1 - c0, y0 = cb * R, nr = min(R, cny - y0);
+      for (int i = threadIdx.x; i < w * nr; i += blockDim.x) {
+        const int cn = (y0 + i / w) * cnx + c0 + i % w;
+        *reinterpret_cast<double2*>(bc + 2 * cn) = restrict_node<true>(nx, ny, ffm, r, cnx, cfm, cn);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        st_release(cready + (size_t)cb * kSeg + s, ctag);
+      }
+    }
+  }
+}
+
+// x_alpha's residual row of the overlapped descent levels, with k_level_apply<true>'s
+// reduction tree (same grid, same per-thread order): r_alpha = b_alpha - (border.x +
+// corner x_alpha), copied into the coarser b_alpha as k_restrict does
+__global__ void __launch_bounds__(256) k_alpha_residual(int nnodes, int ngrid, const double* __restrict__ border,
+                                                        const double* __restrict__ corner_ptr, const double* x,
+                                                        const double* b, double* r, double* bc_alpha,
+                                                        double* partials, unsigned* counter, const int* skip) {
+  pdl_enter();
+  if (skip && *skip) return;
+  __shared__ double scratch[256 / 32];
+  const double xa = __ldcg(x + ngrid);
+  double acc[1] = {0.0};
+  for (int nd = blockIdx.x * blockDim.x + threadIdx.x; nd < nnodes; nd += gridDim.x * blockDim.x) {
+    const double2 bd = *reinterpret_cast<const double2*>(border + 2 * nd);
+    const double2 xv = __ldcg(reinterpret_cast<const double2*>(x + 2 * nd));
+    acc[0] = fma(bd.x, xv.x, acc[0]);
+    acc[0] = fma(bd.y, xv.y, acc[0]);
+  }
+  double tot[1];
+  if (last_block_reduce<1>(acc, scratch, partials, counter, tot) && threadIdx.x == 0) {
+    const double ya = fma(*corner_ptr, xa, tot[0]);
+    const double ra = __ldcg(b + ngrid) - ya;
+    r[ngrid] = ra;
+    *bc_alpha = ra;
+  }
+}
+
+// coarse levels' x_alpha = 0 (k_alpha_init) for the whole descent at once
+struct AlphaSlots {
+  double* p[16];
+  int n;
+};
+__global__ void k_alpha_zero(AlphaSlots a, const int* skip) {
+  pdl_enter();
+  if (skip && *skip) return;
+  if ((int)threadIdx.x < a.n) *a.p[threadIdx.x] = 0.0;
 }
 
 // ---------------------------------------------------------------------------
@@ -679,8 +796,12 @@ struct GsBand {
   const double* xa_src;     // bordered vector holding x_alpha (slot ngrid)
   double* xfer;                // cross-cluster handoff rows of this sweep, [bands][nx] nodes
   unsigned long long* bdone;   // ascent overlap, sweep B: band finished (epoch-tagged), or null
-  const unsigned long long* ready;  // ascent overlap, sweep A: band's x_old prolongated (tagged), or null
+  // overlap gating, or null: ascent pairs wait for x_old of a band (k_prolong_rows),
+  // descent pairs for its right-hand side b (k_residual_restrict_rows); ready_seg
+  // flags per band, each >= ready_tag when done
+  const unsigned long long* ready;
   unsigned long long ready_tag;
+  int ready_seg;
   unsigned long long* stored;  // sweep A's stored-window counters (pair only)
   unsigned long long epoch;    // pair launch tag of the stored counters
   const double* b;             // ROLE 2 builders: right-hand side, border, old-value half-stencil,
@@ -755,6 +876,15 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
   }
   // every CTA's barriers exist (and its ring is zeroed) before any remote st.async lands
   asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+  // overlap gating: every segment flag of band bb done (bb < bands)
+  auto wait_ready = [&](int bb) {
+    for (int j = 0; j < G.ready_seg; ++j)
+      while (ld_acquire(G.ready + (size_t)bb * G.ready_seg + j) < G.ready_tag) {
+      }
+  };
+  // forward boxes of window w reach into the next band's first row (skewed
+  // positions past the last column) once W (w + 1) > nx
+  auto wraps_next = [&](int w) { return W * (w + 1) > nx; };
   // band row l -> grid row; box row of band row l; slot position of step st
   auto grid_row = [&](int l) {
     const int r = band * R + l;
@@ -768,9 +898,20 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
   } else if (warp == 1) {  // ---------------- loader (one thread, TMA boxes)
     if (lane == 0) {
       const int iy0 = band * R, iyb = ny - 1 - band * R;
+      const bool gate = ZERO && G.ready;  // descent overlap: b of the band is restricted
+      bool next_ok = !(gate && band + 1 < bands);
+      if (gate) {
+        wait_ready(band);
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
       for (int w = 0; w < nwin; ++w) {
         const int s = w % NS;
         if (w >= NS) mbar_wait(&S.empty_in[s], ((w / NS) - 1) & 1);
+        if (!next_ok && wraps_next(w)) {
+          wait_ready(band + 1);
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          next_ok = true;
+        }
         // node index of box element (p = 0, box row 0)
         const int node0 = FWD ? iy0 * nx + W * w : (iyb - R + 2) * nx - W * (w + 1) + SKEW * (R - 1);
         const int c1 = node0 + pad_nodes;
@@ -916,16 +1057,12 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
     if (lane == 0) {
       const unsigned long long tag = G.epoch << 32;
       const int iy0 = band * R, iyb = ny - 1 - band * R;
-      if (!kGated && G.ready) {
+      if (!kGated && !FWD && G.ready) {
         // ascent overlap: x_old of this band and of the next band's first row is
         // prolongated by k_prolong_rows while the coarser level still sweeps
         // (band - 1: the box's skewed rows wrap into its last row, read times exact zeros)
-        for (int b2 = max(band - 1, 0); b2 <= band; ++b2)
-          while (ld_acquire(G.ready + b2) < G.ready_tag) {
-          }
-        if (band + 1 < bands)
-          while (ld_acquire(G.ready + band + 1) < G.ready_tag) {
-          }
+        for (int b2 = max(band - 1, 0); b2 <= band; ++b2) wait_ready(b2);
+        if (band + 1 < bands) wait_ready(band + 1);
         asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores -> this warp's TMA reads
       }
       for (int w = 0; w < nwin; ++w) {
@@ -951,9 +1088,20 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
     // previous window -- ahead of the compute ring, which frees slots later
     if (lane == 0) {
       const int iy0 = band * R, iyb = ny - 1 - band * R;
+      const bool gate = FWD && G.ready;  // descent overlap: b of the band is restricted
+      bool next_ok = !(gate && band + 1 < bands);
+      if (gate) {
+        wait_ready(band);
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
       for (int w = 0; w < nwin; ++w) {
         const int sb = w % NSB;
         if (w >= NSB) mbar_wait(&S.bempty[sb], ((w / NSB) - 1) & 1);
+        if (!next_ok && wraps_next(w)) {
+          wait_ready(band + 1);
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          next_ok = true;
+        }
         const int node0 = FWD ? iy0 * nx + W * w : (iyb - R + 2) * nx - W * (w + 1) + SKEW * (R - 1);
         const int c1 = node0 + pad_nodes;
         mbar_expect_tx(&S.loaded[sb], (unsigned)(sizeof(S.bin[sb].u) + sizeof(S.bin[sb].b) + sizeof(S.bin[sb].qb)));
@@ -1041,7 +1189,7 @@ __global__ void __launch_bounds__(32 * gs::kWarps, 1)
   pdl_enter();
   if (skip && *skip) return;
   GsBand G{nx, ny, ngrid, pad_nodes, bands, (int)blockIdx.x, &mapS, &mapP, &mapQ, &mapQ, &mapQ, &mapQ, x, x,
-           xfer, nullptr, nullptr, 0ull, nullptr, 0ull, nullptr, nullptr, nullptr, nullptr};
+           xfer, nullptr, nullptr, 0ull, 1, nullptr, 0ull, nullptr, nullptr, nullptr, nullptr};
   gs_band<FWD, ZERO, 0>(G);
 }
 
@@ -1060,7 +1208,7 @@ __global__ void __launch_bounds__(32 * gs::kWarpsPair, 1)
               unsigned long long* flags, double* xfer, int groups, unsigned long long epoch,
               const double* __restrict__ b,
               const double* __restrict__ border, const double* __restrict__ half_old,
-              const unsigned long long* ready, unsigned long long ready_tag, int mode, const int* skip) {
+              const unsigned long long* ready, unsigned long long ready_tag, int ready_seg, int mode, const int* skip) {
   // mode bit 0 (ascent overlap): this launch runs beside the coarser level's pair and
   // the prolongation (k_prolong_rows), ordered by the ready flags only, so it must
   // not wait for the previous grid; bit 1: publish sweep B's band-done flags
@@ -1077,11 +1225,11 @@ __global__ void __launch_bounds__(32 * gs::kWarpsPair, 1)
     // sweep A: with the zero guess P = b - border x_alpha from TMA boxes (mapPA, mapQA);
     // otherwise built from x (mapXA), the old-value half (mapUB), b and border
     GsBand G{nx, ny, ngrid, pad_nodes, bands, (int)blockIdx.x, &mapSA, &mapPA, ZERO_A ? &mapQA : &mapQB, &mapBB,
-             &mapXA, &mapUB, x1, x, xfer, nullptr, ready, ready_tag, flags + 2 * groups, epoch, b, border, half_old, x};
+             &mapXA, &mapUB, x1, x, xfer, nullptr, ready, ready_tag, ready_seg, flags + 2 * groups, epoch, b, border, half_old, x};
     gs_band<FWD, ZERO_A, 1>(G);
   } else {
     GsBand G{nx, ny, ngrid, pad_nodes, bands, (int)blockIdx.x - nA, &mapSB, &mapSB, &mapQB, &mapBB, &mapXB, &mapUB, x, x,
-             xfer + 2 * (size_t)groups * nx, (mode & 2) ? flags : nullptr, ready, ready_tag, flags + 2 * groups, epoch, b,
+             xfer + 2 * (size_t)groups * nx, (mode & 2) ? flags : nullptr, ready, ready_tag, ready_seg, flags + 2 * groups, epoch, b,
              border, half_old, x1};
     gs_band<FWD, false, 2>(G);
   }
@@ -1598,7 +1746,7 @@ static int pair_shape(Ctx* c, int k, bool forward, bool zero_a, int* cs_out, int
 // mode / ready / ready_tag: the ascent overlap (k_gs_pair's mode bits).
 static int gs_pair(Ctx* c, int k, const double* b, double* x, bool forward, bool zero_a, const int* skip,
                    bool* launched, int mode = 0, const unsigned long long* ready = nullptr,
-                   unsigned long long ready_tag = 0) {
+                   unsigned long long ready_tag = 0, int ready_seg = 1) {
   *launched = false;
   if (int rc = gs_prepare()) return rc;
   LevelBuf& L = c->lv[k];
@@ -1638,15 +1786,15 @@ static int gs_pair(Ctx* c, int k, const double* b, double* x, bool forward, bool
   if (forward && zero_a)
     VTS_CUDA(cudaLaunchKernelEx(&cfg, k_gs_pair<true, true>, L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, bands, mSA,
                                 mPA, mQA, mSB, mBB, mQB, mXB, mUB, mXA, L.x1, x, L.gs_flags, L.gs_xfer, L.gs_groups, epoch, b,
-                                (const double*)L.d.border, old_half, ready, ready_tag, mode, skip));
+                                (const double*)L.d.border, old_half, ready, ready_tag, ready_seg, mode, skip));
   else if (forward)
     VTS_CUDA(cudaLaunchKernelEx(&cfg, k_gs_pair<true, false>, L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, bands, mSA,
                                 mPA, mQA, mSB, mBB, mQB, mXB, mUB, mXA, L.x1, x, L.gs_flags, L.gs_xfer, L.gs_groups, epoch, b,
-                                (const double*)L.d.border, old_half, ready, ready_tag, mode, skip));
+                                (const double*)L.d.border, old_half, ready, ready_tag, ready_seg, mode, skip));
   else
     VTS_CUDA(cudaLaunchKernelEx(&cfg, k_gs_pair<false, false>, L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, bands,
                                 mSA, mPA, mQA, mSB, mBB, mQB, mXB, mUB, mXA, L.x1, x, L.gs_flags, L.gs_xfer, L.gs_groups, epoch, b,
-                                (const double*)L.d.border, old_half, ready, ready_tag, mode, skip));
+                                (const double*)L.d.border, old_half, ready, ready_tag, ready_seg, mode, skip));
   VTS_LAUNCHED(c);
   if (pe) VTS_CUDA(cudaEventRecord(pe->b, c->stream));
   *launched = true;
@@ -1680,6 +1828,15 @@ static int ovl_workers() {
   return n;
 }
 
+// blocks of k_residual_restrict_rows (VTS_DOVL_WORKERS, A/B timing)
+static int dovl_workers() {
+  static const int n = [] {
+    const char* e = getenv("VTS_DOVL_WORKERS");
+    return e ? std::max(1, atoi(e)) : 48;
+  }();
+  return n;
+}
+
 // the two sweeps of a smoothing step: pipelined when possible
 static int gs_two_sweeps(Ctx* c, int k, const double* b, double* x, bool forward, bool zero_first, const int* skip) {
   if (pair_enabled()) {
@@ -1708,19 +1865,84 @@ int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
   size_t bot_smem = 0;
   const int kb = fused_bottom_enabled() ? bottom_plan(c, &plan, &bot_smem) : 0;
   const int lo = kb >= 1 ? kb + 1 : 1;  // lowest level handled by separate launches
-  // descent
+  // descent; with the overlap, level k's residual and restriction
+  // (k_residual_restrict_rows) and level k-1's pair start while level k's pair still
+  // sweeps, gated band by band on flags; x_alpha's residual rows follow at the end
+  const bool ovl = overlap_enabled() && pdl_enabled() && pair_enabled() && !c->prof;
+  auto pairs_fwd = [&](int k) {
+    int cs = 0, ncl = 0;
+    pair_shape(c, k, true, true, &cs, &ncl);
+    return cs > 0;
+  };
+  if (ovl && top > lo) {
+    AlphaSlots a{};
+    for (int k = lo; k < top; ++k) a.p[a.n++] = c->lv[k].x + c->lv[k].d.ngrid;
+    VTS_CUDA(launch_pdl(k_alpha_zero, dim3(1), dim3(32), 0, c->stream, a, skip));
+    VTS_LAUNCHED(c);
+  }
+  bool dprev = false;  // level k+1's residual feeds this level through flags
+  int chain_top = -1;  // highest level of the current overlapped chain
   for (int k = top; k >= lo; --k) {
     LevelBuf& L = c->lv[k];
+    LevelBuf& C = c->lv[k - 1];
     const double* b = (k == top) ? b_top : L.b;
     double* x = (k == top) ? z_top : L.x;
-    VTS_CUDA(launch_pdl(k_alpha_init, dim3(1), dim3(1), 0, c->stream, L.d.ngrid, b, x, c->d_corner, k == top ? 1 : 0, skip));
-    VTS_LAUNCHED(c);
-    if (int rc = gs_two_sweeps(c, k, b, x, true, true, skip)) return rc;
-    if (int rc = level_residual_grid(c, k, x, b, L.r, skip)) return rc;
-    LevelBuf& C = c->lv[k - 1];
-    VTS_CUDA(launch_pdl(k_restrict, dim3(div_up(C.d.nnodes + 1, 256)), dim3(256), 0, c->stream, L.d.nx, L.d.ny, L.d.free_mask, L.r, C.d.nx,
-                                                                     C.d.ny, C.d.free_mask, C.b, 1, skip));
-    VTS_LAUNCHED(c);
+    if (k == top || !ovl || top == lo) {
+      VTS_CUDA(launch_pdl(k_alpha_init, dim3(1), dim3(1), 0, c->stream, L.d.ngrid, b, x, c->d_corner, k == top ? 1 : 0, skip));
+      VTS_LAUNCHED(c);
+    }
+    const bool dpub = ovl && k > lo && pairs_fwd(k) && pairs_fwd(k - 1);
+    const int mode = (dprev ? 1 : 0) | (dpub ? 2 : 0);
+    if (mode) {
+      bool launched = false;
+      if (int rc = gs_pair(c, k, b, x, true, true, skip, &launched, mode, dprev ? L.ovl_bready : nullptr,
+                           L.bready_epoch, kSeg))
+        return rc;
+      if (!launched) {
+        set_error(5, "vcycle: overlapped descent pair did not launch");
+        return 5;
+      }
+    } else if (int rc = gs_two_sweeps(c, k, b, x, true, true, skip)) {
+      return rc;
+    }
+    if (dpub) {
+      if (chain_top < 0) chain_top = k;
+      const unsigned long long rtag = ++L.rdone_epoch, ctag = ++C.bready_epoch;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(dovl_workers());
+      cfg.blockDim = dim3(1024);
+      cfg.stream = c->stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      VTS_CUDA(cudaLaunchKernelEx(&cfg, k_residual_restrict_rows, L.d.nx, L.d.ny, (const double*)L.d.stL,
+                                  (const double*)L.d.stU, (const double*)L.d.border, (const uint8_t*)L.d.free_mask,
+                                  (const double*)x, b, L.r, C.d.nx, C.d.ny, (const uint8_t*)C.d.free_mask, C.b,
+                                  (const unsigned long long*)L.gs_flags, L.pair_epoch,
+                                  dprev ? (const unsigned long long*)L.ovl_bready : nullptr,
+                                  L.bready_epoch, L.ovl_rdone, rtag, C.ovl_bready, ctag, L.d.ngrid, skip));
+      VTS_LAUNCHED(c);
+    } else {
+      // x_alpha's residual rows of the overlapped levels above, in descent order
+      for (int j = chain_top; j > k && chain_top >= 0; --j) {
+        LevelBuf& J = c->lv[j];
+        const double* bj = (j == top) ? b_top : J.b;
+        const double* xj = (j == top) ? z_top : J.x;
+        const int grid = (int)std::min<long long>(div_up(J.d.nnodes, 256), kReduceGridCap);
+        VTS_CUDA(launch_pdl(k_alpha_residual, dim3(grid), dim3(256), 0, c->stream, J.d.nnodes, J.d.ngrid,
+                            (const double*)J.d.border, (const double*)c->d_corner, xj, bj, J.r,
+                            c->lv[j - 1].b + c->lv[j - 1].d.ngrid, c->partials, c->counters + 5, skip));
+        VTS_LAUNCHED(c);
+      }
+      chain_top = -1;
+      if (int rc = level_residual_grid(c, k, x, b, L.r, skip)) return rc;
+      VTS_CUDA(launch_pdl(k_restrict, dim3(div_up(C.d.nnodes + 1, 256)), dim3(256), 0, c->stream, L.d.nx, L.d.ny, L.d.free_mask, L.r, C.d.nx,
+                                                                       C.d.ny, C.d.free_mask, C.b, 1, skip));
+      VTS_LAUNCHED(c);
+    }
+    dprev = dpub;
   }
   if (kb >= 1) {
     if (int rc = vcycle_bottom(c, plan, bot_smem, skip)) return rc;
@@ -1739,7 +1961,6 @@ int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
     pair_shape(c, k, false, false, &cs, &ncl);
     return cs > 0;
   };
-  const bool ovl = overlap_enabled() && pdl_enabled() && pair_enabled() && !c->prof;
   bool prev_pub = false, prev_ovl = false;
   for (int k = lo; k <= top; ++k) {
     LevelBuf& L = c->lv[k];

@@ -14,6 +14,11 @@ VTS_DEVICE_INLINE unsigned long long ld_acquire(const unsigned long long* p) {
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+// a double2 through L1 (CG = false) or L2 only
+template <bool CG>
+VTS_DEVICE_INLINE double2 ld2(const double* p) {
+  return CG ? __ldcg(reinterpret_cast<const double2*>(p)) : *reinterpret_cast<const double2*>(p);
+}
 VTS_DEVICE_INLINE int ld_relaxed_i32(const int* p) {
   int v;
   asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
