@@ -334,6 +334,7 @@ __global__ void __launch_bounds__(256) k_level_apply(int nx, int ny, int ngrid, 
   pdl_enter();
   if (skip && *skip) return;
   __shared__ double scratch[256 / 32];
+  VTS_TL_BEGIN(RESIDUAL ? 6 : 9, nx);
   const int nnodes = nx * ny;
   const double xa = x[ngrid];
   double acc[1] = {0.0};

@@ -288,6 +288,7 @@ __device__ void bot_coarse(const BotLevel& C, double* sm, const BotArgs& A) {
 __global__ void __launch_bounds__(kBotThreads, 1) k_vcycle_bottom(const __grid_constant__ BotArgs A, const int* skip) {
   pdl_enter();
   if (skip && *skip) return;
+  VTS_TL_BEGIN(4, 5);
   extern __shared__ __align__(16) double sm[];
   const int tid = threadIdx.x;
   {
@@ -332,6 +333,7 @@ __global__ void __launch_bounds__(kBotThreads, 1) k_vcycle_bottom(const __grid_c
     const BotLevel& T = A.lv[A.kb];
     for (int i = tid; i <= T.ngrid; i += blockDim.x) A.gx[i] = sm[T.off_x + i];
   }
+  VTS_TL_END(4, 5);
 }
 
 // Highest level the fused kernel can take (0 = none): below the top, <= 32

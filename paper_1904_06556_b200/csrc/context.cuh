@@ -22,10 +22,9 @@ struct LevelBuf {
   double* b = nullptr;           // [ngrid + 1] V-cycle right-hand side
   double* x = nullptr;           // [ngrid + 1] V-cycle iterate
   double* r = nullptr;           // [ngrid + 1] residual / scratch
-  // GS wavefront progress flags, 4 x gs_groups, all tagged and never reset:
-  // [0, G) sweep B's band done (pair epoch, overlap), [G, 2G) unused,
-  // [2G, 3G) sweep A's stored windows, [3G, 4G) x_old of the band prolongated
-  // (k_prolong_rows, ready_epoch)
+  // GS wavefront progress flags, 3 x gs_groups, all tagged and never reset:
+  // [0, G) sweep B's stored windows ((pair epoch << 32) | windows; overlap only),
+  // [G, 2G) unused, [2G, 3G) sweep A's stored windows
   unsigned long long* gs_flags = nullptr;
   int gs_groups = 0;
   unsigned long long pair_epoch = 0;   // launches of the pipelined sweep pair on this level
@@ -33,6 +32,8 @@ struct LevelBuf {
   // descent overlap, [gs_groups x kSeg] (row band x column segment), tagged:
   unsigned long long* ovl_bready = nullptr;  // b restricted into this level (bready_epoch)
   unsigned long long* ovl_rdone = nullptr;   // residual of this level computed (rdone_epoch)
+  // ascent overlap, [gs_groups x kChunk column chunks]: x_old prolongated (ready_epoch)
+  unsigned long long* ovl_xready = nullptr;
   unsigned long long bready_epoch = 0;
   unsigned long long rdone_epoch = 0;
   double* x1 = nullptr;               // [ngrid + 1] sweep A's result inside a pair
@@ -134,6 +135,28 @@ int cuda_check(cudaError_t e, const char* what);
 // grid has completed and its memory is visible, then allow the next launch.
 // (A kernel launched without the attribute passes both instructions at once.)
 // VTS_NO_PDL=1 launches everything plainly (A/B checks).
+// Kernel timeline probe (tools/probe/tl_probe, -DVTS_TIMELINE): first block start /
+// last block end per (kernel kind, level) in globaltimer ns; level from nx = 4 * 2^k + 1
+#ifdef VTS_TIMELINE
+__device__ unsigned long long g_tl[160][2];
+__device__ __forceinline__ unsigned long long tl_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ int tl_slot(int kind, int nx) {
+  const int k = 31 - __clz(max(nx - 1, 4)) - 2;
+  return kind * 16 + min(max(k, 0), 15);
+}
+#define VTS_TL_BEGIN(kind, nx) \
+  do { if (threadIdx.x == 0) atomicMin(&g_tl[tl_slot(kind, nx)][0], tl_now()); } while (0)
+#define VTS_TL_END(kind, nx) \
+  do { __syncthreads(); if (threadIdx.x == 0) atomicMax(&g_tl[tl_slot(kind, nx)][1], tl_now()); } while (0)
+#else
+#define VTS_TL_BEGIN(kind, nx) do {} while (0)
+#define VTS_TL_END(kind, nx) do {} while (0)
+#endif
+
 __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");

@@ -293,6 +293,7 @@ __global__ void k_restrict(int fnx, int fny, const uint8_t* __restrict__ ffm, co
                            int bordered, const int* skip) {
   pdl_enter();
   if (skip && *skip) return;
+  VTS_TL_BEGIN(7, fnx);
   const int cn = blockIdx.x * blockDim.x + threadIdx.x;
   const int cnn = cnx * cny;
   if (cn > cnn) return;
@@ -339,6 +340,7 @@ __global__ void k_prolong_add(int fnx, int fny, const uint8_t* __restrict__ ffm,
                               const int* skip) {
   pdl_enter();
   if (skip && *skip) return;
+  VTS_TL_BEGIN(8, fnx);
   const int fi = blockIdx.x * blockDim.x + threadIdx.x;
   const int fnn = fnx * fny;
   if (fi > fnn) return;
@@ -349,65 +351,85 @@ __global__ void k_prolong_add(int fnx, int fny, const uint8_t* __restrict__ ffm,
   *reinterpret_cast<double2*>(xf + 2 * fi) = prolong_node(fnx, ffm, xf, cnx, cfm, xc, fi);
 }
 
-// Ascent overlap (VTS_NO_OVERLAP=1 turns it off): xf += P xc for one fine row band
-// per block, in the backward sweep's band order, each band as soon as the coarser
-// level's ascent pair has finished the coarse bands it reads (cdone >= ctag), then
-// ready[band] = tag for the finer level's pair, which is already resident and
-// waits on it.  Launched with PDL behind the coarser pair and never waits for it
-// as a grid.  Same arithmetic per node as k_prolong_add.  A few blocks take the
-// bands round robin: every block holds an SM the pair of this level may need.
+// Ascent overlap (VTS_NO_OVERLAP=1 turns it off): xf += P xc in items of one fine
+// row band x kChunk columns (backward sweep order: chunk j holds the columns
+// [fnx - kChunk (j+1), fnx - kChunk j)), each as soon as the coarser level's
+// ascent pair has stored, in every coarse band the item reads, the windows that
+// cover its coarse columns (cdone = (pair epoch << 32) | windows); then
+// ready[band][chunk] = tag for the finer level's pair, which is already resident
+// and gates each window's x_old box on it.  Launched with PDL behind the coarser
+// pair and never waits for it as a grid.  Same arithmetic per node as k_prolong_add.
+// Items run roughly in the order the coarse windows complete (fb + 2 j), round robin
+// over a few blocks: every block holds an SM the pairs may need.
+constexpr int kChunk = 128;
 __global__ void __launch_bounds__(1024) k_prolong_rows(int fnx, int fny, const uint8_t* __restrict__ ffm, double* xf,
-                                                      int cnx, int cny, const uint8_t* __restrict__ cfm, const double* xc,
-                                                      const unsigned long long* cdone, unsigned long long ctag,
-                                                      const unsigned long long* cready, unsigned long long cready_tag,
-                                                      unsigned long long* ready, unsigned long long tag, const int* skip) {
+                                                       int cnx, int cny, const uint8_t* __restrict__ cfm, const double* xc,
+                                                       const unsigned long long* cdone, unsigned long long cepoch,
+                                                       int cW, int cspan, int cnwin,
+                                                       const unsigned long long* cready, unsigned long long cready_tag,
+                                                       unsigned long long* ready, unsigned long long tag, const int* skip) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (skip && ld_relaxed_i32(skip)) return;
   constexpr int R = 16;  // gs::R (row band height of the sweeps)
-  const int fbands = (fny + R - 1) / R;
-  for (int fb = blockIdx.x; fb < fbands; fb += gridDim.x) {
-    const int yhi = fny - 1 - fb * R, ylo = max(0, yhi - R + 1);
-    if (threadIdx.x == 0) {
-      // coarse rows ylo/2 .. (yhi+1)/2, in the coarse backward bands (cny-1-row)/R
-      const int cb_first = (cny - 1 - (yhi + 1) / 2) / R, cb_last = (cny - 1 - ylo / 2) / R;
-      for (int cb = cb_first; cb <= cb_last; ++cb)
-        while (ld_acquire(cdone + cb) < ctag) {
-        }
-      // the coarse x_alpha, added by the coarser prolongation's band-0 block
-      if (fb == 0 && cready)
-        while (ld_acquire(cready) < cready_tag) {
-        }
-    }
-    __syncthreads();
-    // latency-bound (L2 loads of x_c): kU nodes per thread in flight
-    constexpr int kU = 4;
-    const int n0 = ylo * fnx, n1 = (yhi + 1) * fnx;
-    for (int base = n0 + (int)threadIdx.x; base < n1; base += kU * blockDim.x) {
-      double2 o[kU];
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int fi = base + u * blockDim.x;
-        if (fi < n1) o[u] = prolong_node<true>(fnx, ffm, xf, cnx, cfm, xc, fi);
+  const int fbands = (fny + R - 1) / R, nch = (fnx + kChunk - 1) / kChunk;
+  VTS_TL_BEGIN(3, fnx);
+  int g = 0;
+  for (int d = 0; d <= fbands - 1 + 2 * (nch - 1); ++d) {
+    for (int fb = 0; fb < fbands && fb <= d; ++fb) {
+      if ((d - fb) & 1) continue;
+      const int j = (d - fb) >> 1;
+      if (j >= nch) continue;
+      if (g++ % (int)gridDim.x != (int)blockIdx.x) continue;
+      const int yhi = fny - 1 - fb * R, ylo = max(0, yhi - R + 1);
+      const int c0 = max(0, fnx - kChunk * (j + 1)), c1 = fnx - kChunk * j;
+      if (threadIdx.x == 0) {
+        // coarse rows ylo/2 .. (yhi+1)/2 in the coarse backward bands (cny-1-row)/R, their
+        // columns >= c0/2: stored once every row of the band is through window w
+        // (row R-1 lags: columns >= cnx - cW (w+1) + cspan)
+        const int cb_first = (cny - 1 - (yhi + 1) / 2) / R, cb_last = (cny - 1 - ylo / 2) / R;
+        const int wneed = min(cnwin, (cnx + cspan - c0 / 2 + cW - 1) / cW);
+        const unsigned long long need = (cepoch << 32) | (unsigned long long)wneed;
+        for (int cb = cb_first; cb <= cb_last; ++cb)
+          while (ld_acquire(cdone + cb) < need) {
+          }
+        // the coarse x_alpha, added by the coarser prolongation's first item
+        if (fb == 0 && j == 0 && cready)
+          while (ld_acquire(cready) < cready_tag) {
+          }
       }
+      __syncthreads();
+      // latency-bound (L2 loads of x_c): kU nodes per thread in flight
+      constexpr int kU = 2;
+      const int w = c1 - c0, n = w * (yhi - ylo + 1);
+      for (int base = threadIdx.x; base < n; base += kU * blockDim.x) {
+        double2 o[kU];
 #pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int fi = base + u * blockDim.x;
-        if (fi < n1) *reinterpret_cast<double2*>(xf + 2 * fi) = o[u];
+        for (int u = 0; u < kU; ++u) {
+          const int i = base + u * blockDim.x;
+          if (i < n) o[u] = prolong_node<true>(fnx, ffm, xf, cnx, cfm, xc, (ylo + i / w) * fnx + c0 + i % w);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int i = base + u * blockDim.x;
+          if (i < n) *reinterpret_cast<double2*>(xf + 2 * ((ylo + i / w) * fnx + c0 + i % w)) = o[u];
+        }
       }
-    }
-    if (fb == 0 && threadIdx.x == 0) xf[2 * fnx * fny] += __ldcg(xc + 2 * cnx * cny);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      st_release(ready + fb, tag);
+      if (fb == 0 && j == 0 && threadIdx.x == 0) xf[2 * fnx * fny] += __ldcg(xc + 2 * cnx * cny);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        st_release(ready + (size_t)fb * nch + j, tag);
+      }
     }
   }
+  VTS_TL_END(3, fnx);
 }
 
 // Descent overlap: level k's residual r = b - A x and its restriction into the
 // coarser level's b, band by band behind level k's descent pair (forward sweep
 // order), in kSeg column segments per band:
 //   R(fb, s): r on fine band fb once the pair's sweep B finished bands fb-1..fb+1
+//             (bdone >= btag = (pair epoch << 32) | windows)
 //             (and, below the top, b on the band is restricted) -> rdone[fb][s]
 //   P(cb, s): the coarse band's rows of b_c = R r once r on the fine bands
 //             2cb-1 .. 2cb+1 is done -> cready[cb][s]; the coarser pair waits on it
@@ -430,6 +452,7 @@ __global__ void __launch_bounds__(1024) k_residual_restrict_rows(
   constexpr int R = 16;
   const int fbands = (ny + R - 1) / R, cbands = (cny + R - 1) / R;
   const int items = cbands * 3 * kSeg;
+  VTS_TL_BEGIN(2, nx);
   const double xa = __ldcg(x + ngrid);
   for (int it = blockIdx.x; it < items; it += gridDim.x) {
     const int cb = it / (3 * kSeg), j = (it / kSeg) % 3, s = it % kSeg;
@@ -480,6 +503,7 @@ __global__ void __launch_bounds__(1024) k_residual_restrict_rows(
       }
     }
   }
+  VTS_TL_END(2, nx);
 }
 
 // x_alpha's residual row of the overlapped descent levels, with k_level_apply<true>'s
@@ -492,6 +516,7 @@ __global__ void __launch_bounds__(256) k_alpha_residual(int nnodes, int ngrid, c
   pdl_enter();
   if (skip && *skip) return;
   __shared__ double scratch[256 / 32];
+  VTS_TL_BEGIN(5, (int)sqrtf(2.0f * nnodes) + 1);
   const double xa = __ldcg(x + ngrid);
   double acc[1] = {0.0};
   for (int nd = blockIdx.x * blockDim.x + threadIdx.x; nd < nnodes; nd += gridDim.x * blockDim.x) {
@@ -714,6 +739,7 @@ constexpr int kBuild = 6;  // pipelined pair, sweep B: builder warps (<= 2 nodes
 // issue sweep B's builder-input boxes (x_A after an acquire-poll, and U, b,
 // border), warp 4 is the (cross-cluster) stager: all light loops.
 constexpr int kWarpsPair = 16;
+constexpr int gs_chunk = kChunk;  // columns per k_prolong_rows item
 constexpr int kXLoadWarp = 8;
 constexpr int kReleaseWarp = 7;  // sweep A: publishes the stored-window counters (backs off while waiting)
 constexpr int kBLoadWarp = 12;
@@ -744,7 +770,6 @@ struct Smem {
   unsigned long long xloaded[NSB];   // sweep B: a builder slot's x_A box has landed
   unsigned long long bempty[NSB];    // sweep B: the builders are done with a builder slot
   unsigned stored_cnt;                // sweep A: windows x {storer, publisher} whose stores are issued
-  unsigned done_cnt;                  // sweep B (ascent overlap): storer and publisher finished the band
   unsigned long long full_above[NSA], empty_above[NSA];
   int armed;  // (producer side) highest above-ring chunk the consumer has armed
 };
@@ -860,7 +885,6 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
     }
     S.armed = NSA - 1;  // the consumer arms above slots 0 .. NSA-1 before the first cluster barrier
     S.stored_cnt = 0;
-    S.done_cnt = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (dsm_in) {
       for (int a = 0; a < NSA && a <= nwin; ++a) mbar_expect_tx(&S.full_above[a], above_bytes(a));
@@ -988,23 +1012,9 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
       }
       __syncwarp();
       if (lane == 0) {
-        if (ROLE == 1)  // this warp's part of window w is issued to global memory
+        if (ROLE == 1 || G.bdone)  // this warp's part of window w is issued to global memory
           asm volatile("red.release.cta.shared::cta.add.u32 [%0], 1;" ::"r"(smem_u32(&S.stored_cnt)) : "memory");
         mbar_arrive(&S.empty_out[s]);
-      }
-    }
-    if (ROLE == 2 && G.bdone) {
-      // the band's rows are final: the second of the two warps to get here
-      // publishes it (the finer level's prolongation waits on it)
-      __threadfence();
-      __syncwarp();
-      if (lane == 0) {
-        unsigned prev;
-        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(prev) : "r"(smem_u32(&S.done_cnt)) : "memory");
-        if (prev == 1u) {
-          __threadfence();
-          st_release(G.bdone + band, G.epoch);
-        }
       }
     }
   } else if (warp == 4) {  // ---------------- stager (previous band's last row -> above ring)
@@ -1035,7 +1045,9 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
   } else if (warp == 0) {
     gs_compute<FWD, ZERO>(S, nx, ngrid, band + (ROLE == 2 ? 128 : 0), rows_here, has_above, dsm_in, crank, nwin,
                           G.xa_src);  // (band only labels the probe timeline)
-  } else if (ROLE == 1 && warp == kReleaseWarp) {  // ---------------- sweep A: stored-window counter
+  } else if ((ROLE == 1 || G.bdone) && warp == kReleaseWarp) {  // ---------------- stored-window counter
+    // (sweep B with G.bdone: the same counter for the finer level's prolongation or
+    // this level's residual, which read the band's final rows window by window)
     // storer and publisher count their issued windows in stored_cnt (release, CTA
     // scope; a counter, not an mbarrier: nothing gates them on this warp, so they can
     // run a whole ring ahead); the release here (gpu scope, cumulative over what this
@@ -1048,7 +1060,8 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
         __nanosleep(64);  // shares a sub-partition with the publisher
       }
       __threadfence();
-      if (lane == 0) st_release(G.stored + band, (G.epoch << 32) | (unsigned long long)(w + 1));
+      if (lane == 0)
+        st_release(ROLE == 1 ? G.stored + band : G.bdone + band, (G.epoch << 32) | (unsigned long long)(w + 1));
     }
   } else if (kBuilt && warp == kXLoadWarp) {  // ---------------- built P: x box loader
     // window w's box of sweep A's result (rows of the window and the next, up to 3
@@ -1057,17 +1070,26 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
     if (lane == 0) {
       const unsigned long long tag = G.epoch << 32;
       const int iy0 = band * R, iyb = ny - 1 - band * R;
-      if (!kGated && !FWD && G.ready) {
-        // ascent overlap: x_old of this band and of the next band's first row is
-        // prolongated by k_prolong_rows while the coarser level still sweeps
-        // (band - 1: the box's skewed rows wrap into its last row, read times exact zeros)
-        for (int b2 = max(band - 1, 0); b2 <= band; ++b2) wait_ready(b2);
-        if (band + 1 < bands) wait_ready(band + 1);
-        asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores -> this warp's TMA reads
-      }
+      // ascent overlap: x_old of this band and of the next band's first row is
+      // prolongated by k_prolong_rows, chunk by chunk, while the coarser level still
+      // sweeps; window w's builders read columns >= nx - W (w+1) - 1 (the wrapped
+      // box positions they never read)
+      const bool chunked = !kGated && !FWD && G.ready;
+      int got = 0;
       for (int w = 0; w < nwin; ++w) {
         const int sb = w % NSB;
         if (w >= NSB) mbar_wait(&S.bempty[sb], ((w / NSB) - 1) & 1);
+        if (chunked) {
+          const int need = min(G.ready_seg, (W * (w + 1) + 1 + gs_chunk - 1) / gs_chunk);
+          if (need > got) {
+            for (int bb = band; bb <= min(band + 1, bands - 1); ++bb)
+              for (int j = got; j < need; ++j)
+                while (ld_acquire(G.ready + (size_t)bb * G.ready_seg + j) < G.ready_tag) {
+                }
+            got = need;
+            asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores -> this warp's TMA reads
+          }
+        }
         if (kGated) {
           while (ld_acquire(G.stored + band) < (tag | (unsigned long long)min(w + 2, nwin))) {
           }
@@ -1144,6 +1166,12 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
         const int k = i / W, p = i - (i / W) * W;
         const int n = node0 + k * (nx - SKEW) + p;
         if (n < 0 || n >= nnodes) continue;
+        // the box position's grid row and column: past a row end the box holds wrapped
+        // nodes, whose P is never stored -- 0 here, so that nothing depends on them
+        const int bl = FWD ? k : R - 1 - k;
+        const int col = FWD ? W * w - SKEW * k + p : nx - W * (w + 1) + SKEW * bl + p;
+        const int row = FWD ? iy0 + k : iyb - bl;
+        if (col < 0 || col >= nx) continue;
         // box coordinates of the node (C) and of its later neighbours NE N NW E (slots 0..3)
         const int ck = FWD ? k : k + 1, cp = FWD ? p : p + SKEW + 1;
         const int nk[4] = {FWD ? k + 1 : k, FWD ? k + 1 : k, FWD ? k + 1 : k, ck};
@@ -1161,7 +1189,13 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
         o.dv = *reinterpret_cast<const double2*>(&in.qb[k][p][0]);
         o.xo = *reinterpret_cast<const double2*>(&in.xb[ck][cp][0]);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) o.v[q] = *reinterpret_cast<const double2*>(&in.xb[nk[q]][np[q]][0]);
+        for (int q = 0; q < 4; ++q) {
+          // later neighbours outside the grid are 0, as in the multi-launch pass
+          const int dx = (FWD ? 1 : -1) * (q == 0 ? 1 : q == 1 ? 0 : q == 2 ? -1 : 1);
+          const int dy = (FWD ? 1 : -1) * (q == 3 ? 0 : 1);
+          const bool in_grid = col + dx >= 0 && col + dx < nx && row + dy >= 0 && row + dy < ny;
+          o.v[q] = in_grid ? *reinterpret_cast<const double2*>(&in.xb[nk[q]][np[q]][0]) : make_double2(0.0, 0.0);
+        }
         pv[it] = gs_old_eval<FWD>(o, xa);
       }
       __syncwarp();
@@ -1220,6 +1254,7 @@ __global__ void __launch_bounds__(32 * gs::kWarpsPair, 1)
     if (skip && *skip) return;
     ready = nullptr;
   }
+  VTS_TL_BEGIN(FWD ? 0 : 1, nx);
   const int nA = (int)gridDim.x / 2;
   if ((int)blockIdx.x < nA) {
     // sweep A: with the zero guess P = b - border x_alpha from TMA boxes (mapPA, mapQA);
@@ -1233,6 +1268,7 @@ __global__ void __launch_bounds__(32 * gs::kWarpsPair, 1)
              border, half_old, x1};
     gs_band<FWD, false, 2>(G);
   }
+  VTS_TL_END(FWD ? 0 : 1, nx);
 }
 
 
@@ -1810,6 +1846,9 @@ static bool pair_enabled() {
   return on;
 }
 
+// windows of one band of a level's wavefront sweep
+static int pair_nwin(const LevelBuf& L) { return div_up(L.d.nx + gs::SKEW * (gs::R - 1), gs::W); }
+
 // VTS_NO_OVERLAP=1 runs the ascent level by level (A/B checks)
 static bool overlap_enabled() {
   static const bool on = [] {
@@ -1823,7 +1862,7 @@ static bool overlap_enabled() {
 static int ovl_workers() {
   static const int n = [] {
     const char* e = getenv("VTS_OVL_WORKERS");
-    return e ? std::max(1, atoi(e)) : 8;
+    return e ? std::max(1, atoi(e)) : 16;
   }();
   return n;
 }
@@ -1909,7 +1948,8 @@ int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
       if (chain_top < 0) chain_top = k;
       const unsigned long long rtag = ++L.rdone_epoch, ctag = ++C.bready_epoch;
       cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(dovl_workers());
+      const int items = div_up(C.d.ny, gs::R) * 3 * kSeg;
+      cfg.gridDim = dim3(std::max(2, std::min(items / 8, dovl_workers())));
       cfg.blockDim = dim3(1024);
       cfg.stream = c->stream;
       cudaLaunchAttribute at[1];
@@ -1920,7 +1960,7 @@ int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
       VTS_CUDA(cudaLaunchKernelEx(&cfg, k_residual_restrict_rows, L.d.nx, L.d.ny, (const double*)L.d.stL,
                                   (const double*)L.d.stU, (const double*)L.d.border, (const uint8_t*)L.d.free_mask,
                                   (const double*)x, b, L.r, C.d.nx, C.d.ny, (const uint8_t*)C.d.free_mask, C.b,
-                                  (const unsigned long long*)L.gs_flags, L.pair_epoch,
+                                  (const unsigned long long*)L.gs_flags, (L.pair_epoch << 32) | (unsigned long long)pair_nwin(L),
                                   dprev ? (const unsigned long long*)L.ovl_bready : nullptr,
                                   L.bready_epoch, L.ovl_rdone, rtag, C.ovl_bready, ctag, L.d.ngrid, skip));
       VTS_LAUNCHED(c);
@@ -1971,9 +2011,12 @@ int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
     const int mode = pub ? 2 : 0;
     if (prev_pub) {
       const unsigned long long tag = ++L.ready_epoch;
-      unsigned long long* ready = L.gs_flags + 3 * L.gs_groups;
+      unsigned long long* ready = L.ovl_xready;
+      const int nch = div_up(L.d.nx, kChunk);
       cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(std::min(div_up(L.d.ny, gs::R), ovl_workers()));
+      // blocks scale with the level's items (every block holds an SM the pairs need)
+      const int items = div_up(L.d.ny, gs::R) * div_up(L.d.nx, kChunk);
+      cfg.gridDim = dim3(std::max(1, std::min(items / 4, ovl_workers())));
       cfg.blockDim = dim3(1024);
       cfg.stream = c->stream;
       cudaLaunchAttribute at[1];
@@ -1983,12 +2026,12 @@ int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
       cfg.numAttrs = 1;
       VTS_CUDA(cudaLaunchKernelEx(&cfg, k_prolong_rows, L.d.nx, L.d.ny, (const uint8_t*)L.d.free_mask, x, C.d.nx, C.d.ny,
                                   (const uint8_t*)C.d.free_mask, (const double*)C.x,
-                                  (const unsigned long long*)C.gs_flags, C.pair_epoch,
-                                  prev_ovl ? (const unsigned long long*)(C.gs_flags + 3 * C.gs_groups) : nullptr,
+                                  (const unsigned long long*)C.gs_flags, C.pair_epoch, gs::W, gs::SKEW * (gs::R - 1),
+                                  pair_nwin(C), prev_ovl ? (const unsigned long long*)C.ovl_xready : nullptr,
                                   C.ready_epoch, ready, tag, skip));
       VTS_LAUNCHED(c);
       bool launched = false;
-      if (int rc = gs_pair(c, k, b, x, false, false, skip, &launched, 1 | mode, ready, tag)) return rc;
+      if (int rc = gs_pair(c, k, b, x, false, false, skip, &launched, 1 | mode, ready, tag, nch)) return rc;
       if (!launched) {
         set_error(5, "vcycle: overlapped ascent pair did not launch");
         return 5;

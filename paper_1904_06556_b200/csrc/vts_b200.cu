@@ -307,9 +307,10 @@ static int create(Ctx** out, int levels, const int32_t* ex, const int32_t* ey, c
     dalloc_pad(arena, &L.r, ng + 1, 2 * L.pad_nodes);
     dalloc_pad(arena, &L.x1, ng + 1, 2 * L.pad_nodes);
     L.gs_groups = div_up(L.d.ny, 8);  // >= bands of any GS row-band height used
-    dalloc(arena, &L.gs_flags, 4 * (size_t)L.gs_groups);
+    dalloc(arena, &L.gs_flags, 3 * (size_t)L.gs_groups);
     dalloc(arena, &L.ovl_bready, (size_t)kSeg * L.gs_groups);
     dalloc(arena, &L.ovl_rdone, (size_t)kSeg * L.gs_groups);
+    dalloc(arena, &L.ovl_xready, (size_t)div_up(L.d.nx, kChunk) * L.gs_groups);
     dalloc(arena, &L.gs_xfer, 2 * 2 * (size_t)L.gs_groups * L.d.nx);
   }
   const LevelBuf& F = c->lv[levels - 1];

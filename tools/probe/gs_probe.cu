@@ -130,6 +130,47 @@ int main(int argc, char** argv) {
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
   printf("V-cycle: %.1f us (%s)\n", ms * 1e3 / 5, cudaGetErrorString(err));
+#ifdef VTS_TIMELINE
+  for (int rep = 0; rep < 2; ++rep) {  // kernel timeline of one V-cycle (first block start, last block end)
+    std::vector<unsigned long long> tl(160 * 2);
+    for (int i = 0; i < 160; ++i) {
+      tl[2 * i] = ~0ull;
+      tl[2 * i + 1] = 0;
+    }
+    cudaMemcpyToSymbol(vts::g_tl, tl.data(), tl.size() * 8);
+    cudaDeviceSynchronize();
+    vts::vcycle_grid(c, xin, yout, nullptr);
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(tl.data(), vts::g_tl, tl.size() * 8);
+    unsigned long long t0 = ~0ull, t1 = 0;
+    for (int i = 0; i < 160; ++i)
+      if (tl[2 * i] != ~0ull) t0 = std::min(t0, tl[2 * i]), t1 = std::max(t1, tl[2 * i + 1]);
+    static const char* names[10] = {"desc pair", "asc pair", "resid+restrict rows", "prolong rows", "bottom",
+                                     "alpha residual", "residual", "restrict", "prolong_add", "level apply"};
+    printf("timeline rep %d: %.1f us first start -> last end\n", rep, (t1 - t0) / 1e3);
+    std::vector<std::pair<unsigned long long, int>> order;
+    for (int i = 0; i < 160; ++i)
+      if (tl[2 * i] != ~0ull) order.push_back({tl[2 * i], i});
+    std::sort(order.begin(), order.end());
+    for (auto& o : order) {
+      const int i = o.second;
+      printf("  %-20s L%-2d start %7.1f  end %7.1f  (%6.1f us)\n", names[i / 16], i % 16, (tl[2 * i] - t0) / 1e3,
+             tl[2 * i + 1] ? (tl[2 * i + 1] - t0) / 1e3 : -1.0, tl[2 * i + 1] ? (tl[2 * i + 1] - tl[2 * i]) / 1e3 : 0.0);
+    }
+#ifdef VTS_GS_PROBE
+    if (rep == 1) {  // bands of the last pair of the V-cycle (the finest ascent pair)
+      std::vector<long long> pr(4 * 256);
+      cudaMemcpyFromSymbol(pr.data(), vts::g_gs_probe, pr.size() * 8);
+      const int bands = (c->lv[levels - 1].d.ny + vts::gs::R - 1) / vts::gs::R;
+      for (int b = 0; b < bands; ++b)
+        printf("  finest asc band %2d: A start %7.1f first %7.1f end %7.1f | B start %7.1f first %7.1f end %7.1f\n", b,
+               (pr[4 * b] - (long long)t0) / 1e3, (pr[4 * b + 1] - (long long)t0) / 1e3, (pr[4 * b + 2] - (long long)t0) / 1e3,
+               (pr[4 * (b + 128)] - (long long)t0) / 1e3, (pr[4 * (b + 128) + 1] - (long long)t0) / 1e3,
+               (pr[4 * (b + 128) + 2] - (long long)t0) / 1e3);
+    }
+#endif
+  }
+#endif
 #ifdef VTS_BOT_PROBE
   {
     int zero = 0;
