@@ -87,6 +87,12 @@ struct Ctx {
   // reductions
   double* partials = nullptr;   // [kMaxBlocks * kMaxPartials]
   unsigned int* counters = nullptr;  // last-block counters
+  // descent overlap: x_alpha residual rows per level (k_residual_restrict_rows),
+  // partials [16 levels x kReduceGridCap], last-block counters [16], and flags [16]:
+  // b_alpha of the level is restricted (tagged like the level's bready_epoch)
+  double* ovl_part = nullptr;
+  unsigned* ovl_cnt = nullptr;
+  unsigned long long* ovl_aflag = nullptr;
   double* dscal = nullptr;      // device scalars [64]
   double* hscal = nullptr;      // pinned host scalars [64]
   unsigned* dflags = nullptr;   // device warning flags

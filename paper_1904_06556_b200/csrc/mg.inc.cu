@@ -434,8 +434,8 @@ __global__ void __launch_bounds__(1024) k_prolong_rows(int fnx, int fny, const u
 //   P(cb, s): the coarse band's rows of b_c = R r once r on the fine bands
 //             2cb-1 .. 2cb+1 is done -> cready[cb][s]; the coarser pair waits on it
 // Items run in dependency order, round robin over the blocks.  x_alpha's part of
-// the residual is a reduction over the whole level: k_alpha_residual, after the
-// overlapped levels.  Same arithmetic per node as k_level_apply<true> / k_restrict.
+// the residual is a reduction over the whole level: the blocks' last phase, with
+// k_level_apply<true>'s reduction tree.  Same arithmetic per node as k_level_apply<true> / k_restrict.
 constexpr int kSeg = 8;
 VTS_DEVICE_INLINE void seg_cols(int n, int s, int& c0, int& c1) {
   c0 = (int)((long long)n * s / kSeg);
@@ -446,7 +446,9 @@ __global__ void __launch_bounds__(1024) k_residual_restrict_rows(
     const uint8_t* __restrict__ ffm, const double* x, const double* b, double* r, int cnx, int cny,
     const uint8_t* __restrict__ cfm, double* bc, const unsigned long long* bdone, unsigned long long btag,
     const unsigned long long* bready, unsigned long long bready_tag, unsigned long long* rdone, unsigned long long rtag,
-    unsigned long long* cready, unsigned long long ctag, int ngrid, const int* skip) {
+    unsigned long long* cready, unsigned long long ctag, int ngrid, const double* __restrict__ corner,
+    double* apart, unsigned* acnt, const unsigned long long* aflag_in, unsigned long long* aflag_out, int cngrid,
+    const int* skip) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (skip && ld_relaxed_i32(skip)) return;
   constexpr int R = 16;
@@ -503,34 +505,79 @@ __global__ void __launch_bounds__(1024) k_residual_restrict_rows(
       }
     }
   }
+  // x_alpha's residual row with k_level_apply<true>'s reduction tree: its grid of
+  // 256-thread blocks (G = min(nodes / 256, kReduceGridCap)) as virtual blocks, four
+  // per block here, each thread's nodes in the same grid-stride order, block_sum's
+  // warp trees and sequential warp totals; the last block adds the partials as
+  // last_block_reduce does and stores r_alpha into r and the coarser b
+  {
+    const int nnodes = nx * ny;
+    const int G = min((nnodes + 255) / 256, kReduceGridCap);
+    __shared__ double sc[32];
+    __shared__ bool s_last;
+    if (threadIdx.x == 0)
+      for (int bb = 0; bb < fbands; ++bb)  // every row of x is final
+        while (ld_acquire(bdone + bb) < btag) {
+        }
+    __syncthreads();
+    const int grp = threadIdx.x >> 8, gt = threadIdx.x & 255, lane = threadIdx.x & 31, wg = gt >> 5;
+    for (int base = blockIdx.x * 4; base < G; base += gridDim.x * 4) {
+      const int vb = base + grp;
+      double acc = 0.0;
+      if (vb < G)
+        for (int nd = vb * 256 + gt; nd < nnodes; nd += G * 256) {
+          const double2 bd = *reinterpret_cast<const double2*>(border + 2 * nd);
+          const double2 xv = __ldcg(reinterpret_cast<const double2*>(x + 2 * nd));
+          acc = fma(bd.x, xv.x, acc);
+          acc = fma(bd.y, xv.y, acc);
+        }
+      acc = warp_sum(acc);
+      if (lane == 0) sc[grp * 8 + wg] = acc;
+      __syncthreads();
+      if (gt == 0 && vb < G) {
+        double v = 0.0;
+        for (int q = 0; q < 8; ++q) v += sc[grp * 8 + q];
+        apart[vb] = v;
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      __threadfence();
+      s_last = atomicAdd(acnt, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x < 256) {
+      __threadfence();
+      double tot = 0.0;
+      for (int q = threadIdx.x; q < G; q += 256) tot += __ldcg(apart + q);
+      tot = warp_sum(tot);
+      if (lane == 0) sc[wg] = tot;
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (threadIdx.x == 0) {
+        double v = 0.0;
+        for (int q = 0; q < 8; ++q) v += sc[q];
+        const double ya = fma(*corner, xa, v);
+        if (aflag_in)  // b_alpha of this level comes from the finer level's residual row
+          while (ld_acquire(aflag_in) < bready_tag) {
+          }
+        const double ra = __ldcg(b + ngrid) - ya;
+        r[ngrid] = ra;
+        bc[cngrid] = ra;
+        *acnt = 0u;
+        __threadfence();
+        st_release(aflag_out, ctag);
+      }
+    }
+  }
   VTS_TL_END(2, nx);
 }
 
-// x_alpha's residual row of the overlapped descent levels, with k_level_apply<true>'s
-// reduction tree (same grid, same per-thread order): r_alpha = b_alpha - (border.x +
-// corner x_alpha), copied into the coarser b_alpha as k_restrict does
-__global__ void __launch_bounds__(256) k_alpha_residual(int nnodes, int ngrid, const double* __restrict__ border,
-                                                        const double* __restrict__ corner_ptr, const double* x,
-                                                        const double* b, double* r, double* bc_alpha,
-                                                        double* partials, unsigned* counter, const int* skip) {
+// waits until a flag reaches its tag (the level below the overlapped descent reads
+// b_alpha, which the overlapped residual rows restrict)
+__global__ void k_wait_flag(const unsigned long long* flag, unsigned long long tag, const int* skip) {
   pdl_enter();
   if (skip && *skip) return;
-  __shared__ double scratch[256 / 32];
-  VTS_TL_BEGIN(5, (int)sqrtf(2.0f * nnodes) + 1);
-  const double xa = __ldcg(x + ngrid);
-  double acc[1] = {0.0};
-  for (int nd = blockIdx.x * blockDim.x + threadIdx.x; nd < nnodes; nd += gridDim.x * blockDim.x) {
-    const double2 bd = *reinterpret_cast<const double2*>(border + 2 * nd);
-    const double2 xv = __ldcg(reinterpret_cast<const double2*>(x + 2 * nd));
-    acc[0] = fma(bd.x, xv.x, acc[0]);
-    acc[0] = fma(bd.y, xv.y, acc[0]);
-  }
-  double tot[1];
-  if (last_block_reduce<1>(acc, scratch, partials, counter, tot) && threadIdx.x == 0) {
-    const double ya = fma(*corner_ptr, xa, tot[0]);
-    const double ra = __ldcg(b + ngrid) - ya;
-    r[ngrid] = ra;
-    *bc_alpha = ra;
+  while (ld_acquire(flag) < tag) {
   }
 }
 
@@ -1962,18 +2009,16 @@ int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
                                   (const double*)x, b, L.r, C.d.nx, C.d.ny, (const uint8_t*)C.d.free_mask, C.b,
                                   (const unsigned long long*)L.gs_flags, (L.pair_epoch << 32) | (unsigned long long)pair_nwin(L),
                                   dprev ? (const unsigned long long*)L.ovl_bready : nullptr,
-                                  L.bready_epoch, L.ovl_rdone, rtag, C.ovl_bready, ctag, L.d.ngrid, skip));
+                                  L.bready_epoch, L.ovl_rdone, rtag, C.ovl_bready, ctag, L.d.ngrid,
+                                  (const double*)c->d_corner, c->ovl_part + (size_t)k * kReduceGridCap, c->ovl_cnt + k,
+                                  dprev ? (const unsigned long long*)(c->ovl_aflag + k) : nullptr, c->ovl_aflag + (k - 1),
+                                  C.d.ngrid, skip));
       VTS_LAUNCHED(c);
     } else {
-      // x_alpha's residual rows of the overlapped levels above, in descent order
-      for (int j = chain_top; j > k && chain_top >= 0; --j) {
-        LevelBuf& J = c->lv[j];
-        const double* bj = (j == top) ? b_top : J.b;
-        const double* xj = (j == top) ? z_top : J.x;
-        const int grid = (int)std::min<long long>(div_up(J.d.nnodes, 256), kReduceGridCap);
-        VTS_CUDA(launch_pdl(k_alpha_residual, dim3(grid), dim3(256), 0, c->stream, J.d.nnodes, J.d.ngrid,
-                            (const double*)J.d.border, (const double*)c->d_corner, xj, bj, J.r,
-                            c->lv[j - 1].b + c->lv[j - 1].d.ngrid, c->partials, c->counters + 5, skip));
+      // b_alpha of this level: the overlapped residual rows above restrict it last
+      if (chain_top >= 0) {
+        VTS_CUDA(launch_pdl(k_wait_flag, dim3(1), dim3(1), 0, c->stream, (const unsigned long long*)(c->ovl_aflag + k),
+                            L.bready_epoch, skip));
         VTS_LAUNCHED(c);
       }
       chain_top = -1;

@@ -330,6 +330,9 @@ static int create(Ctx** out, int levels, const int32_t* ex, const int32_t* ey, c
   const size_t rap = levels > 1 ? (size_t)c->lv[levels - 2].d.nnodes * kStencilStride : 1;
   dalloc(arena, &c->rap_tmp, rap);
   dalloc(arena, &c->partials, (size_t)kMaxBlocks * kMaxPartials);
+  dalloc(arena, &c->ovl_part, (size_t)16 * kReduceGridCap);
+  dalloc(arena, &c->ovl_cnt, 16);
+  dalloc(arena, &c->ovl_aflag, 16);
   dalloc(arena, &c->counters, 64);
   dalloc(arena, &c->dscal, 64);
   dalloc(arena, &c->dflags, 4);
