@@ -9,7 +9,7 @@ returns zero for a zero right-hand side (test_linalg_multigrid.py:94-139).
 The same properties are checked here on the device operators, on the small
 configs and on the 1024x512 microbench system (C3), where no CPU oracle
 finishes in test time.  The A/B switches of the library (modal vs dense
-Newton apply, programmatic dependent launch) are checked against each other.
+Newton apply, programmatic dependent launch, overlapped levels) are checked against each other.
 """
 
 from __future__ import annotations
@@ -169,3 +169,14 @@ def test_modal_apply_matches_the_dense_products(tmp_path, key):
     np.testing.assert_array_equal(modal[:nz], dense[:nz])  # the V-cycle does not use the apply
     x_m, x_d = modal[nz:-1], dense[nz:-1]
     assert np.abs(x_m - x_d).max() <= 1e-8 * np.abs(x_d).max()
+
+
+@pytest.mark.parametrize("key", ["C2", "C3"])
+def test_overlapped_levels_are_bitwise_identical_to_level_by_level(tmp_path, key):
+    """The descent / ascent overlap (residual, restriction and prolongation passes
+    running band by band beside the pairs, gated on flags) computes the same bits
+    as the level-by-level V-cycle (VTS_NO_OVERLAP=1)."""
+    a = _ab(tmp_path, "overlap", key, {})
+    b = _ab(tmp_path, "level_by_level", key, {"VTS_NO_OVERLAP": "1"})
+    assert a.tobytes() == b.tobytes()
+
