@@ -428,11 +428,12 @@ __global__ void __launch_bounds__(1024) k_prolong_rows(int fnx, int fny, const u
 // Descent overlap: level k's residual r = b - A x and its restriction into the
 // coarser level's b, band by band behind level k's descent pair (forward sweep
 // order), in kSeg column segments per band:
-//   R(fb, s): r on fine band fb once the pair's sweep B finished bands fb-1..fb+1
-//             (bdone >= btag = (pair epoch << 32) | windows)
+//   R(fb, s): r on fine band fb, segment s, once the pair's sweep B has stored
+//             bands fb-1..fb+1 through the segment's columns (+1)
 //             (and, below the top, b on the band is restricted) -> rdone[fb][s]
-//   P(cb, s): the coarse band's rows of b_c = R r once r on the fine bands
-//             2cb-1 .. 2cb+1 is done -> cready[cb][s]; the coarser pair waits on it
+//   P(cb, s): the coarse band's rows of b_c = R r, segment s, once r on the fine
+//             bands 2cb-1 .. 2cb+1 and the segments under its columns is done ->
+//             cready[cb][s]; the coarser pair's boxes wait on it window by window
 // Items run in dependency order, round robin over the blocks.  x_alpha's part of
 // the residual is a reduction over the whole level: the blocks' last phase, with
 // k_level_apply<true>'s reduction tree.  Same arithmetic per node as k_level_apply<true> / k_restrict.
@@ -444,7 +445,8 @@ VTS_DEVICE_INLINE void seg_cols(int n, int s, int& c0, int& c1) {
 __global__ void __launch_bounds__(1024) k_residual_restrict_rows(
     int nx, int ny, const double* __restrict__ stL, const double* __restrict__ stU, const double* __restrict__ border,
     const uint8_t* __restrict__ ffm, const double* x, const double* b, double* r, int cnx, int cny,
-    const uint8_t* __restrict__ cfm, double* bc, const unsigned long long* bdone, unsigned long long btag,
+    const uint8_t* __restrict__ cfm, double* bc, const unsigned long long* bdone, unsigned long long bepoch, int nwin,
+    int gW, int gspan,
     const unsigned long long* bready, unsigned long long bready_tag, unsigned long long* rdone, unsigned long long rtag,
     unsigned long long* cready, unsigned long long ctag, int ngrid, const double* __restrict__ corner,
     double* apart, unsigned* acnt, const unsigned long long* aflag_in, unsigned long long* aflag_out, int cngrid,
@@ -457,13 +459,31 @@ __global__ void __launch_bounds__(1024) k_residual_restrict_rows(
   VTS_TL_BEGIN(2, nx);
   const double xa = __ldcg(x + ngrid);
   for (int it = blockIdx.x; it < items; it += gridDim.x) {
-    const int cb = it / (3 * kSeg), j = (it / kSeg) % 3, s = it % kSeg;
+    // a coarse band's items in column order: R(2cb, 0) R(2cb+1, 0), then per segment
+    // t = 1..kSeg-1: R(2cb, t) R(2cb+1, t) P(cb, t-1), and P(cb, kSeg-1) last
+    const int cb = it / (3 * kSeg), q = it % (3 * kSeg);
+    int j, s;
+    if (q < 2) {
+      j = q;
+      s = 0;
+    } else if (q == 3 * kSeg - 1) {
+      j = 2;
+      s = kSeg - 1;
+    } else {
+      j = (q - 2) % 3;
+      s = (q - 2) / 3 + 1 - (j == 2 ? 1 : 0);
+    }
     if (j < 2) {
       const int fb = 2 * cb + j;
       if (fb >= fbands) continue;
       if (threadIdx.x == 0) {
+        // x on columns <= c1 of the rows fb*R-1 .. fb*R+R: sweep B has stored every
+        // row of those bands through the window where row R-1 passes column c1
+        int c0, c1;
+        seg_cols(nx, s, c0, c1);
+        const int wcount = min(nwin, (min(nx - 1, c1) + gspan) / gW + 1);
         for (int bb = max(fb - 1, 0); bb <= min(fb + 1, fbands - 1); ++bb)
-          while (ld_acquire(bdone + bb) < btag) {
+          while (ld_acquire(bdone + bb) < (bepoch | (unsigned long long)wcount)) {
           }
         if (bready)
           while (ld_acquire(bready + (size_t)fb * kSeg + s) < bready_tag) {
@@ -485,10 +505,18 @@ __global__ void __launch_bounds__(1024) k_residual_restrict_rows(
       }
     } else {
       if (threadIdx.x == 0) {
+        // r on the fine segments holding columns 2 c0 - 1 .. 2 (c1 - 1) + 1
+        int c0, c1;
+        seg_cols(cnx, s, c0, c1);
+        const int flo = max(0, 2 * c0 - 1), fhi = min(nx - 1, 2 * (c1 - 1) + 1);
         for (int fb = max(2 * cb - 1, 0); fb <= min(2 * cb + 1, fbands - 1); ++fb)
-          for (int q = 0; q < kSeg; ++q)
-            while (ld_acquire(rdone + (size_t)fb * kSeg + q) < rtag) {
+          for (int qq = 0; qq < kSeg; ++qq) {
+            int f0, f1;
+            seg_cols(nx, qq, f0, f1);
+            if (f1 <= flo || f0 > fhi) continue;
+            while (ld_acquire(rdone + (size_t)fb * kSeg + qq) < rtag) {
             }
+          }
       }
       __syncthreads();
       int c0, c1;
@@ -517,7 +545,7 @@ __global__ void __launch_bounds__(1024) k_residual_restrict_rows(
     __shared__ bool s_last;
     if (threadIdx.x == 0)
       for (int bb = 0; bb < fbands; ++bb)  // every row of x is final
-        while (ld_acquire(bdone + bb) < btag) {
+        while (ld_acquire(bdone + bb) < (bepoch | (unsigned long long)nwin)) {
         }
     __syncthreads();
     const int grp = threadIdx.x >> 8, gt = threadIdx.x & 255, lane = threadIdx.x & 31, wg = gt >> 5;
@@ -947,15 +975,34 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
   }
   // every CTA's barriers exist (and its ring is zeroed) before any remote st.async lands
   asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
-  // overlap gating: every segment flag of band bb done (bb < bands)
-  auto wait_ready = [&](int bb) {
-    for (int j = 0; j < G.ready_seg; ++j)
-      while (ld_acquire(G.ready + (size_t)bb * G.ready_seg + j) < G.ready_tag) {
+  // descent overlap, per window w of a forward box: the band's column segments
+  // holding columns <= W (w+1) - 1, and once the box wraps past the last column
+  // (W (w+1) > nx: row R-1 continues in the next band's first row), the next band's
+  // segments holding the wrapped columns <= W (w+1) - 1 - nx
+  auto gate_window = [&](int w, int& got, int& got_next) {
+    bool waited = false;
+    const int cmax = min(nx - 1, W * (w + 1) - 1);
+    for (; got < G.ready_seg; ++got) {
+      int c0, c1;
+      seg_cols(nx, got, c0, c1);
+      if (c0 > cmax) break;
+      while (ld_acquire(G.ready + (size_t)band * G.ready_seg + got) < G.ready_tag) {
       }
+      waited = true;
+    }
+    if (band + 1 < bands && W * (w + 1) > nx) {
+      const int wmax = W * (w + 1) - 1 - nx;
+      for (; got_next < G.ready_seg; ++got_next) {
+        int c0, c1;
+        seg_cols(nx, got_next, c0, c1);
+        if (c0 > wmax) break;
+        while (ld_acquire(G.ready + (size_t)(band + 1) * G.ready_seg + got_next) < G.ready_tag) {
+        }
+        waited = true;
+      }
+    }
+    if (waited) asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores -> this warp's TMA reads
   };
-  // forward boxes of window w reach into the next band's first row (skewed
-  // positions past the last column) once W (w + 1) > nx
-  auto wraps_next = [&](int w) { return W * (w + 1) > nx; };
   // band row l -> grid row; box row of band row l; slot position of step st
   auto grid_row = [&](int l) {
     const int r = band * R + l;
@@ -969,20 +1016,12 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
   } else if (warp == 1) {  // ---------------- loader (one thread, TMA boxes)
     if (lane == 0) {
       const int iy0 = band * R, iyb = ny - 1 - band * R;
-      const bool gate = ZERO && G.ready;  // descent overlap: b of the band is restricted
-      bool next_ok = !(gate && band + 1 < bands);
-      if (gate) {
-        wait_ready(band);
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-      }
+      const bool gate = ZERO && G.ready;  // descent overlap: b of the window is restricted
+      int got = 0, got_next = 0;
       for (int w = 0; w < nwin; ++w) {
         const int s = w % NS;
         if (w >= NS) mbar_wait(&S.empty_in[s], ((w / NS) - 1) & 1);
-        if (!next_ok && wraps_next(w)) {
-          wait_ready(band + 1);
-          asm volatile("fence.proxy.async.global;" ::: "memory");
-          next_ok = true;
-        }
+        if (gate) gate_window(w, got, got_next);
         // node index of box element (p = 0, box row 0)
         const int node0 = FWD ? iy0 * nx + W * w : (iyb - R + 2) * nx - W * (w + 1) + SKEW * (R - 1);
         const int c1 = node0 + pad_nodes;
@@ -1157,20 +1196,12 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
     // previous window -- ahead of the compute ring, which frees slots later
     if (lane == 0) {
       const int iy0 = band * R, iyb = ny - 1 - band * R;
-      const bool gate = FWD && G.ready;  // descent overlap: b of the band is restricted
-      bool next_ok = !(gate && band + 1 < bands);
-      if (gate) {
-        wait_ready(band);
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-      }
+      const bool gate = FWD && G.ready;  // descent overlap: b of the window is restricted
+      int got = 0, got_next = 0;
       for (int w = 0; w < nwin; ++w) {
         const int sb = w % NSB;
         if (w >= NSB) mbar_wait(&S.bempty[sb], ((w / NSB) - 1) & 1);
-        if (!next_ok && wraps_next(w)) {
-          wait_ready(band + 1);
-          asm volatile("fence.proxy.async.global;" ::: "memory");
-          next_ok = true;
-        }
+        if (gate) gate_window(w, got, got_next);
         const int node0 = FWD ? iy0 * nx + W * w : (iyb - R + 2) * nx - W * (w + 1) + SKEW * (R - 1);
         const int c1 = node0 + pad_nodes;
         mbar_expect_tx(&S.loaded[sb], (unsigned)(sizeof(S.bin[sb].u) + sizeof(S.bin[sb].b) + sizeof(S.bin[sb].qb)));
@@ -2007,7 +2038,8 @@ int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
       VTS_CUDA(cudaLaunchKernelEx(&cfg, k_residual_restrict_rows, L.d.nx, L.d.ny, (const double*)L.d.stL,
                                   (const double*)L.d.stU, (const double*)L.d.border, (const uint8_t*)L.d.free_mask,
                                   (const double*)x, b, L.r, C.d.nx, C.d.ny, (const uint8_t*)C.d.free_mask, C.b,
-                                  (const unsigned long long*)L.gs_flags, (L.pair_epoch << 32) | (unsigned long long)pair_nwin(L),
+                                  (const unsigned long long*)L.gs_flags, L.pair_epoch << 32, pair_nwin(L), gs::W,
+                                  gs::SKEW * (gs::R - 1),
                                   dprev ? (const unsigned long long*)L.ovl_bready : nullptr,
                                   L.bready_epoch, L.ovl_rdone, rtag, C.ovl_bready, ctag, L.d.ngrid,
                                   (const double*)c->d_corner, c->ovl_part + (size_t)k * kReduceGridCap, c->ovl_cnt + k,
