@@ -361,7 +361,15 @@ __global__ void k_prolong_add(int fnx, int fny, const uint8_t* __restrict__ ffm,
 // pair and never waits for it as a grid.  Same arithmetic per node as k_prolong_add.
 // Items run roughly in the order the coarse windows complete (fb + 2 j), round robin
 // over a few blocks: every block holds an SM the pairs may need.
+#ifndef VTS_OVL_SLEEP
+#define VTS_OVL_SLEEP 128
+#endif
 constexpr int kChunk = 128;
+// spin of a helper pass on a flag: backs off so that its polls stay out of the
+// L2 traffic of the pairs it runs beside
+VTS_DEVICE_INLINE void wait_flag_backoff(const unsigned long long* f, unsigned long long need) {
+  while (ld_acquire(f) < need) __nanosleep(VTS_OVL_SLEEP);
+}
 __global__ void __launch_bounds__(1024) k_prolong_rows(int fnx, int fny, const uint8_t* __restrict__ ffm, double* xf,
                                                        int cnx, int cny, const uint8_t* __restrict__ cfm, const double* xc,
                                                        const unsigned long long* cdone, unsigned long long cepoch,
@@ -389,9 +397,7 @@ __global__ void __launch_bounds__(1024) k_prolong_rows(int fnx, int fny, const u
         const int cb_first = (cny - 1 - (yhi + 1) / 2) / R, cb_last = (cny - 1 - ylo / 2) / R;
         const int wneed = min(cnwin, (cnx + cspan - c0 / 2 + cW - 1) / cW);
         const unsigned long long need = (cepoch << 32) | (unsigned long long)wneed;
-        for (int cb = cb_first; cb <= cb_last; ++cb)
-          while (ld_acquire(cdone + cb) < need) {
-          }
+        for (int cb = cb_first; cb <= cb_last; ++cb) wait_flag_backoff(cdone + cb, need);
         // the coarse x_alpha, added by the coarser prolongation's first item
         if (fb == 0 && j == 0 && cready)
           while (ld_acquire(cready) < cready_tag) {
@@ -483,8 +489,7 @@ __global__ void __launch_bounds__(1024) k_residual_restrict_rows(
         seg_cols(nx, s, c0, c1);
         const int wcount = min(nwin, (min(nx - 1, c1) + gspan) / gW + 1);
         for (int bb = max(fb - 1, 0); bb <= min(fb + 1, fbands - 1); ++bb)
-          while (ld_acquire(bdone + bb) < (bepoch | (unsigned long long)wcount)) {
-          }
+          wait_flag_backoff(bdone + bb, bepoch | (unsigned long long)wcount);
         if (bready)
           while (ld_acquire(bready + (size_t)fb * kSeg + s) < bready_tag) {
           }
@@ -514,8 +519,7 @@ __global__ void __launch_bounds__(1024) k_residual_restrict_rows(
             int f0, f1;
             seg_cols(nx, qq, f0, f1);
             if (f1 <= flo || f0 > fhi) continue;
-            while (ld_acquire(rdone + (size_t)fb * kSeg + qq) < rtag) {
-            }
+            wait_flag_backoff(rdone + (size_t)fb * kSeg + qq, rtag);
           }
       }
       __syncthreads();
@@ -545,8 +549,7 @@ __global__ void __launch_bounds__(1024) k_residual_restrict_rows(
     __shared__ bool s_last;
     if (threadIdx.x == 0)
       for (int bb = 0; bb < fbands; ++bb)  // every row of x is final
-        while (ld_acquire(bdone + bb) < (bepoch | (unsigned long long)nwin)) {
-        }
+        wait_flag_backoff(bdone + bb, bepoch | (unsigned long long)nwin);
     __syncthreads();
     const int grp = threadIdx.x >> 8, gt = threadIdx.x & 255, lane = threadIdx.x & 31, wg = gt >> 5;
     for (int base = blockIdx.x * 4; base < G; base += gridDim.x * 4) {
