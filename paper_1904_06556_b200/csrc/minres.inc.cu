@@ -12,6 +12,15 @@
 
 namespace vts {
 
+// VTS_MEMCPY_STATE=1 reads the MINRES state back with a copy-engine transfer (A/B)
+static bool publish_kernel() {
+  static const bool on = [] {
+    const char* e = getenv("VTS_MEMCPY_STATE");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
 __global__ void k_mr_scale(int len, const double* __restrict__ y, double* __restrict__ v, const MinresDev* st) {
   pdl_enter();
   if (st->stopped) return;
@@ -123,6 +132,19 @@ __global__ void k_mr_update(int len, const double* __restrict__ v, const double*
       st->stopped = 1;
     }
   }
+}
+
+// the iteration's state into the pinned host mirror (cudaMallocHost memory is
+// device-accessible under unified addressing): a kernel, so the next iteration's
+// launches stay in the programmatic-launch chain, which a copy-engine transfer breaks
+__global__ void k_mr_publish(const MinresDev* __restrict__ st, MinresDev* host) {
+  pdl_enter();
+  constexpr int kWords = sizeof(MinresDev) / 8;
+  static_assert(sizeof(MinresDev) % 8 == 0, "state copied in 8-byte words");
+  if ((int)threadIdx.x < kWords)
+    reinterpret_cast<volatile unsigned long long*>(host)[threadIdx.x] =
+        reinterpret_cast<const unsigned long long*>(st)[threadIdx.x];
+  __threadfence_system();
 }
 
 // true residual after a verify apply: relres = ||b - Ax|| / ||b||  (linalg.py:231-239)
@@ -332,7 +354,13 @@ int minres(Ctx* c, const double* b_free, double* x_free, double tol, int max_ite
     x_in[it & 1] = x;
     x_out[it & 1] = xalt;
     std::swap(x, xalt);
-    VTS_CUDA(cudaMemcpyAsync(c->hmst + (it & 1), c->mst, sizeof(MinresDev), cudaMemcpyDeviceToHost, c->stream));
+    if (publish_kernel()) {
+      static_assert(sizeof(MinresDev) / 8 <= 64, "one block of 64 threads copies the state");
+      VTS_CUDA(launch_pdl(k_mr_publish, dim3(1), dim3(64), 0, c->stream, (const MinresDev*)c->mst, c->hmst + (it & 1)));
+      VTS_LAUNCHED(c);
+    } else {
+      VTS_CUDA(cudaMemcpyAsync(c->hmst + (it & 1), c->mst, sizeof(MinresDev), cudaMemcpyDeviceToHost, c->stream));
+    }
     VTS_CUDA(cudaEventRecord(c->mr_ev[it & 1], c->stream));
     return 0;
   };
