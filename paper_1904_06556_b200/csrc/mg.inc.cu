@@ -898,7 +898,7 @@ struct GsBand {
   double* x;                // the sweep's result
   const double* xa_src;     // bordered vector holding x_alpha (slot ngrid)
   double* xfer;                // cross-cluster handoff rows of this sweep, [bands][nx] nodes
-  unsigned long long* bdone;   // ascent overlap, sweep B: band finished (epoch-tagged), or null
+  unsigned long long* bdone;   // overlap, sweep B: per-window progress ((epoch << 32) | windows), or null
   // overlap gating, or null: ascent pairs wait for x_old of a band (k_prolong_rows),
   // descent pairs for its right-hand side b (k_residual_restrict_rows); ready_seg
   // flags per band, each >= ready_tag when done
@@ -1326,7 +1326,7 @@ __global__ void __launch_bounds__(32 * gs::kWarpsPair, 1)
               const unsigned long long* ready, unsigned long long ready_tag, int ready_seg, int mode, const int* skip) {
   // mode bit 0 (ascent overlap): this launch runs beside the coarser level's pair and
   // the prolongation (k_prolong_rows), ordered by the ready flags only, so it must
-  // not wait for the previous grid; bit 1: publish sweep B's band-done flags
+  // not wait for the previous grid; bit 1: publish sweep B's per-window progress
   if (mode & 1) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (skip && ld_relaxed_i32(skip)) return;
