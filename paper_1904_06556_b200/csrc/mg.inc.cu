@@ -1324,9 +1324,10 @@ __global__ void __launch_bounds__(32 * gs::kWarpsPair, 1)
               const double* __restrict__ b,
               const double* __restrict__ border, const double* __restrict__ half_old,
               const unsigned long long* ready, unsigned long long ready_tag, int ready_seg, int mode, const int* skip) {
-  // mode bit 0 (ascent overlap): this launch runs beside the coarser level's pair and
-  // the prolongation (k_prolong_rows), ordered by the ready flags only, so it must
-  // not wait for the previous grid; bit 1: publish sweep B's per-window progress
+  // mode bit 0 (overlap): this launch runs beside the neighbouring level's pair and
+  // its residual/restriction or prolongation pass, ordered by the ready flags only,
+  // so it must not wait for the previous grid; bit 1: publish sweep B's per-window
+  // progress
   if (mode & 1) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (skip && ld_relaxed_i32(skip)) return;
