@@ -1980,6 +1980,26 @@ static bool fused_bottom_enabled() {
   return on;
 }
 
+// blocks of the overlap passes of level k (each holds an SM)
+static int dovl_blocks(const Ctx* c, int k) {  // k_residual_restrict_rows, level k -> k-1
+  const int items = div_up(c->lv[k - 1].d.ny, gs::R) * 3 * kSeg;
+  return std::max(2, std::min(items / 8, dovl_workers()));
+}
+static int aovl_blocks(const Ctx* c, int k) {  // k_prolong_rows into level k
+  const int items = div_up(c->lv[k].d.ny, gs::R) * div_up(c->lv[k].d.nx, kChunk);
+  return std::max(1, std::min(items / 4, ovl_workers()));
+}
+static int sm_count() {
+  static const int n = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+// pair CTAs of level k (one per SM)
+static int pair_ctas(const Ctx* c, int k) { return 2 * div_up(c->lv[k].d.ny, gs::R); }
+
 int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
   const int top = c->L - 1;
   BotArgs plan{};
@@ -2012,7 +2032,10 @@ int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
       VTS_CUDA(launch_pdl(k_alpha_init, dim3(1), dim3(1), 0, c->stream, L.d.ngrid, b, x, c->d_corner, k == top ? 1 : 0, skip));
       VTS_LAUNCHED(c);
     }
-    const bool dpub = ovl && k > lo && pairs_fwd(k) && pairs_fwd(k - 1);
+    // overlap only where level k's pair, its residual pass and level k-1's pair fit
+    // on the GPU together (else the pass would crawl on the few SMs left beside the pair)
+    const bool dpub = ovl && k > lo && pairs_fwd(k) && pairs_fwd(k - 1) &&
+                      pair_ctas(c, k) + dovl_blocks(c, k) + pair_ctas(c, k - 1) <= sm_count();
     const int mode = (dprev ? 1 : 0) | (dpub ? 2 : 0);
     if (mode) {
       bool launched = false;
@@ -2030,8 +2053,7 @@ int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
       if (chain_top < 0) chain_top = k;
       const unsigned long long rtag = ++L.rdone_epoch, ctag = ++C.bready_epoch;
       cudaLaunchConfig_t cfg = {};
-      const int items = div_up(C.d.ny, gs::R) * 3 * kSeg;
-      cfg.gridDim = dim3(std::max(2, std::min(items / 8, dovl_workers())));
+      cfg.gridDim = dim3(dovl_blocks(c, k));
       cfg.blockDim = dim3(1024);
       cfg.stream = c->stream;
       cudaLaunchAttribute at[1];
@@ -2088,7 +2110,9 @@ int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
     LevelBuf& C = c->lv[k - 1];
     const double* b = (k == top) ? b_top : L.b;
     double* x = (k == top) ? z_top : L.x;
-    const bool pub = ovl && k < top && pairs(k) && pairs(k + 1);  // level k+1 overlaps this pair
+    // level k+1 overlaps this pair (where both pairs and the prolongation fit together)
+    const bool pub = ovl && k < top && pairs(k) && pairs(k + 1) &&
+                     pair_ctas(c, k) + aovl_blocks(c, k + 1) + pair_ctas(c, k + 1) <= sm_count();
     const int mode = pub ? 2 : 0;
     if (prev_pub) {
       const unsigned long long tag = ++L.ready_epoch;
@@ -2096,8 +2120,7 @@ int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
       const int nch = div_up(L.d.nx, kChunk);
       cudaLaunchConfig_t cfg = {};
       // blocks scale with the level's items (every block holds an SM the pairs need)
-      const int items = div_up(L.d.ny, gs::R) * div_up(L.d.nx, kChunk);
-      cfg.gridDim = dim3(std::max(1, std::min(items / 4, ovl_workers())));
+      cfg.gridDim = dim3(aovl_blocks(c, k));
       cfg.blockDim = dim3(1024);
       cfg.stream = c->stream;
       cudaLaunchAttribute at[1];
