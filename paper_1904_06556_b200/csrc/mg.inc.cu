@@ -1052,8 +1052,11 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
       const int s = w % NS;
       mbar_wait(&S.full_out[s], (w / NS) & 1);
       if (!pub) {
-        // sweep A of a pair also stores the last row, so its stored counter covers every row
-        for (int i = lane; i < (R - 1) * W; i += 32) {
+        // in a pair the storer also stores the last row, so its stored counter alone
+        // covers every row and the publisher (on the band handoff's critical path)
+        // issues no release
+        constexpr int kRows = ROLE == 0 ? R - 1 : R;
+        for (int i = lane; i < kRows * W; i += 32) {
           const int l = i / W, p = i - (i / W) * W;
           if (l >= rows_here) continue;
           const int ix = grid_ix(w, l, p);
@@ -1068,7 +1071,7 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
           const int ix = grid_ix(w, l, lane);
           if (ix >= 0 && ix < nx) {
             const double2 v = S.out[s][l][lane];
-            *reinterpret_cast<double2*>(x + 2 * ((size_t)grid_row(l) * nx + ix)) = v;
+            if (ROLE == 0) *reinterpret_cast<double2*>(x + 2 * ((size_t)grid_row(l) * nx + ix)) = v;
             // the next band is in another cluster: each value is its own ready flag,
             // no fence or counter (the consumer polls the value slots)
             if (publish)
@@ -1101,7 +1104,7 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
       }
       __syncwarp();
       if (lane == 0) {
-        if (ROLE == 1 || G.bdone)  // this warp's part of window w is issued to global memory
+        if (!pub && (ROLE == 1 || G.bdone))  // window w's rows are issued to global memory
           asm volatile("red.release.cta.shared::cta.add.u32 [%0], 1;" ::"r"(smem_u32(&S.stored_cnt)) : "memory");
         mbar_arrive(&S.empty_out[s]);
       }
@@ -1137,7 +1140,7 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
   } else if ((ROLE == 1 || G.bdone) && warp == kReleaseWarp) {  // ---------------- stored-window counter
     // (sweep B with G.bdone: the same counter for the finer level's prolongation or
     // this level's residual, which read the band's final rows window by window)
-    // storer and publisher count their issued windows in stored_cnt (release, CTA
+    // the storer counts its issued windows in stored_cnt (release, CTA
     // scope; a counter, not an mbarrier: nothing gates them on this warp, so they can
     // run a whole ring ahead); the release here (gpu scope, cumulative over what this
     // warp acquired) publishes them to sweep B without stalling the storer on the drain
@@ -1145,7 +1148,7 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
       unsigned cnt = 0;
       while (true) {
         asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(cnt) : "r"(smem_u32(&S.stored_cnt)) : "memory");
-        if (cnt >= 2u * (unsigned)(w + 1)) break;
+        if (cnt >= (unsigned)(w + 1)) break;
         __nanosleep(64);  // shares a sub-partition with the publisher
       }
       __threadfence();
