@@ -99,17 +99,22 @@ __global__ void k_mr_givens(int len, const double* __restrict__ r2, const double
   }
 }
 
-// w_new = (v - oldeps w1 - delta w2)/gamma ; x_new = x + phi w_new  (linalg.py:223-229)
-__global__ void k_mr_update(int len, const double* __restrict__ v, const double* __restrict__ w1,
+// w_new = (v - oldeps w1 - delta w2)/gamma ; x_new = x + phi w_new  (linalg.py:223-229);
+// then the next iteration's v = y / beta in place (k_mr_scale's product: beta is
+// already the next one, linalg.py:193-194), saving that launch
+__global__ void k_mr_update(int len, double* __restrict__ v, const double* __restrict__ w1,
                             const double* __restrict__ w2, double* __restrict__ wn, const double* __restrict__ x,
-                            double* __restrict__ xn, MinresDev* st, double* partials, unsigned* counter) {
+                            double* __restrict__ xn, const double* __restrict__ ynext, MinresDev* st, double* partials,
+                            unsigned* counter) {
   pdl_enter();
   if (st->stopped) return;
   __shared__ double scratch[kThreads / 32];
   const double oldeps = st->oldeps, delta = st->delta, gamma = st->gamma, phi = st->phi;
+  const double s = 1.0 / st->beta;
   double acc[1] = {0.0};
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x) {
     const double w = __dsub_rn(__dsub_rn(v[i], __dmul_rn(oldeps, w1[i])), __dmul_rn(delta, w2[i])) / gamma;
+    v[i] = s * ynext[i];
     wn[i] = w;
     const double xv = __dadd_rn(x[i], __dmul_rn(phi, w));
     xn[i] = xv;
@@ -311,8 +316,10 @@ int minres(Ctx* c, const double* b_free, double* x_free, double tol, int max_ite
   double* x_in[2] = {nullptr, nullptr};
   double* x_out[2] = {nullptr, nullptr};
   auto enqueue = [&](int it) -> int {
-    VTS_CUDA(launch_pdl(k_mr_scale, dim3(grid), dim3(kThreads), 0, c->stream, len, y, v, c->mst));
-    VTS_LAUNCHED(c);
+    if (it == 0) {  // later iterations' v comes from the previous update
+      VTS_CUDA(launch_pdl(k_mr_scale, dim3(grid), dim3(kThreads), 0, c->stream, len, y, v, c->mst));
+      VTS_LAUNCHED(c);
+    }
     if (int rc = newton_apply_grid(c, v, y, stopped)) return rc;
     VTS_CUDA(launch_pdl(k_mr_lanczos, dim3(grid), dim3(kThreads), 0, c->stream, len, y, r1, v, c->mst, c->partials, c->counters + 8));
     VTS_LAUNCHED(c);
@@ -336,8 +343,8 @@ int minres(Ctx* c, const double* b_free, double* x_free, double tol, int max_ite
     double* w1 = w2;
     w2 = w;
     double* wn = wfree;
-    VTS_CUDA(launch_pdl(k_mr_update, dim3(grid), dim3(kThreads), 0, c->stream, len, v, w1, w2, wn, x, xalt, c->mst, c->partials,
-                                                  c->counters + 10));
+    VTS_CUDA(launch_pdl(k_mr_update, dim3(grid), dim3(kThreads), 0, c->stream, len, v, w1, w2, wn, x, xalt,
+                        (const double*)y, c->mst, c->partials, c->counters + 10));
     VTS_LAUNCHED(c);
     wfree = w1;
     w = wn;
