@@ -71,7 +71,14 @@ def test_vtk_rejects_bad_shapes(tmp_path):
     with pytest.raises(ValueError):
         vtkio.write_density_vtk(tmp_path / "x.vtk", (4, 4), 1.0, np.zeros(15))
     with pytest.raises(ValueError):
-        vtkio.write_density_vtk(tmp_path / "x.vtk", (4, 4, 2), 1.0, np.zeros(32))
+        vtkio.write_density_vtk(tmp_path / "x.vtk", (4, 4, 2), 1.0, np.zeros(31))
+    with pytest.raises(ValueError):
+        vtkio.write_density_vtk(tmp_path / "x.vtk", (4,), 1.0, np.zeros(4))
+    # a 3D element grid (the reference's own layout) round-trips
+    vtkio.write_density_vtk(tmp_path / "x3.vtk", (4, 4, 2), 0.5, np.arange(32.0))
+    assert "DIMENSIONS 5 5 3" in (tmp_path / "x3.vtk").read_text()
+    shape, spacing, values = vtkio.read_density_vtk(tmp_path / "x3.vtk")
+    assert shape == (4, 4, 2) and spacing == 0.5 and np.array_equal(values, np.arange(32.0))
     (tmp_path / "bad.vtk").write_text("# vtk\nnothing\n")
     with pytest.raises(ValueError):
         vtkio.read_density_vtk(tmp_path / "bad.vtk")
