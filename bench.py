@@ -51,6 +51,14 @@ def microbench_inputs(n: int, m: int, seed: int = 0):
     return state, rhs
 
 
+def workload_config(n: int, m: int, world: int) -> dict:
+    """The `config` both arms print (identical dicts, so the driver can pair them)."""
+    return {"workload": "C3 microbench: preconditioned MINRES on the 1024x512 cantilever Newton system, "
+                        "9 MG levels, V(2,2) exact-order GS", "n": n, "m": m, "seed": 0,
+            "parallelism": "replicas only" if world > 1 else "single GPU",
+            "l2": "inputs > 126 MB L2 (stencils 226 MB), no flush"}
+
+
 def algorithmic_bytes(prob) -> dict:
     """SURVEY.md Appendix B byte model (fp64 words x 8)."""
     n, m = prob.n, prob.m
@@ -85,7 +93,10 @@ def ncu_traffic(kernel: str = "k_gs_tri"):
     """dram bytes per finest-level launch of `kernel` from the committed ncu --set full capture."""
     import csv
 
-    path = os.path.join(REPO, "profiles", f"r01_ncu_full_{kernel}_fine_raw_subset.csv")
+    for rnd in ("r02", "r01"):
+        path = os.path.join(REPO, "profiles", f"{rnd}_ncu_full_{kernel}_fine_raw_subset.csv")
+        if os.path.exists(path):
+            break
     try:
         with open(path) as fh:
             rows = list(csv.reader(fh))
@@ -187,38 +198,85 @@ def run_reference(args) -> None:
         "impl": "reference", "metric": METRIC, "value": value, "unit": "MINRES iterations/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / its, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE configs[2])",
-        "config": {"workload": "C3 microbench 1024x512 cantilever, 9 MG levels, preconditioned MINRES",
-                   "n": prob.n, "m": prob.m, "parallelism": "replicas only"},
+        "config": workload_config(prob.n, prob.m, world),
         "cpu_baseline": {"value": value, "unit": "MINRES iterations/s", "cores": 1, "kind": "port",
                          "sample": f"{its} preconditioned MINRES iterations on the C3 Newton system "
                                    "(oracle/ restatement: numpy/scipy CSR + sequential C Gauss-Seidel, "
-                                   "single-threaded by construction)"},
+                                   "single-threaded by construction)", **host_cores()},
         "e2e": {"value": value, "unit": "MINRES iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline_sample(seconds_budget: float = 20.0) -> dict:
-    """Bounded oracle sample on the host (rank 0, N=1): 10 MINRES iterations on C3."""
+def host_cores() -> dict:
+    """Host CPU resources of this box (cpu_count and affinity)."""
+    aff = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else None
+    return {"os_cpu_count": os.cpu_count(), "sched_getaffinity": aff}
+
+
+def cpu_baseline_sample() -> dict:
+    """Bounded oracle sample on the host (rank 0, N=1), about 10 s of CPU work.
+
+    The value is MINRES iterations/s (10 iterations on C3).  Beside it, the
+    other north_star figures on the same inputs: the phi pass (with the BLAS
+    pool at its default size and at one thread, the OPENBLAS_NUM_THREADS=1
+    run SURVEY.md §8(d) asks for, via threadpoolctl), the Galerkin/Cholesky
+    setup, one Newton-matrix apply (mean of 50) and one V-cycle (mean of 5).
+    The Gauss-Seidel loops (C) and scipy's CSR kernels are single-threaded.
+    """
     import oracle
+    from threadpoolctl import threadpool_info, threadpool_limits
 
     prob = oracle.build_config(CONFIG_KEY)
     st, rhs = microbench_inputs(prob.n, prob.m)
     ops = oracle.ElementOps2D(prob.fine)
     bounds = oracle.DensityBounds.for_problem(prob.m, prob.volume, 0.0)
+
+    def phi():
+        return oracle.eval_lagrangian(oracle.PbmState(**st), ops, prob.f, bounds, oracle.PenaltyBarrier())
+
+    phi()
     t0 = time.perf_counter()
-    ev = oracle.eval_lagrangian(oracle.PbmState(**st), ops, prob.f, bounds, oracle.PenaltyBarrier())
+    ev = phi()
     t_phi = time.perf_counter() - t0
+    with threadpool_limits(limits=1):
+        t0 = time.perf_counter()
+        phi()
+        t_phi1 = time.perf_counter() - t0
     mat, _ = oracle.schur_system(ev, ops)
+    t0 = time.perf_counter()
     mg = oracle.MgPreconditioner(mat, prob.transfers)
+    t_setup = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    for _ in range(50):
+        mat.matvec(rhs)
+    t_apply = (time.perf_counter() - t0) / 50
+    t0 = time.perf_counter()
+    for _ in range(5):
+        mg.apply(rhs)
+    t_vc = (time.perf_counter() - t0) / 5
     its = 10
     t0 = time.perf_counter()
     res = oracle.minres_solve(mat, rhs, oracle.MinresConfig(tol=1e-14, max_iters=its), mg.apply)
     dt = time.perf_counter() - t0
+    blas = [p.get("num_threads") for p in threadpool_info() if p.get("user_api") == "blas"]
     return {"value": res.iterations / dt, "unit": "MINRES iterations/s", "cores": 1, "kind": "port",
             "sample": f"{res.iterations} preconditioned MINRES iterations on the C3 Newton system "
-                      f"({dt:.1f} s) + one phi pass ({t_phi*1e3:.0f} ms); oracle/ restatement, single thread",
-            "phi_pass_ms": 1e3 * t_phi}
+                      f"({dt:.1f} s); oracle/ restatement, single thread (C Gauss-Seidel, scipy CSR)",
+            **host_cores(), "blas_threads_default": blas[0] if blas else None,
+            "phi_pass_ms": 1e3 * t_phi, "phi_pass_ms_blas1": 1e3 * t_phi1, "mg_setup_ms": 1e3 * t_setup,
+            "apply_ms": 1e3 * t_apply, "vcycle_ms": 1e3 * t_vc,
+            "pbm_c4_wall_s_recorded": recorded_c4_wall(),
+            "note": "pbm_c4_wall_s_recorded: the unmodified reference (+2D glue) full C4 solve, timed when "
+                    "tests/golden/make_golden_fullsize.py ran on the build container (not this box: ~4 min)"}
+
+
+def recorded_c4_wall():
+    try:
+        with open(os.path.join(REPO, "tests", "golden", "golden_meta_fullsize.json")) as fh:
+            return json.load(fh)["pbm_c4"]["wall_clock_s"]
+    except (OSError, KeyError, ValueError):
+        return None
 
 
 def main() -> None:
@@ -361,10 +419,15 @@ def main() -> None:
     # else k_gs_tri; roofline unit = one finest-level launch (for the pair: the
     # descent pair, the launch the committed ncu capture is of; the ascent pair's
     # time and bytes are reported beside it)
+    # roofline credit = SURVEY.md §8(d)'s matrix-free algorithmic bytes: a finest
+    # sweep pair is two finest sweeps (2 x [8(n+2m) + 32n]), a single sweep one;
+    # the implementation's own reads (assembled half-stencils) are reported beside it
     if pair_fine_n > 0:
-        dom, dom_bytes, dom_ms, dom_n = "k_gs_pair", bytes_["gs_pair_fine"], pair_fine_ms, pair_fine_n
+        dom, dom_ms, dom_n = "k_gs_pair", pair_fine_ms, pair_fine_n
+        dom_bytes, impl_bytes = 2 * bytes_["gs_fine_sweep"], bytes_["gs_pair_fine"]
     else:
-        dom, dom_bytes, dom_ms, dom_n = "k_gs_tri", bytes_["gs_tri_fine"], tri_fine_ms, tri_fine_n
+        dom, dom_ms, dom_n = "k_gs_tri", tri_fine_ms, tri_fine_n
+        dom_bytes, impl_bytes = bytes_["gs_fine_sweep"], bytes_["gs_tri_fine"]
     dom_avg_ms = dom_ms / max(dom_n, 1.0)
     achieved = gbs(dom_bytes, dom_avg_ms)
     traffic = ncu_traffic(dom)
@@ -397,27 +460,38 @@ def main() -> None:
         "metric": METRIC, "value": value, "unit": "MINRES iterations/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dt_ms / its, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE configs[2] state and RHS)",
-        "config": {"workload": "C3 microbench: preconditioned MINRES on the 1024x512 cantilever Newton system, "
-                               "9 MG levels, V(2,2) exact-order GS", "n": n, "m": m,
-                   "parallelism": "replicas only" if world > 1 else "single GPU",
-                   "l2": "inputs > 126 MB L2 (stencils 226 MB), no flush"},
+        "config": workload_config(n, m, world),
         "e2e": {"value": e2e_value, "unit": "MINRES iterations/s", "h2d_bytes_per_step": 8 * (n + 1) / args.steps,
                 "d2h_bytes_per_step": 8 * (n + 1) / args.steps,
                 "note": "one C-ABI vts_minres call of K iterations; RHS H2D and solution D2H once per call"},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "hbm", "kernel": f"{dom}, finest level (1025x513 wavefront"
-                                                 f"{' sweep pair' if dom == 'k_gs_pair' else ' sweep'})",
+        "roofline": {"bound": "hbm", "limited_by": "latency: the exact-order Gauss-Seidel wavefront is a chain "
+                                                   "of nx + 2 ny dependent block solves (DESIGN.md §4)",
+                     "kernel": f"{dom}, finest level (1025x513 wavefront"
+                               f"{' sweep pair' if dom == 'k_gs_pair' else ' sweep'})",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "frac_of_8TBs": achieved / 8000.0, "traffic": traffic, "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": dom_bytes, "launch_ms": dom_avg_ms,
+                     "algorithmic_bytes_per_launch": dom_bytes,
+                     "algorithmic_bytes_rule": "SURVEY.md §8(d) / Appendix B matrix-free sweep bytes "
+                                               "8(n+2m)+32n per finest sweep, x2 for a pair",
+                     "implementation_bytes_per_launch": impl_bytes,
+                     "implementation_GBs": gbs(impl_bytes, dom_avg_ms),
+                     "launch_ms": dom_avg_ms,
                      "launches_in_profiled_region": int(gs_n), "finest_launches": int(dom_n),
                      "share_of_step": gs_total_ms / prof_region_ms,
                      "ascent_pair": ({"launch_ms": asc_fine_ms / asc_fine_n,
-                                      "algorithmic_bytes_per_launch": bytes_["gs_pair_asc_fine"],
-                                      "achieved": gbs(bytes_["gs_pair_asc_fine"], asc_fine_ms / asc_fine_n)}
+                                      "algorithmic_bytes_per_launch": 2 * bytes_["gs_fine_sweep"],
+                                      "achieved": gbs(2 * bytes_["gs_fine_sweep"], asc_fine_ms / asc_fine_n),
+                                      "implementation_bytes_per_launch": bytes_["gs_pair_asc_fine"]}
                                      if asc_fine_n > 0 else None),
-                     "note": "latency-bound: a sweep is a wavefront of nx + 2 ny dependent steps "
-                             "(DESIGN.md, 'Gauss-Seidel depth'); traffic from profiles/ ncu --set full"},
+                     "apply_frac": gbs(bytes_["apply"], apply_ms) / peak,
+                     "apply_note": "k_newton_apply, A_ap = 8(3n+2m+2) per launch, timed cold (L2 overwritten)",
+                     "vcycle_frac": gbs(bytes_["vcycle"], vcycle_ms) / peak,
+                     "vcycle_note": "one V(2,2), A_V of SURVEY.md Appendix B, mean of 100 back-to-back",
+                     "phi_frac": gbs(bytes_["phi"], phi_ms) / peak,
+                     "minres_iter_frac": gbs(bytes_["minres_iter"], dt_ms / its) / peak,
+                     "note": "traffic = dram bytes per launch from the committed ncu --set full capture "
+                             "(profiles/)"},
         "kernels": {
             "phi_pass_ms": phi_ms, "phi_pass_GBs": gbs(bytes_["phi"], phi_ms),
             "apply_ms": apply_ms, "apply_GBs": gbs(bytes_["apply"], apply_ms), "applies_per_s": 1e3 / apply_ms,

@@ -148,9 +148,13 @@ def test_full_pbm_matches_reference(name, args):
         # well-conditioned: the discrete trajectory is identical
         np.testing.assert_array_equal(counts, ref)
     else:
-        # 32x16 MBB needs ~140 MINRES iterations per late Newton step; rounding
-        # moves individual counts by a few (the reference's own FMA-perturbed
-        # run does the same), the total stays within 1 %
+        # 32x16 MBB needs ~140 MINRES iterations per late Newton step, where single
+        # per-Newton counts move under rounding: the unmodified reference with only
+        # its Gauss-Seidel products fused moves its own total by the amount recorded
+        # in tests/golden/fma_sensitivity.npz (tests/golden/fma_sensitivity.py); the
+        # GPU's total must stay within 1 % and the per-step counts within that spread
+        sens = load("fma_sensitivity")
+        assert not bool(sens["mbb32_same_counts"])  # the reference itself is count-sensitive here
         assert abs(int(counts.sum()) - int(ref.sum())) <= 0.01 * ref.sum()
 
 
@@ -158,20 +162,25 @@ def test_full_pbm_c2_mbb_matches_reference():
     """C2 (256x128 MBB, 6 levels).
 
     Counts, outer iterations and compliance match the reference exactly /
-    to 1e-13.  The thickness field is compared in the 2-norm at 1e-6: in the
-    max norm, single near-bound elements differ by ~2e-6, which is the
-    reference's OWN rounding sensitivity -- re-running the unmodified
-    reference with only its Gauss-Seidel products fused (FMA) moves the same
-    sample by 2.13e-6 with identical counts ("Parity").  The
-    max-norm bound is set at 5e-6 accordingly.
+    to 1e-13.  The thickness field: 2-norm within 1e-6 relative; in the max
+    norm the bound is the reference's OWN rounding sensitivity, measured and
+    committed: `tests/golden/fma_sensitivity.py` re-runs the unmodified
+    reference with only its Gauss-Seidel products fused (FMA, as on the GPU)
+    and records how far that moves the same 512-element sample
+    (`fma_sensitivity.npz`: 1.9e-6, identical counts).  The GPU may differ
+    from the stock reference by at most twice that perturbation.
     """
     fx = load("pbm_c2")
+    sens = load("fma_sensitivity")
     rep = vts.solve_pbm(vts.build_config("C2"))
     assert rep.converged
     assert abs(rep.outer_iterations - int(fx["outer"])) <= 1
     np.testing.assert_array_equal(np.array(rep.extras["minres_per_newton"]), fx["minres_per_newton"])
     assert rep.objective == pytest.approx(float(fx["objective"]), rel=1e-6)
+    np.testing.assert_array_equal(sens["c2_rho_sample_idx"], fx["rho_sample_idx"])
     rho = rep.rho[torch.as_tensor(fx["rho_sample_idx"], device="cuda")].cpu().numpy()
     ref = fx["rho_sample"]
     assert np.linalg.norm(rho - ref) <= 1e-6 * np.linalg.norm(ref)
-    assert np.abs(rho - ref).max() <= 5e-6 * np.abs(ref).max()
+    ref_own = float(sens["c2_max_abs_diff_vs_stock"])
+    assert 1e-7 < ref_own < 5e-6
+    assert np.abs(rho - ref).max() <= 2.0 * ref_own, (np.abs(rho - ref).max(), ref_own)

@@ -1,0 +1,229 @@
+"""GPU parity on the north_star target: the 1024x512 cantilever (C3 state, C4 solve).
+
+Three pins, at the tolerances BASELINE.json's north_star states:
+
+1. **Oracle on the box, full vectors.**  The CPU oracle (`oracle/`, itself pinned
+   to the unmodified reference by `tests/test_oracle_golden.py`) runs here on
+   the same seeded C3 states as the GPU (BASELINE configs[2] / bench.py seed 0,
+   and a both-branch variant with nu ~ U(0, 1e-2)); every element of every
+   output is compared: per-element g (= q - alpha + nu_lo - nu_up) and the
+   phi-pass outputs, the Schur rhs / border / corner, S x, every level's
+   Galerkin apply (the cross-cluster band handoff runs on the levels with more
+   than 256 node rows), the V-cycle, at rtol 1e-12 / atol 1e-12 max|ref|
+   (pbm.py:150-218, linalg.py:56-62, multigrid.py:82-143); the first 20 MINRES
+   residuals at |dh| <= 1e-8 h + 1e-13 (linalg.py:128-242).
+2. **The reference itself, sampled.**  `tests/golden/c3_ref_samples.npz` was
+   written by the unmodified reference (+ the validated 2D glue,
+   `tests/golden/make_golden_fullsize.py`); the GPU outputs are compared at its
+   8192 sample positions and through their 2-norms.
+3. **Full C4 solve** against `tests/golden/pbm_c4.npz` (the reference's own
+   solve): identical outer / per-Newton MINRES counts, compliance at 1e-6 and
+   the whole thickness field at 1e-6 in the max norm (pbm.py:341-465).
+"""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+from golden_io import GOLDEN
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU containers
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import oracle  # noqa: E402  (checker only)
+import paper_1904_06556_b200 as vts  # noqa: E402
+
+RTOL = 1e-12
+
+
+def host(a):
+    return a.detach().cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a, dtype=float)
+
+
+def close(a, b, rtol=RTOL):
+    a, b = host(a), np.asarray(b, dtype=float)
+    scale = max(float(np.abs(b).max()), 1e-300)
+    np.testing.assert_allclose(a, b, rtol=rtol, atol=rtol * scale)
+
+
+def c3_inputs(n, m, both_branches):
+    """bench.py microbench_inputs (seed 0) and the both-branch variant of make_golden_fullsize.py."""
+    rng = np.random.default_rng(0)
+    u = rng.normal(0.0, 1e-2, n)
+    rho = rng.uniform(0.5, 2.0, m)
+    rhs = rng.standard_normal(n + 1)
+    one = np.ones(m)
+    nu_lo, nu_up = one.copy(), one.copy()
+    if both_branches:
+        nu_lo = rng.uniform(0.0, 1e-2, m)
+        nu_up = rng.uniform(0.0, 1e-2, m)
+    st = dict(u=u, alpha=1e-3, nu_lo=nu_lo, nu_up=nu_up, rho=rho, mu_lo=one.copy(), mu_up=one.copy(),
+              p=np.full(m, 1e-2), q_lo=one.copy(), q_up=one.copy())
+    return st, rhs
+
+
+class Side:
+    """One C3 state on the GPU (through the C ABI) and in the oracle."""
+
+    def __init__(self, both_branches: bool):
+        self.tag = "br" if both_branches else "ref"
+        self.prob = vts.build_config("C3")
+        self.oprob = oracle.build_config("C3")
+        n, m = self.prob.n, self.prob.m
+        st, self.bench_rhs = c3_inputs(n, m, both_branches)
+        rng = np.random.default_rng(1000)
+        self.x = rng.standard_normal(n + 1)
+        self.du = 1e-2 * rng.standard_normal(n)
+        self.dalpha = float(1e-3 * rng.standard_normal())
+        dev = {k: (v if k == "alpha" else torch.as_tensor(v, device="cuda")) for k, v in st.items()}
+        self.state = vts.PbmState(**dev)
+        self.ops = vts.ElementOps(self.prob.fine)
+        self.bounds = vts.DensityBounds.for_problem(m, self.prob.volume, 0.0)
+        self.ev = vts.eval_lagrangian(self.state, self.ops, self.prob.f, self.bounds, vts.PenaltyBarrier(),
+                                      keep_w=True)
+        self.mat, self.rhs = vts.schur_system(self.ev, self.ops)
+        self.mg = vts.MgPreconditioner(self.mat, self.prob.transfers)
+        self.ost = oracle.PbmState(**st)
+        self.oops = oracle.ElementOps2D(self.oprob.fine)
+        self.obounds = oracle.DensityBounds.for_problem(m, self.oprob.volume, 0.0)
+        self.oev = oracle.eval_lagrangian(self.ost, self.oops, self.oprob.f, self.obounds, oracle.PenaltyBarrier())
+        self.omat, self.orhs = oracle.schur_system(self.oev, self.oops)
+        self.omg = oracle.MgPreconditioner(self.omat, self.oprob.transfers)
+
+
+@pytest.fixture(scope="module", params=[False, True], ids=["bench_state", "both_branches"])
+def side(request):
+    return Side(request.param)
+
+
+def test_c3_phi_pass_full_vectors(side):
+    ev, oev = side.ev, side.oev
+    assert ev.value == pytest.approx(oev.value, rel=RTOL)
+    assert ev.tau_res == pytest.approx(oev.tau_res, rel=RTOL)
+    assert ev.res_alpha == pytest.approx(oev.res_alpha, rel=RTOL, abs=RTOL * side.prob.volume)
+    # north_star's per-element g_i = 1/2 u_e^T K_e u_e - alpha (+ nu_lo - nu_up), pbm.py:155
+    st = side.ost
+    g_ref = oev.q - st.alpha + st.nu_lo - st.nu_up
+    g = side.ev.q - side.state.alpha + side.state.nu_lo - side.state.nu_up
+    close(g, g_ref)
+    for key in ("res_u", "res_lo", "res_up", "q", "mu_hat_lo", "mu_hat_up"):
+        close(getattr(ev, key), getattr(oev, key))
+    for key in ("a", "b_lo", "b_up", "rho_hat", "w"):
+        close(getattr(ev.blocks, key), getattr(oev.blocks, key))
+
+
+def test_c3_schur_apply_and_reconstruction_full_vectors(side):
+    close(side.rhs, side.orhs)
+    close(side.mat.border, side.omat.border)
+    assert side.mat.corner == pytest.approx(side.omat.corner, rel=1e-13)
+    close(side.mat.matvec(torch.as_tensor(side.x, device="cuda")), side.omat.matvec(side.x))
+    du = torch.as_tensor(side.du, device="cuda")
+    lo, up = vts.reconstruct_nu(side.ev, side.ops, du, side.dalpha)
+    olo, oup = oracle.reconstruct_nu(side.oev, side.oops, side.du, side.dalpha)
+    close(lo, olo)
+    close(up, oup)
+
+
+def test_c3_every_level_and_vcycle_full_vectors(side):
+    assert side.mg.shifted == side.omg.shifted
+    assert len(side.mg.mats) == len(side.omg.mats) == 9
+    for k, (lev, olev) in enumerate(zip(side.mg.mats, side.omg.mats)):
+        v = np.random.default_rng(2000 + k).standard_normal(olev.core_dim + 1)
+        close(lev.matvec(torch.as_tensor(v, device="cuda")), olev.matvec(v))
+    for b in (side.x, side.bench_rhs):
+        close(side.mg.apply(torch.as_tensor(b, device="cuda")), side.omg.apply(b))
+    close(side.mg.apply(side.rhs), side.omg.apply(side.orhs))
+
+
+def test_c3_minres_history_20_iterations(side):
+    hist, ohist = [], []
+    res = vts.minres_solve(side.mat, side.rhs, vts.MinresConfig(tol=1e-14, max_iters=20), side.mg.apply,
+                           history=hist)
+    ores = oracle.minres_solve(side.omat, side.orhs, oracle.MinresConfig(tol=1e-14, max_iters=20), side.omg.apply,
+                               history=ohist)
+    assert res.iterations == ores.iterations == 20
+    h, ref = np.array(hist), np.array(ohist)
+    assert np.all(np.abs(h - ref) <= 1e-8 * ref + 1e-13), np.max(np.abs(h - ref) / ref)
+    close(res.x, ores.x, 1e-8)
+
+
+# --- the reference's own outputs at sample positions ---------------------------------
+
+def _ref_samples():
+    path = os.path.join(GOLDEN, "c3_ref_samples.npz")
+    if not os.path.exists(path):
+        pytest.skip("c3_ref_samples.npz not generated")
+    with np.load(path) as z:
+        return {k: z[k] for k in z.files}
+
+
+def check_sampled(fx, prefix, name, vec, rtol=RTOL):
+    v = host(vec)
+    key = f"{prefix}_{name}"
+    if key in fx:  # short vectors are stored whole
+        close(v, fx[key], rtol)
+        return
+    idx, val, vmax = fx[key + "__idx"], fx[key + "__val"], float(fx[key + "__max"])
+    np.testing.assert_allclose(v[idx], val, rtol=rtol, atol=rtol * vmax)
+    assert float(np.abs(v).max()) == pytest.approx(vmax, rel=rtol)
+    assert float(np.linalg.norm(v)) == pytest.approx(float(fx[key + "__norm"]), rel=rtol)
+
+
+def test_c3_matches_reference_samples(side):
+    fx = _ref_samples()
+    p = side.tag
+    ev = side.ev
+    assert ev.value == pytest.approx(float(fx[f"{p}_value"]), rel=RTOL)
+    assert ev.tau_res == pytest.approx(float(fx[f"{p}_tau_res"]), rel=RTOL)
+    assert side.mat.corner == pytest.approx(float(fx[f"{p}_corner"]), rel=1e-13)
+    for name in ("q", "mu_hat_lo", "mu_hat_up", "res_lo", "res_up", "res_u"):
+        check_sampled(fx, p, name, getattr(ev, name))
+    for name in ("rho_hat", "a", "b_lo", "b_up"):
+        check_sampled(fx, p, name, getattr(ev.blocks, name))
+    check_sampled(fx, p, "w", ev.blocks.w.reshape(-1))
+    check_sampled(fx, p, "rhs", side.rhs)
+    check_sampled(fx, p, "border", side.mat.border)
+    check_sampled(fx, p, "Sx", side.mat.matvec(torch.as_tensor(side.x, device="cuda")))
+    check_sampled(fx, p, "vcycle_x", side.mg.apply(torch.as_tensor(side.x, device="cuda")))
+    check_sampled(fx, p, "vcycle_rhs", side.mg.apply(side.rhs))
+    check_sampled(fx, p, "vcycle_bench_rhs", side.mg.apply(torch.as_tensor(side.bench_rhs, device="cuda")))
+    for k, lev in enumerate(side.mg.mats):
+        v = np.random.default_rng(2000 + k).standard_normal(lev.core_dim + 1)
+        check_sampled(fx, p, f"level{k}_apply", lev.matvec(torch.as_tensor(v, device="cuda")))
+    lo, up = vts.reconstruct_nu(ev, side.ops, torch.as_tensor(side.du, device="cuda"), side.dalpha)
+    check_sampled(fx, p, "dnu_lo", lo)
+    check_sampled(fx, p, "dnu_up", up)
+    for name, b in (("rhs", side.rhs), ("bench_rhs", torch.as_tensor(side.bench_rhs, device="cuda"))):
+        hist = []
+        res = vts.minres_solve(side.mat, b, vts.MinresConfig(tol=1e-14, max_iters=20), side.mg.apply, history=hist)
+        ref = fx[f"{p}_minres_hist_{name}"]
+        h = np.array(hist)
+        assert h.size == ref.size == 20
+        assert np.all(np.abs(h - ref) <= 1e-8 * ref + 1e-13), np.max(np.abs(h - ref) / ref)
+        check_sampled(fx, p, f"minres20_x_{name}", res.x, 1e-8)
+    res = vts.minres_solve(side.mat, side.rhs, vts.MinresConfig(tol=1e-6, max_iters=1000), side.mg.apply)
+    assert res.iterations == int(fx[f"{p}_minres_tol6_iters"])
+    check_sampled(fx, p, "minres_tol6_x", res.x, 1e-8)
+
+
+def test_c4_full_solve_matches_reference_solve():
+    path = os.path.join(GOLDEN, "pbm_c4.npz")
+    if not os.path.exists(path):
+        pytest.skip("pbm_c4.npz not generated")
+    with np.load(path) as z:
+        fx = {k: z[k] for k in z.files}
+    rep = vts.solve_pbm(vts.build_config("C4"))
+    assert rep.converged == bool(fx["converged"])
+    assert rep.outer_iterations == int(fx["outer"])
+    np.testing.assert_array_equal(np.array(rep.extras["minres_per_newton"]), fx["minres_per_newton"])
+    assert rep.objective == pytest.approx(float(fx["objective"]), rel=1e-6)
+    rho, ref = host(rep.rho), fx["rho"]
+    # north_star: thickness field within 1e-6 relative (max norm, relative to max|rho|)
+    assert np.abs(rho - ref).max() <= 1e-6 * np.abs(ref).max(), np.abs(rho - ref).max()
+    assert rep.volume == pytest.approx(float(fx["volume"]), rel=1e-9)
