@@ -129,6 +129,41 @@ int vts_minres(vts_ctx* ctx, const double* b, double* x, double tol, int32_t max
                int32_t* converged, double* history);
 
 /*
+ * Diagnostic probe (no reference counterpart): one smoothing step of level
+ * `level` as the V-cycle runs it -- two lexicographic Gauss-Seidel sweeps
+ * (forward or backward, multigrid.py:35-64 via _smooth :145-154) on
+ * A_k x = b - border x_alpha, x_alpha = x[last]; `zero_first` takes the
+ * first forward sweep from x = 0 (the pre-smoothing start).  b, x: level-k
+ * bordered free vectors (x in/out).
+ */
+int vts_debug_smooth(vts_ctx* ctx, int32_t level, int32_t forward, int32_t zero_first, const double* b, double* x);
+
+/*
+ * vts_minres with a warm start: `x0` (device, n+1 entries, or n for a bound
+ * stiffness, may be NULL) is the initial iterate of minres_solve(..., x0=...)
+ * (linalg.py:144-154): r = b - A x0, and when ||r||/||b|| <= floor_tol x0 is
+ * returned with 0 iterations.  On errors x holds the last sound iterate (x0
+ * when none was taken).
+ */
+int vts_minres_warm(vts_ctx* ctx, const double* b, double* x, const double* x0, double tol, int32_t max_iters,
+                    double floor_tol, int32_t precondition, int32_t* iterations, double* relres,
+                    int32_t* converged, double* history);
+
+/*
+ * minres_solve for an arbitrary operator (linalg.py:118-242 with `a` a CSR
+ * matrix, ndarray or callable and `precond` any callable, _as_matvec
+ * linalg.py:118-125).  `op(user, in, out)` and `precond(user, in, out)` apply
+ * the operator / preconditioner to device vectors of `len` entries and return
+ * 0 (nonzero aborts with that code); `precond` may be NULL.  The callbacks are
+ * called with the context stream drained and must leave `out` complete.  The
+ * Lanczos / Givens recurrences are the device kernels of vts_minres.
+ */
+typedef int (*vts_apply_fn)(void* user, const double* in, double* out);
+int vts_minres_generic(vts_ctx* ctx, int64_t len, const double* b, double* x, const double* x0, double tol,
+                       int32_t max_iters, double floor_tol, vts_apply_fn op, vts_apply_fn precond, void* user,
+                       int32_t* iterations, double* relres, int32_t* converged, double* history);
+
+/*
  * Bound-multiplier back-substitution + directional derivative:
  * reconstruct_nu (pbm.py:221-232) and the slope (pbm.py:290-295).
  * HOST `slope` (may be NULL).
@@ -224,6 +259,45 @@ int vts_ip_reconstruct(vts_ctx* ctx, const double* u, const double* du, double d
 int vts_ip_step_bounds(vts_ctx* ctx, const double* rho, const double* drho, const double* nu_lo,
                        const double* dnu_lo, const double* nu_up, const double* dnu_up, const double* lower,
                        const double* upper, double* mins);
+
+/*
+ * DOC reuse (doc.py:111-208).
+ *
+ * vts_bind_stiffness: bind K(rho) = sum_e rho_e K_e (fem.py:211-219,
+ * `ElementOps.assemble_stiffness`) as the context's system.  vts_newton_apply,
+ * vts_mg_setup / vts_vcycle / vts_level_apply (multigrid.py:82-154 on an
+ * unbordered matrix) and vts_minres_warm then act on it with n-entry vectors.
+ * HOST `warn_flags` bit 1: some rho < 0 (the reference's RuntimeWarning).
+ */
+int vts_bind_stiffness(vts_ctx* ctx, const double* rho, uint32_t* warn_flags);
+/*
+ * ElementOps.element_products (fem.py:175-180) for a free-dof u: w (m x 8,
+ * element-local u_e K_e; may be NULL) and q_e = u_e . w_e / 2 (m).
+ */
+int vts_element_products(vts_ctx* ctx, const double* u, double* w, double* q);
+/*
+ * doc_update (doc.py:63-75): rho_new = clip(rho * z^exponent / alpha, lower,
+ * upper) with z = z_scale * z_in (z_scale 1 for the reference's z, 2 when
+ * `z` holds the energies q and z = 2 q, doc.py:149; both exact).
+ */
+int vts_doc_update(vts_ctx* ctx, const double* rho, const double* z, double z_scale, double alpha, double exponent,
+                   const double* lower, const double* upper, double* rho_new);
+/*
+ * bisect_volume (doc.py:78-108) over that update: one cooperative launch for
+ * the whole bisection; `rho_new` = the update at the last multiplier tried,
+ * HOST `alpha` its value, HOST `status` 0 ok, 1 the bracket is invalid
+ * (ValueError, doc.py:92-97), 2 not closed in `cap` steps (doc.py:107-108).
+ */
+int vts_doc_bisect(vts_ctx* ctx, const double* rho, const double* z, double z_scale, const double* lower,
+                   const double* upper, double volume, double exponent, double alpha_hi, double tol, int32_t cap,
+                   double* rho_new, double* alpha, int32_t* status);
+/*
+ * The per-iteration measures of solve_doc (doc.py:148-155): HOST out[5] =
+ * {max |rho_new - rho|, f.u, best_alpha_gap's gap, its alpha (model.py:69-98),
+ * sum(rho_new)}.
+ */
+int vts_doc_measure(vts_ctx* ctx, const double* rho_new, const double* rho, const double* q, const double* u,
+                    const double* f, const double* lower, const double* upper, double volume, double* out);
 
 /*
  * Benchmark helper (no reference counterpart): average device time in ms of

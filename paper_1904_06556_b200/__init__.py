@@ -9,7 +9,17 @@ C ABI of `include/vts_b200.h` (built in-tree as `_build/libvts_b200.so`).
 from .problem import CONFIGS, MeshLevel, Problem, StructuredTransfer, build_config, build_problem
 from .fem import DensityBounds, ElementOps, quad_stiffness
 from .penalty import PenaltyBarrier
-from .linalg import MinresConfig, MinresError, MinresResult, NewtonMatrix, StagnationTolerance, minres_solve
+from .linalg import (
+    ComplementarityTolerance,
+    FixedTolerance,
+    MinresConfig,
+    MinresError,
+    MinresResult,
+    NewtonMatrix,
+    StagnationTolerance,
+    StiffnessMatrix,
+    minres_solve,
+)
 from .multigrid import MgPreconditioner
 from .pbm import (
     HessianBlocks,
@@ -25,6 +35,7 @@ from .pbm import (
     schur_system,
     solve_pbm,
 )
+from .doc import DocConfig, bisect_volume, doc_update, solve_doc
 
 __version__ = "0.1.0"
 
@@ -43,6 +54,9 @@ __all__ = [
     "MinresError",
     "MinresResult",
     "NewtonMatrix",
+    "StiffnessMatrix",
+    "FixedTolerance",
+    "ComplementarityTolerance",
     "StagnationTolerance",
     "minres_solve",
     "MgPreconditioner",
@@ -58,4 +72,8 @@ __all__ = [
     "reconstruct_nu",
     "schur_system",
     "solve_pbm",
+    "DocConfig",
+    "doc_update",
+    "bisect_volume",
+    "solve_doc",
 ]

@@ -63,10 +63,21 @@ SIGNATURES = {
     "vts_ip_schur_system": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _D, _P, _P, _P, _PD]),
     "vts_ip_reconstruct": (ctypes.c_int, [_P, _P, _P, _D, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "vts_ip_step_bounds": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _PD]),
+    "vts_debug_smooth": (ctypes.c_int, [_P, _I32, _I32, _I32, _P, _P]),
+    "vts_minres_warm": (ctypes.c_int, [_P, _P, _P, _P, _D, _I32, _D, _I32, _PI32, _PD, _PI32, _PD]),
+    "vts_minres_generic": (ctypes.c_int, [_P, _I64, _P, _P, _P, _D, _I32, _D, _P, _P, _P, _PI32, _PD, _PI32, _PD]),
+    "vts_bind_stiffness": (ctypes.c_int, [_P, _P, _PU32]),
+    "vts_element_products": (ctypes.c_int, [_P, _P, _P, _P]),
+    "vts_doc_update": (ctypes.c_int, [_P, _P, _P, _D, _D, _D, _P, _P, _P]),
+    "vts_doc_bisect": (ctypes.c_int, [_P, _P, _P, _D, _P, _P, _D, _D, _D, _D, _I32, _P, _PD, _PI32]),
+    "vts_doc_measure": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _D, _PD]),
     "vts_kernel_launches": (ctypes.c_int64, [_P]),
     "vts_profile_begin": (ctypes.c_int, [_P]),
     "vts_profile_end": (ctypes.c_int, [_P, _PD]),
 }
+
+# int (*vts_apply_fn)(void* user, const double* in, double* out): device vectors
+APPLY_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
 
 _lib = None
 

@@ -70,6 +70,10 @@ struct Ctx {
   double* d_corner = nullptr;   // device copy of corner
   bool system_bound = false;
   bool border_flip = false;    // the bound system is E S+ E (an IP system, ip.inc.cu): flip x_alpha at the API edge
+  // the bound system is the plain stiffness K(rho) (fem.py:211-219, doc.inc.cu): held as
+  // [[K, 0], [0, 1]] so every bordered kernel runs unchanged; API vectors have n entries
+  // and the grid's border slot is zero on input (then stays exactly zero)
+  bool unbordered = false;
   bool mg_ready = false;
   int shifted = 0;
 
@@ -99,6 +103,10 @@ struct Ctx {
   MinresDev* mst = nullptr;     // device MINRES state
   MinresDev* hmst = nullptr;    // pinned host mirror, [2]: the two iterations in flight
   cudaEvent_t mr_ev[2] = {nullptr, nullptr};  // their state copies have landed
+
+  // DOC workspace (doc.inc.cu: sorted energies, scans, CUB scratch), allocated on first use
+  void* doc_ws = nullptr;
+  size_t doc_tmp_bytes = 0;
 
   long long launches = 0;
   std::vector<void*> allocs;  // the device arena holding every array of the context
@@ -237,18 +245,34 @@ int level_residual_grid(Ctx* c, int k, const double* x, const double* b, double*
 // ---- multigrid (mg.cu) ----
 int mg_setup(Ctx* c, double shift_scale);
 int vcycle_grid(Ctx* c, const double* b, double* z, const int* skip);
+int debug_smooth(Ctx* c, int k, bool forward, bool zero_first, const double* b_free, double* x_free);
 int profile_begin(Ctx* c);
 int profile_end(Ctx* c, double* out);
 
 // ---- MINRES (minres.cu) ----
 int minres(Ctx* c, const double* b_free, double* x_free, double tol, int max_iters,
            double floor_tol, int precondition, int* iters, double* relres, int* converged,
-           double* history);
+           double* history, const double* x0_free = nullptr);
 
 // ---- generic reductions (elem_kernels.cu) ----
 // dot of two grid vectors (free dofs only are nonzero) incl. the border slot
 // when `bordered`; result written to dst (device) ; deterministic.
 int dot_grid(Ctx* c, int level, const double* a, const double* b, bool bordered, double* dst,
              const int* skip);
+
+int minres_generic(Ctx* c, long long len, const double* b, double* x_out, const double* x0, double tol,
+                   int max_iters, double floor_tol, vts_apply_fn op, vts_apply_fn prec, void* user,
+                   int* iters_out, double* relres_out, int* conv_out, double* history);
+
+// ---- DOC reuse (doc.inc.cu) ----
+int bind_stiffness(Ctx* c, const double* rho, unsigned* warn);
+int element_energy(Ctx* c, const double* u, double* w, double* q);
+int doc_bisect(Ctx* c, const double* rho, const double* q, double zscale, const double* lower,
+               const double* upper, double volume, double exponent, double alpha_hi, double tol, int cap,
+               double* rho_new, double* alpha_out, int* status);
+int doc_update(Ctx* c, const double* rho, const double* z, double zscale, double alpha, double exponent,
+               const double* lower, const double* upper, double* rho_new);
+int doc_measure(Ctx* c, const double* rho_new, const double* rho, const double* q, const double* u,
+                const double* f, const double* lower, const double* upper, double volume, double* out5);
 
 }  // namespace vts

@@ -127,7 +127,8 @@ __global__ void k_free_to_grid(int ngrid, int nfree, const int32_t* __restrict__
     const int f = g2f[i];
     dst[i] = f >= 0 ? src[f] : 0.0;
   } else if (i == ngrid && bordered) {
-    dst[ngrid] = bordered < 0 ? -src[nfree] : src[nfree];  // -1: the bound system is E S+ E (ip.inc.cu)
+    // -1: the bound system is E S+ E (ip.inc.cu); 2: unbordered K (no slot in src)
+    dst[ngrid] = bordered == 2 ? 0.0 : (bordered < 0 ? -src[nfree] : src[nfree]);
   }
 }
 
@@ -136,7 +137,7 @@ __global__ void k_grid_to_free(int nfree, int ngrid, const int32_t* __restrict__
                                int bordered) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < nfree) dst[i] = src[f2g[i]];
-  else if (i == nfree && bordered) dst[nfree] = bordered < 0 ? -src[ngrid] : src[ngrid];
+  else if (i == nfree && bordered && bordered != 2) dst[nfree] = bordered < 0 ? -src[ngrid] : src[ngrid];
 }
 
 // trial displacement u + kappa du on the grid, with f . (u + kappa du)
@@ -556,6 +557,13 @@ __global__ void k_gap_finish(int nb, const double* __restrict__ pe, const double
 // ---------------------------------------------------------------------------
 // host wrappers
 // ---------------------------------------------------------------------------
+// border-slot mode of an API vector of the bound system (k_free_to_grid / k_grid_to_free)
+static int border_mode(const Ctx* c, bool bordered) {
+  if (!bordered) return 0;
+  if (c->unbordered) return 2;
+  return c->border_flip ? -1 : 1;
+}
+
 static int reduce_grid(long long work) {
   return (int)std::min<long long>(std::max<long long>(1, (work + kThreads - 1) / kThreads), kReduceGridCap);
 }
@@ -570,7 +578,7 @@ int free_to_grid(Ctx* c, int level, const double* src, double* dst, bool bordere
   const LevelBuf& L = c->lv[level];
   const int total = L.d.ngrid + 1;
   k_free_to_grid<<<div_up(total, kThreads), kThreads, 0, c->stream>>>(L.d.ngrid, L.d.nfree, L.grid2free,
-                                                                      src, dst, bordered ? (c->border_flip ? -1 : 1) : 0);
+                                                                      src, dst, border_mode(c, bordered));
   VTS_LAUNCHED(c);
   return 0;
 }
@@ -579,7 +587,7 @@ int grid_to_free(Ctx* c, int level, const double* src, double* dst, bool bordere
   const LevelBuf& L = c->lv[level];
   const int total = L.d.nfree + 1;
   k_grid_to_free<<<div_up(total, kThreads), kThreads, 0, c->stream>>>(L.d.nfree, L.d.ngrid, L.d.free2grid,
-                                                                      src, dst, bordered ? (c->border_flip ? -1 : 1) : 0);
+                                                                      src, dst, border_mode(c, bordered));
   VTS_LAUNCHED(c);
   return 0;
 }
@@ -648,6 +656,7 @@ int schur_system(Ctx* c, const double* u, const double* res_u, double res_alpha,
   if (corner) *corner = c->corner;
   c->system_bound = true;
   c->border_flip = false;
+  c->unbordered = false;
   c->mg_ready = false;
   return 0;
 }

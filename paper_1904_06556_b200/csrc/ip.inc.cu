@@ -316,6 +316,7 @@ int ip_schur_system(Ctx* c, const double* u, const double* rho, const double* nu
   if (corner) *corner = c->corner;
   c->system_bound = true;
   c->border_flip = true;
+  c->unbordered = false;
   c->mg_ready = false;
   return 0;
 }

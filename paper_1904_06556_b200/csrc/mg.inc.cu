@@ -151,10 +151,15 @@ __global__ void __launch_bounds__(128) k_fine_stencil(int nx, int ny, int ex, in
 // coarse operator P^T A P (unsymmetrised): block D of coarse node I
 // ---------------------------------------------------------------------------
 // One thread per (I, D), D = the 3x3 position of the coarse neighbour J = I + D.
-// Entry (r, c) of the block is sum_{fine i near I} sum_{fine j = i + b}
-// P(i, I)_r A(i, j)_{rc} P(j, J)_c, accumulated with one fma per (i, b) in the
-// order fine row, fine column, b; at most one parent of j is J, so each entry
-// sees exactly the chain a whole-node loop over (i, b, parents of j) gives it.
+// Entry (r, c) of the block is sum_{fine i near I} P(i, I)_r (AP)(i, J)_{rc},
+// (AP)(i, J)_{rc} = sum_{fine j = i + b} A(i, j)_{rc} P(j, J)_c, summed in the
+// order of the reference's `p.T @ (core @ p)` (linalg.py:78, scipy's
+// csr_matmat): the inner sum over j in increasing (CSR column) order and
+// rounded, then the outer sum over i in increasing order.  The weights are
+// powers of two, so every product is exact and only the sums round -- in the
+// same order as the reference's.  (A single fused sum over (i, j) moved the
+// 9-level V-cycle by ~3e-12; the reference itself moves by ~1e-12 when only
+// its inner sums are reordered: tests/golden/vcycle_sensitivity.py.)
 // A block is 9 warps over the same 32 coarse nodes, warp w computing D = w, so
 // D is warp-uniform and, per D, the (i, b) pairs that can reach J and both
 // prolongation weights are compile-time: only grid edges and Dirichlet masks
@@ -174,6 +179,7 @@ VTS_DEVICE_INLINE void rap_block(int fnx, int fny, const double* __restrict__ fL
       const double wI = (ox == 0 ? 1.0 : 0.5) * (oy == 0 ? 1.0 : 0.5);
       const double pr0 = (ff.x && fI.x) ? wI : 0.0, pr1 = (ff.y && fI.y) ? wI : 0.0;
       const bool use_i = vi && !(pr0 == 0.0 && pr1 == 0.0);
+      double t[4] = {0.0, 0.0, 0.0, 0.0};  // (AP)(i, J), rows r = 0, 1 x columns c = 0, 1
 #pragma unroll
       for (int b = 0; b < 9; ++b) {
         const int bx = b % 3 - 1, by = b / 3 - 1;
@@ -190,11 +196,15 @@ VTS_DEVICE_INLINE void rap_block(int fnx, int fny, const double* __restrict__ fL
         // an invalid pair adds an exact zero (finite operands, zero weight),
         // which keeps the loop branch-free so every load can issue up front
         const double pc0 = (v && fj.x && fJ.x) ? wJ : 0.0, pc1 = (v && fj.y && fJ.y) ? wJ : 0.0;
-        acc[0] = fma(pr0 * a00, pc0, acc[0]);
-        acc[1] = fma(pr0 * a01, pc1, acc[1]);
-        acc[2] = fma(pr1 * a10, pc0, acc[2]);
-        acc[3] = fma(pr1 * a11, pc1, acc[3]);
+        t[0] = fma(a00, pc0, t[0]);
+        t[1] = fma(a01, pc1, t[1]);
+        t[2] = fma(a10, pc0, t[2]);
+        t[3] = fma(a11, pc1, t[3]);
       }
+      acc[0] = fma(pr0, t[0], acc[0]);
+      acc[1] = fma(pr0, t[1], acc[1]);
+      acc[2] = fma(pr1, t[2], acc[2]);
+      acc[3] = fma(pr1, t[3], acc[3]);
     }
   }
 }
@@ -2002,6 +2012,23 @@ static int sm_count() {
 }
 // pair CTAs of level k (one per SM)
 static int pair_ctas(const Ctx* c, int k) { return 2 * div_up(c->lv[k].d.ny, gs::R); }
+
+// One smoothing step of level k exactly as the V-cycle runs it (two sweeps, the
+// border term b - border x_alpha with x_alpha from x's last entry): the probe
+// behind vts_debug_smooth (parity diagnostics of multigrid.py:145-154).
+int debug_smooth(Ctx* c, int k, bool forward, bool zero_first, const double* b_free, double* x_free) {
+  if (!c->mg_ready || k < 1 || k >= c->L) {
+    set_error(4, "debug_smooth: bad level or multigrid not set up");
+    return 4;
+  }
+  LevelBuf& L = c->lv[k];
+  if (int rc = free_to_grid(c, k, b_free, L.b, true)) return rc;
+  if (int rc = free_to_grid(c, k, x_free, L.x, true)) return rc;
+  if (int rc = gs_two_sweeps(c, k, L.b, L.x, forward, zero_first, nullptr)) return rc;
+  if (int rc = grid_to_free(c, k, L.x, x_free, true)) return rc;
+  VTS_CUDA(cudaStreamSynchronize(c->stream));
+  return 0;
+}
 
 int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
   const int top = c->L - 1;

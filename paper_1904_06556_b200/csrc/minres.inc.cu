@@ -217,9 +217,23 @@ __global__ void k_resnorm(int len, const double* __restrict__ b, const double* _
   if (last_block_reduce<1>(acc, scratch, partials, counter, tot) && threadIdx.x == 0) *out = tot[0];
 }
 
+// r = b - ax and ||r||^2 (the warm start's initial residual, linalg.py:150-152)
+__global__ void k_sub_norm(int len, const double* __restrict__ b, const double* __restrict__ ax,
+                           double* __restrict__ r, double* out, double* partials, unsigned* counter) {
+  __shared__ double scratch[kThreads / 32];
+  double acc[1] = {0.0};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x) {
+    const double ri = b[i] - ax[i];
+    r[i] = ri;
+    acc[0] = fma(ri, ri, acc[0]);
+  }
+  double tot[1];
+  if (last_block_reduce<1>(acc, scratch, partials, counter, tot) && threadIdx.x == 0) *out = tot[0];
+}
+
 int minres(Ctx* c, const double* b_free, double* x_free, double tol, int max_iters, double floor_tol,
-           int precondition, int* iters_out, double* relres_out, int* conv_out, double* history) {
-  (void)floor_tol;  // only used with a warm start, which this entry point does not take
+           int precondition, int* iters_out, double* relres_out, int* conv_out, double* history,
+           const double* x0_free) {
   if (!c->system_bound || (precondition && !c->mg_ready)) {
     set_error(4, "minres: bind the Newton system (and set up the multigrid) first");
     return 4;
@@ -239,18 +253,40 @@ int minres(Ctx* c, const double* b_free, double* x_free, double tol, int max_ite
   VTS_CUDA(cudaStreamSynchronize(c->stream));
   const double bnorm = sqrt(c->hscal[30]);
   const int n = c->n;
-  const int cap = max_iters > 0 ? max_iters : 3 * (n + 1);
+  const int napi = c->unbordered ? n : n + 1;  // entries of the caller's vectors
+  const int cap = max_iters > 0 ? max_iters : 3 * napi;
   if (bnorm == 0.0) {
-    VTS_CUDA(cudaMemsetAsync(x_free, 0, sizeof(double) * (n + 1), c->stream));
+    VTS_CUDA(cudaMemsetAsync(x_free, 0, sizeof(double) * napi, c->stream));
+    VTS_CUDA(cudaStreamSynchronize(c->stream));
     *iters_out = 0;
     *relres_out = 0.0;
     *conv_out = 1;
     return 0;
   }
-  // r1 = b (copy), y = M r1
+  // x = x0 or 0; r1 = b - A x0 or b (linalg.py:144-152); y = M r1
   double* r1 = pool[0];
   double* y = pool[1];
-  VTS_CUDA(cudaMemcpyAsync(r1, B, sizeof(double) * len, cudaMemcpyDeviceToDevice, c->stream));
+  double rel0 = 1.0;  // ||b - A x|| / ||b|| at the start
+  if (x0_free) {
+    if (int rc = free_to_grid(c, F, x0_free, X[0], true)) return rc;
+    if (int rc = newton_apply_grid(c, X[0], T, nullptr)) return rc;
+    k_sub_norm<<<grid, kThreads, 0, c->stream>>>(len, B, T, r1, c->dscal + 31, c->partials, c->counters + 7);
+    VTS_LAUNCHED(c);
+    VTS_CUDA(cudaMemcpyAsync(c->hscal + 31, c->dscal + 31, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    VTS_CUDA(cudaStreamSynchronize(c->stream));
+    rel0 = sqrt(c->hscal[31]) / bnorm;
+    if (rel0 <= floor_tol) {  // the warm start already meets the floor (linalg.py:153-154)
+      if (int rc = grid_to_free(c, F, X[0], x_free, true)) return rc;
+      VTS_CUDA(cudaStreamSynchronize(c->stream));
+      *iters_out = 0;
+      *relres_out = rel0;
+      *conv_out = 1;
+      return 0;
+    }
+  } else {
+    VTS_CUDA(cudaMemcpyAsync(r1, B, sizeof(double) * len, cudaMemcpyDeviceToDevice, c->stream));
+    VTS_CUDA(cudaMemsetAsync(X[0], 0, sizeof(double) * len, c->stream));
+  }
   if (precondition) {
     if (int rc = vcycle_grid(c, r1, y, nullptr)) return rc;
   } else {
@@ -264,16 +300,17 @@ int minres(Ctx* c, const double* b_free, double* x_free, double tol, int max_ite
     VTS_CUDA(cudaStreamSynchronize(c->stream));
   }
   double beta1 = c->hscal[31];
-  VTS_CUDA(cudaMemsetAsync(X[0], 0, sizeof(double) * len, c->stream));
+  if (beta1 < 0.0 || beta1 == 0.0) {  // the start iterate is the answer (or the last sound one)
+    if (int rc = grid_to_free(c, F, X[0], x_free, true)) return rc;
+    VTS_CUDA(cudaStreamSynchronize(c->stream));
+  }
   if (beta1 < 0.0) {
-    VTS_CUDA(cudaMemsetAsync(x_free, 0, sizeof(double) * (n + 1), c->stream));
     set_error(1, "preconditioner is indefinite: <M r, r> < 0");
     return 1;
   }
   if (beta1 == 0.0) {
-    VTS_CUDA(cudaMemsetAsync(x_free, 0, sizeof(double) * (n + 1), c->stream));
     *iters_out = 0;
-    *relres_out = 1.0;  // ||b - A 0|| / ||b||
+    *relres_out = rel0;  // ||b - A x|| / ||b||
     *conv_out = 1;
     return 0;
   }
@@ -423,6 +460,229 @@ int minres(Ctx* c, const double* b_free, double* x_free, double tol, int max_ite
     relres = sqrt(c->hscal[31]) / bnorm;
   }
   if (int rc = grid_to_free(c, F, x, x_free, true)) return rc;
+  *iters_out = s.iters;
+  *relres_out = relres;
+  *conv_out = (status == kConverged) || (status == kCap && relres <= tol);
+  if (status == kIndefinite) {
+    set_error(1, "preconditioner is indefinite: <M r, r> < 0");
+    return 1;
+  }
+  if (status == kBreakdown) {
+    set_error(2, "MINRES recurrence broke down");
+    return 2;
+  }
+  if (status == kNonfinite) {
+    set_error(3, "NaN/inf encountered in MINRES recurrences");
+    return 3;
+  }
+  return 0;
+}
+
+}  // namespace vts
+
+namespace vts {
+
+// ---------------------------------------------------------------------------
+// minres_solve for an arbitrary operator / preconditioner (linalg.py:118-242):
+// `a` and `precond` are host callbacks that apply the operator to a device
+// vector (a CSR matrix, a dense matrix or a user callable on the reference's
+// side, _as_matvec linalg.py:118-125).  The recurrences are the same device
+// kernels as the bound-system solver, on plain vectors of length `len`; every
+// callback runs with the context stream drained and must leave its output
+// complete on return.  One state read-back per iteration (no look-ahead: the
+// callbacks synchronise anyway).
+// ---------------------------------------------------------------------------
+int minres_generic(Ctx* c, long long len_ll, const double* b, double* x_out, const double* x0, double tol,
+                   int max_iters, double floor_tol, vts_apply_fn op, vts_apply_fn prec, void* user,
+                   int* iters_out, double* relres_out, int* conv_out, double* history) {
+  if (!op || len_ll < 1 || len_ll > INT32_MAX) {
+    set_error(4, "minres: bad operator or length");
+    return 4;
+  }
+  const int len = (int)len_ll;
+  const int grid = (int)std::min<long long>(div_up(len, kThreads), kReduceGridCap);
+  double* base = nullptr;
+  constexpr int kVecs = 12;
+  VTS_CUDA(cudaMalloc(&base, sizeof(double) * (size_t)len * kVecs + sizeof(MinresDev) + 256));
+  struct Guard {
+    double* p;
+    ~Guard() { cudaFree(p); }
+  } guard{base};
+  double* vec[kVecs];
+  for (int i = 0; i < kVecs; ++i) vec[i] = base + (size_t)i * len;
+  MinresDev* st = reinterpret_cast<MinresDev*>(base + (size_t)kVecs * len);
+  double* r1 = vec[0];
+  double* r2 = vec[1];
+  double* y = vec[2];
+  double* v = vec[3];
+  double* w1 = vec[4];
+  double* w2 = vec[5];
+  double* wn = vec[6];
+  double* x = vec[7];
+  double* xn = vec[8];
+  double* T = vec[9];
+  double* spare = vec[10];
+  auto call = [&](vts_apply_fn fn, const double* in, double* out) -> int {
+    VTS_CUDA(cudaStreamSynchronize(c->stream));
+    if (int rc = fn(user, in, out)) {
+      set_error(4, "minres: operator callback failed");
+      return rc;
+    }
+    VTS_CUDA(cudaDeviceSynchronize());
+    return 0;
+  };
+  auto scalar = [&](const double* dptr) -> double {
+    double h = 0.0;
+    cudaMemcpyAsync(&h, dptr, sizeof(double), cudaMemcpyDeviceToHost, c->stream);
+    cudaStreamSynchronize(c->stream);
+    return h;
+  };
+  auto finish_x = [&](const double* src) -> int {
+    VTS_CUDA(cudaMemcpyAsync(x_out, src, sizeof(double) * len, cudaMemcpyDeviceToDevice, c->stream));
+    VTS_CUDA(cudaStreamSynchronize(c->stream));
+    return 0;
+  };
+  k_norm2<<<grid, kThreads, 0, c->stream>>>(len, b, c->dscal + 30, c->partials, c->counters + 7);
+  VTS_LAUNCHED(c);
+  const double bnorm = sqrt(scalar(c->dscal + 30));
+  const int cap = max_iters > 0 ? max_iters : 3 * len;
+  *iters_out = 0;
+  if (bnorm == 0.0) {
+    VTS_CUDA(cudaMemsetAsync(x_out, 0, sizeof(double) * len, c->stream));
+    VTS_CUDA(cudaStreamSynchronize(c->stream));
+    *relres_out = 0.0;
+    *conv_out = 1;
+    return 0;
+  }
+  double rel0 = 1.0;
+  if (x0) {
+    VTS_CUDA(cudaMemcpyAsync(x, x0, sizeof(double) * len, cudaMemcpyDeviceToDevice, c->stream));
+    if (int rc = call(op, x, T)) return rc;
+    k_sub_norm<<<grid, kThreads, 0, c->stream>>>(len, b, T, r1, c->dscal + 31, c->partials, c->counters + 7);
+    VTS_LAUNCHED(c);
+    rel0 = sqrt(scalar(c->dscal + 31)) / bnorm;
+    if (rel0 <= floor_tol) {
+      *relres_out = rel0;
+      *conv_out = 1;
+      return finish_x(x);
+    }
+  } else {
+    VTS_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * len, c->stream));
+    VTS_CUDA(cudaMemcpyAsync(r1, b, sizeof(double) * len, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  if (prec) {
+    if (int rc = call(prec, r1, y)) return rc;
+  } else {
+    VTS_CUDA(cudaMemcpyAsync(y, r1, sizeof(double) * len, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  k_dot<<<grid, kThreads, 0, c->stream>>>(len, r1, y, c->partials, c->counters + 0, c->dscal + 31, nullptr);
+  VTS_LAUNCHED(c);
+  double beta1 = scalar(c->dscal + 31);
+  if (beta1 < 0.0 || beta1 == 0.0) {
+    if (int rc = finish_x(x)) return rc;
+  }
+  if (beta1 < 0.0) {
+    set_error(1, "preconditioner is indefinite: <M r, r> < 0");
+    return 1;
+  }
+  if (beta1 == 0.0) {
+    *relres_out = rel0;
+    *conv_out = 1;
+    return 0;
+  }
+  beta1 = sqrt(beta1);
+  MinresDev h{};
+  h.beta1 = beta1;
+  h.beta = beta1;
+  h.phibar = beta1;
+  h.cs = -1.0;
+  h.verify_at = tol;
+  h.relres = INFINITY;
+  h.tol = tol;
+  h.bnorm = bnorm;
+  h.max_iters = cap;
+  h.status = kRunning;
+  h.no_verify = 1;
+  VTS_CUDA(cudaMemcpyAsync(st, &h, sizeof(MinresDev), cudaMemcpyHostToDevice, c->stream));
+  VTS_CUDA(cudaMemsetAsync(w1, 0, sizeof(double) * len, c->stream));
+  VTS_CUDA(cudaMemsetAsync(w2, 0, sizeof(double) * len, c->stream));
+  VTS_CUDA(cudaStreamSynchronize(c->stream));
+  // r2 aliases r1 at the start (linalg.py:189); buffers rotate like minres()
+  r2 = r1;
+  double* freeb[3] = {vec[1], spare, vec[11]};
+  int nfree = 3;
+  double* w = w2;     // current w (zero)
+  double* wcur2 = w1; // current w2 (zero)
+  double* wfree = wn;
+  double* x_sound = x;
+  MinresDev s{};
+  int status = kRunning;
+  for (int it = 0; it < cap; ++it) {
+    if (it == 0) {  // later iterations' v comes from the previous update (k_mr_update)
+      k_mr_scale<<<grid, kThreads, 0, c->stream>>>(len, y, v, st);
+      VTS_LAUNCHED(c);
+    }
+    if (int rc = call(op, v, y)) return rc;
+    k_mr_lanczos<<<grid, kThreads, 0, c->stream>>>(len, y, r1, v, st, c->partials, c->counters + 8);
+    VTS_LAUNCHED(c);
+    k_mr_axpy2<<<grid, kThreads, 0, c->stream>>>(len, y, r2, st);
+    VTS_LAUNCHED(c);
+    double* dead = (r1 == r2) ? nullptr : r1;
+    r1 = r2;
+    r2 = y;
+    if (dead) freeb[nfree++] = dead;
+    y = freeb[--nfree];
+    if (prec) {
+      if (int rc = call(prec, r2, y)) return rc;
+    } else {
+      VTS_CUDA(cudaMemcpyAsync(y, r2, sizeof(double) * len, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    k_mr_givens<<<grid, kThreads, 0, c->stream>>>(len, r2, y, st, c->partials, c->counters + 9);
+    VTS_LAUNCHED(c);
+    double* wold1 = wcur2;
+    wcur2 = w;
+    // k_mr_update also writes the next iteration's v = y / beta
+    k_mr_update<<<grid, kThreads, 0, c->stream>>>(len, v, wold1, wcur2, wfree, x, xn, (const double*)y, st,
+                                                 c->partials, c->counters + 10);
+    VTS_LAUNCHED(c);
+    w = wfree;
+    wfree = wold1;
+    VTS_CUDA(cudaMemcpyAsync(&s, st, sizeof(MinresDev), cudaMemcpyDeviceToHost, c->stream));
+    VTS_CUDA(cudaStreamSynchronize(c->stream));
+    if (s.status == kIndefinite || s.status == kBreakdown || s.status == kNonfinite) {
+      status = s.status;
+      break;
+    }
+    std::swap(x, xn);
+    x_sound = x;
+    if (history || !s.no_verify) {
+      if (int rc = call(op, x, T)) return rc;
+    }
+    if (history) {
+      k_mr_history<<<grid, kThreads, 0, c->stream>>>(len, b, T, st, c->dscal + 32, c->partials, c->counters + 11);
+      VTS_LAUNCHED(c);
+      history[s.iters - 1] = scalar(c->dscal + 32);
+    }
+    if (!s.no_verify) {
+      k_mr_verify<<<grid, kThreads, 0, c->stream>>>(len, b, T, st, c->partials, c->counters + 12);
+      VTS_LAUNCHED(c);
+      VTS_CUDA(cudaMemcpyAsync(&s, st, sizeof(MinresDev), cudaMemcpyDeviceToHost, c->stream));
+      VTS_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    if (s.stopped) {
+      status = s.status;
+      break;
+    }
+  }
+  if (status == kRunning) status = kCap;
+  double relres = s.relres;
+  if (status == kCap) {
+    if (int rc = call(op, x_sound, T)) return rc;
+    k_resnorm<<<grid, kThreads, 0, c->stream>>>(len, b, T, c->dscal + 31, c->partials, c->counters + 7);
+    VTS_LAUNCHED(c);
+    relres = sqrt(scalar(c->dscal + 31)) / bnorm;
+  }
+  if (int rc = finish_x(x_sound)) return rc;
   *iters_out = s.iters;
   *relres_out = relres;
   *conv_out = (status == kConverged) || (status == kCap && relres <= tol);

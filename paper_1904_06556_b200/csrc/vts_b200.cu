@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <type_traits>
@@ -26,6 +27,7 @@
 #include "mg.inc.cu"
 #include "minres.inc.cu"
 #include "ip.inc.cu"
+#include "doc.inc.cu"
 
 namespace vts {
 
@@ -43,13 +45,42 @@ int cuda_check(cudaError_t e, const char* what) {
   return VTS_E_CUDA;
 }
 
-// the element stiffness is a module-wide constant; contexts with different K_e
-// re-upload it (stream-ordered) before their kernels run
+// The element stiffness is a module-wide __constant__ (uniform operands in every
+// element kernel).  Contexts whose K_e equals the loaded one share it with no
+// ordering at all.  A context with a different K_e takes the constant over in
+// stream order: its stream first waits for everything enqueued so far on every
+// stream that used the loaded constant (one event per stream), then uploads.
+// Calls of a context with the old K_e hand it back the same way, so no kernel
+// ever reads a constant that is not its context's, whatever streams they use.
+static double g_ke_loaded[64 + 8];
+static bool g_ke_valid = false;
+static std::vector<cudaStream_t> g_ke_users;  // streams that used the loaded constant
+static std::map<cudaStream_t, int> g_stream_refs;  // live contexts per stream
+static cudaEvent_t g_ke_event = nullptr;
+
 static int ensure_ke(Ctx* c) {
   std::lock_guard<std::mutex> lock(g_ke_mutex);
   if (g_ke_owner == c) return 0;
+  double want[64 + 8];
+  std::memcpy(want, c->ke, sizeof(double) * 64);
+  std::memcpy(want + 64, c->modal, sizeof(double) * 8);
+  if (g_ke_valid && std::memcmp(want, g_ke_loaded, sizeof(want)) == 0) {
+    if (std::find(g_ke_users.begin(), g_ke_users.end(), c->stream) == g_ke_users.end())
+      g_ke_users.push_back(c->stream);
+    g_ke_owner = c;
+    return 0;
+  }
+  if (!g_ke_event) VTS_CUDA(cudaEventCreateWithFlags(&g_ke_event, cudaEventDisableTiming));
+  for (cudaStream_t s : g_ke_users) {
+    if (s == c->stream) continue;
+    VTS_CUDA(cudaEventRecord(g_ke_event, s));
+    VTS_CUDA(cudaStreamWaitEvent(c->stream, g_ke_event, 0));
+  }
   VTS_CUDA(cudaMemcpyToSymbolAsync(c_ke, c->ke, sizeof(double) * 64, 0, cudaMemcpyHostToDevice, c->stream));
   VTS_CUDA(cudaMemcpyToSymbolAsync(c_modal, c->modal, sizeof(double) * 8, 0, cudaMemcpyHostToDevice, c->stream));
+  std::memcpy(g_ke_loaded, want, sizeof(want));
+  g_ke_valid = true;
+  g_ke_users.assign(1, c->stream);
   g_ke_owner = c;
   return 0;
 }
@@ -172,9 +203,17 @@ static void free_ctx(Ctx* c) {
     cudaEventDestroy(e.b);
   }
   if (c->hscal) pinned_release(c->hscal);
+  if (c->doc_ws) cudaFree(c->doc_ws);
   {
+    // after the synchronisation above nothing of this context is in flight; its
+    // stream may be destroyed by its owner, so it leaves the user list unless a
+    // live context still runs on it
     std::lock_guard<std::mutex> lock(g_ke_mutex);
     if (g_ke_owner == c) g_ke_owner = nullptr;
+    if (--g_stream_refs[c->stream] == 0) {
+      g_stream_refs.erase(c->stream);
+      g_ke_users.erase(std::remove(g_ke_users.begin(), g_ke_users.end(), c->stream), g_ke_users.end());
+    }
   }
   delete c;
 }
@@ -237,6 +276,10 @@ static int create(Ctx** out, int levels, const int32_t* ex, const int32_t* ey, c
   Ctx* c = new Ctx();
   c->L = levels;
   c->stream = reinterpret_cast<cudaStream_t>(stream);
+  {
+    std::lock_guard<std::mutex> lock(g_ke_mutex);
+    ++g_stream_refs[c->stream];
+  }
   std::memcpy(c->ke, ke, sizeof(double) * 64);
   modal_form(c);
   c->lv.resize(levels);
@@ -508,6 +551,103 @@ int vts_minres(vts_ctx* ctx, const double* b, double* x, double tol, int32_t max
   if (relres) *relres = rr;
   if (converged) *converged = conv;
   return rc;
+}
+
+int vts_debug_smooth(vts_ctx* ctx, int32_t level, int32_t forward, int32_t zero_first, const double* b,
+                     double* x) {
+  VTS_REQUIRE_CTX(ctx);
+  return vts::debug_smooth(C(ctx), level, forward != 0, zero_first != 0, b, x);
+}
+
+int vts_minres_warm(vts_ctx* ctx, const double* b, double* x, const double* x0, double tol, int32_t max_iters,
+                    double floor_tol, int32_t precondition, int32_t* iterations, double* relres, int32_t* converged,
+                    double* history) {
+  VTS_REQUIRE_CTX(ctx);
+  int it = 0, conv = 0;
+  double rr = 0.0;
+  const int rc = vts::minres(C(ctx), b, x, tol, max_iters, floor_tol, precondition, &it, &rr, &conv, history, x0);
+  if (iterations) *iterations = it;
+  if (relres) *relres = rr;
+  if (converged) *converged = conv;
+  return rc;
+}
+
+int vts_minres_generic(vts_ctx* ctx, int64_t len, const double* b, double* x, const double* x0, double tol,
+                       int32_t max_iters, double floor_tol, vts_apply_fn op, vts_apply_fn precond, void* user,
+                       int32_t* iterations, double* relres, int32_t* converged, double* history) {
+  VTS_REQUIRE_CTX(ctx);
+  if (!b || !x) {
+    vts::set_error(VTS_E_ARGUMENT, "vts_minres_generic: NULL vector");
+    return VTS_E_ARGUMENT;
+  }
+  int it = 0, conv = 0;
+  double rr = 0.0;
+  const int rc = vts::minres_generic(C(ctx), len, b, x, x0, tol, max_iters, floor_tol, op, precond, user, &it, &rr,
+                                     &conv, history);
+  if (iterations) *iterations = it;
+  if (relres) *relres = rr;
+  if (converged) *converged = conv;
+  return rc;
+}
+
+int vts_bind_stiffness(vts_ctx* ctx, const double* rho, uint32_t* warn_flags) {
+  VTS_REQUIRE_CTX(ctx);
+  if (!rho) {
+    vts::set_error(VTS_E_ARGUMENT, "vts_bind_stiffness: NULL rho");
+    return VTS_E_ARGUMENT;
+  }
+  unsigned warn = 0;
+  const int rc = vts::bind_stiffness(C(ctx), rho, &warn);
+  if (warn_flags) *warn_flags = warn;
+  return rc;
+}
+
+int vts_element_products(vts_ctx* ctx, const double* u, double* w, double* q) {
+  VTS_REQUIRE_CTX(ctx);
+  if (!u || !q) {
+    vts::set_error(VTS_E_ARGUMENT, "vts_element_products: NULL argument");
+    return VTS_E_ARGUMENT;
+  }
+  return vts::element_energy(C(ctx), u, w, q);
+}
+
+int vts_doc_bisect(vts_ctx* ctx, const double* rho, const double* z, double z_scale, const double* lower,
+                   const double* upper, double volume, double exponent, double alpha_hi, double tol, int32_t cap,
+                   double* rho_new, double* alpha, int32_t* status) {
+  VTS_REQUIRE_CTX(ctx);
+  if (!rho || !z || !lower || !upper || !rho_new || !alpha || !status || cap < 0 || !(alpha_hi > 0.0)) {
+    vts::set_error(VTS_E_ARGUMENT, "vts_doc_bisect: bad arguments");
+    return VTS_E_ARGUMENT;
+  }
+  int st = 0;
+  const int rc = vts::doc_bisect(C(ctx), rho, z, z_scale, lower, upper, volume, exponent, alpha_hi, tol, cap,
+                                 rho_new, alpha, &st);
+  *status = st;
+  return rc;
+}
+
+int vts_doc_update(vts_ctx* ctx, const double* rho, const double* z, double z_scale, double alpha, double exponent,
+                   const double* lower, const double* upper, double* rho_new) {
+  VTS_REQUIRE_CTX(ctx);
+  if (!rho || !z || !lower || !upper || !rho_new) {
+    vts::set_error(VTS_E_ARGUMENT, "vts_doc_update: NULL argument");
+    return VTS_E_ARGUMENT;
+  }
+  if (!(alpha > 0.0)) {
+    vts::set_error(VTS_E_ARGUMENT, "volume multiplier must be positive");
+    return VTS_E_ARGUMENT;
+  }
+  return vts::doc_update(C(ctx), rho, z, z_scale, alpha, exponent, lower, upper, rho_new);
+}
+
+int vts_doc_measure(vts_ctx* ctx, const double* rho_new, const double* rho, const double* q, const double* u,
+                    const double* f, const double* lower, const double* upper, double volume, double* out) {
+  VTS_REQUIRE_CTX(ctx);
+  if (!rho_new || !rho || !q || !u || !f || !lower || !upper || !out) {
+    vts::set_error(VTS_E_ARGUMENT, "vts_doc_measure: NULL argument");
+    return VTS_E_ARGUMENT;
+  }
+  return vts::doc_measure(C(ctx), rho_new, rho, q, u, f, lower, upper, volume, out);
 }
 
 int vts_reconstruct_nu(vts_ctx* ctx, const double* u, const double* du, double dalpha, const double* res_u,

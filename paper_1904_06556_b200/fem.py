@@ -131,6 +131,44 @@ class ElementOps:
     def vec(self, size: int) -> torch.Tensor:
         return torch.empty(size, dtype=torch.float64, device="cuda")
 
+    # -- element-vector plumbing and assembly (fem.py:175-180, 211-219) --------------
+
+    def element_products(self, u) -> tuple[torch.Tensor, torch.Tensor]:
+        """Per-element w_e = u_e K_e (m x 8, local frame) and q_e = u_e . w_e / 2 (fem.py:175-180)."""
+        u = self.check_vec(u, self.n, "u")
+        w = torch.empty((self.m, 8), dtype=torch.float64, device="cuda")
+        q = self.vec(self.m)
+        _lib.check(self._lib.vts_element_products(self.handle, ptr(u), ptr(w), ptr(q)), "vts_element_products")
+        return w, q
+
+    def assemble_stiffness(self, rho):
+        """K(rho) = sum_e rho_e K_e on the free dofs (fem.py:211-219), bound matrix-free
+        in this context (it supersedes the context's previous system)."""
+        import warnings
+
+        from .linalg import StiffnessMatrix
+
+        rho = self.check_vec(rho, self.m, "rho")
+        flags = ctypes.c_uint32(0)
+        _lib.check(self._lib.vts_bind_stiffness(self.handle, ptr(rho), ctypes.byref(flags)), "vts_bind_stiffness")
+        if flags.value & 1:
+            warnings.warn("assembling K(rho) with negative densities; the operator may be indefinite",
+                          RuntimeWarning, stacklevel=2)
+        self._system_version = getattr(self, "_system_version", 0) + 1
+        return StiffnessMatrix(self, self._system_version)
+
+    _scratch = None
+
+    @classmethod
+    def scratch(cls) -> "ElementOps":
+        """A minimal context (one 1x1 cantilever level) for solves that bind no mesh:
+        minres_solve on a user operator needs only its device scratch and stream."""
+        if cls._scratch is None:
+            from .problem import build_problem
+
+            cls._scratch = cls(build_problem("cantilever", 1, 1, 1, 0.5).fine)
+        return cls._scratch
+
     def check_vec(self, t: torch.Tensor, size: int, name: str) -> torch.Tensor:
         if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
             raise TypeError(f"{name} must be a contiguous CUDA float64 tensor")

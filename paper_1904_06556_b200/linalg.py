@@ -3,12 +3,14 @@
 * `NewtonMatrix` — the bordered Schur matrix [[A, c], [c^T, d]] of
   `schur_system` held matrix-free in the device context; `matvec` is
   `BorderedMatrix.matvec` (linalg.py:56-62) without the CSR.
+  `StiffnessMatrix` — the unbordered K(rho) of the DOC state solves.
 * `minres_solve` — `linalg.py:128-242` run entirely on the device (vector
   recurrences and Givens scalars), same contract: convergence means the true
   relative residual is <= tol; errors raise `MinresError` carrying the last
   sound iterate.
-* `MinresConfig`, `MinresResult`, `MinresError`, `StagnationTolerance` keep
-  the reference's fields and semantics (linalg.py:84-115, 260-286).
+* `MinresConfig`, `MinresResult`, `MinresError`, `FixedTolerance`,
+  `StagnationTolerance`, `ComplementarityTolerance` keep the reference's
+  fields and semantics (linalg.py:84-115, 250-308).
 """
 
 from __future__ import annotations
@@ -25,6 +27,8 @@ from .fem import ptr
 class NewtonMatrix:
     """Matrix-free bordered Schur matrix bound in an `ElementOps` context."""
 
+    bordered = True
+
     def __init__(self, ops, border: torch.Tensor, corner: float, version: int):
         self.ops = ops
         self.border = border
@@ -39,18 +43,38 @@ class NewtonMatrix:
     def core_dim(self) -> int:
         return self.ops.n
 
+    @property
+    def dim(self) -> int:
+        return self.shape[0]
+
     def _check_current(self) -> None:
         if self.ops._system_version != self._version:
-            raise RuntimeError("this Newton matrix was superseded by a later schur_system call")
+            raise RuntimeError("this matrix was superseded by a later system bound in the same context")
 
     def matvec(self, x: torch.Tensor) -> torch.Tensor:
         self._check_current()
-        x = self.ops.check_vec(x, self.ops.n + 1, "x")
-        y = self.ops.vec(self.ops.n + 1)
+        x = self.ops.check_vec(x, self.dim, "x")
+        y = self.ops.vec(self.dim)
         _lib.check(_lib.load().vts_newton_apply(self.ops.handle, ptr(x), ptr(y)), "vts_newton_apply")
         return y
 
     __matmul__ = matvec
+
+
+class StiffnessMatrix(NewtonMatrix):
+    """K(rho) = sum_e rho_e K_e on the free dofs, matrix-free in the context
+    (`ElementOps.assemble_stiffness`, fem.py:211-219): the unbordered operator of
+    the DOC state solves (doc.py:137-146).  `border` is None like the
+    reference's plain CSR matrix (linalg.py:49-53)."""
+
+    bordered = False
+
+    def __init__(self, ops, version: int):
+        super().__init__(ops, None, 0.0, version)
+
+    @property
+    def shape(self):
+        return (self.ops.n, self.ops.n)
 
 
 @dataclass
@@ -89,44 +113,153 @@ _ERRORS = {
 }
 
 
+def _own_mg(precond, a) -> bool:
+    """precond is the `apply` of an MgPreconditioner built on the bound matrix `a`."""
+    from .multigrid import MgPreconditioner
+
+    owner = getattr(precond, "__self__", None)
+    return (isinstance(owner, MgPreconditioner) and owner.ops is a.ops
+            and getattr(precond, "__func__", None) is MgPreconditioner.apply and owner._version == a._version)
+
+
+def _dev_view(addr: int, length: int) -> torch.Tensor:
+    """A torch view of `length` doubles of device memory owned by the library."""
+
+    class _Buf:
+        __cuda_array_interface__ = {"shape": (length,), "typestr": "<f8", "data": (addr, False), "version": 3}
+
+    return torch.as_tensor(_Buf(), device="cuda")
+
+
+def _as_operator(a):
+    """_as_matvec (linalg.py:118-125): bound matrices, dense / sparse tensors, callables."""
+    if isinstance(a, NewtonMatrix):
+        return a.matvec, a.dim
+    if isinstance(a, torch.Tensor):
+        if a.dim() != 2 or a.shape[0] != a.shape[1]:
+            raise ValueError("the operator must be a square matrix")
+        mat = a if a.is_cuda else a.to("cuda")
+        return (lambda v: mat @ v), a.shape[0]
+    if hasattr(a, "tocsr") or hasattr(a, "__array__"):  # scipy sparse / numpy: move to the device once
+        import numpy as np
+        import scipy.sparse as sp
+
+        if sp.issparse(a):
+            c = a.tocsr()
+            mat = torch.sparse_csr_tensor(torch.as_tensor(c.indptr, dtype=torch.int64),
+                                          torch.as_tensor(c.indices, dtype=torch.int64),
+                                          torch.as_tensor(c.data, dtype=torch.float64), size=c.shape).to("cuda")
+        else:
+            mat = torch.as_tensor(np.asarray(a, dtype=np.float64), device="cuda")
+        return (lambda v: mat @ v), mat.shape[0]
+    if callable(a):
+        return a, None
+    raise TypeError(f"cannot use {type(a).__name__} as a MINRES operator")
+
+
 def minres_solve(a, b: torch.Tensor, config: MinresConfig, precond=None, x0=None, history: list | None = None
                  ) -> MinresResult:
-    """Preconditioned MINRES for the bound Newton matrix (linalg.py:128-242).
+    """Preconditioned MINRES (linalg.py:128-242), same contract: convergence means
+    the true relative residual is <= tol; errors raise `MinresError` carrying the
+    last sound iterate.
 
-    `a` must be the `NewtonMatrix` returned by `schur_system`; `precond` is
-    None or the `apply` of an `MgPreconditioner` built on it.  `history`, when
-    a list, receives the true relative residual after every iteration.
+    `a` is the bound Newton matrix of `schur_system` or the bound stiffness of
+    `ElementOps.assemble_stiffness` (then with `precond` None or its own
+    `MgPreconditioner.apply` the whole solve runs in the context: vts_minres_warm),
+    or any operator the reference accepts (linalg.py:118-125) -- a dense or
+    sparse matrix, or a callable on device vectors -- with any callable
+    preconditioner (vts_minres_generic: the same device recurrences, the
+    operator applied through a callback).  `x0` warm-starts (linalg.py:144-154).
+    `history`, when a list, receives the true relative residual after every
+    iteration.
     """
-    if not isinstance(a, NewtonMatrix):
-        raise TypeError("minres_solve runs on the device Newton matrix returned by schur_system")
-    if x0 is not None:
-        raise NotImplementedError("warm starts are not used on the PBM path (pbm.py:282-285)")
-    a._check_current()
-    ops = a.ops
-    use_mg = 0
-    if precond is not None:
-        owner = getattr(precond, "__self__", None)
-        from .multigrid import MgPreconditioner
+    lib = _lib.load()
+    if isinstance(a, NewtonMatrix) and (precond is None or _own_mg(precond, a)):
+        a._check_current()
+        ops = a.ops
+        if precond is not None:
+            precond.__self__._check_current()
+        b = ops.check_vec(b, a.dim, "b")
+        if x0 is not None:
+            x0 = ops.check_vec(torch.as_tensor(x0, dtype=torch.float64, device="cuda").contiguous(), a.dim, "x0")
+        x = ops.vec(a.dim)
+        cap = config.max_iters if config.max_iters > 0 else 3 * a.dim
+        hist = (ctypes.c_double * cap)() if history is not None else None
+        it, rel, conv = ctypes.c_int32(0), ctypes.c_double(0.0), ctypes.c_int32(0)
+        rc = lib.vts_minres_warm(ops.handle, ptr(b), ptr(x), ptr(x0), config.tol, cap, config.floor,
+                                 1 if precond is not None else 0, ctypes.byref(it), ctypes.byref(rel),
+                                 ctypes.byref(conv), hist)
+        if history is not None:
+            history.extend(hist[: it.value])
+        if rc in _ERRORS:
+            raise MinresError(_ERRORS[rc], x)
+        _lib.check(rc, "vts_minres_warm")
+        return MinresResult(x, it.value, rel.value, bool(conv.value))
+    return _minres_generic(a, b, config, precond, x0, history)
 
-        if not isinstance(owner, MgPreconditioner) or owner.ops is not ops or precond.__func__ is not MgPreconditioner.apply:
-            raise TypeError("precond must be MgPreconditioner.apply of a preconditioner built on this matrix")
-        owner._check_current()
-        use_mg = 1
-    b = ops.check_vec(b, ops.n + 1, "b")
-    x = ops.vec(ops.n + 1)
-    cap = config.max_iters if config.max_iters > 0 else 3 * (ops.n + 1)
+
+def _minres_generic(a, b, config, precond, x0, history):
+    from .fem import ElementOps
+
+    op, dim = _as_operator(a)
+    if not (isinstance(b, torch.Tensor) and b.is_cuda and b.dtype == torch.float64):
+        b = torch.as_tensor(b, dtype=torch.float64, device="cuda")
+    b = b.contiguous()
+    n = b.numel()
+    if dim is not None and dim != n:
+        raise ValueError(f"b has {n} entries, the operator {dim}")
+    if x0 is not None:
+        x0 = torch.as_tensor(x0, dtype=torch.float64, device="cuda").contiguous()
+        if x0.numel() != n:
+            raise ValueError(f"x0 has {x0.numel()} entries, expected {n}")
+    ops = a.ops if isinstance(a, NewtonMatrix) else ElementOps.scratch()
+    errors: list = []
+
+    def wrap(fn):
+        def cb(_user, pin, pout):
+            try:
+                res = fn(_dev_view(pin, n))
+                out = _dev_view(pout, n)
+                out.copy_(torch.as_tensor(res, dtype=torch.float64, device="cuda").reshape(-1))
+                torch.cuda.current_stream().synchronize()
+                return 0
+            except Exception as exc:  # re-raised after the library returns
+                errors.append(exc)
+                return 1
+        return _lib.APPLY_FN(cb)
+
+    op_cb = wrap(op)
+    pre_cb = wrap(precond) if precond is not None else None
+    x = torch.empty(n, dtype=torch.float64, device="cuda")
+    cap = config.max_iters if config.max_iters > 0 else 3 * n
     hist = (ctypes.c_double * cap)() if history is not None else None
-    it = ctypes.c_int32(0)
-    rel = ctypes.c_double(0.0)
-    conv = ctypes.c_int32(0)
-    rc = _lib.load().vts_minres(ops.handle, ptr(b), ptr(x), config.tol, cap, config.floor, use_mg,
-                                ctypes.byref(it), ctypes.byref(rel), ctypes.byref(conv), hist)
+    it, rel, conv = ctypes.c_int32(0), ctypes.c_double(0.0), ctypes.c_int32(0)
+    torch.cuda.current_stream().synchronize()
+    rc = _lib.load().vts_minres_generic(ops.handle, n, ptr(b), ptr(x), ptr(x0), config.tol, cap, config.floor,
+                                        ctypes.cast(op_cb, ctypes.c_void_p),
+                                        ctypes.cast(pre_cb, ctypes.c_void_p) if pre_cb is not None else None, None,
+                                        ctypes.byref(it), ctypes.byref(rel), ctypes.byref(conv), hist)
+    if errors:
+        raise errors[0]
     if history is not None:
         history.extend(hist[: it.value])
     if rc in _ERRORS:
         raise MinresError(_ERRORS[rc], x)
-    _lib.check(rc, "vts_minres")
+    _lib.check(rc, "vts_minres_generic")
     return MinresResult(x, it.value, rel.value, bool(conv.value))
+
+
+@dataclass
+class FixedTolerance:
+    """Constant inner tolerance (linalg.py:250-257), the DOC state solves' policy."""
+
+    tol: float = 1e-4
+
+    def current(self) -> float:
+        return self.tol
+
+    def observe(self, *_args) -> None:
+        pass
 
 
 @dataclass

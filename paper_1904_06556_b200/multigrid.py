@@ -1,6 +1,7 @@
 """Galerkin V(2,2) multigrid preconditioner on the device (multigrid.py of the reference).
 
-`MgPreconditioner(fine, transfers)` builds, for the bound Newton matrix, the
+`MgPreconditioner(fine, transfers)` builds, for the bound Newton matrix (or
+the unbordered stiffness K(rho) of the DOC state solves, multigrid.py:85-86), the
 finest-level block stencil, every coarse operator P^T A P (symmetrised), the
 restricted borders and the dense Cholesky factor of the coarsest bordered
 matrix with the reference's trace-scaled shift fallback
@@ -24,18 +25,21 @@ log = logging.getLogger("paper_1904_06556_b200.multigrid")
 
 
 class LevelOperator:
-    """Probe handle for one level operator (MgPreconditioner.mats[k])."""
+    """Probe handle for one level operator (MgPreconditioner.mats[k]): bordered
+    (core_dim + 1 entries) over a Newton matrix, plain (core_dim) over K(rho)."""
 
     def __init__(self, pre: "MgPreconditioner", k: int):
         self._pre = pre
         self.level = k
         self.core_dim = pre.ops.level_size(k)
+        self.bordered = pre.bordered
+        self.dim = self.core_dim + (1 if self.bordered else 0)
 
     def matvec(self, x: torch.Tensor) -> torch.Tensor:
         self._pre._check_current()
         ops = self._pre.ops
-        x = ops.check_vec(x, self.core_dim + 1, "x")
-        y = ops.vec(self.core_dim + 1)
+        x = ops.check_vec(x, self.dim, "x")
+        y = ops.vec(self.dim)
         _lib.check(_lib.load().vts_level_apply(ops.handle, self.level, ptr(x), ptr(y)), "vts_level_apply")
         return y
 
@@ -43,7 +47,8 @@ class LevelOperator:
 class MgPreconditioner:
     def __init__(self, fine: NewtonMatrix, transfers, sweeps: int = 2, shift_scale: float = 1e-12):
         if not isinstance(fine, NewtonMatrix):
-            raise TypeError("MgPreconditioner takes the NewtonMatrix returned by schur_system")
+            raise TypeError("MgPreconditioner takes a matrix bound in the device context: the NewtonMatrix of "
+                            "schur_system or the StiffnessMatrix of ElementOps.assemble_stiffness")
         if sweeps != 2:
             raise ValueError("the device V-cycle implements the reference's V(2,2) (sweeps=2)")
         fine._check_current()
@@ -56,9 +61,15 @@ class MgPreconditioner:
             if tuple(t.shape) != (hier.levels[k + 1].n, hier.levels[k].n):
                 raise ValueError(f"transfer {k} does not match the hierarchy")
         self.sweeps = sweeps
+        self.bordered = fine.bordered  # multigrid.py:85-86: a plain matrix gets no border
+        self.dim = fine.dim
         self._version = fine._version
         shifted = ctypes.c_int32(0)
         rc = _lib.load().vts_mg_setup(self.ops.handle, shift_scale, ctypes.byref(shifted))
+        if rc == _lib.VTS_E_CHOLESKY:  # the shifted retry failed too: cho_factor's error (multigrid.py:102)
+            import numpy as np
+
+            raise np.linalg.LinAlgError(_lib.last_error())
         _lib.check(rc, "vts_mg_setup")
         self.shifted = bool(shifted.value)
         if self.shifted:
@@ -75,7 +86,7 @@ class MgPreconditioner:
 
     def apply(self, v: torch.Tensor) -> torch.Tensor:
         self._check_current()
-        v = self.ops.check_vec(v, self.ops.n + 1, "v")
-        z = self.ops.vec(self.ops.n + 1)
+        v = self.ops.check_vec(v, self.dim, "v")
+        z = self.ops.vec(self.dim)
         _lib.check(_lib.load().vts_vcycle(self.ops.handle, ptr(v), ptr(z)), "vts_vcycle")
         return z

@@ -371,6 +371,11 @@ def solve_pbm(problem, cfg: PbmConfig | None = None, trace: dict | None = None, 
         if out.stalled:
             notes.append(f"final-pass stall accepted near optimum: {out.note}")
 
+    volume = rows[-1][5] if rows else float("nan")
+    if not converged and ev is not None:
+        # the cap path ends with a safeguarded update after the last row: the
+        # report's volume is sum(rho) after it, like the reference (pbm.py:451)
+        volume = _measure(ops, state, ev, f, bounds)[3]
     torch.cuda.current_stream().synchronize()
     certificate = None
     if converged:
@@ -378,7 +383,7 @@ def solve_pbm(problem, cfg: PbmConfig | None = None, trace: dict | None = None, 
     return SolveReport(
         method="pbm", problem=problem.name, tol=cfg.tol, converged=converged, columns=columns, rows=rows,
         count_columns=("newton", "minres"), objective=0.5 * fu, dual_objective=d_val, gap_scaled=gap_scaled,
-        tau_res=ev.tau_res if ev is not None else float("inf"), volume=rows[-1][5] if rows else float("nan"),
+        tau_res=ev.tau_res if ev is not None else float("inf"), volume=volume,
         rho=state.rho.clone(), wall_clock=time.perf_counter() - t0, notes="; ".join(notes),
         certificate=certificate,
         extras={"u": state.u, "alpha": state.alpha, "nu_lo": state.nu_lo, "nu_up": state.nu_up,

@@ -14,7 +14,8 @@ so the distance between this run and the stock run is the size of a
 rounding-level perturbation of the reference itself.
 
 It does the same for the 32x16 MBB of `pbm_mbb32.npz` (~140 MINRES iterations
-per late Newton step, where single per-Newton counts move under rounding).
+per late Newton step, where single per-Newton counts move under rounding) and,
+with the argument `c4`, for the full 1024x512 solve of `pbm_c4.npz`.
 
 Output `fma_sensitivity.npz`: for both runs the FMA run's counts, objective
 and thickness field (C2: at `pbm_c2.npz`'s 512 sample positions), plus the
@@ -74,8 +75,8 @@ def fused_instructions() -> int:
 
 def run(prob, stock: dict, with_vectors: bool) -> dict:
     out, rep = mg_.pbm_fixture(prob, with_vectors=with_vectors)
-    sample = out["rho"] if with_vectors else out["rho_sample"]
-    ref = stock["rho"] if with_vectors else stock["rho_sample"]
+    key = "rho" if with_vectors else "rho_sample"  # whole field, or pbm_c2.npz's 512 samples
+    sample, ref = out[key], stock[key]
     d = sample - ref
     res = {
         "objective": rep.objective, "outer": rep.outer_iterations,
@@ -91,20 +92,29 @@ def run(prob, stock: dict, with_vectors: bool) -> dict:
     return res
 
 
-def main() -> None:
+def main(argv) -> None:
     mg_.rmg._gs_forward = _gs_forward_fma
     mg_.rmg._gs_backward = _gs_backward_fma
-    c2 = run(mg_.build_config("C2"), dict(np.load(os.path.join(HERE, "pbm_c2.npz"))), with_vectors=False)
-    mbb = run(mg_.build_problem2d("mbb", 4, 2, 4, 0.4), dict(np.load(os.path.join(HERE, "pbm_mbb32.npz"))),
-              with_vectors=True)
+    path = os.path.join(HERE, "fma_sensitivity.npz")
+    out = dict(np.load(path)) if os.path.exists(path) else {}
+    which = set(argv) or {"c2", "mbb32"}
+    if "c2" in which:
+        c2 = run(mg_.build_config("C2"), dict(np.load(os.path.join(HERE, "pbm_c2.npz"))), with_vectors=False)
+        out.update({f"c2_{k}": v for k, v in c2.items()})
+    if "mbb32" in which:
+        mbb = run(mg_.build_problem2d("mbb", 4, 2, 4, 0.4), dict(np.load(os.path.join(HERE, "pbm_mbb32.npz"))),
+                  with_vectors=True)
+        out.update({f"mbb32_{k}": v for k, v in mbb.items()})
+    if "c4" in which:  # the north_star target (~6 min): the thickness field's own sensitivity
+        c4 = run(mg_.build_config("C4"), dict(np.load(os.path.join(HERE, "pbm_c4.npz"))), with_vectors=True)
+        c4.pop("rho_sample")  # 4 MB; the distances are what the tests use
+        out.update({f"c4_{k}": v for k, v in c4.items()})
     nfma = fused_instructions()
     assert nfma > 0, "the host compiler did not contract the Gauss-Seidel products"
-    out = {"fma_instructions": nfma}
-    out.update({f"c2_{k}": v for k, v in c2.items()})
-    out.update({f"mbb32_{k}": v for k, v in mbb.items()})
-    np.savez_compressed(os.path.join(HERE, "fma_sensitivity.npz"), **out)
+    out["fma_instructions"] = nfma
+    np.savez_compressed(path, **out)
     print({k: v for k, v in out.items() if np.ndim(v) == 0})
 
 
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1:])

@@ -59,6 +59,7 @@ def put(out: dict, name: str, vec, seed: int) -> None:
     out[f"{name}__val"] = v[idx]
     out[f"{name}__norm"] = float(np.linalg.norm(v))
     out[f"{name}__sum"] = float(v.sum())
+    out[f"{name}__max"] = float(np.abs(v).max())
 
 
 def c3_state(prob, seed: int, both_branches: bool):
