@@ -60,6 +60,20 @@ int vts_version(void);
  */
 int vts_ctx_create(vts_ctx** out, int32_t levels, const int32_t* ex, const int32_t* ey,
                    const int64_t* const* dof_maps, const double* ke, int64_t stream);
+/*
+ * Context over one HEXAHEDRAL hierarchy -- the reference's own 3D
+ * discretisation (mesh.py:216-287: trilinear 8-node cubes, three dofs per
+ * node, whole nodes fixed; fem.py:150-162).  `ez[k]` adds the third axis,
+ * `dof_maps[k]` is a HOST int64 array (n_nodes_k x 3), `ke` a HOST row-major
+ * 24x24 element stiffness of the finest level (fem.hex_stiffness with the
+ * finest edge).  Every other entry point below works on either kind of
+ * context with the same conventions (element products w are m x 24 here);
+ * the benchmark probes and the interior-point blocks are 2D only.
+ */
+int vts_ctx_create3(vts_ctx** out, int32_t levels, const int32_t* ex, const int32_t* ey, const int32_t* ez,
+                    const int64_t* const* dof_maps, const double* ke, int64_t stream);
+/* 2 or 3: the context's discretisation */
+int vts_ctx_dim(const vts_ctx* ctx);
 int vts_ctx_destroy(vts_ctx* ctx);
 /* n (free dofs of the finest level) and m (elements); HOST outputs */
 int vts_ctx_sizes(const vts_ctx* ctx, int64_t* n, int64_t* m);

@@ -41,6 +41,9 @@ SIGNATURES = {
     "vts_last_error": (ctypes.c_char_p, []),
     "vts_version": (ctypes.c_int, []),
     "vts_ctx_create": (ctypes.c_int, [ctypes.POINTER(_P), _I32, _PI32, _PI32, ctypes.POINTER(_PI64), _PD, _I64]),
+    "vts_ctx_create3": (ctypes.c_int, [ctypes.POINTER(_P), _I32, _PI32, _PI32, _PI32, ctypes.POINTER(_PI64), _PD,
+                                       _I64]),
+    "vts_ctx_dim": (ctypes.c_int, [_P]),
     "vts_ctx_destroy": (ctypes.c_int, [_P]),
     "vts_ctx_sizes": (ctypes.c_int, [_P, _PI64, _PI64]),
     "vts_eval_lagrangian": (ctypes.c_int, [_P, _P, _D] + [_P] * 11 + [_D, _D, _D, _D] + [_P] * 11 + [_PD, _PU32]),

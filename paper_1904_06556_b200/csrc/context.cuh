@@ -53,7 +53,11 @@ struct MinresDev {
 
 enum MinresStatus { kRunning = 0, kConverged = 1, kCap = 2, kIndefinite = -1, kBreakdown = -2, kNonfinite = -3 };
 
+struct Hex;  // 3D hexahedral data (hex3d.inc.cu)
+
 struct Ctx {
+  int dim = 2;                  // 2: Q1 plane stress (this file's levels); 3: trilinear hexahedra (hex)
+  Hex* hex = nullptr;
   int L = 0;                    // number of levels (index 0 = coarsest)
   std::vector<LevelBuf> lv;
   cudaStream_t stream = nullptr;
@@ -262,7 +266,7 @@ int dot_grid(Ctx* c, int level, const double* a, const double* b, bool bordered,
 
 int minres_generic(Ctx* c, long long len, const double* b, double* x_out, const double* x0, double tol,
                    int max_iters, double floor_tol, vts_apply_fn op, vts_apply_fn prec, void* user,
-                   int* iters_out, double* relres_out, int* conv_out, double* history);
+                   int* iters_out, double* relres_out, int* conv_out, double* history, bool native = false);
 
 // ---- DOC reuse (doc.inc.cu) ----
 int bind_stiffness(Ctx* c, const double* rho, unsigned* warn);

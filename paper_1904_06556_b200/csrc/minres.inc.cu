@@ -494,7 +494,7 @@ namespace vts {
 // ---------------------------------------------------------------------------
 int minres_generic(Ctx* c, long long len_ll, const double* b, double* x_out, const double* x0, double tol,
                    int max_iters, double floor_tol, vts_apply_fn op, vts_apply_fn prec, void* user,
-                   int* iters_out, double* relres_out, int* conv_out, double* history) {
+                   int* iters_out, double* relres_out, int* conv_out, double* history, bool native) {
   if (!op || len_ll < 1 || len_ll > INT32_MAX) {
     set_error(4, "minres: bad operator or length");
     return 4;
@@ -522,13 +522,15 @@ int minres_generic(Ctx* c, long long len_ll, const double* b, double* x_out, con
   double* xn = vec[8];
   double* T = vec[9];
   double* spare = vec[10];
+  // foreign (Python) callbacks run on other streams: drain around them; native
+  // ones (the 3D operators) enqueue on the context stream, in order
   auto call = [&](vts_apply_fn fn, const double* in, double* out) -> int {
-    VTS_CUDA(cudaStreamSynchronize(c->stream));
+    if (!native) VTS_CUDA(cudaStreamSynchronize(c->stream));
     if (int rc = fn(user, in, out)) {
-      set_error(4, "minres: operator callback failed");
+      if (!native) set_error(4, "minres: operator callback failed");
       return rc;
     }
-    VTS_CUDA(cudaDeviceSynchronize());
+    if (!native) VTS_CUDA(cudaDeviceSynchronize());
     return 0;
   };
   auto scalar = [&](const double* dptr) -> double {

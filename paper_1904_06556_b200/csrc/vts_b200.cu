@@ -28,6 +28,7 @@
 #include "minres.inc.cu"
 #include "ip.inc.cu"
 #include "doc.inc.cu"
+#include "hex3d.inc.cu"
 
 namespace vts {
 
@@ -58,8 +59,33 @@ static std::vector<cudaStream_t> g_ke_users;  // streams that used the loaded co
 static std::map<cudaStream_t, int> g_stream_refs;  // live contexts per stream
 static cudaEvent_t g_ke_event = nullptr;
 
+static double g_ke3_loaded[576];
+static bool g_ke3_valid = false;
+static std::vector<cudaStream_t> g_ke3_users;
+
+// the 3D path's K_e (c_ke3, 24 x 24) under the same ownership rule
+static int ensure_ke3(Ctx* c) {
+  if (g_ke3_valid && std::memcmp(c->hex->ke, g_ke3_loaded, sizeof(g_ke3_loaded)) == 0) {
+    if (std::find(g_ke3_users.begin(), g_ke3_users.end(), c->stream) == g_ke3_users.end())
+      g_ke3_users.push_back(c->stream);
+    return 0;
+  }
+  if (!g_ke_event) VTS_CUDA(cudaEventCreateWithFlags(&g_ke_event, cudaEventDisableTiming));
+  for (cudaStream_t s : g_ke3_users) {
+    if (s == c->stream) continue;
+    VTS_CUDA(cudaEventRecord(g_ke_event, s));
+    VTS_CUDA(cudaStreamWaitEvent(c->stream, g_ke_event, 0));
+  }
+  VTS_CUDA(cudaMemcpyToSymbolAsync(c_ke3, c->hex->ke, sizeof(double) * 576, 0, cudaMemcpyHostToDevice, c->stream));
+  std::memcpy(g_ke3_loaded, c->hex->ke, sizeof(g_ke3_loaded));
+  g_ke3_valid = true;
+  g_ke3_users.assign(1, c->stream);
+  return 0;
+}
+
 static int ensure_ke(Ctx* c) {
   std::lock_guard<std::mutex> lock(g_ke_mutex);
+  if (c->dim == 3) return ensure_ke3(c);
   if (g_ke_owner == c) return 0;
   double want[64 + 8];
   std::memcpy(want, c->ke, sizeof(double) * 64);
@@ -213,8 +239,10 @@ static void free_ctx(Ctx* c) {
     if (--g_stream_refs[c->stream] == 0) {
       g_stream_refs.erase(c->stream);
       g_ke_users.erase(std::remove(g_ke_users.begin(), g_ke_users.end(), c->stream), g_ke_users.end());
+      g_ke3_users.erase(std::remove(g_ke3_users.begin(), g_ke3_users.end(), c->stream), g_ke3_users.end());
     }
   }
+  delete c->hex;
   delete c;
 }
 
@@ -414,6 +442,8 @@ static int create(Ctx** out, int levels, const int32_t* ex, const int32_t* ey, c
 
 }  // namespace vts
 
+#include "hex3d_host.inc.cu"
+
 using vts::Ctx;
 using vts::cuda_check;
 
@@ -433,6 +463,15 @@ static const Ctx* C(const vts_ctx* p) { return reinterpret_cast<const Ctx*>(p); 
     if (int _rc = vts::ensure_ke(C(ctx))) return _rc;        \
   } while (0)
 
+// entry points of the 2D path only (benchmark probes, the interior-point blocks)
+#define VTS_REQUIRE_2D(ctx)                                                   \
+  do {                                                                        \
+    if (C(ctx)->dim != 2) {                                                   \
+      vts::set_error(VTS_E_ARGUMENT, "this entry point exists for 2D contexts only"); \
+      return VTS_E_ARGUMENT;                                                  \
+    }                                                                         \
+  } while (0)
+
 extern "C" {
 
 const char* vts_last_error(void) { return vts::g_last_error.c_str(); }
@@ -448,6 +487,17 @@ int vts_ctx_create(vts_ctx** out, int32_t levels, const int32_t* ex, const int32
   return 0;
 }
 
+int vts_ctx_create3(vts_ctx** out, int32_t levels, const int32_t* ex, const int32_t* ey, const int32_t* ez,
+                    const int64_t* const* dof_maps, const double* ke, int64_t stream) {
+  Ctx* c = nullptr;
+  const int rc = vts::h3_create(&c, levels, ex, ey, ez, dof_maps, ke, stream);
+  if (rc) return rc;
+  *out = reinterpret_cast<vts_ctx*>(c);
+  return 0;
+}
+
+int vts_ctx_dim(const vts_ctx* ctx) { return ctx ? C(ctx)->dim : 0; }
+
 int vts_ctx_destroy(vts_ctx* ctx) {
   if (ctx) vts::free_ctx(C(ctx));
   return 0;
@@ -462,7 +512,7 @@ int vts_ctx_sizes(const vts_ctx* ctx, int64_t* n, int64_t* m) {
 
 int vts_level_size(const vts_ctx* ctx, int32_t level, int64_t* n) {
   if (!ctx || level < 0 || level >= C(ctx)->L) return VTS_E_ARGUMENT;
-  *n = C(ctx)->lv[level].d.nfree;
+  *n = C(ctx)->dim == 3 ? C(ctx)->hex->lv[level].nfree : C(ctx)->lv[level].d.nfree;
   return 0;
 }
 
@@ -475,7 +525,8 @@ int vts_eval_lagrangian(vts_ctx* ctx, const double* u, double alpha, const doubl
                         double* scalars, uint32_t* warn_flags) {
   VTS_REQUIRE_CTX(ctx);
   unsigned warn = 0;
-  const int rc = vts::eval_lagrangian(C(ctx), u, alpha, nu_lo, nu_up, rho, mu_lo, mu_up, p, q_lo, q_up, f, lower,
+  auto* fn = C(ctx)->dim == 3 ? vts::h3_eval_lagrangian : vts::eval_lagrangian;
+  const int rc = fn(C(ctx), u, alpha, nu_lo, nu_up, rho, mu_lo, mu_up, p, q_lo, q_up, f, lower,
                                       upper, volume, norm_f, norm_bounds, branch, res_u, res_lo, res_up, q,
                                       mu_hat_lo, mu_hat_up, a, b_lo, b_up, rho_hat, w_out, scalars, &warn);
   if (warn_flags) *warn_flags = warn ? VTS_W_SATURATED : 0u;
@@ -486,13 +537,15 @@ int vts_schur_system(vts_ctx* ctx, const double* u, const double* res_u, double 
                      const double* res_up, const double* a, const double* b_lo, const double* b_up,
                      const double* rho_hat, double* chat, double* rhs, double* border, double* corner) {
   VTS_REQUIRE_CTX(ctx);
-  return vts::schur_system(C(ctx), u, res_u, res_alpha, res_lo, res_up, a, b_lo, b_up, rho_hat, chat, rhs, border,
+  auto* fn = C(ctx)->dim == 3 ? vts::h3_schur_system : vts::schur_system;
+  return fn(C(ctx), u, res_u, res_alpha, res_lo, res_up, a, b_lo, b_up, rho_hat, chat, rhs, border,
                            corner);
 }
 
 int vts_newton_apply(vts_ctx* ctx, const double* x, double* y) {
   VTS_REQUIRE_CTX(ctx);
   Ctx* c = C(ctx);
+  if (c->dim == 3) return vts::h3_newton_apply(c, x, y);
   if (!c->system_bound) {
     vts::set_error(VTS_E_ARGUMENT, "vts_newton_apply: no Newton system bound");
     return VTS_E_ARGUMENT;
@@ -507,7 +560,7 @@ int vts_newton_apply(vts_ctx* ctx, const double* x, double* y) {
 
 int vts_mg_setup(vts_ctx* ctx, double shift_scale, int32_t* shifted) {
   VTS_REQUIRE_CTX(ctx);
-  const int rc = vts::mg_setup(C(ctx), shift_scale);
+  const int rc = C(ctx)->dim == 3 ? vts::h3_mg_setup(C(ctx), shift_scale) : vts::mg_setup(C(ctx), shift_scale);
   if (shifted) *shifted = C(ctx)->shifted;
   return rc;
 }
@@ -515,6 +568,7 @@ int vts_mg_setup(vts_ctx* ctx, double shift_scale, int32_t* shifted) {
 int vts_vcycle(vts_ctx* ctx, const double* b, double* z) {
   VTS_REQUIRE_CTX(ctx);
   Ctx* c = C(ctx);
+  if (c->dim == 3) return vts::h3_vcycle(c, b, z);
   if (!c->mg_ready) {
     vts::set_error(VTS_E_ARGUMENT, "vts_vcycle: multigrid not set up");
     return VTS_E_ARGUMENT;
@@ -530,6 +584,7 @@ int vts_vcycle(vts_ctx* ctx, const double* b, double* z) {
 int vts_level_apply(vts_ctx* ctx, int32_t level, const double* x, double* y) {
   VTS_REQUIRE_CTX(ctx);
   Ctx* c = C(ctx);
+  if (c->dim == 3) return vts::h3_level_apply(c, level, x, y);
   if (level < 0 || level >= c->L || !c->mg_ready) {
     vts::set_error(VTS_E_ARGUMENT, "vts_level_apply: bad level or multigrid not set up");
     return VTS_E_ARGUMENT;
@@ -546,7 +601,10 @@ int vts_minres(vts_ctx* ctx, const double* b, double* x, double tol, int32_t max
   VTS_REQUIRE_CTX(ctx);
   int it = 0, conv = 0;
   double rr = 0.0;
-  const int rc = vts::minres(C(ctx), b, x, tol, max_iters, floor_tol, precondition, &it, &rr, &conv, history);
+  const int rc = C(ctx)->dim == 3
+                     ? vts::h3_minres(C(ctx), b, x, nullptr, tol, max_iters, floor_tol, precondition, &it, &rr, &conv,
+                                      history)
+                     : vts::minres(C(ctx), b, x, tol, max_iters, floor_tol, precondition, &it, &rr, &conv, history);
   if (iterations) *iterations = it;
   if (relres) *relres = rr;
   if (converged) *converged = conv;
@@ -556,6 +614,7 @@ int vts_minres(vts_ctx* ctx, const double* b, double* x, double tol, int32_t max
 int vts_debug_smooth(vts_ctx* ctx, int32_t level, int32_t forward, int32_t zero_first, const double* b,
                      double* x) {
   VTS_REQUIRE_CTX(ctx);
+  VTS_REQUIRE_2D(ctx);
   return vts::debug_smooth(C(ctx), level, forward != 0, zero_first != 0, b, x);
 }
 
@@ -565,7 +624,10 @@ int vts_minres_warm(vts_ctx* ctx, const double* b, double* x, const double* x0, 
   VTS_REQUIRE_CTX(ctx);
   int it = 0, conv = 0;
   double rr = 0.0;
-  const int rc = vts::minres(C(ctx), b, x, tol, max_iters, floor_tol, precondition, &it, &rr, &conv, history, x0);
+  const int rc = C(ctx)->dim == 3
+                     ? vts::h3_minres(C(ctx), b, x, x0, tol, max_iters, floor_tol, precondition, &it, &rr, &conv,
+                                      history)
+                     : vts::minres(C(ctx), b, x, tol, max_iters, floor_tol, precondition, &it, &rr, &conv, history, x0);
   if (iterations) *iterations = it;
   if (relres) *relres = rr;
   if (converged) *converged = conv;
@@ -597,7 +659,7 @@ int vts_bind_stiffness(vts_ctx* ctx, const double* rho, uint32_t* warn_flags) {
     return VTS_E_ARGUMENT;
   }
   unsigned warn = 0;
-  const int rc = vts::bind_stiffness(C(ctx), rho, &warn);
+  const int rc = C(ctx)->dim == 3 ? vts::h3_bind_stiffness(C(ctx), rho, &warn) : vts::bind_stiffness(C(ctx), rho, &warn);
   if (warn_flags) *warn_flags = warn;
   return rc;
 }
@@ -608,7 +670,7 @@ int vts_element_products(vts_ctx* ctx, const double* u, double* w, double* q) {
     vts::set_error(VTS_E_ARGUMENT, "vts_element_products: NULL argument");
     return VTS_E_ARGUMENT;
   }
-  return vts::element_energy(C(ctx), u, w, q);
+  return C(ctx)->dim == 3 ? vts::h3_element_products(C(ctx), u, w, q) : vts::element_energy(C(ctx), u, w, q);
 }
 
 int vts_doc_bisect(vts_ctx* ctx, const double* rho, const double* z, double z_scale, const double* lower,
@@ -654,6 +716,9 @@ int vts_reconstruct_nu(vts_ctx* ctx, const double* u, const double* du, double d
                        double res_alpha, const double* res_lo, const double* res_up, const double* a,
                        const double* b_lo, const double* b_up, double* dnu_lo, double* dnu_up, double* slope) {
   VTS_REQUIRE_CTX(ctx);
+  if (C(ctx)->dim == 3)
+    return vts::h3_reconstruct_nu(C(ctx), u, du, dalpha, res_u, res_alpha, res_lo, res_up, a, b_lo, b_up, dnu_lo,
+                                  dnu_up, slope);
   const int rc = vts::reconstruct_nu(C(ctx), u, du, dalpha, res_u, res_alpha, res_lo, res_up, a, b_lo, b_up,
                                      dnu_lo, dnu_up, slope);
   if (rc) return rc;
@@ -668,7 +733,8 @@ int vts_al_value(vts_ctx* ctx, const double* u, double alpha, const double* nu_l
                  double branch, double* value, uint32_t* warn_flags) {
   VTS_REQUIRE_CTX(ctx);
   unsigned warn = 0;
-  const int rc = vts::al_value(C(ctx), u, alpha, nu_lo, nu_up, du, dalpha, dnu_lo, dnu_up, kappa, rho, p, mu_lo,
+  auto* fn = C(ctx)->dim == 3 ? vts::h3_al_value : vts::al_value;
+  const int rc = fn(C(ctx), u, alpha, nu_lo, nu_up, du, dalpha, dnu_lo, dnu_up, kappa, rho, p, mu_lo,
                                mu_up, q_lo, q_up, f, lower, upper, volume, branch, value, &warn);
   if (warn_flags) *warn_flags = warn ? VTS_W_SATURATED : 0u;
   return rc;
@@ -705,11 +771,13 @@ int vts_penalty_eval(vts_ctx* ctx, int64_t n, const double* tau, double branch, 
 
 int vts_time_kernels(vts_ctx* ctx, int32_t reps, double* ms) {
   VTS_REQUIRE_CTX(ctx);
+  VTS_REQUIRE_2D(ctx);
   return vts::time_kernels(C(ctx), reps, ms);
 }
 
 int vts_time_cold(vts_ctx* ctx, int32_t reps, void* flush, int64_t flush_bytes, double* ms) {
   VTS_REQUIRE_CTX(ctx);
+  VTS_REQUIRE_2D(ctx);
   if (reps < 1 || !flush || flush_bytes <= 0 || !ms) {
     vts::set_error(4, "vts_time_cold: bad arguments");
     return 4;
@@ -722,6 +790,7 @@ int vts_ip_residual(vts_ctx* ctx, const double* u, double alpha, const double* r
                     const double* f, double norm_f, double* q, double* res_c, double* res_lo, double* res_up,
                     double* res_u, double* scalars) {
   VTS_REQUIRE_CTX(ctx);
+  VTS_REQUIRE_2D(ctx);
   if (!u || !rho || !nu_lo || !nu_up || !lower || !upper || !f || !q || !res_c || !res_lo || !res_up || !res_u ||
       !scalars) {
     vts::set_error(VTS_E_ARGUMENT, "vts_ip_residual: NULL argument");
@@ -736,6 +805,7 @@ int vts_ip_schur_system(vts_ctx* ctx, const double* u, const double* rho, const 
                         const double* res_up, const double* res_u, double res_alpha, double* dcoef, double* g,
                         double* rhs, double* corner) {
   VTS_REQUIRE_CTX(ctx);
+  VTS_REQUIRE_2D(ctx);
   if (!u || !rho || !nu_lo || !nu_up || !lower || !upper || !res_c || !res_lo || !res_up || !res_u || !dcoef || !g ||
       !rhs) {
     vts::set_error(VTS_E_ARGUMENT, "vts_ip_schur_system: NULL argument");
@@ -750,6 +820,7 @@ int vts_ip_reconstruct(vts_ctx* ctx, const double* u, const double* du, double d
                        const double* rho, const double* nu_lo, const double* nu_up, const double* lower,
                        const double* upper, double* drho, double* dnu_up, double* dnu_lo) {
   VTS_REQUIRE_CTX(ctx);
+  VTS_REQUIRE_2D(ctx);
   if (!u || !du || !dcoef || !g || !res_c || !res_lo || !res_up || !rho || !nu_lo || !nu_up || !lower || !upper ||
       !drho || !dnu_up || !dnu_lo) {
     vts::set_error(VTS_E_ARGUMENT, "vts_ip_reconstruct: NULL argument");
@@ -763,6 +834,7 @@ int vts_ip_step_bounds(vts_ctx* ctx, const double* rho, const double* drho, cons
                        const double* dnu_lo, const double* nu_up, const double* dnu_up, const double* lower,
                        const double* upper, double* mins) {
   VTS_REQUIRE_CTX(ctx);
+  VTS_REQUIRE_2D(ctx);
   if (!rho || !drho || !nu_lo || !dnu_lo || !nu_up || !dnu_up || !lower || !upper || !mins) {
     vts::set_error(VTS_E_ARGUMENT, "vts_ip_step_bounds: NULL argument");
     return VTS_E_ARGUMENT;
@@ -774,6 +846,7 @@ int64_t vts_kernel_launches(const vts_ctx* ctx) { return ctx ? C(ctx)->launches 
 
 int vts_profile_begin(vts_ctx* ctx) {
   VTS_REQUIRE_CTX(ctx);
+  VTS_REQUIRE_2D(ctx);
   return vts::profile_begin(C(ctx));
 }
 

@@ -87,27 +87,36 @@ class ElementOps:
         hier = getattr(level, "hierarchy", None)
         if hier is None or hier.fine is not level:
             raise ValueError("ElementOps needs the finest MeshLevel of a build_problem hierarchy")
+        from .mesh3d import HexLevel, hex_stiffness
+
         self.level = level
         self.problem = hier
         self.n = level.n
         self.m = level.m
-        self.ke = quad_stiffness(e_mod, nu)
+        self.dim = 3 if isinstance(level, HexLevel) else 2
+        self.nodes_per_elem = 8 if self.dim == 3 else 4
+        self.dofs_per_elem = self.dim * self.nodes_per_elem  # 24 (fem.py:154) or 8
+        # K_e of the finest level (the only one PBM uses; coarse operators are Galerkin)
+        self.ke = hex_stiffness(e_mod, nu, level.edge) if self.dim == 3 else quad_stiffness(e_mod, nu)
         self._lib = _lib.load()
         self.stream = stream if stream is not None else torch.cuda.current_stream()
         levels = hier.levels
-        ex = (ctypes.c_int32 * len(levels))(*[lv.ex for lv in levels])
-        ey = (ctypes.c_int32 * len(levels))(*[lv.ey for lv in levels])
+        nl = len(levels)
+        ex = (ctypes.c_int32 * nl)(*[lv.ex for lv in levels])
+        ey = (ctypes.c_int32 * nl)(*[lv.ey for lv in levels])
         self._dofs = [np.ascontiguousarray(lv.dof.reshape(-1), dtype=np.int64) for lv in levels]
-        maps = (ctypes.POINTER(ctypes.c_int64) * len(levels))(
+        maps = (ctypes.POINTER(ctypes.c_int64) * nl)(
             *[d.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)) for d in self._dofs]
         )
         ke = np.ascontiguousarray(self.ke, dtype=np.float64)
+        kep = ke.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
         handle = ctypes.c_void_p()
-        rc = self._lib.vts_ctx_create(
-            ctypes.byref(handle), len(levels), ex, ey, maps,
-            ke.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), self.stream.cuda_stream,
-        )
-        _lib.check(rc, "vts_ctx_create")
+        if self.dim == 3:
+            ez = (ctypes.c_int32 * nl)(*[lv.ez for lv in levels])
+            rc = self._lib.vts_ctx_create3(ctypes.byref(handle), nl, ex, ey, ez, maps, kep, self.stream.cuda_stream)
+        else:
+            rc = self._lib.vts_ctx_create(ctypes.byref(handle), nl, ex, ey, maps, kep, self.stream.cuda_stream)
+        _lib.check(rc, "vts_ctx_create3" if self.dim == 3 else "vts_ctx_create")
         self.handle = handle
         self.norm_f = float(np.linalg.norm(level.load))
         self._level_n = [lv.n for lv in levels]
@@ -136,7 +145,7 @@ class ElementOps:
     def element_products(self, u) -> tuple[torch.Tensor, torch.Tensor]:
         """Per-element w_e = u_e K_e (m x 8, local frame) and q_e = u_e . w_e / 2 (fem.py:175-180)."""
         u = self.check_vec(u, self.n, "u")
-        w = torch.empty((self.m, 8), dtype=torch.float64, device="cuda")
+        w = torch.empty((self.m, self.dofs_per_elem), dtype=torch.float64, device="cuda")
         q = self.vec(self.m)
         _lib.check(self._lib.vts_element_products(self.handle, ptr(u), ptr(w), ptr(q)), "vts_element_products")
         return w, q

@@ -127,7 +127,7 @@ def eval_lagrangian(state: PbmState, ops: ElementOps, f, bounds: DensityBounds, 
     out = {k: ops.vec(m) for k in ("res_lo", "res_up", "q", "mu_hat_lo", "mu_hat_up", "a", "b_lo", "b_up",
                                   "rho_hat")}
     res_u = ops.vec(n)
-    w = torch.empty((m, 8), dtype=torch.float64, device="cuda") if keep_w else None
+    w = torch.empty((m, ops.dofs_per_elem), dtype=torch.float64, device="cuda") if keep_w else None
     sc = (ctypes.c_double * 8)()
     flags = ctypes.c_uint32(0)
     rc = _lib.load().vts_eval_lagrangian(

@@ -179,9 +179,19 @@ class Problem:
         return self._f_dev
 
 
-def build_problem(family: str, mx: int, my: int, levels: int, vol_frac: float) -> Problem:
+def build_problem(family: str, mx: int | None = None, my: int | None = None, levels: int | None = None,
+                  vol_frac: float | None = None):
+    """A 2D Q1 hierarchy `build_problem(family, mx, my, levels, vol_frac)`, or the
+    reference's own 3D instances by name: `build_problem("CANT-2-2-2-3",
+    vol_frac=0.35, levels=None)` (mesh.py:216-239, mesh3d.build_hex_problem)."""
+    if mx is None and isinstance(family, str) and "-" in family:
+        from .mesh3d import build_hex_problem
+
+        return build_hex_problem(family, vol_frac=0.35 if vol_frac is None else vol_frac, levels=levels)
     if family not in FAMILIES:
         raise ValueError(f"unknown problem family {family!r}")
+    if mx is None or my is None or levels is None or vol_frac is None:
+        raise ValueError("a 2D problem needs family, mx, my, levels and vol_frac")
     if min(mx, my, levels) < 1:
         raise ValueError("mx, my and levels must be positive integers")
     if not 0.0 < vol_frac < 1.0:
