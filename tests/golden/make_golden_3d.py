@@ -2,7 +2,7 @@
 
 Run HERE (the build container, where /root/reference is mounted):
 
-    NUMBA_CACHE_DIR=/tmp/numba_vtsopt python tests/golden/make_golden_3d.py
+    NUMBA_CACHE_DIR=/tmp/numba_vtsopt python tests/golden/make_golden_3d.py [mesh]
 
 The reference is 3D (mesh.py, fem.py:31-97), so these fixtures come from its
 own `build_problem`, `ElementOps`, `eval_lagrangian`, `schur_system`,
@@ -119,5 +119,29 @@ def main() -> None:
     print(json.dumps(meta, indent=1, default=float))
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "mesh" not in sys.argv[1:]:
     main()
+
+
+def mesh_fixture() -> None:
+    """`hex_mesh.npz`: the reference's own hierarchies and element stiffness for the CPU mesh test."""
+    out = {}
+    for name in ("CANT-2-2-2-3", "BRIDGE-4-2-2-2", "CANT-3-1-2-2", "BRIDGE-3-3-2-2"):
+        prob = rmesh.build_problem(name)
+        tag = name.replace("-", "_")
+        out[f"{tag}__volume"] = prob.volume
+        for k, lv in enumerate(prob.levels):
+            out[f"{tag}__L{k}_dof"] = lv.dof
+            out[f"{tag}__L{k}_load"] = lv.load
+            out[f"{tag}__L{k}_shape"] = np.array(lv.shape)
+            out[f"{tag}__L{k}_conn"] = lv.conn
+        for k, p in enumerate(prob.transfers):
+            c = p.tocoo()
+            out[f"{tag}__P{k}"] = np.stack([c.row.astype(float), c.col.astype(float), c.data])
+    for edge in (1.0, 0.5, 0.25):
+        out[f"ke_{edge}"] = rfem.hex_stiffness(1.0, 0.3, edge)
+    np.savez_compressed(os.path.join(HERE, "hex_mesh.npz"), **out)
+
+
+if __name__ == "__main__" and "mesh" in sys.argv[1:]:
+    mesh_fixture()
