@@ -23,6 +23,12 @@ constexpr int kReduceGridCap = 148 * 8;  // grid-stride reductions: 8 CTAs per S
 // Every block contributes NV partial sums; the last block to finish sums them
 // in block order (each thread a fixed strided subset, then the fixed block
 // tree) and returns true with the totals in tot[] (valid in thread 0).
+#ifndef VTS_REDUCE_SC
+#define VTS_REDUCE_SC 0
+#endif
+// VTS_REDUCE_SC=1 (compile time) restores the sequentially consistent fence + atomic (A/B)
+VTS_DEVICE_INLINE constexpr bool reduce_acq_rel() { return VTS_REDUCE_SC == 0; }
+
 template <int NV>
 __device__ bool last_block_reduce(double (&v)[NV], double* scratch, double* partials,
                                   unsigned* counter, double (&tot)[NV]) {
@@ -31,18 +37,39 @@ __device__ bool last_block_reduce(double (&v)[NV], double* scratch, double* part
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int i = 0; i < NV; ++i) partials[blockIdx.x * NV + i] = v[i];
-    __threadfence();
-    const unsigned ticket = atomicAdd(counter, 1u);
+    unsigned ticket;
+    if (reduce_acq_rel()) {
+      // release: this block's partials before its ticket; acquire: the last block
+      // sees every partial released before the tickets it counted (the other
+      // threads of the block are ordered behind thread 0 by the barrier below)
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(ticket) : "l"(counter) : "memory");
+    } else {
+      __threadfence();
+      ticket = atomicAdd(counter, 1u);
+    }
     s_last = (ticket == gridDim.x - 1);
   }
   __syncthreads();
   if (!s_last) return false;
-  __threadfence();
+  if (!reduce_acq_rel()) __threadfence();
 #pragma unroll
   for (int i = 0; i < NV; ++i) tot[i] = 0.0;
-  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+  // thread t sums blocks t, t + blockDim, ... in that order; the loads of a
+  // round of kU blocks are all issued before the first add (one L2 round
+  // trip per round instead of one per block; absent blocks add +0.0)
+  constexpr int kU = 8;
+  for (int b0 = threadIdx.x; b0 < (int)gridDim.x; b0 += kU * blockDim.x) {
+    double v[kU][NV];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) tot[i] += __ldcg(partials + b * NV + i);
+    for (int u = 0; u < kU; ++u) {
+      const int b = b0 + u * blockDim.x;
+#pragma unroll
+      for (int i = 0; i < NV; ++i) v[u][i] = b < (int)gridDim.x ? __ldcg(partials + b * NV + i) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+#pragma unroll
+      for (int i = 0; i < NV; ++i) tot[i] += v[u][i];
   }
   block_sum<NV>(tot, scratch);
   if (threadIdx.x == 0) *counter = 0u;

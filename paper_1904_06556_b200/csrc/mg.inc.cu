@@ -2349,7 +2349,31 @@ int time_kernels(Ctx* c, int reps, double* ms) {
 // from HBM as it does inside a MINRES iteration (where the V-cycle streams
 // ~0.5 GB between two applies).  ms[0] Newton apply, ms[1] finest residual:
 // the average over `reps` launches, each bracketed by its own event pair.
+// Diagnostic floor of the cold harness: a plain grid-stride kernel over the
+// apply's bytes (x and u, 16 B per node; rho_hat and chat, 8 B each per element; y written)
+__global__ void k_stream_floor(int nodes, int m, const double2* __restrict__ x, const double2* __restrict__ u,
+                               const double* __restrict__ rh, const double* __restrict__ ch, double2* __restrict__ y) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nodes; i += gridDim.x * blockDim.x) {
+    const double2 a = x[i], b = u[i];
+    const double r = i < m ? rh[i] : 0.0, c = i < m ? ch[i] : 0.0;
+    y[i] = make_double2(fma(a.x, r, b.x), fma(a.y, c, b.y));
+  }
+}
+
+// reads the flush buffer (writes only if a value is NaN, which the fill pattern never is)
+__global__ void k_read_flush(const double2* __restrict__ buf, size_t n, double* sink) {
+  double acc = 0.0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const double2 v = __ldcg(buf + i);
+    acc += v.x + v.y;
+  }
+  if (acc != acc) sink[0] = acc;
+}
+
 int time_cold(Ctx* c, int reps, void* flush, size_t flush_bytes, double* ms) {
+  // VTS_COLD_FLUSH=read: evict with a read sweep (clean L2) instead of a memset (dirty L2)
+  const char* cf = getenv("VTS_COLD_FLUSH");
+  const bool read_flush = cf && strcmp(cf, "read") == 0;
   if (!c->mg_ready) {
     set_error(4, "time_cold: multigrid not set up");
     return 4;
@@ -2365,7 +2389,12 @@ int time_cold(Ctx* c, int reps, void* flush, size_t flush_bytes, double* ms) {
     if (int rc = body()) return rc;  // warm (code, descriptors)
     double total = 0.0;
     for (int r = 0; r < reps; ++r) {
-      VTS_CUDA(cudaMemsetAsync(flush, r & 0xff, flush_bytes, c->stream));
+      if (read_flush) {  // L2 holds clean lines of the flush buffer (ncu's cache-control flush)
+        k_read_flush<<<148 * 4, 256, 0, c->stream>>>(reinterpret_cast<const double2*>(flush), flush_bytes / 16,
+                                                    reinterpret_cast<double*>(flush));
+      } else {  // L2 holds dirty lines: every miss of the timed kernel also writes one back
+        VTS_CUDA(cudaMemsetAsync(flush, r & 0xff, flush_bytes, c->stream));
+      }
       VTS_CUDA(cudaEventRecord(e0, c->stream));
       if (int rc = body()) return rc;
       VTS_CUDA(cudaEventRecord(e1, c->stream));
@@ -2379,7 +2408,17 @@ int time_cold(Ctx* c, int reps, void* flush, size_t flush_bytes, double* ms) {
   };
   int rc = 0;
   rc = rc ? rc : timed([&] { return newton_apply_grid(c, xin, yout, nullptr); }, ms + 0);
-  rc = rc ? rc : timed([&] { return level_residual_grid(c, top, F.x, xin, F.r, nullptr); }, ms + 1);
+  const char* fl = getenv("VTS_TIME_FLOOR");
+  if (fl && fl[0] == '1') {  // diagnostic: a plain streaming kernel over the apply's bytes instead of the residual
+    rc = rc ? rc : timed([&] {
+      k_stream_floor<<<2 * 148 * 8, 256, 0, c->stream>>>(F.d.nnodes, c->m, reinterpret_cast<const double2*>(xin),
+                                                        reinterpret_cast<const double2*>(c->u_grid), c->rho_hat,
+                                                        c->chat, reinterpret_cast<double2*>(yout));
+      return (int)cudaGetLastError();
+    }, ms + 1);
+  } else {
+    rc = rc ? rc : timed([&] { return level_residual_grid(c, top, F.x, xin, F.r, nullptr); }, ms + 1);
+  }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   return rc;
