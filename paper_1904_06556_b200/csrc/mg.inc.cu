@@ -375,6 +375,9 @@ __global__ void k_prolong_add(int fnx, int fny, const uint8_t* __restrict__ ffm,
 #define VTS_OVL_SLEEP 128
 #endif
 constexpr int kChunk = 128;
+// Row band height of the wavefront sweeps (gs::R, defined with the sweeps below):
+// the overlap passes index the sweeps' per-band flags with it
+constexpr int kBandRows = 16;
 // spin of a helper pass on a flag: backs off so that its polls stay out of the
 // L2 traffic of the pairs it runs beside
 VTS_DEVICE_INLINE void wait_flag_backoff(const unsigned long long* f, unsigned long long need) {
@@ -388,7 +391,7 @@ __global__ void __launch_bounds__(1024) k_prolong_rows(int fnx, int fny, const u
                                                        unsigned long long* ready, unsigned long long tag, const int* skip) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (skip && ld_relaxed_i32(skip)) return;
-  constexpr int R = 16;  // gs::R (row band height of the sweeps)
+  constexpr int R = kBandRows;
   const int fbands = (fny + R - 1) / R, nch = (fnx + kChunk - 1) / kChunk;
   VTS_TL_BEGIN(3, fnx);
   int g = 0;
@@ -469,7 +472,7 @@ __global__ void __launch_bounds__(1024) k_residual_restrict_rows(
     const int* skip) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (skip && ld_relaxed_i32(skip)) return;
-  constexpr int R = 16;
+  constexpr int R = kBandRows;
   const int fbands = (ny + R - 1) / R, cbands = (cny + R - 1) / R;
   const int items = cbands * 3 * kSeg;
   VTS_TL_BEGIN(2, nx);
@@ -804,6 +807,7 @@ VTS_DEVICE_INLINE long long gtimer() {
 #endif
 namespace gs {
 constexpr int R = 16;      // grid rows (compute lanes) per band / CTA
+static_assert(R == kBandRows, "the overlap passes (k_prolong_rows, k_residual_restrict_rows) assume this band height");
 #ifndef VTS_GS_W
 #define VTS_GS_W 17
 #endif
@@ -1025,7 +1029,11 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
   auto grid_ix = [&](int w, int l, int p) { return FWD ? W * w - SKEW * l + p : nx - W * (w + 1) + SKEW * l + p; };
 
   if (!real) {
-    // padding CTA of the last cluster: only the cluster barriers
+    // padding CTA of the last cluster: no peer reads or writes its shared memory
+    // (it neither sends nor receives a band handoff), so it leaves after the
+    // start-up barrier and frees its SM; barrier.cluster.wait only waits for
+    // threads that have not exited (pair_ctas counts real bands only)
+    return;
   } else if (warp == 1) {  // ---------------- loader (one thread, TMA boxes)
     if (lane == 0) {
       const int iy0 = band * R, iyb = ny - 1 - band * R;
@@ -2010,7 +2018,10 @@ static int sm_count() {
   }();
   return n;
 }
-// pair CTAs of level k (one per SM)
+// pair CTAs of level k that hold an SM for the whole sweep (one per SM): two per band.
+// gs_pair pads each half of the grid to whole clusters (2 cs ncl CTAs), but a
+// padding CTA (band >= bands) leaves right after the start-up cluster barrier
+// (gs_band), so it holds no SM the overlap passes need.
 static int pair_ctas(const Ctx* c, int k) { return 2 * div_up(c->lv[k].d.ny, gs::R); }
 
 // One smoothing step of level k exactly as the V-cycle runs it (two sweeps, the
