@@ -331,6 +331,63 @@ int vts_time_kernels(vts_ctx* ctx, int32_t reps, double* ms);
  */
 int vts_time_cold(vts_ctx* ctx, int32_t reps, void* flush, int64_t flush_bytes, double* ms);
 
+/*
+ * One damped Newton step of newton_inner (pbm.py:273-325) resident on the
+ * device: schur_system (pbm.py:202-218), MgPreconditioner (multigrid.py:82-103,
+ * the shifted retry of the coarse factor decided on the device), minres_solve
+ * (linalg.py:128-242: its start-up checks on the device, the iteration loop
+ * polled without stalling the stream), the direction's bound-multiplier part
+ * and slope (pbm.py:221-232, 290-295), the Armijo search (pbm.py:296-318: the
+ * trial steps, the sufficient-decrease test and the halving on the device), the
+ * update of u, alpha, nu (pbm.py:320-323, in place) and eval_lagrangian at the
+ * new point (pbm.py:324) -- with one host synchronisation after the MINRES loop
+ * in the common case (a second when the search needs more than two trials).
+ * The Newton-system setup and the search/update/evaluation phase are replayed
+ * as CUDA graphs when the buffers are the ones of the previous step.
+ * Every pointer is a DEVICE pointer; `args` and `result` are HOST structs.
+ * Returns VTS_OK (result->status: 0 step taken, 1 non-descent direction,
+ * 2 line search exhausted -- newton_inner's stall outcomes; the state and the
+ * evaluation are then unchanged), a MINRES error code (the solve's last sound
+ * iterate is in `du`), or VTS_E_CHOLESKY.
+ */
+typedef struct {
+  /* state: u (n), nu_lo, nu_up (m) updated in place; alpha in/out through result */
+  double* u;
+  double* nu_lo;
+  double* nu_up;
+  double alpha;
+  const double *rho, *p, *mu_lo, *mu_up, *q_lo, *q_up;
+  /* problem data (f free order, bounds per element) */
+  const double *f, *lower, *upper;
+  double volume, norm_f, norm_bounds, branch;
+  /* evaluation at the current point (eval_lagrangian's outputs), overwritten with the one at the new point */
+  double *res_u, *res_lo, *res_up, *q, *mu_hat_lo, *mu_hat_up, *a, *b_lo, *b_up, *rho_hat;
+  double value, res_alpha;
+  /* workspace owned by the caller: chat (m), rhs (n+1), border (n), du (n+1), dnu_lo, dnu_up (m) */
+  double *chat, *rhs, *border, *du, *dnu_lo, *dnu_up;
+  /* controls (PbmConfig / MinresConfig) */
+  double minres_tol, minres_floor;
+  int32_t minres_cap;
+  double armijo_c1, armijo_shrink;
+  int32_t armijo_max_halvings;
+  double shift_scale;
+} vts_newton_step_args;
+
+typedef struct {
+  int32_t status;          /* 0 step taken; 1 non-descent direction; 2 line search exhausted */
+  int32_t minres_iterations, minres_converged;
+  double minres_relres;
+  double kappa, slope, dalpha;
+  double alpha;            /* alpha after the step */
+  double scalars[8];       /* eval_lagrangian's scalars at the new point (value, res_alpha, tau_res, ...) */
+  uint32_t warnings;       /* VTS_W_SATURATED / VTS_W_SHIFTED raised during the step */
+  int32_t trials;          /* Armijo trial values evaluated */
+  int32_t host_syncs;      /* host synchronisations the step made (MINRES status polls excluded) */
+  int32_t graphs;          /* CUDA graph launches of the step */
+} vts_newton_step_result;
+
+int vts_newton_step(vts_ctx* ctx, const vts_newton_step_args* args, vts_newton_step_result* result);
+
 /* Number of kernels this context launched since creation (evidence counter). */
 int64_t vts_kernel_launches(const vts_ctx* ctx);
 

@@ -79,6 +79,31 @@ SIGNATURES = {
     "vts_profile_end": (ctypes.c_int, [_P, _PD]),
 }
 
+
+class NewtonStepArgs(ctypes.Structure):
+    """vts_newton_step_args (include/vts_b200.h): device pointers, scalars, controls."""
+
+    _fields_ = ([("u", _P), ("nu_lo", _P), ("nu_up", _P), ("alpha", _D)]
+                + [(k, _P) for k in ("rho", "p", "mu_lo", "mu_up", "q_lo", "q_up", "f", "lower", "upper")]
+                + [(k, _D) for k in ("volume", "norm_f", "norm_bounds", "branch")]
+                + [(k, _P) for k in ("res_u", "res_lo", "res_up", "q", "mu_hat_lo", "mu_hat_up", "a", "b_lo", "b_up",
+                                     "rho_hat")]
+                + [("value", _D), ("res_alpha", _D)]
+                + [(k, _P) for k in ("chat", "rhs", "border", "du", "dnu_lo", "dnu_up")]
+                + [("minres_tol", _D), ("minres_floor", _D), ("minres_cap", _I32), ("armijo_c1", _D),
+                   ("armijo_shrink", _D), ("armijo_max_halvings", _I32), ("shift_scale", _D)])
+
+
+class NewtonStepResult(ctypes.Structure):
+    """vts_newton_step_result (include/vts_b200.h)."""
+
+    _fields_ = [("status", _I32), ("minres_iterations", _I32), ("minres_converged", _I32), ("minres_relres", _D),
+                ("kappa", _D), ("slope", _D), ("dalpha", _D), ("alpha", _D), ("scalars", _D * 8),
+                ("warnings", ctypes.c_uint32), ("trials", _I32), ("host_syncs", _I32), ("graphs", _I32)]
+
+
+SIGNATURES["vts_newton_step"] = (ctypes.c_int, [_P, ctypes.POINTER(NewtonStepArgs), ctypes.POINTER(NewtonStepResult)])
+
 # int (*vts_apply_fn)(void* user, const double* in, double* out): device vectors
 APPLY_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
 

@@ -51,7 +51,8 @@ struct MinresDev {
   int iters, max_iters, stopped, status, no_verify, pad;
 };
 
-enum MinresStatus { kRunning = 0, kConverged = 1, kCap = 2, kIndefinite = -1, kBreakdown = -2, kNonfinite = -3 };
+enum MinresStatus { kRunning = 0, kConverged = 1, kCap = 2, kIndefinite = -1, kBreakdown = -2, kNonfinite = -3,
+                    kCholFail = -4 };
 
 struct Hex;  // 3D hexahedral data (hex3d.inc.cu)
 
@@ -86,6 +87,7 @@ struct Ctx {
   double* chol = nullptr;       // [N0 * N0] lower factor (row-major)
   double* chol_rdiag = nullptr; // [N0] correctly rounded reciprocals of its diagonal
   int* chol_status = nullptr;   // device status
+  int* chol_retry = nullptr;    // device: the plain factor failed, the shifted one was built (device-gated setup)
 
   double* rap_tmp = nullptr;    // unsymmetrised coarse stencil of the largest coarse level
 
@@ -107,6 +109,9 @@ struct Ctx {
   MinresDev* mst = nullptr;     // device MINRES state
   MinresDev* hmst = nullptr;    // pinned host mirror, [2]: the two iterations in flight
   cudaEvent_t mr_ev[2] = {nullptr, nullptr};  // their state copies have landed
+
+  // device-resident Newton step (step.inc.cu), allocated on first use
+  struct StepState* step = nullptr;
 
   // DOC workspace (doc.inc.cu: sorted energies, scans, CUB scratch), allocated on first use
   void* doc_ws = nullptr;
@@ -205,7 +210,7 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 inline int div_up(long long a, long long b) { return (int)((a + b - 1) / b); }
 
 // ---- element / nodal passes (elem_kernels.cu) ----
-int free_to_grid(Ctx* c, int level, const double* src, double* dst, bool bordered);
+int free_to_grid(Ctx* c, int level, const double* src, double* dst, bool bordered, const int* skip = nullptr);
 int grid_to_free(Ctx* c, int level, const double* src, double* dst, bool bordered);
 int eval_lagrangian(Ctx* c, const double* u, double alpha, const double* nu_lo, const double* nu_up,
                     const double* rho, const double* mu_lo, const double* mu_up, const double* p,
@@ -213,11 +218,12 @@ int eval_lagrangian(Ctx* c, const double* u, double alpha, const double* nu_lo, 
                     const double* upper, double volume, double norm_f, double norm_bounds,
                     double branch, double* res_u, double* res_lo, double* res_up, double* q,
                     double* mu_hat_lo, double* mu_hat_up, double* a, double* b_lo, double* b_up,
-                    double* rho_hat, double* w_out, double* scalars, unsigned* warn);
+                    double* rho_hat, double* w_out, double* scalars, unsigned* warn,
+                    const double* alpha_dev = nullptr, const int* skip = nullptr);
 int schur_system(Ctx* c, const double* u, const double* res_u, double res_alpha,
                  const double* res_lo, const double* res_up, const double* a, const double* b_lo,
                  const double* b_up, const double* rho_hat, double* chat, double* rhs,
-                 double* border, double* corner);
+                 double* border, double* corner, const double* res_alpha_dev = nullptr);
 int reconstruct_nu(Ctx* c, const double* u, const double* du, double dalpha, const double* res_u,
                    double res_alpha, const double* res_lo, const double* res_up, const double* a,
                    const double* b_lo, const double* b_up, double* dnu_lo, double* dnu_up,
@@ -247,7 +253,9 @@ int level_apply_grid(Ctx* c, int k, const double* x, double* y, const int* skip)
 int level_residual_grid(Ctx* c, int k, const double* x, const double* b, double* r, const int* skip);
 
 // ---- multigrid (mg.cu) ----
-int mg_setup(Ctx* c, double shift_scale);
+// device_gate: the coarse factor's shifted retry (multigrid.py:92-103) is enqueued
+// behind device flags instead of a host read-back of the factor status (no sync)
+int mg_setup(Ctx* c, double shift_scale, bool device_gate = false);
 int vcycle_grid(Ctx* c, const double* b, double* z, const int* skip);
 int debug_smooth(Ctx* c, int k, bool forward, bool zero_first, const double* b_free, double* x_free);
 int profile_begin(Ctx* c);
@@ -256,7 +264,7 @@ int profile_end(Ctx* c, double* out);
 // ---- MINRES (minres.cu) ----
 int minres(Ctx* c, const double* b_free, double* x_free, double tol, int max_iters,
            double floor_tol, int precondition, int* iters, double* relres, int* converged,
-           double* history, const double* x0_free = nullptr);
+           double* history, const double* x0_free = nullptr, bool device_init = false);
 
 // ---- generic reductions (elem_kernels.cu) ----
 // dot of two grid vectors (free dofs only are nonzero) incl. the border slot
@@ -267,6 +275,9 @@ int dot_grid(Ctx* c, int level, const double* a, const double* b, bool bordered,
 int minres_generic(Ctx* c, long long len, const double* b, double* x_out, const double* x0, double tol,
                    int max_iters, double floor_tol, vts_apply_fn op, vts_apply_fn prec, void* user,
                    int* iters_out, double* relres_out, int* conv_out, double* history, bool native = false);
+
+// ---- device-resident Newton step (step.inc.cu) ----
+int newton_step(Ctx* c, const vts_newton_step_args* a, vts_newton_step_result* r);
 
 // ---- DOC reuse (doc.inc.cu) ----
 int bind_stiffness(Ctx* c, const double* rho, unsigned* warn);

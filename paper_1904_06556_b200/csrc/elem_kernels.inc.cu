@@ -148,7 +148,8 @@ VTS_DEVICE_INLINE NodeElems node_elems(int ix, int iy, int ex, int ey) {
 // ---------------------------------------------------------------------------
 __global__ void k_free_to_grid(int ngrid, int nfree, const int32_t* __restrict__ g2f,
                                const double* __restrict__ src, double* __restrict__ dst,
-                               int bordered) {
+                               int bordered, const int* skip = nullptr) {
+  if (skip && *skip) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < ngrid) {
     const int f = g2f[i];
@@ -168,10 +169,15 @@ __global__ void k_grid_to_free(int nfree, int ngrid, const int32_t* __restrict__
 }
 
 // trial displacement u + kappa du on the grid, with f . (u + kappa du)
+// kappa_dev / skip (device-resident Newton step, step.inc.cu): the trial step from device
+// memory, and the launch is a no-op once the line search has decided
 __global__ void k_trial_grid(int ngrid, const int32_t* __restrict__ g2f, const double* __restrict__ u,
                              const double* __restrict__ du, double kappa,
                              const double* __restrict__ f, double* __restrict__ out,
-                             double* partials, unsigned* counter, double* result) {
+                             double* partials, unsigned* counter, double* result,
+                             const double* kappa_dev = nullptr, const int* skip = nullptr) {
+  if (skip && *skip) return;
+  if (kappa_dev) kappa = *kappa_dev;
   __shared__ double scratch[kThreads / 32];
   double acc[1] = {0.0};
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ngrid; i += gridDim.x * blockDim.x) {
@@ -200,7 +206,10 @@ __global__ void k_dot(long long len, const double* __restrict__ a, const double*
   if (last_block_reduce<1>(acc, scratch, partials, counter, tot) && threadIdx.x == 0) result[0] = tot[0];
 }
 
-__global__ void k_axpy(long long len, double kappa, const double* __restrict__ dx, double* x) {
+__global__ void k_axpy(long long len, double kappa, const double* __restrict__ dx, double* x,
+                       const double* kappa_dev = nullptr, const int* skip = nullptr) {
+  if (skip && *skip) return;
+  if (kappa_dev) kappa = *kappa_dev;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < len;
        i += (long long)gridDim.x * blockDim.x)
     x[i] = __dadd_rn(x[i], __dmul_rn(kappa, dx[i]));
@@ -215,12 +224,16 @@ struct PhiElemArgs {
   double alpha, branch;
   const double *nu_lo, *nu_up, *rho, *mu_lo, *mu_up, *p, *q_lo, *q_up, *lower, *upper;
   double *q, *rho_hat, *mu_hat_lo, *mu_hat_up, *a, *b_lo, *b_up, *res_lo, *res_up, *w_out;
+  const double* alpha_dev = nullptr;  // device-resident Newton step: alpha from device memory
+  const int* skip = nullptr;          //   and the evaluation is skipped while *skip != 0
 };
 
 __global__ void __launch_bounds__(kThreads, 2) k_phi_elem(PhiElemArgs A, double* partials, unsigned* flags) {
+  if (A.skip && *A.skip) return;
   __shared__ double scratch[7 * kThreads / 32];
   double acc[7] = {0, 0, 0, 0, 0, 0, 0};
   unsigned sat = 0;
+  const double alpha = A.alpha_dev ? *A.alpha_dev : A.alpha;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < A.m; e += gridDim.x * blockDim.x) {
     int nd[4];
     elem_nodes(e, A.ex, A.nx, nd);
@@ -233,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_phi_elem(PhiElemArgs A, double*
     qq = 0.5 * qq;
     const double nlo = A.nu_lo[e], nup = A.nu_up[e], pe = A.p[e], qlo = A.q_lo[e], qup = A.q_up[e];
     const double rh = A.rho[e], mlo = A.mu_lo[e], mup = A.mu_up[e];
-    const double s = __dsub_rn(__dadd_rn(__dsub_rn(qq, A.alpha), nlo), nup);
+    const double s = __dsub_rn(__dadd_rn(__dsub_rn(qq, alpha), nlo), nup);
     const PhiOut f1 = phi_eval(s / pe, A.branch, &sat);
     const PhiOut f2 = phi_eval(-nlo / qlo, A.branch, &sat);
     const PhiOut f3 = phi_eval(-nup / qup, A.branch, &sat);
@@ -274,7 +287,9 @@ __global__ void __launch_bounds__(kThreads) k_phi_node(int nnodes, int nx, int e
                                                      const double* __restrict__ rho_hat,
                                                      const double* __restrict__ f,
                                                      const int32_t* __restrict__ g2f,
-                                                     double* __restrict__ res_u, double* partials) {
+                                                     double* __restrict__ res_u, double* partials,
+                                                     const int* skip = nullptr) {
+  if (skip && *skip) return;
   __shared__ double scratch[2 * kThreads / 32];
   double acc[2] = {0, 0};
   for (int nd = blockIdx.x * blockDim.x + threadIdx.x; nd < nnodes; nd += gridDim.x * blockDim.x) {
@@ -312,7 +327,10 @@ __global__ void __launch_bounds__(kThreads) k_phi_node(int nnodes, int nx, int e
 // sums the two partial arrays and forms the eval scalars
 __global__ void k_phi_finish(int nb_e, const double* __restrict__ pe, int nb_n,
                              const double* __restrict__ pn, double alpha, double volume,
-                             double norm_f, double norm_bounds, double* out) {
+                             double norm_f, double norm_bounds, double* out, const double* alpha_dev = nullptr,
+                             const int* skip = nullptr) {
+  if (skip && *skip) return;
+  if (alpha_dev) alpha = *alpha_dev;
   __shared__ double scratch[9 * kThreads / 32];
   double t[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (int b = threadIdx.x; b < nb_e; b += blockDim.x)
@@ -412,7 +430,8 @@ __global__ void __launch_bounds__(kThreads) k_schur_node(int nnodes, int nx, int
 }
 
 __global__ void k_schur_finish(int nb, const double* __restrict__ pe, double res_alpha, double sign, int n,
-                               double* rhs, double* d_corner, double* out) {
+                               double* rhs, double* d_corner, double* out, const double* res_alpha_dev = nullptr) {
+  if (res_alpha_dev) res_alpha = *res_alpha_dev;
   __shared__ double scratch[2 * kThreads / 32];
   double t[2] = {0, 0};
   for (int b = threadIdx.x; b < nb; b += blockDim.x) {
@@ -440,9 +459,10 @@ __global__ void __launch_bounds__(kThreads) k_recon_elem(int m, int ex, int nx,
                                                        const double* __restrict__ b_lo,
                                                        const double* __restrict__ b_up,
                                                        double* dnu_lo, double* dnu_up,
-                                                       double* partials) {
+                                                       double* partials, const double* dalpha_dev = nullptr) {
   __shared__ double scratch[2 * kThreads / 32];
   double acc[2] = {0, 0};
+  if (dalpha_dev) dalpha = *dalpha_dev;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
     int nd[4];
     elem_nodes(e, ex, nx, nd);
@@ -473,12 +493,26 @@ struct AlElemArgs {
   const double* ug;  // trial u on the grid
   double alpha, kappa, branch;
   const double *nu_lo, *nu_up, *dnu_lo, *dnu_up, *rho, *p, *mu_lo, *mu_up, *q_lo, *q_up, *lower, *upper;
+  // device-resident Newton step: alpha, kappa and dalpha from device memory (the trial
+  // alpha + kappa dalpha then formed here, in pbm.py:301's two roundings); skip: the
+  // line search has decided
+  const double *alpha_dev = nullptr, *kappa_dev = nullptr, *dalpha_dev = nullptr;
+  const int* skip = nullptr;
 };
 
+VTS_DEVICE_INLINE double trial_alpha(double alpha, double kappa, double dalpha) {
+  return __dadd_rn(alpha, __dmul_rn(kappa, dalpha));
+}
+
 __global__ void __launch_bounds__(kThreads) k_al_elem(AlElemArgs A, double* partials, unsigned* flags) {
+  if (A.skip && *A.skip) return;
   __shared__ double scratch[5 * kThreads / 32];
   double acc[5] = {0, 0, 0, 0, 0};
   unsigned sat = 0;
+  if (A.kappa_dev) {
+    A.kappa = *A.kappa_dev;
+    A.alpha = trial_alpha(*A.alpha_dev, A.kappa, *A.dalpha_dev);
+  }
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < A.m; e += gridDim.x * blockDim.x) {
     int nd[4];
     elem_nodes(e, A.ex, A.nx, nd);
@@ -507,7 +541,11 @@ __global__ void __launch_bounds__(kThreads) k_al_elem(AlElemArgs A, double* part
 }
 
 __global__ void k_al_finish(int nb, const double* __restrict__ pe, const double* __restrict__ fu_ptr,
-                            double alpha, double volume, double* out) {
+                            double alpha, double volume, double* out, const double* alpha_dev = nullptr,
+                            const double* kappa_dev = nullptr, const double* dalpha_dev = nullptr,
+                            const int* skip = nullptr) {
+  if (skip && *skip) return;
+  if (kappa_dev) alpha = trial_alpha(*alpha_dev, *kappa_dev, *dalpha_dev);
   __shared__ double scratch[5 * kThreads / 32];
   double t[5] = {0, 0, 0, 0, 0};
   for (int b = threadIdx.x; b < nb; b += blockDim.x)
@@ -601,11 +639,11 @@ static int sync_scalars(Ctx* c, int count) {
   return 0;
 }
 
-int free_to_grid(Ctx* c, int level, const double* src, double* dst, bool bordered) {
+int free_to_grid(Ctx* c, int level, const double* src, double* dst, bool bordered, const int* skip) {
   const LevelBuf& L = c->lv[level];
   const int total = L.d.ngrid + 1;
   k_free_to_grid<<<div_up(total, kThreads), kThreads, 0, c->stream>>>(L.d.ngrid, L.d.nfree, L.grid2free,
-                                                                      src, dst, border_mode(c, bordered));
+                                                                      src, dst, border_mode(c, bordered), skip);
   VTS_LAUNCHED(c);
   return 0;
 }
@@ -627,32 +665,37 @@ int dot_grid(Ctx* c, int level, const double* a, const double* b, bool bordered,
   return 0;
 }
 
+// alpha_dev != null (device-resident Newton step, step.inc.cu): alpha is read from
+// device memory, nothing is read back (the eight scalars stay in dscal[0..7], the
+// saturation bit accumulates in dflags) and the stream is not synchronised
 int eval_lagrangian(Ctx* c, const double* u, double alpha, const double* nu_lo, const double* nu_up,
                     const double* rho, const double* mu_lo, const double* mu_up, const double* p,
                     const double* q_lo, const double* q_up, const double* f, const double* lower,
                     const double* upper, double volume, double norm_f, double norm_bounds,
                     double branch, double* res_u, double* res_lo, double* res_up, double* q,
                     double* mu_hat_lo, double* mu_hat_up, double* a, double* b_lo, double* b_up,
-                    double* rho_hat, double* w_out, double* scalars, unsigned* warn) {
+                    double* rho_hat, double* w_out, double* scalars, unsigned* warn, const double* alpha_dev,
+                    const int* skip) {
   const int F = c->L - 1;
   const LevelDev& d = c->lv[F].d;
   double* ug = c->fvec[0];
-  if (int rc = free_to_grid(c, F, u, ug, false)) return rc;
-  VTS_CUDA(cudaMemsetAsync(c->dflags, 0, sizeof(unsigned), c->stream));
+  if (int rc = free_to_grid(c, F, u, ug, false, skip)) return rc;
+  if (!alpha_dev) VTS_CUDA(cudaMemsetAsync(c->dflags, 0, sizeof(unsigned), c->stream));
   PhiElemArgs A{c->m, d.ex, d.nx, ug, alpha, branch, nu_lo, nu_up, rho, mu_lo, mu_up, p, q_lo,
                 q_up, lower, upper, q, rho_hat, mu_hat_lo, mu_hat_up, a, b_lo, b_up, res_lo,
-                res_up, w_out};
+                res_up, w_out, alpha_dev, skip};
   const int ge = reduce_grid(c->m);
   k_phi_elem<<<ge, kThreads, 0, c->stream>>>(A, c->partials, c->dflags);
   VTS_LAUNCHED(c);
   const int gn = reduce_grid(d.nnodes);
   double* pn = c->partials + kMaxBlocks * 8;
   k_phi_node<<<gn, kThreads, 0, c->stream>>>(d.nnodes, d.nx, d.ex, d.ey, ug, rho_hat, f, c->lv[F].grid2free,
-                                              res_u, pn);
+                                              res_u, pn, skip);
   VTS_LAUNCHED(c);
   k_phi_finish<<<1, kThreads, 0, c->stream>>>(ge, c->partials, gn, pn, alpha, volume, norm_f, norm_bounds,
-                                               c->dscal);
+                                               c->dscal, alpha_dev, skip);
   VTS_LAUNCHED(c);
+  if (alpha_dev) return 0;
   VTS_CUDA(cudaMemcpyAsync(c->hscal + 16, c->dflags, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
   if (int rc = sync_scalars(c, 8)) return rc;
   for (int i = 0; i < 8; ++i) scalars[i] = c->hscal[i];
@@ -660,10 +703,12 @@ int eval_lagrangian(Ctx* c, const double* u, double alpha, const double* nu_lo, 
   return 0;
 }
 
+// res_alpha_dev != null (device-resident Newton step): res_alpha from device memory,
+// no read-back of the corner (it stays in d_corner) and no synchronisation
 int schur_system(Ctx* c, const double* u, const double* res_u, double res_alpha,
                  const double* res_lo, const double* res_up, const double* a, const double* b_lo,
                  const double* b_up, const double* rho_hat, double* chat, double* rhs,
-                 double* border, double* corner) {
+                 double* border, double* corner, const double* res_alpha_dev) {
   const int F = c->L - 1;
   const LevelDev& d = c->lv[F].d;
   if (int rc = free_to_grid(c, F, u, c->u_grid, false)) return rc;
@@ -676,11 +721,14 @@ int schur_system(Ctx* c, const double* u, const double* res_u, double res_alpha,
                                                                    tcoef, c->chat, res_u, c->lv[F].grid2free,
                                                                    rhs, border, c->lv[F].d.border);
   VTS_LAUNCHED(c);
-  k_schur_finish<<<1, kThreads, 0, c->stream>>>(ge, c->partials, res_alpha, 1.0, c->n, rhs, c->d_corner, c->dscal);
+  k_schur_finish<<<1, kThreads, 0, c->stream>>>(ge, c->partials, res_alpha, 1.0, c->n, rhs, c->d_corner, c->dscal,
+                                                res_alpha_dev);
   VTS_LAUNCHED(c);
-  if (int rc = sync_scalars(c, 2)) return rc;
-  c->corner = c->hscal[0];
-  if (corner) *corner = c->corner;
+  if (!res_alpha_dev) {
+    if (int rc = sync_scalars(c, 2)) return rc;
+    c->corner = c->hscal[0];
+    if (corner) *corner = c->corner;
+  }
   c->system_bound = true;
   c->border_flip = false;
   c->unbordered = false;

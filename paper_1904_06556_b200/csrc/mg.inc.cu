@@ -1605,8 +1605,9 @@ __global__ void k_alpha_relax(int ngrid, const double* __restrict__ border, cons
 __global__ void k_dense_coarse(int nx, int ny, const double* __restrict__ stL, const double* __restrict__ stU,
                                const double* __restrict__ border,
                                const int32_t* __restrict__ g2f, const double* corner, int N, double shift,
-                               double* __restrict__ A) {
+                               double* __restrict__ A, const int* gate = nullptr) {
   // one thread per (free row, neighbour block) ; zero-fill first via memset
+  if (gate && *gate == 0) return;  // device-gated retry (mg_setup's device_gate): nothing to redo
   const int nd = blockIdx.x * blockDim.x + threadIdx.x;
   if (nd >= nx * ny) return;
   const int ix = nd % nx, iy = nd / nx;
@@ -1628,8 +1629,9 @@ __global__ void k_dense_coarse(int nx, int ny, const double* __restrict__ stL, c
   if (nd == 0) A[(size_t)(N - 1) * N + (N - 1)] = *corner;
 }
 
-__global__ void k_add_shift(int N, double scale, double* A, double* trace_out) {
+__global__ void k_add_shift(int N, double scale, double* A, double* trace_out, const int* gate = nullptr) {
   // single block: trace, then A += scale * trace / N * I
+  if (gate && *gate == 0) return;
   __shared__ double scratch[1024 / 32];
   double t[1] = {0.0};
   for (int i = threadIdx.x; i < N; i += blockDim.x) t[0] += A[(size_t)i * N + i];
@@ -1644,7 +1646,8 @@ __global__ void k_add_shift(int N, double scale, double* A, double* trace_out) {
 }
 
 // in-place lower Cholesky, left-looking by columns, one CTA; status 0 ok, 1 fail
-__global__ void __launch_bounds__(1024) k_cholesky(int N, double* A, int* status) {
+__global__ void __launch_bounds__(1024) k_cholesky(int N, double* A, int* status, const int* gate = nullptr) {
+  if (gate && *gate == 0) return;
   __shared__ double scratch[1024 / 32];
   __shared__ double s_diag;
   __shared__ int s_fail;
@@ -1680,6 +1683,16 @@ __global__ void __launch_bounds__(1024) k_cholesky(int N, double* A, int* status
 VTS_DEVICE_INLINE double div_by(double y, double d, double r) {
   const double q = y * r;
   return fma(fma(-q, d, y), r, q);
+}
+
+// device-gated retry of the coarse factor: retry = the first attempt failed; then the
+// dense matrix is zeroed for the shifted rebuild (the memset of the host path)
+__global__ void k_chol_retry_prep(int N, double* __restrict__ A, const int* __restrict__ status, int* retry) {
+  const bool failed = *status != 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *retry = failed ? 1 : 0;
+  if (!failed) return;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < (size_t)N * N; i += (size_t)gridDim.x * blockDim.x)
+    A[i] = 0.0;
 }
 
 __global__ void k_chol_rdiag(int N, const double* __restrict__ Lf, double* __restrict__ rdiag) {
@@ -2208,7 +2221,7 @@ int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
   return 0;
 }
 
-int mg_setup(Ctx* c, double shift_scale) {
+int mg_setup(Ctx* c, double shift_scale, bool device_gate) {
   if (!c->system_bound) {
     set_error(4, "mg_setup: no Newton system bound (call vts_schur_system first)");
     return 4;
@@ -2239,6 +2252,25 @@ int mg_setup(Ctx* c, double shift_scale) {
   // coarsest dense factor
   LevelBuf& C = c->lv[0];
   const int N = c->N0;
+  if (device_gate) {
+    // the same two attempts (multigrid.py:92-103) with the retry decided on the device:
+    // chol_retry = the plain factor failed (then the shifted factor's status is final)
+    VTS_CUDA(cudaMemsetAsync(c->chol, 0, sizeof(double) * N * N, c->stream));
+    k_dense_coarse<<<div_up(C.d.nnodes, 128), 128, 0, c->stream>>>(C.d.nx, C.d.ny, C.d.stL, C.d.stU, C.d.border,
+                                                                    C.grid2free, c->d_corner, N, 0.0, c->chol);
+    k_cholesky<<<1, 1024, 0, c->stream>>>(N, c->chol, c->chol_status);
+    k_chol_retry_prep<<<div_up((long long)N * N, 256), 256, 0, c->stream>>>(N, c->chol, c->chol_status, c->chol_retry);
+    k_dense_coarse<<<div_up(C.d.nnodes, 128), 128, 0, c->stream>>>(C.d.nx, C.d.ny, C.d.stL, C.d.stU, C.d.border,
+                                                                    C.grid2free, c->d_corner, N, 0.0, c->chol,
+                                                                    c->chol_retry);
+    k_add_shift<<<1, 1024, 0, c->stream>>>(N, shift_scale, c->chol, c->dscal + 20, c->chol_retry);
+    k_cholesky<<<1, 1024, 0, c->stream>>>(N, c->chol, c->chol_status, c->chol_retry);
+    k_chol_rdiag<<<1, 256, 0, c->stream>>>(c->N0, c->chol, c->chol_rdiag);
+    c->launches += 7;
+    VTS_CUDA(cudaGetLastError());
+    c->mg_ready = true;
+    return 0;
+  }
   auto build = [&](double shift_scale_now) -> int {
     VTS_CUDA(cudaMemsetAsync(c->chol, 0, sizeof(double) * N * N, c->stream));
     k_dense_coarse<<<div_up(C.d.nnodes, 128), 128, 0, c->stream>>>(C.d.nx, C.d.ny, C.d.stL, C.d.stU, C.d.border,

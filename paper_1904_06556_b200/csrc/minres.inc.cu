@@ -231,9 +231,59 @@ __global__ void k_sub_norm(int len, const double* __restrict__ b, const double* 
   if (last_block_reduce<1>(acc, scratch, partials, counter, tot) && threadIdx.x == 0) *out = tot[0];
 }
 
+// Device-side start of a solve (device_init): the checks the host path makes on
+// read-back scalars (||b|| = 0, beta1 <= 0, linalg.py:144-180) are made by these two
+// one-thread kernels, which set the state so that the iteration loop's launches are
+// no-ops and its first status poll reports the outcome.
+__global__ void k_mr_init0(const double* __restrict__ bnorm2, MinresDev* st, double tol, int cap) {
+  MinresDev h{};
+  h.bnorm = sqrt(*bnorm2);
+  h.tol = tol;
+  h.max_iters = cap;
+  h.verify_at = tol;
+  h.relres = INFINITY;
+  h.cs = -1.0;
+  h.no_verify = 1;
+  h.status = kRunning;
+  if (h.bnorm == 0.0) {  // x = 0 is exact (linalg.py:141-142)
+    h.stopped = 1;
+    h.status = kConverged;
+    h.relres = 0.0;
+  }
+  *st = h;
+}
+__global__ void k_mr_init1(const double* __restrict__ beta1_sq, const int* __restrict__ chol_status, MinresDev* st) {
+  if (st->stopped) return;
+  if (chol_status && *chol_status != 0) {  // the (shifted) coarse factor failed: mg_setup's error
+    st->status = kCholFail;
+    st->stopped = 1;
+    return;
+  }
+  const double b1 = *beta1_sq;
+  if (b1 < 0.0) {
+    st->status = kIndefinite;
+    st->stopped = 1;
+    return;
+  }
+  if (b1 == 0.0) {  // the start iterate is the answer; relres = ||b - A 0|| / ||b||
+    st->status = kConverged;
+    st->stopped = 1;
+    st->relres = 1.0;
+    return;
+  }
+  const double beta1 = sqrt(b1);
+  st->beta1 = beta1;
+  st->beta = beta1;
+  st->phibar = beta1;
+}
+
 int minres(Ctx* c, const double* b_free, double* x_free, double tol, int max_iters, double floor_tol,
            int precondition, int* iters_out, double* relres_out, int* conv_out, double* history,
-           const double* x0_free) {
+           const double* x0_free, bool device_init) {
+  if (device_init && (history || x0_free || !precondition)) {
+    set_error(4, "minres: the device-side start needs a preconditioned cold start without history");
+    return 4;
+  }
   if (!c->system_bound || (precondition && !c->mg_ready)) {
     set_error(4, "minres: bind the Newton system (and set up the multigrid) first");
     return 4;
@@ -249,13 +299,19 @@ int minres(Ctx* c, const double* b_free, double* x_free, double tol, int max_ite
   if (int rc = free_to_grid(c, F, b_free, B, true)) return rc;
   k_norm2<<<grid, kThreads, 0, c->stream>>>(len, B, c->dscal + 30, c->partials, c->counters + 7);
   VTS_LAUNCHED(c);
-  VTS_CUDA(cudaMemcpyAsync(c->hscal + 30, c->dscal + 30, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  VTS_CUDA(cudaStreamSynchronize(c->stream));
-  const double bnorm = sqrt(c->hscal[30]);
   const int n = c->n;
   const int napi = c->unbordered ? n : n + 1;  // entries of the caller's vectors
   const int cap = max_iters > 0 ? max_iters : 3 * napi;
-  if (bnorm == 0.0) {
+  double bnorm = 0.0;
+  if (device_init) {
+    k_mr_init0<<<1, 1, 0, c->stream>>>(c->dscal + 30, c->mst, tol, cap);
+    VTS_LAUNCHED(c);
+  } else {
+    VTS_CUDA(cudaMemcpyAsync(c->hscal + 30, c->dscal + 30, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    VTS_CUDA(cudaStreamSynchronize(c->stream));
+    bnorm = sqrt(c->hscal[30]);
+  }
+  if (!device_init && bnorm == 0.0) {
     VTS_CUDA(cudaMemsetAsync(x_free, 0, sizeof(double) * napi, c->stream));
     VTS_CUDA(cudaStreamSynchronize(c->stream));
     *iters_out = 0;
@@ -288,18 +344,24 @@ int minres(Ctx* c, const double* b_free, double* x_free, double tol, int max_ite
     VTS_CUDA(cudaMemsetAsync(X[0], 0, sizeof(double) * len, c->stream));
   }
   if (precondition) {
-    if (int rc = vcycle_grid(c, r1, y, nullptr)) return rc;
+    if (int rc = vcycle_grid(c, r1, y, device_init ? &c->mst->stopped : nullptr)) return rc;
   } else {
     VTS_CUDA(cudaMemcpyAsync(y, r1, sizeof(double) * len, cudaMemcpyDeviceToDevice, c->stream));
   }
-  {
+  if (device_init) {
+    k_dot<<<grid, kThreads, 0, c->stream>>>(len, r1, y, c->partials, c->counters + 0, c->dscal + 31,
+                                            &c->mst->stopped);
+    VTS_LAUNCHED(c);
+    k_mr_init1<<<1, 1, 0, c->stream>>>(c->dscal + 31, c->chol_status, c->mst);
+    VTS_LAUNCHED(c);
+  } else {
     // beta1 = r1 . y
     k_dot<<<grid, kThreads, 0, c->stream>>>(len, r1, y, c->partials, c->counters + 0, c->dscal + 31, nullptr);
     VTS_LAUNCHED(c);
     VTS_CUDA(cudaMemcpyAsync(c->hscal + 31, c->dscal + 31, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     VTS_CUDA(cudaStreamSynchronize(c->stream));
   }
-  double beta1 = c->hscal[31];
+  double beta1 = device_init ? 1.0 : c->hscal[31];
   if (beta1 < 0.0 || beta1 == 0.0) {  // the start iterate is the answer (or the last sound one)
     if (int rc = grid_to_free(c, F, X[0], x_free, true)) return rc;
     VTS_CUDA(cudaStreamSynchronize(c->stream));
@@ -314,27 +376,29 @@ int minres(Ctx* c, const double* b_free, double* x_free, double tol, int max_ite
     *conv_out = 1;
     return 0;
   }
-  beta1 = sqrt(beta1);
-  MinresDev h{};
-  h.beta1 = beta1;
-  h.beta = beta1;
-  h.oldb = 0.0;
-  h.dbar = 0.0;
-  h.epsln = 0.0;
-  h.phibar = beta1;
-  h.cs = -1.0;
-  h.sn = 0.0;
-  h.verify_at = tol;
-  h.relres = INFINITY;
-  h.tol = tol;
-  h.bnorm = bnorm;
-  h.iters = 0;
-  h.max_iters = cap;
-  h.stopped = 0;
-  h.status = kRunning;
-  h.no_verify = 1;
-  *c->hmst = h;
-  VTS_CUDA(cudaMemcpyAsync(c->mst, c->hmst, sizeof(MinresDev), cudaMemcpyHostToDevice, c->stream));
+  if (!device_init) {
+    beta1 = sqrt(beta1);
+    MinresDev h{};
+    h.beta1 = beta1;
+    h.beta = beta1;
+    h.oldb = 0.0;
+    h.dbar = 0.0;
+    h.epsln = 0.0;
+    h.phibar = beta1;
+    h.cs = -1.0;
+    h.sn = 0.0;
+    h.verify_at = tol;
+    h.relres = INFINITY;
+    h.tol = tol;
+    h.bnorm = bnorm;
+    h.iters = 0;
+    h.max_iters = cap;
+    h.stopped = 0;
+    h.status = kRunning;
+    h.no_verify = 1;
+    *c->hmst = h;
+    VTS_CUDA(cudaMemcpyAsync(c->mst, c->hmst, sizeof(MinresDev), cudaMemcpyHostToDevice, c->stream));
+  }
   VTS_CUDA(cudaMemsetAsync(W[0], 0, sizeof(double) * len, c->stream));
   VTS_CUDA(cudaMemsetAsync(W[1], 0, sizeof(double) * len, c->stream));
   // buffers: r1 and r2 alias at the start (linalg.py:189)
@@ -426,7 +490,7 @@ int minres(Ctx* c, const double* b_free, double* x_free, double tol, int max_ite
     VTS_CUDA(cudaEventSynchronize(c->mr_ev[it & 1]));
     const MinresDev s = c->hmst[it & 1];
     last = it;
-    if (s.status == kIndefinite || s.status == kBreakdown || s.status == kNonfinite) {
+    if (s.status == kIndefinite || s.status == kBreakdown || s.status == kNonfinite || s.status == kCholFail) {
       status = s.status;
       xfinal = x_in[it & 1];  // the last sound iterate
       break;
@@ -446,6 +510,8 @@ int minres(Ctx* c, const double* b_free, double* x_free, double tol, int max_ite
   }
   // a look-ahead iteration behind the one that stopped ran as device no-ops
   VTS_CUDA(cudaStreamSynchronize(c->stream));
+  // stopped by the device-side start (||b|| = 0 or beta1 <= 0): no update ran, the answer is x = 0
+  if (device_init && last >= 0 && c->hmst[last & 1].iters == 0) xfinal = x_in[0];
   x = xfinal;
   if (last >= 0) *c->hmst = c->hmst[last & 1];
   if (status == kRunning) status = kCap;
@@ -457,7 +523,7 @@ int minres(Ctx* c, const double* b_free, double* x_free, double tol, int max_ite
     VTS_LAUNCHED(c);
     VTS_CUDA(cudaMemcpyAsync(c->hscal + 31, c->dscal + 31, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     VTS_CUDA(cudaStreamSynchronize(c->stream));
-    relres = sqrt(c->hscal[31]) / bnorm;
+    relres = sqrt(c->hscal[31]) / (device_init ? s.bnorm : bnorm);
   }
   if (int rc = grid_to_free(c, F, x, x_free, true)) return rc;
   *iters_out = s.iters;
@@ -474,6 +540,10 @@ int minres(Ctx* c, const double* b_free, double* x_free, double tol, int max_ite
   if (status == kNonfinite) {
     set_error(3, "NaN/inf encountered in MINRES recurrences");
     return 3;
+  }
+  if (status == kCholFail) {
+    set_error(6, "coarse Cholesky failed even with the shift");
+    return 6;
   }
   return 0;
 }

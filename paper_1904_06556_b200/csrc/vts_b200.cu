@@ -28,6 +28,7 @@
 #include "minres.inc.cu"
 #include "ip.inc.cu"
 #include "doc.inc.cu"
+#include "step.inc.cu"
 #include "hex3d.inc.cu"
 
 namespace vts {
@@ -230,6 +231,7 @@ static void free_ctx(Ctx* c) {
   }
   if (c->hscal) pinned_release(c->hscal);
   if (c->doc_ws) cudaFree(c->doc_ws);
+  delete c->step;
   {
     // after the synchronisation above nothing of this context is in flight; its
     // stream may be destroyed by its owner, so it leaves the user list unless a
@@ -398,6 +400,7 @@ static int create(Ctx** out, int levels, const int32_t* ex, const int32_t* ey, c
   dalloc(arena, &c->chol, (size_t)c->N0 * c->N0);
   dalloc(arena, &c->chol_rdiag, (size_t)c->N0);
   dalloc(arena, &c->chol_status, 1);
+  dalloc(arena, &c->chol_retry, 1);
   const size_t rap = levels > 1 ? (size_t)c->lv[levels - 2].d.nnodes * kStencilStride : 1;
   dalloc(arena, &c->rap_tmp, rap);
   dalloc(arena, &c->partials, (size_t)kMaxBlocks * kMaxPartials);
@@ -525,10 +528,14 @@ int vts_eval_lagrangian(vts_ctx* ctx, const double* u, double alpha, const doubl
                         double* scalars, uint32_t* warn_flags) {
   VTS_REQUIRE_CTX(ctx);
   unsigned warn = 0;
-  auto* fn = C(ctx)->dim == 3 ? vts::h3_eval_lagrangian : vts::eval_lagrangian;
-  const int rc = fn(C(ctx), u, alpha, nu_lo, nu_up, rho, mu_lo, mu_up, p, q_lo, q_up, f, lower,
-                                      upper, volume, norm_f, norm_bounds, branch, res_u, res_lo, res_up, q,
-                                      mu_hat_lo, mu_hat_up, a, b_lo, b_up, rho_hat, w_out, scalars, &warn);
+  const int rc = C(ctx)->dim == 3
+                     ? vts::h3_eval_lagrangian(C(ctx), u, alpha, nu_lo, nu_up, rho, mu_lo, mu_up, p, q_lo, q_up, f,
+                                               lower, upper, volume, norm_f, norm_bounds, branch, res_u, res_lo,
+                                               res_up, q, mu_hat_lo, mu_hat_up, a, b_lo, b_up, rho_hat, w_out,
+                                               scalars, &warn)
+                     : vts::eval_lagrangian(C(ctx), u, alpha, nu_lo, nu_up, rho, mu_lo, mu_up, p, q_lo, q_up, f,
+                                            lower, upper, volume, norm_f, norm_bounds, branch, res_u, res_lo, res_up,
+                                            q, mu_hat_lo, mu_hat_up, a, b_lo, b_up, rho_hat, w_out, scalars, &warn);
   if (warn_flags) *warn_flags = warn ? VTS_W_SATURATED : 0u;
   return rc;
 }
@@ -537,8 +544,10 @@ int vts_schur_system(vts_ctx* ctx, const double* u, const double* res_u, double 
                      const double* res_up, const double* a, const double* b_lo, const double* b_up,
                      const double* rho_hat, double* chat, double* rhs, double* border, double* corner) {
   VTS_REQUIRE_CTX(ctx);
-  auto* fn = C(ctx)->dim == 3 ? vts::h3_schur_system : vts::schur_system;
-  return fn(C(ctx), u, res_u, res_alpha, res_lo, res_up, a, b_lo, b_up, rho_hat, chat, rhs, border,
+  if (C(ctx)->dim == 3)
+    return vts::h3_schur_system(C(ctx), u, res_u, res_alpha, res_lo, res_up, a, b_lo, b_up, rho_hat, chat, rhs,
+                                border, corner);
+  return vts::schur_system(C(ctx), u, res_u, res_alpha, res_lo, res_up, a, b_lo, b_up, rho_hat, chat, rhs, border,
                            corner);
 }
 
@@ -767,6 +776,16 @@ int vts_penalty_eval(vts_ctx* ctx, int64_t n, const double* tau, double branch, 
   const int rc = vts::penalty_eval(C(ctx), n, tau, branch, value, d1, d2, &warn);
   if (warn_flags) *warn_flags = warn ? VTS_W_SATURATED : 0u;
   return rc;
+}
+
+int vts_newton_step(vts_ctx* ctx, const vts_newton_step_args* args, vts_newton_step_result* result) {
+  VTS_REQUIRE_CTX(ctx);
+  VTS_REQUIRE_2D(ctx);
+  if (!args || !result) {
+    vts::set_error(VTS_E_ARGUMENT, "vts_newton_step: NULL argument");
+    return VTS_E_ARGUMENT;
+  }
+  return vts::newton_step(C(ctx), args, result);
 }
 
 int vts_time_kernels(vts_ctx* ctx, int32_t reps, double* ms) {

@@ -12,11 +12,17 @@ every array operation a fused kernel behind the C ABI:
 * `_al_value`        (pbm.py:135-147) -> vts_al_value, fused with x + kappa dx
 * `newton_inner`     (pbm.py:244-338), `solve_pbm` (pbm.py:341-465) — host
   control flow identical to the reference; only scalars cross to the host.
+  On a 2D context each Newton step is one vts_newton_step call (device-resident:
+  Schur system, multigrid setup, MINRES, reconstruction, Armijo search, update
+  and the new evaluation with one host synchronisation; two CUDA graphs);
+  VTS_HOST_NEWTON=1 runs the call-by-call path above instead (same bits).
 """
 
 from __future__ import annotations
 
 import ctypes
+import logging
+import os
 import time
 from dataclasses import dataclass, field, replace
 from math import sqrt
@@ -25,7 +31,7 @@ import torch
 
 from . import _lib
 from .fem import DensityBounds, ElementOps, ptr
-from .linalg import MinresConfig, NewtonMatrix, StagnationTolerance, minres_solve
+from .linalg import _ERRORS, MinresConfig, MinresError, NewtonMatrix, StagnationTolerance, minres_solve
 from .multigrid import MgPreconditioner
 from .penalty import PenaltyBarrier, warn_saturated
 
@@ -206,6 +212,115 @@ def _step(x: torch.Tensor, kappa: float, dx: torch.Tensor, ops) -> torch.Tensor:
     return out
 
 
+_mg_log = logging.getLogger("paper_1904_06556_b200.multigrid")
+
+
+class _StepWork:
+    """Buffers of the device-resident Newton step, owned by one ElementOps: the
+    working copies of u, nu_lo, nu_up, the evaluation the step updates in place,
+    and the Newton system / direction.  Kept across newton_inner calls so that
+    vts_newton_step replays its CUDA graphs (their launches bake the pointers)."""
+
+    _EV = ("res_u", "res_lo", "res_up", "q", "mu_hat_lo", "mu_hat_up", "a", "b_lo", "b_up", "rho_hat")
+
+    def __init__(self, ops):
+        n, m = ops.n, ops.m
+        self.u, self.nu_lo, self.nu_up = ops.vec(n), ops.vec(m), ops.vec(m)
+        self.ev = {k: ops.vec(n if k == "res_u" else m) for k in self._EV}
+        self.chat, self.rhs, self.border = ops.vec(m), ops.vec(n + 1), ops.vec(n)
+        self.du, self.dnu_lo, self.dnu_up = ops.vec(n + 1), ops.vec(m), ops.vec(m)
+
+
+def _device_step_ok(ops) -> bool:
+    return getattr(ops, "dim", 2) == 2 and os.environ.get("VTS_HOST_NEWTON", "0") != "1"
+
+
+def _newton_inner_device(state: PbmState, ops: ElementOps, f, bounds: DensityBounds, pen: PenaltyBarrier,
+                         tol_newton: float, mtol: StagnationTolerance, cfg: PbmConfig, trace: dict | None
+                         ) -> "NewtonOutcome":
+    """newton_inner (pbm.py:244-338) with each step one vts_newton_step call: the
+    same loop control on the host, everything between two residual checks on the
+    device.  The state is rebound to new tensors on return, as the reference rebinds."""
+    mtol.reset()
+    ev = eval_lagrangian(state, ops, f, bounds, pen)
+    W = getattr(ops, "_step_work", None)
+    if W is None:
+        W = ops._step_work = _StepWork(ops)
+    W.u.copy_(state.u)
+    W.nu_lo.copy_(state.nu_lo)
+    W.nu_up.copy_(state.nu_up)
+    for k in _StepWork._EV:
+        W.ev[k].copy_(getattr(ev, k) if hasattr(ev, k) else getattr(ev.blocks, k))
+    alpha, value, res_alpha, tau = float(state.alpha), ev.value, ev.res_alpha, ev.tau_res
+    steps = 0
+    counts: list[int] = []
+    best_tau = float("inf")
+    no_improve = 0
+    lib = _lib.load()
+    a = _lib.NewtonStepArgs()
+    a.u, a.nu_lo, a.nu_up = ptr(W.u), ptr(W.nu_lo), ptr(W.nu_up)
+    for k in ("rho", "p", "mu_lo", "mu_up", "q_lo", "q_up"):
+        setattr(a, k, ptr(getattr(state, k)))
+    a.f, a.lower, a.upper = ptr(f), ptr(bounds.lower), ptr(bounds.upper)
+    a.volume, a.norm_f, a.norm_bounds, a.branch = float(bounds.volume), ops.norm_f, bounds.norm, pen.branch
+    for k in _StepWork._EV:
+        setattr(a, k, ptr(W.ev[k]))
+    a.chat, a.rhs, a.border, a.du, a.dnu_lo, a.dnu_up = (ptr(t) for t in (W.chat, W.rhs, W.border, W.du, W.dnu_lo,
+                                                                          W.dnu_up))
+    a.minres_floor, a.minres_cap = cfg.minres_floor, cfg.minres_cap
+    a.armijo_c1, a.armijo_shrink, a.armijo_max_halvings = cfg.armijo_c1, cfg.armijo_shrink, cfg.armijo_max_halvings
+    a.shift_scale = 1e-12  # MgPreconditioner's default shift_scale (multigrid.py:82)
+    r = _lib.NewtonStepResult()
+    stalled, note = False, ""
+    while tau >= tol_newton:
+        if steps >= cfg.max_newton:
+            stalled, note = True, "newton iteration cap reached"
+            break
+        a.alpha, a.value, a.res_alpha = alpha, value, res_alpha
+        a.minres_tol = min(mtol.current(), 0.99)
+        rc = lib.vts_newton_step(ops.handle, ctypes.byref(a), ctypes.byref(r))
+        ops._system_version = getattr(ops, "_system_version", 0) + 1
+        if rc in _ERRORS:
+            if steps:  # the accepted steps stay, as the reference has rebound the state by then
+                state.u, state.nu_lo, state.nu_up = W.u.clone(), W.nu_lo.clone(), W.nu_up.clone()
+                state.alpha = alpha
+            raise MinresError(_ERRORS[rc], W.du.clone())
+        _lib.check(rc, "vts_newton_step")
+        if r.warnings & _lib.VTS_W_SHIFTED:
+            _mg_log.warning("coarse matrix is not positive definite; retrying Cholesky with a trace-scaled shift")
+        warn_saturated(r.warnings)
+        counts.append(r.minres_iterations)
+        if r.status == 1:
+            stalled, note = True, "non-descent Newton direction"
+            break
+        if r.status == 2:
+            stalled, note = True, "line search exhausted"
+            break
+        if trace is not None:
+            trace.setdefault("kappa", []).append(r.kappa)
+            trace.setdefault("slope", []).append(r.slope)
+        alpha = r.alpha
+        value, res_alpha, tau = r.scalars[0], r.scalars[1], r.scalars[2]
+        steps += 1
+        mtol.observe(tau)
+        if tau < best_tau:
+            best_tau = tau
+            no_improve = 0
+        else:
+            no_improve += 1
+            if no_improve >= cfg.stall_steps:
+                stalled, note = True, "no residual improvement over consecutive steps"
+                break
+    if steps:
+        state.u, state.nu_lo, state.nu_up = W.u.clone(), W.nu_lo.clone(), W.nu_up.clone()
+        state.alpha = alpha
+        out = {k: W.ev[k].clone() for k in _StepWork._EV}
+        blocks = HessianBlocks(None, out["a"], out["b_lo"], out["b_up"], out["rho_hat"])
+        ev = LagrangianEval(value, out["res_u"], res_alpha, out["res_lo"], out["res_up"], tau, out["q"],
+                            out["mu_hat_lo"], out["mu_hat_up"], blocks, state.u)
+    return NewtonOutcome(steps, counts, stalled, note, ev)
+
+
 @dataclass
 class NewtonOutcome:
     steps: int
@@ -219,6 +334,8 @@ def newton_inner(state: PbmState, ops: ElementOps, f, bounds: DensityBounds, pen
                  tol_newton: float, mtol: StagnationTolerance, cfg: PbmConfig, trace: dict | None = None
                  ) -> NewtonOutcome:
     """Damped Newton minimisation of the augmented Lagrangian (pbm.py:244-338)."""
+    if _device_step_ok(ops):
+        return _newton_inner_device(state, ops, f, bounds, pen, tol_newton, mtol, cfg, trace)
     mtol.reset()
     ev = eval_lagrangian(state, ops, f, bounds, pen)
     steps = 0
