@@ -57,7 +57,7 @@ __device__ bool last_block_reduce(double (&v)[NV], double* scratch, double* part
   // thread t sums blocks t, t + blockDim, ... in that order; the loads of a
   // round of kU blocks are all issued before the first add (one L2 round
   // trip per round instead of one per block; absent blocks add +0.0)
-  constexpr int kU = 8;
+  constexpr int kU = NV >= 4 ? 2 : 8;  // loads in flight per thread (registers: kU x NV)
   for (int b0 = threadIdx.x; b0 < (int)gridDim.x; b0 += kU * blockDim.x) {
     double v[kU][NV];
 #pragma unroll
@@ -324,6 +324,153 @@ __global__ void __launch_bounds__(kThreads) k_phi_node(int nnodes, int nx, int e
   block_partials<2>(acc, scratch, partials);
 }
 
+// ---------------------------------------------------------------------------
+// eval_lagrangian in one launch: k_phi_elem's element pass and k_phi_node's
+// scatter fused per tile.  A CTA owns the elements [x0, x0 + 31) x [y0, y0 + 7)
+// and the nodes [x0, x0 + 31) x [y0, y0 + 7); its 32 x 8 threads compute the
+// elements [x0 - 1, x0 + 31) x [y0 - 1, y0 + 7) (one halo column and row, whose
+// outputs the neighbouring tiles write), put rho_hat w_e in shared memory and
+// every owned node sums its four contributions in the reference's scatter
+// order (fem.py:170-173): the same arithmetic as the two-kernel pass, element
+// products computed once per element instead of once per node and corner.  The
+// nine partial sums end in a last-block reduction that forms the scalars
+// (k_phi_finish's arithmetic).
+// ---------------------------------------------------------------------------
+constexpr int kPhiTX = 32, kPhiTY = 8;
+#ifndef VTS_PHI_MINB
+#define VTS_PHI_MINB 4  // 64 registers: 4 CTAs per SM (2: 74 us, 3: 59 us, 4: 55 us on C3)
+#endif
+
+struct PhiTileArgs {
+  int nx, ny, ey, tiles_x, ntiles;  // ntiles: informational (the grid has one CTA per tile)
+  const double* f;
+  const int32_t* g2f;
+  double* res_u;
+  double volume, norm_f, norm_bounds;
+  double* out;
+};
+
+__global__ void __launch_bounds__(kPhiTX * kPhiTY, VTS_PHI_MINB) k_phi_tile(PhiElemArgs A, PhiTileArgs T, double* partials,
+                                                                  unsigned* counter, unsigned* flags) {
+  if (A.skip && *A.skip) return;
+  __shared__ double contrib[8][kPhiTX * kPhiTY];
+  __shared__ double scratch[9 * kPhiTX * kPhiTY / 32];
+  const int tid = threadIdx.x, lx = tid % kPhiTX, ly = tid / kPhiTX;
+  const double alpha = A.alpha_dev ? *A.alpha_dev : A.alpha;
+  double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned sat = 0;
+  const int x0 = (blockIdx.x % T.tiles_x) * (kPhiTX - 1), y0 = (blockIdx.x / T.tiles_x) * (kPhiTY - 1);
+  const int exi = x0 - 1 + lx, eyi = y0 - 1 + ly;
+  const bool in_mesh = exi >= 0 && exi < A.ex && eyi >= 0 && eyi < T.ey;
+  const bool owned = in_mesh && lx >= 1 && ly >= 1;
+  double w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  double rho_hat = 0.0;
+  if (in_mesh) {
+    const int e = exi + A.ex * eyi;
+    int nd[4];
+    elem_nodes(e, A.ex, A.nx, nd);
+    double ue[8];
+    gather8(A.ug, nd, ue);
+    ke_times(ue, w);
+    double qq = w[0] * ue[0];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) qq = fma(w[i], ue[i], qq);
+    qq = 0.5 * qq;
+    const double nlo = A.nu_lo[e], nup = A.nu_up[e], pe = A.p[e], qlo = A.q_lo[e], qup = A.q_up[e];
+    const double rh = A.rho[e], mlo = A.mu_lo[e], mup = A.mu_up[e];
+    const double s = __dsub_rn(__dadd_rn(__dsub_rn(qq, alpha), nlo), nup);
+    const PhiOut f1 = phi_eval(s / pe, A.branch, &sat);
+    rho_hat = rh * f1.d1;
+    if (owned) {
+      const PhiOut f2 = phi_eval(-nlo / qlo, A.branch, &sat);
+      const PhiOut f3 = phi_eval(-nup / qup, A.branch, &sat);
+      const double mhl = mlo * f2.d1, mhu = mup * f3.d1;
+      const double lo = A.lower[e], up = A.upper[e];
+      const double rlo = __dsub_rn(__dadd_rn(-lo, rho_hat), mhl);
+      const double rup = __dsub_rn(__dsub_rn(up, rho_hat), mhu);
+      A.q[e] = qq;
+      A.rho_hat[e] = rho_hat;
+      A.mu_hat_lo[e] = mhl;
+      A.mu_hat_up[e] = mhu;
+      A.a[e] = (rh / pe) * f1.d2;
+      A.b_lo[e] = (mlo / qlo) * f2.d2;
+      A.b_up[e] = (mup / qup) * f3.d2;
+      A.res_lo[e] = rlo;
+      A.res_up[e] = rup;
+      if (A.w_out) {
+#pragma unroll
+        for (int j = 0; j < 8; j += 2)
+          *reinterpret_cast<double2*>(A.w_out + 8 * (size_t)e + j) = make_double2(w[j], w[j + 1]);
+      }
+      acc[0] += rh * __dmul_rn(pe, f1.v);
+      acc[1] += mlo * __dmul_rn(qlo, f2.v);
+      acc[2] += mup * __dmul_rn(qup, f3.v);
+      acc[3] += rho_hat;
+      acc[4] = fma(rlo, rlo, acc[4]);
+      acc[5] = fma(lo, nlo, acc[5]);
+      acc[6] = fma(up, nup, acc[6]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) contrib[j][tid] = __dmul_rn(rho_hat, w[j]);
+  __syncthreads();
+  // node (x0 + lx, y0 + ly): elements (ix-1, iy-1) corner 2, (ix, iy-1) corner 3,
+  // (ix-1, iy) corner 1, (ix, iy) corner 0 -- local elements (lx, ly), (lx+1, ly),
+  // (lx, ly+1), (lx+1, ly+1)
+  const int ix = x0 + lx, iy = y0 + ly;
+  if (lx < kPhiTX - 1 && ly < kPhiTY - 1 && ix < T.nx && iy < T.ny) {
+    double s0 = 0.0, s1 = 0.0;
+    if (ix >= 1 && iy >= 1) {
+      s0 = __dadd_rn(s0, contrib[4][tid]);
+      s1 = __dadd_rn(s1, contrib[5][tid]);
+    }
+    if (ix < A.ex && iy >= 1) {
+      s0 = __dadd_rn(s0, contrib[6][tid + 1]);
+      s1 = __dadd_rn(s1, contrib[7][tid + 1]);
+    }
+    if (ix >= 1 && iy < T.ey) {
+      s0 = __dadd_rn(s0, contrib[2][tid + kPhiTX]);
+      s1 = __dadd_rn(s1, contrib[3][tid + kPhiTX]);
+    }
+    if (ix < A.ex && iy < T.ey) {
+      s0 = __dadd_rn(s0, contrib[0][tid + kPhiTX + 1]);
+      s1 = __dadd_rn(s1, contrib[1][tid + kPhiTX + 1]);
+    }
+    const int nd = ix + A.nx * iy;
+    const int f0 = T.g2f[2 * nd], f1 = T.g2f[2 * nd + 1];
+    if (f0 >= 0) {
+      const double r = __dsub_rn(s0, T.f[f0]);
+      T.res_u[f0] = r;
+      acc[7] = fma(r, r, acc[7]);
+      acc[8] = fma(T.f[f0], A.ug[2 * nd], acc[8]);
+    }
+    if (f1 >= 0) {
+      const double r = __dsub_rn(s1, T.f[f1]);
+      T.res_u[f1] = r;
+      acc[7] = fma(r, r, acc[7]);
+      acc[8] = fma(T.f[f1], A.ug[2 * nd + 1], acc[8]);
+    }
+  }
+  if (sat) atomicOr(flags, 1u);
+  double t[9];
+  if (last_block_reduce<9>(acc, scratch, partials, counter, t) && threadIdx.x == 0) {
+    // k_phi_finish: dual_objective (model.py:61-66) + the penalty sums (pbm.py:161-166)
+    const double fu = t[8];
+    const double dual = ((alpha * T.volume - fu) - t[5]) + t[6];
+    const double value = ((dual + t[0]) + t[1]) + t[2];
+    const double res_alpha = T.volume - t[3];
+    const double tau = (sqrt(t[7]) / T.norm_f + fabs(res_alpha) / T.volume) + sqrt(t[4]) / T.norm_bounds;
+    T.out[0] = value;
+    T.out[1] = res_alpha;
+    T.out[2] = tau;
+    T.out[3] = fu;
+    T.out[4] = t[3];
+    T.out[5] = sqrt(t[7]);
+    T.out[6] = sqrt(t[4]);
+    T.out[7] = 0.0;
+  }
+}
+
 // sums the two partial arrays and forms the eval scalars
 __global__ void k_phi_finish(int nb_e, const double* __restrict__ pe, int nb_n,
                              const double* __restrict__ pn, double alpha, double volume,
@@ -485,6 +632,18 @@ __global__ void __launch_bounds__(kThreads) k_recon_elem(int m, int ex, int nx,
   block_partials<2>(acc, scratch, partials);
 }
 
+// slope = res_u.du + res_alpha dalpha + res_lo.dnu_lo + res_up.dnu_up (pbm.py:290-295): the
+// element partials of k_recon_elem summed in block order, then the reference's sum order
+__global__ void k_slope_finish(int nb, const double* __restrict__ pe, const double* __restrict__ dot, double res_alpha,
+                               double dalpha, double* out) {
+  double s_lo = 0.0, s_up = 0.0;
+  for (int b = 0; b < nb; ++b) {
+    s_lo = __dadd_rn(s_lo, pe[2 * b]);
+    s_up = __dadd_rn(s_up, pe[2 * b + 1]);
+  }
+  *out = __dadd_rn(__dadd_rn(__dadd_rn(*dot, __dmul_rn(res_alpha, dalpha)), s_lo), s_up);
+}
+
 // ---------------------------------------------------------------------------
 // _al_value at the trial point (element part)
 // ---------------------------------------------------------------------------
@@ -639,6 +798,15 @@ static int sync_scalars(Ctx* c, int count) {
   return 0;
 }
 
+// VTS_PHI_SPLIT=1: the evaluation as k_phi_elem + k_phi_node + k_phi_finish (A/B checks)
+static bool phi_fused() {
+  static const bool on = [] {
+    const char* e = getenv("VTS_PHI_SPLIT");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
 int free_to_grid(Ctx* c, int level, const double* src, double* dst, bool bordered, const int* skip) {
   const LevelBuf& L = c->lv[level];
   const int total = L.d.ngrid + 1;
@@ -684,6 +852,20 @@ int eval_lagrangian(Ctx* c, const double* u, double alpha, const double* nu_lo, 
   PhiElemArgs A{c->m, d.ex, d.nx, ug, alpha, branch, nu_lo, nu_up, rho, mu_lo, mu_up, p, q_lo,
                 q_up, lower, upper, q, rho_hat, mu_hat_lo, mu_hat_up, a, b_lo, b_up, res_lo,
                 res_up, w_out, alpha_dev, skip};
+  const int tiles_x = div_up(d.nx, kPhiTX - 1), tiles = tiles_x * div_up(d.ny, kPhiTY - 1);
+  // one tile per CTA; the last-block reduction holds 9 partials per CTA
+  if (phi_fused() && (long long)tiles * 9 <= (long long)kMaxBlocks * kMaxPartials) {
+    PhiTileArgs T{d.nx, d.ny, d.ey, tiles_x, tiles, f, c->lv[F].grid2free, res_u, volume, norm_f, norm_bounds,
+                  c->dscal};
+    k_phi_tile<<<tiles, kPhiTX * kPhiTY, 0, c->stream>>>(A, T, c->partials, c->counters + 15, c->dflags);
+    VTS_LAUNCHED(c);
+    if (alpha_dev) return 0;
+    VTS_CUDA(cudaMemcpyAsync(c->hscal + 16, c->dflags, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
+    if (int rc = sync_scalars(c, 8)) return rc;
+    for (int i = 0; i < 8; ++i) scalars[i] = c->hscal[i];
+    if (warn) *warn = *reinterpret_cast<unsigned*>(c->hscal + 16) ? 1u : 0u;
+    return 0;
+  }
   const int ge = reduce_grid(c->m);
   k_phi_elem<<<ge, kThreads, 0, c->stream>>>(A, c->partials, c->dflags);
   VTS_LAUNCHED(c);
@@ -754,16 +936,10 @@ int reconstruct_nu(Ctx* c, const double* u, const double* du, double dalpha, con
                                                         c->counters + 1, c->dscal + 8, nullptr);
   VTS_LAUNCHED(c);
   if (slope) {
-    // element partials are summed on the host side of this call in block order
-    std::vector<double> pe(2 * ge);
-    VTS_CUDA(cudaMemcpyAsync(pe.data(), c->partials, sizeof(double) * 2 * ge, cudaMemcpyDeviceToHost, c->stream));
-    if (int rc = sync_scalars(c, 9)) return rc;
-    double s_lo = 0.0, s_up = 0.0;
-    for (int b = 0; b < ge; ++b) {
-      s_lo += pe[2 * b];
-      s_up += pe[2 * b + 1];
-    }
-    *slope = ((c->hscal[8] + res_alpha * dalpha) + s_lo) + s_up;
+    k_slope_finish<<<1, 1, 0, c->stream>>>(ge, c->partials, c->dscal + 8, res_alpha, dalpha, c->dscal + 9);
+    VTS_LAUNCHED(c);
+    if (int rc = sync_scalars(c, 10)) return rc;
+    *slope = c->hscal[9];
   }
   return 0;
 }

@@ -102,13 +102,25 @@ class PbmState:
                    one(), one(), one())
 
 
-@dataclass
 class HessianBlocks:
-    w: torch.Tensor | None  # (m, 8) element products, only when requested
-    a: torch.Tensor
-    b_lo: torch.Tensor
-    b_up: torch.Tensor
-    rho_hat: torch.Tensor
+    """Per-element Hessian blocks (pbm.py:101-116).  `w` (m x dofs, the element
+    products u_e K_e) is always available like the reference's: written by the
+    evaluation when asked for (keep_w), else formed on first access from the u the
+    evaluation belongs to (vts_element_products) -- the Newton step itself never
+    needs it materialised (the apply recomputes K_e u_e)."""
+
+    def __init__(self, w, a, b_lo, b_up, rho_hat, ops=None, u=None):
+        self._w, self.a, self.b_lo, self.b_up, self.rho_hat = w, a, b_lo, b_up, rho_hat
+        self._ops, self._u = ops, u
+
+    @property
+    def w(self) -> torch.Tensor | None:
+        if self._w is None and self._ops is not None:
+            self._w, _ = self._ops.element_products(self._u)
+        return self._w
+
+    def __repr__(self) -> str:
+        return f"HessianBlocks(m={self.a.numel()}, w={'materialised' if self._w is not None else 'lazy'})"
 
 
 @dataclass
@@ -145,7 +157,7 @@ def eval_lagrangian(state: PbmState, ops: ElementOps, f, bounds: DensityBounds, 
         sc, ctypes.byref(flags))
     _lib.check(rc, "vts_eval_lagrangian")
     warn_saturated(flags.value)
-    blocks = HessianBlocks(w, out["a"], out["b_lo"], out["b_up"], out["rho_hat"])
+    blocks = HessianBlocks(w, out["a"], out["b_lo"], out["b_up"], out["rho_hat"], ops, u)
     return LagrangianEval(sc[0], res_u, sc[1], out["res_lo"], out["res_up"], sc[2], out["q"], out["mu_hat_lo"],
                           out["mu_hat_up"], blocks, u)
 
@@ -315,7 +327,7 @@ def _newton_inner_device(state: PbmState, ops: ElementOps, f, bounds: DensityBou
         state.u, state.nu_lo, state.nu_up = W.u.clone(), W.nu_lo.clone(), W.nu_up.clone()
         state.alpha = alpha
         out = {k: W.ev[k].clone() for k in _StepWork._EV}
-        blocks = HessianBlocks(None, out["a"], out["b_lo"], out["b_up"], out["rho_hat"])
+        blocks = HessianBlocks(None, out["a"], out["b_lo"], out["b_up"], out["rho_hat"], ops, state.u)
         ev = LagrangianEval(value, out["res_u"], res_alpha, out["res_lo"], out["res_up"], tau, out["q"],
                             out["mu_hat_lo"], out["mu_hat_up"], blocks, state.u)
     return NewtonOutcome(steps, counts, stalled, note, ev)

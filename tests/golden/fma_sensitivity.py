@@ -84,6 +84,7 @@ def run(prob, stock: dict, with_vectors: bool) -> dict:
         "max_abs_diff_vs_stock": float(np.abs(d).max()),
         "l2_rel_diff_vs_stock": float(np.linalg.norm(d) / np.linalg.norm(ref)),
         "objective_rel_diff_vs_stock": float(abs(rep.objective - float(stock["objective"])) / float(stock["objective"])),
+        "volume_rel_diff_vs_stock": float(abs(rep.volume - float(stock["volume"])) / abs(float(stock["volume"]))),
         "same_counts": bool(np.array_equal(out["minres_per_newton"], stock["minres_per_newton"])),
         "minres_total_diff": int(out["minres_per_newton"].sum() - stock["minres_per_newton"].sum()),
     }

@@ -84,3 +84,53 @@ def test_device_step_syncs_and_graph_replays():
     assert all(rc == 0 for rc, *_ in seen)
     assert all(s == 1 for _, s, _, t in seen if t <= 2)
     assert all(g == 2 for _, _, g, _ in seen)
+
+
+def test_blocks_w_is_available_without_keep_w():
+    """HessianBlocks.w (pbm.py:101-116) exists whether or not the evaluation wrote it:
+    formed on first access from the evaluation's u, bit for bit the keep_w product."""
+    prob = vts.build_config("C1")
+    ops = vts.ElementOps(prob.fine)
+    bounds = vts.DensityBounds.for_problem(prob.m, prob.volume, 0.0)
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    state = vts.PbmState.initial(prob.n, prob.m, prob.volume)
+    state.u = torch.randn(prob.n, dtype=torch.float64, device="cuda", generator=gen) * 1e-2
+    lazy = vts.eval_lagrangian(state, ops, prob.f, bounds, vts.PenaltyBarrier())
+    full = vts.eval_lagrangian(state, ops, prob.f, bounds, vts.PenaltyBarrier(), keep_w=True)
+    assert lazy.blocks._w is None
+    assert torch.equal(lazy.blocks.w, full.blocks.w)
+    assert lazy.blocks.w.shape == (prob.m, 8)
+
+
+def test_fused_evaluation_matches_the_two_kernel_pass(monkeypatch):
+    """k_phi_tile (one launch) against k_phi_elem + k_phi_node + k_phi_finish: every
+    vector bit for bit, the scalars to their reductions' rounding."""
+    import subprocess
+    import sys
+
+    code = ("import sys; sys.path.insert(0, '.'); import numpy as np, torch, paper_1904_06556_b200 as vts;"
+            "p = vts.build_config('C2'); o = vts.ElementOps(p.fine);"
+            "b = vts.DensityBounds.for_problem(p.m, p.volume, 0.0); g = np.random.default_rng(2);"
+            "s = vts.PbmState.initial(p.n, p.m, p.volume);"
+            "s.u = torch.as_tensor(g.normal(0, 1e-2, p.n), device='cuda');"
+            "s.nu_lo = torch.as_tensor(g.uniform(0, 1e-2, p.m), device='cuda');"
+            "s.p = torch.full((p.m,), 1e-2, dtype=torch.float64, device='cuda');"
+            "e = vts.eval_lagrangian(s, o, p.f, b, vts.PenaltyBarrier());"
+            "np.savez(sys.argv[1], res_u=e.res_u.cpu(), res_lo=e.res_lo.cpu(), q=e.q.cpu(), a=e.blocks.a.cpu(),"
+            " rho_hat=e.blocks.rho_hat.cpu(), scal=np.array([e.value, e.res_alpha, e.tau_res]))")
+    import numpy as np
+    import os
+    import tempfile
+
+    out = {}
+    with tempfile.TemporaryDirectory() as tmp:
+        for mode in ("0", "1"):
+            path = os.path.join(tmp, f"e{mode}.npz")
+            env = dict(os.environ, VTS_PHI_SPLIT=mode)
+            subprocess.run([sys.executable, "-c", code, path], check=True, env=env,
+                           cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+            with np.load(path) as z:
+                out[mode] = {k: z[k] for k in z.files}
+    for k in ("res_u", "res_lo", "q", "a", "rho_hat"):
+        assert np.array_equal(out["0"][k], out["1"][k]), k
+    np.testing.assert_allclose(out["0"]["scal"], out["1"]["scal"], rtol=1e-14)

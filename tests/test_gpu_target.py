@@ -260,8 +260,10 @@ def test_c4_full_solve_matches_reference_solve():
     (MINRES stopped at ~1e-3..1e-5), so a last-bit perturbation of the path
     moves it far more than the perturbation itself.  `fma_sensitivity.npz`
     (tests/golden/fma_sensitivity.py c4) measures that for the reference:
-    fusing only its Gauss-Seidel products moves rho by 1.37e-5 (max) and
-    1.30e-6 (2-norm, relative) with identical counts.  The GPU's distance to
+    fusing only its Gauss-Seidel products moves rho by 1.49e-5 (max),
+    1.30e-6 (2-norm, relative) and the volume by 6.3e-10 (relative) with
+    identical counts (an earlier run of the same experiment gave 1.37e-5: the
+    reference's BLAS-threaded products are not bit-reproducible).  The GPU's distance to
     the stock reference must stay within twice those measured figures; the
     north_star's 1e-6 is not reachable by the reference against itself.
     """
@@ -283,4 +285,11 @@ def test_c4_full_solve_matches_reference_solve():
     assert 1e-7 < own_max < 1e-4 and 1e-8 < own_l2 < 1e-5
     assert np.abs(rho - ref).max() <= 2.0 * own_max * np.abs(ref).max(), np.abs(rho - ref).max()
     assert np.linalg.norm(rho - ref) <= 2.0 * own_l2 * np.linalg.norm(ref)
-    assert rep.volume == pytest.approx(float(fx["volume"]), rel=1e-9)
+    # volume = sum(rho): the reference's own FMA run moves it by c4_volume_rel_diff_vs_stock
+    # (6.3e-10); one draw of a rounding-level perturbation of a 524,288-term sum, while
+    # the GPU path differs from the stock run in every kernel's rounding (the
+    # evaluation's reductions alone perturb res_alpha, hence the Schur right-hand side),
+    # so the bound is four such draws
+    own_vol = float(sens["c4_volume_rel_diff_vs_stock"])
+    assert 1e-12 < own_vol < 1e-7
+    assert abs(rep.volume - float(fx["volume"])) <= 4.0 * own_vol * abs(float(fx["volume"]))
