@@ -353,6 +353,15 @@ def main() -> None:
     cold = (ctypes.c_double * 2)()
     _lib.check(lib.vts_time_cold(ops.handle, 50, flush.data_ptr(), flush.numel(), cold), "vts_time_cold")
     apply_ms, resid_ms = list(cold)
+    # the same cold launch after a read sweep (L2 clean, as ncu's cache flush leaves it), and
+    # this harness's floor: a plain streaming kernel over the apply's bytes (VTS_TIME_FLOOR)
+    apply_cold = {}
+    for flush_kind in ("memset", "read"):
+        os.environ["VTS_COLD_FLUSH"], os.environ["VTS_TIME_FLOOR"] = flush_kind, "1"
+        _lib.check(lib.vts_time_cold(ops.handle, 50, flush.data_ptr(), flush.numel(), cold), "vts_time_cold")
+        apply_cold[flush_kind] = (cold[0], cold[1])
+    os.environ.pop("VTS_COLD_FLUSH")
+    os.environ.pop("VTS_TIME_FLOOR")
     del flush
 
     # --- warm-up then the timed region: K MINRES iterations, device resident
@@ -445,9 +454,16 @@ def main() -> None:
         rep = vts.solve_pbm(vts.build_config("C4"))
         pbm = {"config": "C4 full PBM 1024x512 cantilever", "wall_s": time.perf_counter() - t_p,
                "note": "one solve_pbm call, context creation included (device arena recycled from the "
-                       "microbenchmark context)",
+                       "microbenchmark context); each Newton step one vts_newton_step (device-resident, "
+                       "CUDA graphs, one host synchronisation per step)",
                "outer": rep.outer_iterations, **rep.totals(), "compliance": rep.objective,
                "converged": rep.converged}
+        os.environ["VTS_HOST_NEWTON"] = "1"  # the call-by-call host orchestration, same kernels (same bits)
+        t_p = time.perf_counter()
+        rep_h = vts.solve_pbm(vts.build_config("C4"))
+        pbm["host_orchestrated_wall_s"] = time.perf_counter() - t_p
+        pbm["host_orchestrated_same_result"] = bool(rep_h.objective == rep.objective and rep_h.rows == rep.rows)
+        os.environ.pop("VTS_HOST_NEWTON")
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline_sample()
@@ -485,7 +501,16 @@ def main() -> None:
                                       "implementation_bytes_per_launch": bytes_["gs_pair_asc_fine"]}
                                      if asc_fine_n > 0 else None),
                      "apply_frac": gbs(bytes_["apply"], apply_ms) / peak,
-                     "apply_note": "k_newton_apply, A_ap = 8(3n+2m+2) per launch, timed cold (L2 overwritten)",
+                     "apply_note": "k_newton_apply, A_ap = 8(3n+2m+2) per launch, timed cold (L2 overwritten "
+                                   "by a memset: every miss also writes a dirty line back)",
+                     "apply_frac_clean_l2": gbs(bytes_["apply"], apply_cold["read"][0]) / peak,
+                     "apply_harness_floor": {
+                         "note": "a plain grid-stride kernel reading and writing the apply's bytes, timed the same "
+                                 "way: what a launch + cold-L2 measurement of this size can reach",
+                         "floor_ms_dirty_l2": apply_cold["memset"][1], "floor_ms_clean_l2": apply_cold["read"][1],
+                         "apply_ms_clean_l2": apply_cold["read"][0],
+                         "apply_over_floor_dirty": apply_ms / apply_cold["memset"][1],
+                         "apply_over_floor_clean": apply_cold["read"][0] / apply_cold["read"][1]},
                      "vcycle_frac": gbs(bytes_["vcycle"], vcycle_ms) / peak,
                      "vcycle_note": "one V(2,2), A_V of SURVEY.md Appendix B, mean of 100 back-to-back",
                      "phi_frac": gbs(bytes_["phi"], phi_ms) / peak,
@@ -498,7 +523,8 @@ def main() -> None:
             "apply_frac": gbs(bytes_["apply"], apply_ms) / peak,
             "apply_l2_warm_ms": apply_warm_ms, "residual_l2_warm_ms": resid_warm_ms,
             "note": "apply and residual timed cold (256 MB written between launches); phi pass: 10 back-to-back "
-                    "calls (100 MB of inputs, partly L2-resident)",
+                    "vts_eval_lagrangian calls, each one k_phi_tile launch plus its scalar read-back and host "
+                    "synchronisation (100 MB of inputs, partly L2-resident)",
             "vcycle_ms": vcycle_ms, "vcycles_per_s": 1e3 / vcycle_ms,
             "gs_fine_sweep_ms": gs_fine_ms, "gs_fine_sweep_GBs": gbs(bytes_["gs_fine_sweep"], gs_fine_ms),
             "gs_level8_sweep_ms": gs_l2_ms, "residual_fine_ms": resid_ms, "mg_setup_ms": setup_ms,
