@@ -2014,14 +2014,33 @@ static bool fused_bottom_enabled() {
   return on;
 }
 
+// items per block of the overlap passes (VTS_DOVL_DIV / VTS_OVL_DIV, A/B timing)
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? std::max(1, atoi(e)) : dflt;
+}
+// per-level override "n_top,n_top-1,..." (VTS_DOVL_BLOCKS / VTS_OVL_BLOCKS, tuning runs): 0 = default
+static int env_level(const char* name, int depth) {
+  const char* e = getenv(name);
+  if (!e) return 0;
+  for (int i = 0; i < depth && e; ++i) {
+    e = strchr(e, ',');
+    if (e) ++e;
+  }
+  return e ? std::max(0, atoi(e)) : 0;
+}
 // blocks of the overlap passes of level k (each holds an SM)
 static int dovl_blocks(const Ctx* c, int k) {  // k_residual_restrict_rows, level k -> k-1
+  static const int div = env_int("VTS_DOVL_DIV", 6);  // 6: 888 vs 878 it/s for 8 (tools/checks/tune_overlap.py)
+  if (int o = env_level("VTS_DOVL_BLOCKS", c->L - 1 - k)) return o;
   const int items = div_up(c->lv[k - 1].d.ny, gs::R) * 3 * kSeg;
-  return std::max(2, std::min(items / 8, dovl_workers()));
+  return std::max(2, std::min(items / div, dovl_workers()));
 }
 static int aovl_blocks(const Ctx* c, int k) {  // k_prolong_rows into level k
+  static const int div = env_int("VTS_OVL_DIV", 4);
+  if (int o = env_level("VTS_OVL_BLOCKS", c->L - 1 - k)) return o;
   const int items = div_up(c->lv[k].d.ny, gs::R) * div_up(c->lv[k].d.nx, kChunk);
-  return std::max(1, std::min(items / 4, ovl_workers()));
+  return std::max(1, std::min(items / div, ovl_workers()));
 }
 static int sm_count() {
   static const int n = [] {
