@@ -139,24 +139,28 @@ __global__ void k_mr_update(int len, double* __restrict__ v, const double* __res
   }
 }
 
-// the iteration's state into the pinned host mirror (cudaMallocHost memory is
-// device-accessible under unified addressing): a kernel, so the next iteration's
-// launches stay in the programmatic-launch chain, which a copy-engine transfer breaks
-__global__ void k_mr_publish(const MinresDev* __restrict__ st, MinresDev* host) {
-  pdl_enter();
+// The iteration's state goes into the pinned host mirror (cudaMallocHost memory is
+// device-accessible under unified addressing) from a kernel, so the next iteration's
+// launches stay in the programmatic-launch chain, which a copy-engine transfer breaks.
+// the iteration's state into the pinned host mirror, by one thread (k_mr_verify's tail)
+VTS_DEVICE_INLINE void publish_state(const MinresDev* st, MinresDev* host) {
   constexpr int kWords = sizeof(MinresDev) / 8;
-  static_assert(sizeof(MinresDev) % 8 == 0, "state copied in 8-byte words");
-  if ((int)threadIdx.x < kWords)
-    reinterpret_cast<volatile unsigned long long*>(host)[threadIdx.x] =
-        reinterpret_cast<const unsigned long long*>(st)[threadIdx.x];
+  for (int i = 0; i < kWords; ++i)
+    reinterpret_cast<volatile unsigned long long*>(host)[i] = reinterpret_cast<const volatile unsigned long long*>(st)[i];
   __threadfence_system();
 }
 
-// true residual after a verify apply: relres = ||b - Ax|| / ||b||  (linalg.py:231-239)
+// true residual after a verify apply: relres = ||b - Ax|| / ||b||  (linalg.py:231-239); with
+// `host`, the iteration's final state is then published to the pinned mirror (formerly a
+// separate one-block kernel: one launch less per iteration): by block 0 when there is nothing to verify, else by
+// the block that finishes the residual
 __global__ void k_mr_verify(int len, const double* __restrict__ b, const double* __restrict__ ax, MinresDev* st,
-                            double* partials, unsigned* counter) {
+                            double* partials, unsigned* counter, MinresDev* host = nullptr) {
   pdl_enter();
-  if (st->no_verify) return;
+  if (st->no_verify) {
+    if (host && blockIdx.x == 0 && threadIdx.x == 0) publish_state(st, host);
+    return;
+  }
   __shared__ double scratch[kThreads / 32];
   double acc[1] = {0.0};
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x) {
@@ -171,13 +175,14 @@ __global__ void k_mr_verify(int len, const double* __restrict__ b, const double*
     if (rel <= st->tol) {
       st->status = kConverged;
       st->stopped = 1;
-      return;
+    } else {
+      st->verify_at = st->est * fmin(0.5, st->tol / rel);
+      if (st->iters >= st->max_iters) {
+        st->status = kCap;
+        st->stopped = 1;
+      }
     }
-    st->verify_at = st->est * fmin(0.5, st->tol / rel);
-    if (st->iters >= st->max_iters) {
-      st->status = kCap;
-      st->stopped = 1;
-    }
+    if (host) publish_state(st, host);
   }
 }
 
@@ -455,7 +460,8 @@ int minres(Ctx* c, const double* b_free, double* x_free, double tol, int max_ite
       VTS_LAUNCHED(c);
     }
     if (int rc = newton_apply_grid(c, xalt, T, nover)) return rc;
-    VTS_CUDA(launch_pdl(k_mr_verify, dim3(grid), dim3(kThreads), 0, c->stream, len, B, T, c->mst, c->partials, c->counters + 12));
+    VTS_CUDA(launch_pdl(k_mr_verify, dim3(grid), dim3(kThreads), 0, c->stream, len, B, T, c->mst, c->partials, c->counters + 12,
+                        publish_kernel() ? c->hmst + (it & 1) : (MinresDev*)nullptr));
     VTS_LAUNCHED(c);
     // assume the update succeeds (the next iteration reads x_out); a failed or
     // stopped iteration makes every later launch a no-op on the device
@@ -463,9 +469,7 @@ int minres(Ctx* c, const double* b_free, double* x_free, double tol, int max_ite
     x_out[it & 1] = xalt;
     std::swap(x, xalt);
     if (publish_kernel()) {
-      static_assert(sizeof(MinresDev) / 8 <= 64, "one block of 64 threads copies the state");
-      VTS_CUDA(launch_pdl(k_mr_publish, dim3(1), dim3(64), 0, c->stream, (const MinresDev*)c->mst, c->hmst + (it & 1)));
-      VTS_LAUNCHED(c);
+      // k_mr_verify published the state
     } else {
       VTS_CUDA(cudaMemcpyAsync(c->hmst + (it & 1), c->mst, sizeof(MinresDev), cudaMemcpyDeviceToHost, c->stream));
     }

@@ -1,0 +1,5 @@
+#!/bin/bash
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out/tl3
+cd tools/probe && nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -DVTS_TIMELINE -DVTS_GS_PROBE -o gs_probe_tl gs_probe.cu -lcuda > ../../gpurun_out/tl3/build.log 2>&1; cd ../..
+VTS_OVL_BLOCKS=16,4,2,1 timeout 200 ./tools/probe/gs_probe_tl 9 > gpurun_out/tl3/timeline_ovl.txt 2>&1
+VTS_OVL_BLOCKS=8,8,4,1 timeout 200 ./tools/probe/gs_probe_tl 9 > gpurun_out/tl3/timeline_ovl8.txt 2>&1
