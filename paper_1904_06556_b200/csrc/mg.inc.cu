@@ -388,7 +388,8 @@ __global__ void __launch_bounds__(1024) k_prolong_rows(int fnx, int fny, const u
                                                        const unsigned long long* cdone, unsigned long long cepoch,
                                                        int cW, int cspan, int cnwin,
                                                        const unsigned long long* cready, unsigned long long cready_tag,
-                                                       unsigned long long* ready, unsigned long long tag, const int* skip) {
+                                                       unsigned long long* ready, unsigned long long tag, const int* skip,
+                                                       int coff) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (skip && ld_relaxed_i32(skip)) return;
   constexpr int R = kBandRows;
@@ -407,7 +408,10 @@ __global__ void __launch_bounds__(1024) k_prolong_rows(int fnx, int fny, const u
         // coarse rows ylo/2 .. (yhi+1)/2 in the coarse backward bands (cny-1-row)/R, their
         // columns >= c0/2: stored once every row of the band is through window w
         // (row R-1 lags: columns >= cnx - cW (w+1) + cspan)
-        const int cb_first = (cny - 1 - (yhi + 1) / 2) / R, cb_last = (cny - 1 - ylo / 2) / R;
+        // (the coarse pair's sweep B bands are offset by coff rows)
+        const int cbands = (cny + R - 1) / R;
+        const int cb_first = (cny - 1 - (yhi + 1) / 2 + coff) / R;
+        const int cb_last = min((cny - 1 - ylo / 2 + coff) / R, cbands - 1);
         const int wneed = min(cnwin, (cnx + cspan - c0 / 2 + cW - 1) / cW);
         const unsigned long long need = (cepoch << 32) | (unsigned long long)wneed;
         for (int cb = cb_first; cb <= cb_last; ++cb) wait_flag_backoff(cdone + cb, need);
@@ -925,6 +929,10 @@ struct GsBand {
   const double* border;        //   sweep A's result
   const double* half_old;
   const double* x_in;
+  // row offset of this sweep's bands: band b holds sweep rows [R b - offset, R b - offset + R).
+  // Sweep B of a pair is offset by R/2 (pair_offset): its band b then needs sweep A's band b
+  // one window ahead instead of band b+1, the band that starts a whole band lag later
+  int offset = 0;
 };
 
 template <bool FWD, bool ZERO, int ROLE>
@@ -942,7 +950,10 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int band = G.band;
   const bool real = band < bands;  // grids are padded to whole clusters
-  const int rows_here = real ? min(R, ny - band * R) : 0;
+  const int H = G.offset;
+  const int row0 = band * R - H;  // sweep row of band row 0
+  // band rows [l_lo, l_hi) exist (an offset band 0 starts in the padding before row 0)
+  const int l_lo = max(0, -row0), l_hi = real ? min(R, ny - row0) : 0;
   const bool has_above = real && band > 0;
   const int T = nx + SKEW * (R - 1);
   const int nwin = (T + W - 1) / W;
@@ -996,33 +1007,33 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
   // holding columns <= W (w+1) - 1, and once the box wraps past the last column
   // (W (w+1) > nx: row R-1 continues in the next band's first row), the next band's
   // segments holding the wrapped columns <= W (w+1) - 1 - nx
-  auto gate_window = [&](int w, int& got, int& got_next) {
-    bool waited = false;
-    const int cmax = min(nx - 1, W * (w + 1) - 1);
+  // (an offset band's box rows lie in the level's bands band-1 and band, and its wrapped
+  // positions stay inside them)
+  auto gate_band = [&](int bb, int& got, int cmax, bool& waited) {
     for (; got < G.ready_seg; ++got) {
       int c0, c1;
       seg_cols(nx, got, c0, c1);
       if (c0 > cmax) break;
-      while (ld_acquire(G.ready + (size_t)band * G.ready_seg + got) < G.ready_tag) {
+      while (ld_acquire(G.ready + (size_t)bb * G.ready_seg + got) < G.ready_tag) {
       }
       waited = true;
     }
-    if (band + 1 < bands && W * (w + 1) > nx) {
-      const int wmax = W * (w + 1) - 1 - nx;
-      for (; got_next < G.ready_seg; ++got_next) {
-        int c0, c1;
-        seg_cols(nx, got_next, c0, c1);
-        if (c0 > wmax) break;
-        while (ld_acquire(G.ready + (size_t)(band + 1) * G.ready_seg + got_next) < G.ready_tag) {
-        }
-        waited = true;
-      }
+  };
+  auto gate_window = [&](int w, int& got, int& got_next) {
+    bool waited = false;
+    const int cmax = min(nx - 1, W * (w + 1) - 1);
+    if (H) {
+      if (band >= 1) gate_band(band - 1, got_next, cmax, waited);
+      gate_band(band, got, cmax, waited);
+    } else {
+      gate_band(band, got, cmax, waited);
+      if (band + 1 < bands && W * (w + 1) > nx) gate_band(band + 1, got_next, W * (w + 1) - 1 - nx, waited);
     }
     if (waited) asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores -> this warp's TMA reads
   };
   // band row l -> grid row; box row of band row l; slot position of step st
   auto grid_row = [&](int l) {
-    const int r = band * R + l;
+    const int r = row0 + l;
     return FWD ? r : ny - 1 - r;
   };
   // grid column of slot position p in window w for band row l
@@ -1036,7 +1047,7 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
     return;
   } else if (warp == 1) {  // ---------------- loader (one thread, TMA boxes)
     if (lane == 0) {
-      const int iy0 = band * R, iyb = ny - 1 - band * R;
+      const int iy0 = row0, iyb = ny - 1 - row0;
       const bool gate = ZERO && G.ready;  // descent overlap: b of the window is restricted
       int got = 0, got_next = 0;
       for (int w = 0; w < nwin; ++w) {
@@ -1060,7 +1071,7 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
     }
   } else if (warp == 2 || warp == 3) {  // ---------------- storer (rows 0..R-2) / publisher (row R-1)
     const bool pub = warp == 3;
-    const bool publish = pub && rows_here == R && band * R + R < ny && !dsm_out;
+    const bool publish = pub && l_hi == R && row0 + R < ny && !dsm_out;
     uint32_t r_above = 0, r_mbar = 0;  // the next band's above ring / its barriers (cluster addresses)
     if (pub && dsm_out) {
       asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r_above) : "r"(smem_u32(&S.above[0][0])), "r"(crank + 1));
@@ -1076,14 +1087,14 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
         constexpr int kRows = ROLE == 0 ? R - 1 : R;
         for (int i = lane; i < kRows * W; i += 32) {
           const int l = i / W, p = i - (i / W) * W;
-          if (l >= rows_here) continue;
+          if (l < l_lo || l >= l_hi) continue;
           const int ix = grid_ix(w, l, p);
           const int j = FWD ? ix : nx - 1 - ix;
           if (j < 0 || j >= nx || ix < 0 || ix >= nx) continue;
           *reinterpret_cast<double2*>(x + 2 * ((size_t)grid_row(l) * nx + ix)) = S.out[s][l][p];
         }
 
-      } else if (R - 1 < rows_here) {
+      } else if (R - 1 < l_hi) {
         const int l = R - 1;
         if (lane < W) {
           const int ix = grid_ix(w, l, lane);
@@ -1128,7 +1139,7 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
       }
     }
   } else if (warp == 4) {  // ---------------- stager (previous band's last row -> above ring)
-    if (has_above && rows_here > 0 && !dsm_in) {
+    if (has_above && l_hi > l_lo && !dsm_in) {
       double* row = G.xfer + 2 * (size_t)(band - 1) * nx;  // the previous band's last row
       // above slot a = w + 1 holds sweep columns W*w + SKEW + [0, W); a = 0 is the preload
       for (int a = 0; a <= nwin; ++a) {
@@ -1153,7 +1164,7 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
       }
     }
   } else if (warp == 0) {
-    gs_compute<FWD, ZERO>(S, nx, ngrid, band + (ROLE == 2 ? 128 : 0), rows_here, has_above, dsm_in, crank, nwin,
+    gs_compute<FWD, ZERO>(S, nx, ngrid, band + (ROLE == 2 ? 128 : 0), l_hi, has_above, dsm_in, crank, nwin,
                           G.xa_src);  // (band only labels the probe timeline)
   } else if ((ROLE == 1 || G.bdone) && warp == kReleaseWarp) {  // ---------------- stored-window counter
     // (sweep B with G.bdone: the same counter for the finer level's prolongation or
@@ -1179,7 +1190,7 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
     // next band (its first row) through window w-1
     if (lane == 0) {
       const unsigned long long tag = G.epoch << 32;
-      const int iy0 = band * R, iyb = ny - 1 - band * R;
+      const int iy0 = row0, iyb = ny - 1 - row0;
       // ascent overlap: x_old of this band and of the next band's first row is
       // prolongated by k_prolong_rows, chunk by chunk, while the coarser level still
       // sweeps; window w's builders read columns >= nx - W (w+1) - 1 (the wrapped
@@ -1201,11 +1212,24 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
           }
         }
         if (kGated) {
-          while (ld_acquire(G.stored + band) < (tag | (unsigned long long)min(w + 2, nwin))) {
-          }
-          if (band + 1 < bands)
-            while (ld_acquire(G.stored + band + 1) < (tag | (unsigned long long)min(w, nwin))) {
+          // the box's rows and their later neighbours, in sweep A's bands: aligned, A's band
+          // through window w+1 and its next band (first row) through w-1; offset by R/2,
+          // A's band (rows 0 .. R/2) through window w and the previous band (rows R/2 .. R-1)
+          // through w+2 (A computes column c of its row r at step c + SKEW r; this window's
+          // band row l needs columns up to W (w+1) - SKEW l + SKEW)
+          if (H) {
+            while (ld_acquire(G.stored + band) < (tag | (unsigned long long)min(w + 1, nwin))) {
             }
+            if (band >= 1)
+              while (ld_acquire(G.stored + band - 1) < (tag | (unsigned long long)min(w + 3, nwin))) {
+              }
+          } else {
+            while (ld_acquire(G.stored + band) < (tag | (unsigned long long)min(w + 2, nwin))) {
+            }
+            if (band + 1 < bands)
+              while (ld_acquire(G.stored + band + 1) < (tag | (unsigned long long)min(w, nwin))) {
+              }
+          }
           asm volatile("fence.proxy.async.global;" ::: "memory");  // A's generic stores -> this TMA read
         }
         const int node0 = FWD ? iy0 * nx + W * w : (iyb - R + 2) * nx - W * (w + 1) + SKEW * (R - 1);
@@ -1219,7 +1243,7 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
     // U, b and border of window w as soon as the builders are done with the slot's
     // previous window -- ahead of the compute ring, which frees slots later
     if (lane == 0) {
-      const int iy0 = band * R, iyb = ny - 1 - band * R;
+      const int iy0 = row0, iyb = ny - 1 - row0;
       const bool gate = FWD && G.ready;  // descent overlap: b of the window is restricted
       int got = 0, got_next = 0;
       for (int w = 0; w < nwin; ++w) {
@@ -1253,7 +1277,7 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
       __syncwarp();
     }
     const double xa = G.ready ? __ldcg(G.xa_src + ngrid) : G.xa_src[ngrid];
-    const int iy0 = band * R, iyb = ny - 1 - band * R;
+    const int iy0 = row0, iyb = ny - 1 - row0;
     auto build = [&](int w) {
       const int s = w % NS, sb = w % NSB;
       mbar_wait(&S.loaded[sb], (w / NSB) & 1);
@@ -1344,7 +1368,8 @@ __global__ void __launch_bounds__(32 * gs::kWarpsPair, 1)
               unsigned long long* flags, double* xfer, int groups, unsigned long long epoch,
               const double* __restrict__ b,
               const double* __restrict__ border, const double* __restrict__ half_old,
-              const unsigned long long* ready, unsigned long long ready_tag, int ready_seg, int mode, const int* skip) {
+              const unsigned long long* ready, unsigned long long ready_tag, int ready_seg, int mode, const int* skip,
+              int b_offset) {
   // mode bit 0 (overlap): this launch runs beside the neighbouring level's pair and
   // its residual/restriction or prolongation pass, ordered by the ready flags only,
   // so it must not wait for the previous grid; bit 1: publish sweep B's per-window
@@ -1368,7 +1393,7 @@ __global__ void __launch_bounds__(32 * gs::kWarpsPair, 1)
   } else {
     GsBand G{nx, ny, ngrid, pad_nodes, bands, (int)blockIdx.x - nA, &mapSB, &mapSB, &mapQB, &mapBB, &mapXB, &mapUB, x, x,
              xfer + 2 * (size_t)groups * nx, (mode & 2) ? flags : nullptr, ready, ready_tag, ready_seg, flags + 2 * groups, epoch, b,
-             border, half_old, x1};
+             border, half_old, x1, b_offset};
     gs_band<FWD, false, 2>(G);
   }
   VTS_TL_END(FWD ? 0 : 1, nx);
@@ -1848,6 +1873,17 @@ static int gs_sweep(Ctx* c, int k, const double* b, double* x, bool forward, boo
   return launch_tri<false, false>(c, L, mS, mP, mP, x, skip);
 }
 
+// row offset of a pair's sweep B (GsBand::offset): R/2 when its bands still fit the grid
+// (VTS_PAIR_OFFSET=0: aligned bands, A/B checks)
+static int pair_offset(const LevelBuf& L) {
+  static const bool on = [] {
+    const char* e = getenv("VTS_PAIR_OFFSET");
+    return !(e && e[0] == '0');
+  }();
+  const int h = gs::R / 2;
+  return (on && div_up(L.d.ny + h, gs::R) <= div_up(L.d.ny, gs::R)) ? h : 0;
+}
+
 // Two consecutive sweeps of level k as one pipelined launch (k_gs_pair): x <- B(A(x)).
 // Forward pair: A may start from the zero guess (the V-cycle's first pre-smoothing
 // sweep).  Returns 1 (nothing launched) when the 2 x clusters of the grid cannot
@@ -1938,15 +1974,15 @@ static int gs_pair(Ctx* c, int k, const double* b, double* x, bool forward, bool
   if (forward && zero_a)
     VTS_CUDA(cudaLaunchKernelEx(&cfg, k_gs_pair<true, true>, L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, bands, mSA,
                                 mPA, mQA, mSB, mBB, mQB, mXB, mUB, mXA, L.x1, x, L.gs_flags, L.gs_xfer, L.gs_groups, epoch, b,
-                                (const double*)L.d.border, old_half, ready, ready_tag, ready_seg, mode, skip));
+                                (const double*)L.d.border, old_half, ready, ready_tag, ready_seg, mode, skip, pair_offset(L)));
   else if (forward)
     VTS_CUDA(cudaLaunchKernelEx(&cfg, k_gs_pair<true, false>, L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, bands, mSA,
                                 mPA, mQA, mSB, mBB, mQB, mXB, mUB, mXA, L.x1, x, L.gs_flags, L.gs_xfer, L.gs_groups, epoch, b,
-                                (const double*)L.d.border, old_half, ready, ready_tag, ready_seg, mode, skip));
+                                (const double*)L.d.border, old_half, ready, ready_tag, ready_seg, mode, skip, pair_offset(L)));
   else
     VTS_CUDA(cudaLaunchKernelEx(&cfg, k_gs_pair<false, false>, L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, bands,
                                 mSA, mPA, mQA, mSB, mBB, mQB, mXB, mUB, mXA, L.x1, x, L.gs_flags, L.gs_xfer, L.gs_groups, epoch, b,
-                                (const double*)L.d.border, old_half, ready, ready_tag, ready_seg, mode, skip));
+                                (const double*)L.d.border, old_half, ready, ready_tag, ready_seg, mode, skip, pair_offset(L)));
   VTS_LAUNCHED(c);
   if (pe) VTS_CUDA(cudaEventRecord(pe->b, c->stream));
   *launched = true;
@@ -2205,7 +2241,7 @@ int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
                                   (const uint8_t*)C.d.free_mask, (const double*)C.x,
                                   (const unsigned long long*)C.gs_flags, C.pair_epoch, gs::W, gs::SKEW * (gs::R - 1),
                                   pair_nwin(C), prev_ovl ? (const unsigned long long*)C.ovl_xready : nullptr,
-                                  C.ready_epoch, ready, tag, skip));
+                                  C.ready_epoch, ready, tag, skip, pair_offset(C)));
       VTS_LAUNCHED(c);
       bool launched = false;
       if (int rc = gs_pair(c, k, b, x, false, false, skip, &launched, 1 | mode, ready, tag, nch)) return rc;
