@@ -171,6 +171,7 @@ __device__ __forceinline__ int tl_slot(int kind, int nx) {
   const int k = 31 - __clz(max(nx - 1, 4)) - 2;
   return kind * 16 + min(max(k, 0), 15);
 }
+__device__ unsigned long long g_items[1024][4];  // finest residual/restriction items: flag wait start, work start, end, block
 #define VTS_TL_BEGIN(kind, nx) \
   do { if (threadIdx.x == 0) atomicMin(&g_tl[tl_slot(kind, nx)][0], tl_now()); } while (0)
 #define VTS_TL_END(kind, nx) \

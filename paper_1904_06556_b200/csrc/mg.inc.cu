@@ -460,7 +460,10 @@ __global__ void __launch_bounds__(1024) k_prolong_rows(int fnx, int fny, const u
 // Items run in dependency order, round robin over the blocks.  x_alpha's part of
 // the residual is a reduction over the whole level: the blocks' last phase, with
 // k_level_apply<true>'s reduction tree.  Same arithmetic per node as k_level_apply<true> / k_restrict.
-constexpr int kSeg = 8;
+#ifndef VTS_KSEG
+#define VTS_KSEG 8
+#endif
+constexpr int kSeg = VTS_KSEG;  // column segments per row band of the descent overlap items
 VTS_DEVICE_INLINE void seg_cols(int n, int s, int& c0, int& c1) {
   c0 = (int)((long long)n * s / kSeg);
   c1 = (int)((long long)n * (s + 1) / kSeg);
@@ -482,6 +485,13 @@ __global__ void __launch_bounds__(1024) k_residual_restrict_rows(
   VTS_TL_BEGIN(2, nx);
   const double xa = __ldcg(x + ngrid);
   for (int it = blockIdx.x; it < items; it += gridDim.x) {
+#ifdef VTS_TIMELINE
+    const bool trace = nx == 1025 && it < 1024 && threadIdx.x == 0;
+    if (trace) g_items[it][0] = tl_now(), g_items[it][3] = blockIdx.x;
+#define VTS_ITEM_MARK(i) do { if (trace) g_items[it][i] = tl_now(); } while (0)
+#else
+#define VTS_ITEM_MARK(i) do {} while (0)
+#endif
     // a coarse band's items in column order: R(2cb, 0) R(2cb+1, 0), then per segment
     // t = 1..kSeg-1: R(2cb, t) R(2cb+1, t) P(cb, t-1), and P(cb, kSeg-1) last
     const int cb = it / (3 * kSeg), q = it % (3 * kSeg);
@@ -512,6 +522,7 @@ __global__ void __launch_bounds__(1024) k_residual_restrict_rows(
           }
       }
       __syncthreads();
+      VTS_ITEM_MARK(1);
       int c0, c1;
       seg_cols(nx, s, c0, c1);
       const int w = c1 - c0, y0 = fb * R, nr = min(R, ny - y0);
@@ -525,6 +536,7 @@ __global__ void __launch_bounds__(1024) k_residual_restrict_rows(
         __threadfence();
         st_release(rdone + (size_t)fb * kSeg + s, rtag);
       }
+      VTS_ITEM_MARK(2);
     } else {
       if (threadIdx.x == 0) {
         // r on the fine segments holding columns 2 c0 - 1 .. 2 (c1 - 1) + 1
@@ -540,6 +552,7 @@ __global__ void __launch_bounds__(1024) k_residual_restrict_rows(
           }
       }
       __syncthreads();
+      VTS_ITEM_MARK(1);
       int c0, c1;
       seg_cols(cnx, s, c0, c1);
       const int w = c1 - c0, y0 = cb * R, nr = min(R, cny - y0);
@@ -552,6 +565,7 @@ __global__ void __launch_bounds__(1024) k_residual_restrict_rows(
         __threadfence();
         st_release(cready + (size_t)cb * kSeg + s, ctag);
       }
+      VTS_ITEM_MARK(2);
     }
   }
   // x_alpha's residual row with k_level_apply<true>'s reduction tree: its grid of

@@ -157,6 +157,28 @@ int main(int argc, char** argv) {
       printf("  %-20s L%-2d start %7.1f  end %7.1f  (%6.1f us)\n", names[i / 16], i % 16, (tl[2 * i] - t0) / 1e3,
              tl[2 * i + 1] ? (tl[2 * i + 1] - t0) / 1e3 : -1.0, tl[2 * i + 1] ? (tl[2 * i + 1] - tl[2 * i]) / 1e3 : 0.0);
     }
+    if (rep == 1) {  // the finest level's residual/restriction items: wait and work times
+      std::vector<unsigned long long> it(1024 * 4);
+      cudaMemcpyFromSymbol(it.data(), vts::g_items, it.size() * 8);
+      const int R = vts::gs::R, cb = (c->lv[levels - 2].d.ny + R - 1) / R, items = cb * 3 * vts::kSeg;
+      double work_sum = 0.0, wait_sum = 0.0;
+      std::vector<std::pair<double, int>> ends;
+      for (int i = 0; i < items && i < 1024; ++i) {
+        if (!it[4 * i + 2]) continue;
+        work_sum += (it[4 * i + 2] - it[4 * i + 1]) / 1e3;
+        wait_sum += (it[4 * i + 1] - it[4 * i]) / 1e3;
+        ends.push_back({(it[4 * i + 2] - t0) / 1e3, i});
+      }
+      std::sort(ends.begin(), ends.end());
+      printf("  finest resid/restrict items: %d, mean work %.2f us, mean wait %.2f us; last 12:\n", (int)ends.size(),
+             work_sum / std::max<size_t>(1, ends.size()), wait_sum / std::max<size_t>(1, ends.size()));
+      for (size_t k = ends.size() > 12 ? ends.size() - 12 : 0; k < ends.size(); ++k) {
+        const int i = ends[k].second;
+        printf("    item %3d (block %2llu, q %2d): wait from %7.1f, work %7.1f -> %7.1f (%.1f us)\n", i, it[4 * i + 3],
+               i % (3 * vts::kSeg), (it[4 * i] - t0) / 1e3, (it[4 * i + 1] - t0) / 1e3, (it[4 * i + 2] - t0) / 1e3,
+               (it[4 * i + 2] - it[4 * i + 1]) / 1e3);
+      }
+    }
 #ifdef VTS_GS_PROBE
     if (rep == 1) {  // bands of the last pair of the V-cycle (the finest ascent pair)
       std::vector<long long> pr(4 * 256);
