@@ -134,3 +134,88 @@ def test_fused_evaluation_matches_the_two_kernel_pass(monkeypatch):
     for k in ("res_u", "res_lo", "q", "a", "rho_hat"):
         assert np.array_equal(out["0"][k], out["1"][k]), k
     np.testing.assert_allclose(out["0"]["scal"], out["1"]["scal"], rtol=1e-14)
+
+
+def _step_args(prob, ops, state, ev, W, cfg, bounds, pen):
+    from paper_1904_06556_b200 import pbm
+    from paper_1904_06556_b200.fem import ptr
+
+    a = _lib.NewtonStepArgs()
+    a.u, a.nu_lo, a.nu_up = ptr(W.u), ptr(W.nu_lo), ptr(W.nu_up)
+    for k in ("rho", "p", "mu_lo", "mu_up", "q_lo", "q_up"):
+        setattr(a, k, ptr(getattr(state, k)))
+    a.f, a.lower, a.upper = ptr(prob.f), ptr(bounds.lower), ptr(bounds.upper)
+    a.volume, a.norm_f, a.norm_bounds, a.branch = float(bounds.volume), ops.norm_f, bounds.norm, pen.branch
+    for k in pbm._StepWork._EV:
+        setattr(a, k, ptr(W.ev[k]))
+    a.chat, a.rhs, a.border, a.du, a.dnu_lo, a.dnu_up = (ptr(t) for t in (W.chat, W.rhs, W.border, W.du, W.dnu_lo,
+                                                                          W.dnu_up))
+    a.minres_floor, a.minres_cap, a.minres_tol = cfg.minres_floor, cfg.minres_cap, 0.5
+    a.armijo_c1, a.armijo_shrink, a.armijo_max_halvings = cfg.armijo_c1, cfg.armijo_shrink, cfg.armijo_max_halvings
+    a.shift_scale = 1e-12
+    a.alpha, a.value, a.res_alpha = float(state.alpha), ev.value, ev.res_alpha
+    return a
+
+
+def _c1_step_setup():
+    from paper_1904_06556_b200 import pbm
+
+    prob = vts.build_config("C1")
+    ops = vts.ElementOps(prob.fine)
+    cfg = vts.PbmConfig()
+    bounds = vts.DensityBounds.for_problem(prob.m, prob.volume, cfg.rho_lower)
+    pen = vts.PenaltyBarrier(cfg.branch)
+    state = vts.PbmState.initial(prob.n, prob.m, prob.volume)
+    ev = vts.eval_lagrangian(state, ops, prob.f, bounds, pen)
+    W = pbm._StepWork(ops)
+    W.u.copy_(state.u)
+    W.nu_lo.copy_(state.nu_lo)
+    W.nu_up.copy_(state.nu_up)
+    for k in pbm._StepWork._EV:
+        W.ev[k].copy_(getattr(ev, k) if hasattr(ev, k) else getattr(ev.blocks, k))
+    return prob, ops, cfg, bounds, pen, state, ev, W
+
+
+def test_device_step_exhausted_line_search_leaves_the_state():
+    """An unreachable decrease target (value = -1e300): every one of the 41 trials is
+    rejected (pbm.py:299-318), the step reports the exhausted search after 21 host
+    passes of two trials, and neither the state nor the evaluation moves."""
+    prob, ops, cfg, bounds, pen, state, ev, W = _c1_step_setup()
+    a = _step_args(prob, ops, state, ev, W, cfg, bounds, pen)
+    a.value = -1e300
+    u0, nu0, res0 = W.u.clone(), W.nu_lo.clone(), W.ev["res_u"].clone()
+    r = _lib.NewtonStepResult()
+    assert _lib.load().vts_newton_step(ops.handle, ctypes.byref(a), ctypes.byref(r)) == 0
+    assert r.status == 2
+    assert r.trials == cfg.armijo_max_halvings + 1
+    assert r.host_syncs == (cfg.armijo_max_halvings + 2) // 2
+    assert r.slope < 0.0
+    assert torch.equal(W.u, u0) and torch.equal(W.nu_lo, nu0) and torch.equal(W.ev["res_u"], res0)
+    assert r.alpha == float(state.alpha)
+
+
+def test_device_step_minres_error_carries_the_sound_iterate():
+    """A negative density makes the bound Schur matrix indefinite; with a preconditioner
+    built from it MINRES raises (linalg.py:166-169 / 205-206) -- through the device step
+    with the same code as the call-by-call path."""
+    prob, ops, cfg, bounds, pen, state, ev, W = _c1_step_setup()
+    state.rho[: prob.m // 2] = -1.0
+    ev = vts.eval_lagrangian(state, ops, prob.f, bounds, pen)
+    from paper_1904_06556_b200 import pbm
+
+    for k in pbm._StepWork._EV:
+        W.ev[k].copy_(getattr(ev, k) if hasattr(ev, k) else getattr(ev.blocks, k))
+    a = _step_args(prob, ops, state, ev, W, cfg, bounds, pen)
+    r = _lib.NewtonStepResult()
+    rc_dev = _lib.load().vts_newton_step(ops.handle, ctypes.byref(a), ctypes.byref(r))
+    mat, rhs = vts.schur_system(ev, ops)
+    try:
+        mg = vts.MgPreconditioner(mat, prob.transfers)
+        vts.minres_solve(mat, rhs, vts.MinresConfig(tol=0.5, max_iters=cfg.minres_cap), mg.apply)
+        rc_host = 0
+    except vts.MinresError as exc:
+        rc_host = {"preconditioner is indefinite: <M r, r> < 0": 1, "MINRES recurrence broke down": 2}.get(str(exc), 3)
+    except Exception:  # the coarse factor failed even with the shift (multigrid.py:102)
+        rc_host = 6
+    assert rc_dev == rc_host
+    assert rc_dev != 0
