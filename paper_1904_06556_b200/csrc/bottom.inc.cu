@@ -34,6 +34,10 @@ __device__ int g_bot_n;
   } while (0)
 #endif
 constexpr int kBotMaxLevels = 8;
+#ifndef VTS_BOT_EXP
+#define VTS_BOT_EXP 0  // probe-only timing experiments on bot_coarse (results then wrong)
+#endif
+constexpr size_t kBotSmemMax = 227 * 1024;  // the opt-in dynamic shared memory limit of one CTA
 
 struct BotLevel {
   int nx, ny, nn, ngrid;
@@ -59,6 +63,7 @@ struct BotArgs {
   int off_y;
   int off_stage, off_q;  // staged half-stencil and right-hand side, padded ((nn + 2 kBotPad) nodes)
   int off_red;           // reduction scratch: 32 virtual-block partials + 8 x 32 warp sums
+  int off_dblk;          // N0 > 32: two buffers of bot_coarse's diagonal + sub-diagonal blocks
 };
 
 // one Gauss-Seidel sweep of level L: x <- sweep(x; b) (zero_guess: x_old = 0)
@@ -226,7 +231,7 @@ __device__ __noinline__ void bot_residual(const BotLevel& L, double* sm, const B
 }
 
 // x0 = chol^-1 b0 (k_coarse_solve's column order)
-__device__ void bot_coarse(const BotLevel& C, double* sm, const BotArgs& A) {
+__device__ __noinline__ void bot_coarse(const BotLevel& C, double* sm, const BotArgs& A) {
   double* sb = sm + C.off_b;
   double* sx = sm + C.off_x;
   double* y = sm + A.off_y;
@@ -261,20 +266,103 @@ __device__ void bot_coarse(const BotLevel& C, double* sm, const BotArgs& A) {
     __syncthreads();
     BOT_MARK();  // coarse: both substitutions
   } else {
-  for (int j = 0; j < N; ++j) {
-    if (tid == 0) y[j] = div_by(y[j], Lf[(size_t)j * N + j], A.rdiag[j]);
+    // Blocked by 32 columns, bit-identical to the column-by-column substitution of
+    // k_coarse_solve: every y[i] still receives its updates fma(-L[i][j], y[j], .) in
+    // increasing j (decreasing j going back) and is divided right after its last one.
+    // Per block: warp 0 solves the 32 x 32 diagonal block by shuffles (as the N <= 32
+    // path), then every thread applies the block's 32 columns to its own later rows in
+    // column order -- two barriers per block instead of two per column.
+    // Blocks of 32 columns with one block of look-ahead, bit-identical to the
+    // column-by-column substitution of k_coarse_solve: every y[i] still receives its
+    // updates fma(-L[i][j], y[j], .) in increasing j (decreasing j going back) and is
+    // divided right after its last one.  Phase k: warp 0 applies block k-1's columns
+    // to block k's rows, then solves block k's 32 x 32 diagonal block by shuffles;
+    // meanwhile warps 1.. apply block k-1's columns to the rows below block k and
+    // stage block k+1's diagonal and sub-diagonal blocks into shared memory, so the
+    // serial chain of warp 0 reads only shared memory.  One barrier per block.
+    // The loops stay rolled: the fused kernel's sweeps run from the instruction
+    // cache, and fully unrolled substitutions here evicted them (sweeps 6 -> 41 us).
+    // The factor is read from global memory (ld.global.nc): N0 > 32 keeps no copy
+    // in shared memory.
+    const double* __restrict__ G = A.chol;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int nb = (N + 31) / 32;
+    constexpr int kBuf = 2 * 32 * 33 + 32;  // diagonal [32][33], sub-diagonal [32][33], rdiag [32]
+    double* const buf0 = sm + A.off_dblk;
+    // forward block k = columns [32k, min(32k + 32, N)); backward block b = [max(N - 32b - 32, 0), N - 32b)
+    // stage the diagonal block [lo, hi) and the coupling block with [plo, phi) (forward:
+    // sub[r][t] = L[lo + r][plo + t]; backward: sub[r][t] = L[plo + t][lo + r])
+    auto stage = [&](double* B, int lo, int hi, int plo, int phi, bool fwd) {
+      double* D = B;
+      double* S = B + 32 * 33;
+      for (int idx = tid - 32; idx < 32 * 32; idx += blockDim.x - 32) {
+        const int a = idx >> 5, e = idx & 31;
+        const double d = (e <= a && lo + a < hi) ? __ldg(G + (size_t)(lo + a) * N + lo + e) : 0.0;
+        double v = 0.0;
+        if (fwd && lo + a < hi && plo + e < phi) v = __ldg(G + (size_t)(lo + a) * N + plo + e);
+        if (!fwd && plo + a < phi && lo + e < hi) v = __ldg(G + (size_t)(plo + a) * N + lo + e);
+        D[a * 33 + e] = d;
+        S[fwd ? a * 33 + e : e * 33 + a] = v;
+      }
+      if (tid >= 32 && tid < 64 && lo + tid - 32 < hi) B[2 * 32 * 33 + tid - 32] = __ldg(A.rdiag + lo + tid - 32);
+    };
+    if (warp > 0) stage(buf0, 0, min(32, N), 0, 0, true);
     __syncthreads();
-    const double yj = y[j];
-    for (int i = j + 1 + tid; i < N; i += blockDim.x) y[i] = fma(-Lf[(size_t)i * N + j], yj, y[i]);
-    __syncthreads();
-  }
-  for (int j = N - 1; j >= 0; --j) {
-    if (tid == 0) y[j] = div_by(y[j], Lf[(size_t)j * N + j], A.rdiag[j]);
-    __syncthreads();
-    const double yj = y[j];
-    for (int i = tid; i < j; i += blockDim.x) y[i] = fma(-Lf[(size_t)j * N + i], yj, y[i]);
-    __syncthreads();
-  }
+    for (int ph = 0; ph < 2 * nb; ++ph) {
+      const bool fwd = ph < nb;
+      const int k = fwd ? ph : ph - nb;  // block index in this direction
+      const int lo = fwd ? 32 * k : max(N - 32 * k - 32, 0), hi = fwd ? min(32 * k + 32, N) : N - 32 * k;
+      const int plo = k == 0 ? 0 : fwd ? lo - 32 : hi, phi = k == 0 ? 0 : fwd ? lo : min(hi + 32, N);
+      double* const B = buf0 + (ph & 1) * kBuf;
+      if (warp == 0) {
+        // block k-1's columns on block k's rows, then block k's diagonal solve
+        const int r = lo + lane;
+        const bool own = r < hi;
+        double yi = own ? y[r] : 0.0;
+        const double* S = B + 32 * 33 + lane * 33;
+        const int np = phi - plo;
+        if (fwd)
+          for (int t = 0; t < np; ++t) yi = fma(-S[t], y[plo + t], yi);
+        else
+          for (int t = np - 1; t >= 0; --t) yi = fma(-S[t], y[plo + t], yi);
+        const double* D = B;
+        const double* rd = B + 2 * 32 * 33;
+        const int n = hi - lo;
+        for (int u = 0; u < n && VTS_BOT_EXP != 2; ++u) {
+          const int t = fwd ? u : n - 1 - u;
+          const double q = div_by(yi, D[t * 33 + t], rd[t]);
+          yi = lane == t ? q : yi;
+          const double yt = __shfl_sync(0xffffffffu, yi, t);
+          const bool below = fwd ? lane > t : lane < t;
+          const double l = below ? D[fwd ? lane * 33 + t : t * 33 + lane] : 0.0;
+          yi = below ? fma(-l, yt, yi) : yi;
+        }
+        if (own) y[r] = yi;
+      } else {
+        // block k-1's columns on the rows beyond block k; stage block k+1
+        if (k > 0 && VTS_BOT_EXP != 1) {
+          const int i0 = fwd ? hi : 0, i1 = fwd ? N : lo;
+          for (int i = i0 + tid - 32; i < i1; i += blockDim.x - 32) {
+            double yi = y[i];
+            if (fwd) {
+              const double* li = G + (size_t)i * N + plo;
+#pragma unroll 8
+              for (int t = 0; t < 32; ++t) yi = fma(-__ldg(li + t), y[plo + t], yi);  // forward blocks k-1 are full
+            } else {
+#pragma unroll 8
+              for (int t = phi - plo - 1; t >= 0; --t) yi = fma(-__ldg(G + (size_t)(plo + t) * N + i), y[plo + t], yi);
+            }
+            y[i] = yi;
+          }
+        }
+        double* const Bn = buf0 + ((ph + 1) & 1) * kBuf;
+        if (ph + 1 < nb) stage(Bn, lo + 32, min(hi + 32, N), lo, hi, true);
+        else if (ph + 1 == nb) stage(Bn, max(N - 32, 0), N, 0, 0, false);
+        else if (ph + 1 < 2 * nb) stage(Bn, max(lo - 32, 0), lo, lo, hi, false);
+      }
+      __syncthreads();
+    }
+    BOT_MARK();  // coarse: both substitutions
   }
   for (int i = tid; i <= C.ngrid; i += blockDim.x) sx[i] = 0.0;
   __syncthreads();
@@ -374,14 +462,16 @@ static int bottom_plan(Ctx* c, BotArgs* A, size_t* smem_bytes) {
     off += 32 + 32 * 8;
     A->off_y = (int)off;
     off += (size_t)c->N0 + (c->N0 & 1);
+    A->off_dblk = (int)off;
+    if (c->N0 > 32) off += 2 * (2 * 32 * 33 + 32);  // bot_coarse's double-buffered blocks
     const size_t base = off * 8;
     const size_t chol = (size_t)c->N0 * c->N0 * 8;
     A->off_chol = -1;
-    if (base + chol <= 200 * 1024) {
+    if (c->N0 <= 32 && base + chol <= kBotSmemMax) {
       A->off_chol = (int)off;
       off += (size_t)c->N0 * c->N0;
     }
-    if (off * 8 <= 200 * 1024) {
+    if (off * 8 <= kBotSmemMax) {
       *smem_bytes = off * 8;
       A->kb = kb;
       return kb;
@@ -397,7 +487,7 @@ static bool g_bot_attr_set = false;
 // right-hand side, L(kb).x receives the level's result
 static int vcycle_bottom(Ctx* c, const BotArgs& plan, size_t smem, const int* skip) {
   if (!g_bot_attr_set) {
-    VTS_CUDA(cudaFuncSetAttribute(k_vcycle_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    VTS_CUDA(cudaFuncSetAttribute(k_vcycle_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, kBotSmemMax));
     g_bot_attr_set = true;
   }
   BotArgs A = plan;

@@ -60,7 +60,7 @@ def test_full_pbm_bitwise_repeatable():
         assert np.array_equal(r.rho.cpu().numpy(), runs[0].rho.cpu().numpy())
 
 
-def _run_ab(tmp_path, name, env_extra):
+def _run_ab(tmp_path, name, env_extra, key="C2"):
     import os
     import subprocess
     import sys
@@ -68,15 +68,18 @@ def _run_ab(tmp_path, name, env_extra):
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = tmp_path / f"{name}.npy"
     env = dict(os.environ, **env_extra)
-    subprocess.run([sys.executable, os.path.join(repo, "tools", "checks", "ab_vcycle.py"), str(out), "C2"],
+    subprocess.run([sys.executable, os.path.join(repo, "tools", "checks", "ab_vcycle.py"), str(out), key],
                    cwd=repo, env=env, check=True, capture_output=True, timeout=600)
     return np.load(out)
 
 
-@pytest.mark.parametrize("switch", ["VTS_NO_PAIR", "VTS_UNFUSED_BOTTOM"])
-def test_fast_paths_are_bitwise_identical_to_the_plain_path(tmp_path, switch):
+@pytest.mark.parametrize("switch,key", [("VTS_NO_PAIR", "C2"), ("VTS_UNFUSED_BOTTOM", "C2"),
+                                        ("VTS_UNFUSED_BOTTOM", "C1")])
+def test_fast_paths_are_bitwise_identical_to_the_plain_path(tmp_path, switch, key):
     """The pipelined sweep pairs and the fused V-cycle bottom compute exactly what
-    the one-sweep-per-launch path computes (V-cycle output and a MINRES solution)."""
-    fast = _run_ab(tmp_path, "fast", {})
-    plain = _run_ab(tmp_path, "plain", {switch: "1"})
+    the one-sweep-per-launch path computes (V-cycle output and a MINRES solution).
+    C1's coarsest system (290 unknowns) takes the fused bottom's blocked substitution,
+    against k_coarse_solve's column-by-column one."""
+    fast = _run_ab(tmp_path, "fast", {}, key)
+    plain = _run_ab(tmp_path, "plain", {switch: "1"}, key)
     assert np.array_equal(fast, plain)
