@@ -1715,6 +1715,178 @@ __global__ void __launch_bounds__(1024) k_cholesky(int N, double* A, int* status
   if (threadIdx.x == 0) *status = s_fail;
 }
 
+// The same factor, bit for bit, blocked by panels of 32 columns and right-looking
+// (k_cholesky's left-looking column loop costs ~1.5 ms at N0 ~ 300: every column is
+// two barriers, a block reduction and a serial dot product per row).  What stays
+// fixed, per entry: L[i][j] = (A[i][j] - sum_k L[i][k] L[j][k]) / d_j with the fma
+// chain in increasing k, and d_j^2 = A[j][j] - t_j with t_j summed by k_cholesky's
+// tree (block_sum over 1024 threads: thread k holds fma(L[j][k], L[j][k], 0), a
+// shfl_down warp tree per 32 consecutive k, then warp totals added in order from
+// 0.0; warps past j hold exact zeros).  Here the warp totals of finished panels
+// accumulate in pre[j] in that order, and the current panel's warp tree is taken
+// by warp 0 -- the same additions.  Per panel: (1) stage rows kb.. of the panel
+// columns in shared memory; (2) warp 0 factors the 32 x 32 diagonal block
+// (right-looking inside the warp, no CTA barrier per column); (3) one thread per
+// row below solves its 32 panel entries (left-looking over the panel, registers)
+// and adds the row's warp tree to pre[]; (4) the panel goes back to global memory
+// and the trailing lower triangle receives its 32 updates (4 x 4 register tiles,
+// diagonal entries untouched: d_j starts from the original A[j][j]).
+constexpr int kCholThreads = 512;
+__device__ __forceinline__ double warp_tree32(const double (&v)[32]) {  // warp_sum's shfl_down tree, lane 0
+  double a[16];
+#pragma unroll
+  for (int l = 0; l < 16; ++l) a[l] = v[l] + v[l + 16];
+#pragma unroll
+  for (int l = 0; l < 8; ++l) a[l] = a[l] + a[l + 8];
+#pragma unroll
+  for (int l = 0; l < 4; ++l) a[l] = a[l] + a[l + 4];
+#pragma unroll
+  for (int l = 0; l < 2; ++l) a[l] = a[l] + a[l + 2];
+  return a[0] + a[1];
+}
+
+__global__ void __launch_bounds__(kCholThreads, 1) k_cholesky_blk(int N, double* A, int* status, const int* gate = nullptr) {
+  if (gate && *gate == 0) return;
+  extern __shared__ double csm[];
+  double* const pre = csm;          // [N] warp totals of finished panels, added in order from 0.0
+  double* const dg = csm + N;       // [32] d_j of the current panel
+  double* const Pn = csm + N + 32;  // [(N - kb) x 33] panel columns of rows kb..
+  __shared__ int s_fail;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_fail = 0;
+  for (int i = tid; i < N; i += blockDim.x) pre[i] = 0.0;
+  for (int kb = 0; kb < N; kb += 32) {
+    const int nbk = min(32, N - kb), nr = N - kb;
+    // (1) stage
+    for (int idx = tid; idx < nr * 32; idx += blockDim.x) {
+      const int r = idx >> 5, cc = idx & 31;
+      if (cc < nbk && cc <= r) Pn[r * 33 + cc] = A[(size_t)(kb + r) * N + kb + cc];
+    }
+    __syncthreads();
+    // (2) diagonal block, warp 0; lane l = row kb + l
+    if (warp == 0) {
+      bool fail = false;
+      for (int jj = 0; jj < nbk; ++jj) {
+        double t = lane < jj ? fma(Pn[jj * 33 + lane], Pn[jj * 33 + lane], 0.0) : 0.0;
+        t = warp_sum(t);
+        double dj = 0.0;
+        if (lane == 0) {
+          const double d = Pn[jj * 33 + jj] - (pre[kb + jj] + t);
+          fail = !(d > 0.0);
+          dj = sqrt(d);
+          Pn[jj * 33 + jj] = dj;
+          dg[jj] = dj;
+        }
+        dj = __shfl_sync(0xffffffffu, dj, 0);
+        if (__shfl_sync(0xffffffffu, fail ? 1 : 0, 0)) {
+          if (lane == 0) s_fail = 1;
+          break;
+        }
+        double lv = 0.0;
+        if (lane > jj && lane < nbk) {
+          lv = Pn[lane * 33 + jj] / dj;
+          Pn[lane * 33 + jj] = lv;
+        }
+        __syncwarp();
+        if (lane < nbk)
+          for (int q = jj + 1; q < lane; ++q) Pn[lane * 33 + q] = fma(-lv, Pn[q * 33 + jj], Pn[lane * 33 + q]);
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    if (s_fail) break;
+    // (3) rows below the diagonal block (nbk == 32 whenever there are any)
+    for (int r = 32 + tid; r < nr; r += blockDim.x) {
+      double L[32];
+      double* const row = Pn + r * 33;
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) {
+        double s = row[jj];
+#pragma unroll
+        for (int q = 0; q < jj; ++q) s = fma(-L[q], Pn[jj * 33 + q], s);
+        L[jj] = s / dg[jj];
+        row[jj] = L[jj];
+      }
+      double v[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) v[q] = fma(L[q], L[q], 0.0);
+      pre[kb + r] = pre[kb + r] + warp_tree32(v);
+    }
+    __syncthreads();
+    // (4) panel back to global memory; trailing update of rows/columns kb + 32..
+    for (int idx = tid; idx < nr * 32; idx += blockDim.x) {
+      const int r = idx >> 5, cc = idx & 31;
+      if (cc < nbk && cc <= r) A[(size_t)(kb + r) * N + kb + cc] = Pn[r * 33 + cc];
+    }
+    const int T = nr - 32;
+    if (T > 1) {
+      const int nt = (T + 3) / 4, npairs = nt * (nt + 1) / 2;
+      for (int pidx = tid; pidx < npairs; pidx += blockDim.x) {
+        // pidx -> (ti, tj), tj <= ti, row-major over the lower tile triangle
+        int ti = (int)((sqrt(8.0 * pidx + 1.0) - 1.0) * 0.5);
+        while ((ti + 1) * (ti + 2) / 2 <= pidx) ++ti;
+        while (ti * (ti + 1) / 2 > pidx) --ti;
+        const int tj = pidx - ti * (ti + 1) / 2;
+        const int r0 = 32 + 4 * ti, c0 = 32 + 4 * tj;  // panel-relative rows / columns
+        double acc[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const int r = r0 + a, cc = c0 + b;
+            acc[a][b] = (r < nr && cc < r) ? A[(size_t)(kb + r) * N + kb + cc] : 0.0;
+          }
+#pragma unroll 4
+        for (int q = 0; q < 32; ++q) {
+          double li[4], lj[4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) li[a] = r0 + a < nr ? Pn[(r0 + a) * 33 + q] : 0.0;
+#pragma unroll
+          for (int b = 0; b < 4; ++b) lj[b] = c0 + b < nr ? Pn[(c0 + b) * 33 + q] : 0.0;
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b] = fma(-li[a], lj[b], acc[a][b]);
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const int r = r0 + a, cc = c0 + b;
+            if (r < nr && cc < r) A[(size_t)(kb + r) * N + kb + cc] = acc[a][b];
+          }
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) *status = s_fail;
+}
+
+constexpr int kCholSmemMax = 200 * 1024;  // below the opt-in limit less the kernel's static s_fail
+static size_t chol_blk_smem(int N) { return sizeof(double) * ((size_t)N + 32 + (size_t)N * 33); }
+static bool g_chol_attr_set = false;
+
+// the coarse factor: the blocked kernel when its panel fits in shared memory
+// (VTS_CHOL_LEFT=1: k_cholesky, for A/B checks)
+static cudaError_t launch_cholesky(Ctx* c, int N, const int* gate = nullptr) {
+  static const bool left = [] {
+    const char* e = getenv("VTS_CHOL_LEFT");
+    return e && e[0] == '1';
+  }();
+  const size_t smem = chol_blk_smem(N);
+  if (left || smem > kCholSmemMax) {
+    k_cholesky<<<1, 1024, 0, c->stream>>>(N, c->chol, c->chol_status, gate);
+    return cudaGetLastError();
+  }
+  if (!g_chol_attr_set) {
+    const cudaError_t e = cudaFuncSetAttribute(k_cholesky_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, kCholSmemMax);
+    if (e != cudaSuccess) return e;
+    g_chol_attr_set = true;
+  }
+  k_cholesky_blk<<<1, kCholThreads, smem, c->stream>>>(N, c->chol, c->chol_status, gate);
+  return cudaGetLastError();
+}
+
 // y / d from the correctly rounded reciprocal r = 1/d (__drcp_rn, precomputed per
 // column): q = y r, then one fma correction with the exact remainder y - q d
 // (Markstein's quotient refinement) -- three dependent operations where the
@@ -2327,13 +2499,13 @@ int mg_setup(Ctx* c, double shift_scale, bool device_gate) {
     VTS_CUDA(cudaMemsetAsync(c->chol, 0, sizeof(double) * N * N, c->stream));
     k_dense_coarse<<<div_up(C.d.nnodes, 128), 128, 0, c->stream>>>(C.d.nx, C.d.ny, C.d.stL, C.d.stU, C.d.border,
                                                                     C.grid2free, c->d_corner, N, 0.0, c->chol);
-    k_cholesky<<<1, 1024, 0, c->stream>>>(N, c->chol, c->chol_status);
+    VTS_CUDA(launch_cholesky(c, N));
     k_chol_retry_prep<<<div_up((long long)N * N, 256), 256, 0, c->stream>>>(N, c->chol, c->chol_status, c->chol_retry);
     k_dense_coarse<<<div_up(C.d.nnodes, 128), 128, 0, c->stream>>>(C.d.nx, C.d.ny, C.d.stL, C.d.stU, C.d.border,
                                                                     C.grid2free, c->d_corner, N, 0.0, c->chol,
                                                                     c->chol_retry);
     k_add_shift<<<1, 1024, 0, c->stream>>>(N, shift_scale, c->chol, c->dscal + 20, c->chol_retry);
-    k_cholesky<<<1, 1024, 0, c->stream>>>(N, c->chol, c->chol_status, c->chol_retry);
+    VTS_CUDA(launch_cholesky(c, N, c->chol_retry));
     k_chol_rdiag<<<1, 256, 0, c->stream>>>(c->N0, c->chol, c->chol_rdiag);
     c->launches += 7;
     VTS_CUDA(cudaGetLastError());
@@ -2349,7 +2521,7 @@ int mg_setup(Ctx* c, double shift_scale, bool device_gate) {
       k_add_shift<<<1, 1024, 0, c->stream>>>(N, shift_scale_now, c->chol, c->dscal + 20);
       VTS_LAUNCHED(c);
     }
-    k_cholesky<<<1, 1024, 0, c->stream>>>(N, c->chol, c->chol_status);
+    VTS_CUDA(launch_cholesky(c, N));
     VTS_LAUNCHED(c);
     int st = 0;
     VTS_CUDA(cudaMemcpyAsync(&st, c->chol_status, sizeof(int), cudaMemcpyDeviceToHost, c->stream));

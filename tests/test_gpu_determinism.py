@@ -74,12 +74,14 @@ def _run_ab(tmp_path, name, env_extra, key="C2"):
 
 
 @pytest.mark.parametrize("switch,key", [("VTS_NO_PAIR", "C2"), ("VTS_UNFUSED_BOTTOM", "C2"),
-                                        ("VTS_UNFUSED_BOTTOM", "C1")])
+                                        ("VTS_UNFUSED_BOTTOM", "C1"), ("VTS_CHOL_LEFT", "C1"),
+                                        ("VTS_CHOL_LEFT", "C2")])
 def test_fast_paths_are_bitwise_identical_to_the_plain_path(tmp_path, switch, key):
     """The pipelined sweep pairs and the fused V-cycle bottom compute exactly what
     the one-sweep-per-launch path computes (V-cycle output and a MINRES solution).
     C1's coarsest system (290 unknowns) takes the fused bottom's blocked substitution,
-    against k_coarse_solve's column-by-column one."""
+    against k_coarse_solve's column-by-column one.  VTS_CHOL_LEFT: the blocked
+    right-looking coarse factor against k_cholesky's left-looking column loop."""
     fast = _run_ab(tmp_path, "fast", {}, key)
     plain = _run_ab(tmp_path, "plain", {switch: "1"}, key)
     assert np.array_equal(fast, plain)
