@@ -374,7 +374,15 @@ __global__ void k_prolong_add(int fnx, int fny, const uint8_t* __restrict__ ffm,
 #ifndef VTS_OVL_SLEEP
 #define VTS_OVL_SLEEP 128
 #endif
-constexpr int kChunk = 128;
+#ifndef VTS_KCHUNK
+#define VTS_KCHUNK 128
+#endif
+constexpr int kChunk = VTS_KCHUNK;
+// cluster-size cap of the overlapped ascent pairs (pair_cs_cap)
+#ifndef VTS_ASC_CS
+#define VTS_ASC_CS 16
+#endif
+constexpr int kAscClusterCap = VTS_ASC_CS;
 // Row band height of the wavefront sweeps (gs::R, defined with the sweeps below):
 // the overlap passes index the sweeps' per-band flags with it
 constexpr int kBandRows = 16;
@@ -383,7 +391,11 @@ constexpr int kBandRows = 16;
 VTS_DEVICE_INLINE void wait_flag_backoff(const unsigned long long* f, unsigned long long need) {
   while (ld_acquire(f) < need) __nanosleep(VTS_OVL_SLEEP);
 }
-__global__ void __launch_bounds__(1024) k_prolong_rows(int fnx, int fny, const uint8_t* __restrict__ ffm, double* xf,
+#ifndef VTS_PR_THREADS
+#define VTS_PR_THREADS 1024
+#endif
+constexpr int kPRThreads = VTS_PR_THREADS;  // threads per block of k_prolong_rows
+__global__ void __launch_bounds__(kPRThreads) k_prolong_rows(int fnx, int fny, const uint8_t* __restrict__ ffm, double* xf,
                                                        int cnx, int cny, const uint8_t* __restrict__ cfm, const double* xc,
                                                        const unsigned long long* cdone, unsigned long long cepoch,
                                                        int cW, int cspan, int cnwin,
@@ -468,7 +480,14 @@ VTS_DEVICE_INLINE void seg_cols(int n, int s, int& c0, int& c1) {
   c0 = (int)((long long)n * s / kSeg);
   c1 = (int)((long long)n * (s + 1) / kSeg);
 }
-__global__ void __launch_bounds__(1024) k_residual_restrict_rows(
+// threads per block of k_residual_restrict_rows (a multiple of 256: the border row's
+// reduction runs in virtual blocks of 256 threads)
+#ifndef VTS_RR_THREADS
+#define VTS_RR_THREADS 1024
+#endif
+constexpr int kRRThreads = VTS_RR_THREADS;
+static_assert(kRRThreads % 256 == 0 && kRRThreads >= 256 && kRRThreads <= 1024, "virtual blocks of 256 threads");
+__global__ void __launch_bounds__(kRRThreads) k_residual_restrict_rows(
     int nx, int ny, const double* __restrict__ stL, const double* __restrict__ stU, const double* __restrict__ border,
     const uint8_t* __restrict__ ffm, const double* x, const double* b, double* r, int cnx, int cny,
     const uint8_t* __restrict__ cfm, double* bc, const unsigned long long* bdone, unsigned long long bepoch, int nwin,
@@ -569,7 +588,7 @@ __global__ void __launch_bounds__(1024) k_residual_restrict_rows(
     }
   }
   // x_alpha's residual row with k_level_apply<true>'s reduction tree: its grid of
-  // 256-thread blocks (G = min(nodes / 256, kReduceGridCap)) as virtual blocks, four
+  // 256-thread blocks (G = min(nodes / 256, kReduceGridCap)) as virtual blocks, kRRThreads / 256
   // per block here, each thread's nodes in the same grid-stride order, block_sum's
   // warp trees and sequential warp totals; the last block adds the partials as
   // last_block_reduce does and stores r_alpha into r and the coarser b
@@ -583,7 +602,8 @@ __global__ void __launch_bounds__(1024) k_residual_restrict_rows(
         wait_flag_backoff(bdone + bb, bepoch | (unsigned long long)nwin);
     __syncthreads();
     const int grp = threadIdx.x >> 8, gt = threadIdx.x & 255, lane = threadIdx.x & 31, wg = gt >> 5;
-    for (int base = blockIdx.x * 4; base < G; base += gridDim.x * 4) {
+    constexpr int kVB = kRRThreads / 256;  // virtual blocks per block
+    for (int base = blockIdx.x * kVB; base < G; base += gridDim.x * kVB) {
       const int vb = base + grp;
       double acc = 0.0;
       if (vb < G)
@@ -817,6 +837,7 @@ __global__ void __launch_bounds__(256) k_gs_old(int nx, int ny, int ngrid, const
 __device__ long long g_gs_probe[4 * 256];
 __device__ long long g_gs_probe2[2 * 256];
 __device__ long long g_gs_probe3[2 * 256];  // time inside the step loops, time in the end-of-window handoff
+__device__ int g_gs_probe_nx = 0;  // record only the level with this row length (0: every launch)
 VTS_DEVICE_INLINE long long gtimer() {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -1397,15 +1418,26 @@ __global__ void __launch_bounds__(32 * gs::kWarpsPair, 1)
     ready = nullptr;
   }
   VTS_TL_BEGIN(FWD ? 0 : 1, nx);
-  const int nA = (int)gridDim.x / 2;
-  if ((int)blockIdx.x < nA) {
+  // mode bit 2: the clusters of the two sweeps alternate (A0 B0 A1 B1 ...) instead of
+  // all of A's first, so that a grid that becomes resident cluster by cluster (the
+  // ascent: SMs free up as the coarser pairs retire) gets the bands both sweeps need
+  // first; the band of a CTA is the same function of (sweep, cluster, rank) either way
+  int nA = (int)gridDim.x / 2, bid = (int)blockIdx.x;
+  if (mode & 4) {
+    unsigned csize, crank;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(csize));
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+    const int cl = bid / (int)csize;
+    bid = (cl >> 1) * (int)csize + (int)crank + ((cl & 1) ? nA : 0);
+  }
+  if (bid < nA) {
     // sweep A: with the zero guess P = b - border x_alpha from TMA boxes (mapPA, mapQA);
     // otherwise built from x (mapXA), the old-value half (mapUB), b and border
-    GsBand G{nx, ny, ngrid, pad_nodes, bands, (int)blockIdx.x, &mapSA, &mapPA, ZERO_A ? &mapQA : &mapQB, &mapBB,
+    GsBand G{nx, ny, ngrid, pad_nodes, bands, bid, &mapSA, &mapPA, ZERO_A ? &mapQA : &mapQB, &mapBB,
              &mapXA, &mapUB, x1, x, xfer, nullptr, ready, ready_tag, ready_seg, flags + 2 * groups, epoch, b, border, half_old, x};
     gs_band<FWD, ZERO_A, 1>(G);
   } else {
-    GsBand G{nx, ny, ngrid, pad_nodes, bands, (int)blockIdx.x - nA, &mapSB, &mapSB, &mapQB, &mapBB, &mapXB, &mapUB, x, x,
+    GsBand G{nx, ny, ngrid, pad_nodes, bands, bid - nA, &mapSB, &mapSB, &mapQB, &mapBB, &mapXB, &mapUB, x, x,
              xfer + 2 * (size_t)groups * nx, (mode & 2) ? flags : nullptr, ready, ready_tag, ready_seg, flags + 2 * groups, epoch, b,
              border, half_old, x1, b_offset};
     gs_band<FWD, false, 2>(G);
@@ -1458,7 +1490,8 @@ __device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int b
   }
 #ifdef VTS_GS_PROBE
   long long t_first = 0, t_wait_above = 0, t_wait_in = 0, t_wait_out = 0, t_loop = 0, t_end = 0;
-  if (l == 0) g_gs_probe[4 * band] = gtimer();
+  const bool probe_on = l == 0 && (g_gs_probe_nx == 0 || g_gs_probe_nx == nx);
+  if (probe_on) g_gs_probe[4 * band] = gtimer();
 #endif
   for (int w = 0; w < nwin; ++w) {
     const int s = w % NS;
@@ -1601,7 +1634,7 @@ __device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int b
 #endif
   }
 #ifdef VTS_GS_PROBE
-  if (l == 0) {
+  if (probe_on) {
     g_gs_probe[4 * band + 1] = t_first;
     g_gs_probe[4 * band + 2] = gtimer();
     g_gs_probe[4 * band + 3] = t_wait_above;
@@ -2059,6 +2092,42 @@ static int gs_sweep(Ctx* c, int k, const double* b, double* x, bool forward, boo
   return launch_tri<false, false>(c, L, mS, mP, mP, x, skip);
 }
 
+// items per block of the overlap passes (VTS_DOVL_DIV / VTS_OVL_DIV, A/B timing)
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? std::max(1, atoi(e)) : dflt;
+}
+// per-level override "n_top,n_top-1,..." (VTS_DOVL_BLOCKS / VTS_OVL_BLOCKS, tuning runs): 0 = default
+static int env_level(const char* name, int depth) {
+  const char* e = getenv(name);
+  if (!e) return 0;
+  for (int i = 0; i < depth && e; ++i) {
+    e = strchr(e, ',');
+    if (e) ++e;
+  }
+  return e ? std::max(0, atoi(e)) : 0;
+}
+// Largest cluster of a pair on level k.  An overlapped ascent pair becomes resident
+// while the coarser pairs and the prolongation blocks still hold most SMs: clusters of
+// 9-11 CTAs then find no GPC with that many free SMs until whole coarser pairs retire
+// (the finest ascent pair's first CTA starts ~125 us after the ascent begins), small
+// ones fit at once (~28 us).  Measured neutral all the same (session 5):
+// the pair's first window waits ~120 us for the coarser levels' ramp either way.
+// VTS_PAIR_CS_ASC / VTS_PAIR_CS_DESC = "cap_top,cap_top-1,..." override (0 = default).
+static int pair_cs_cap(const Ctx* c, int k, bool forward, bool overlapped) {
+  if (int o = env_level(forward ? "VTS_PAIR_CS_DESC" : "VTS_PAIR_CS_ASC", c->L - 1 - k)) return std::min(o, 16);
+  return (!forward && overlapped) ? kAscClusterCap : 16;
+}
+// VTS_PAIR_INTERLEAVE=1: the clusters of sweeps A and B alternate in the grid (k_gs_pair's
+// mode bit 2) instead of all of A's first.  Measured neutral (session 5): off by default.
+static bool pair_interleave() {
+  static const bool on = [] {
+    const char* e = getenv("VTS_PAIR_INTERLEAVE");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 // row offset of a pair's sweep B (GsBand::offset): R/2 when its bands still fit the grid
 // (VTS_PAIR_OFFSET=0: aligned bands, A/B checks)
 static int pair_offset(const LevelBuf& L) {
@@ -2076,7 +2145,7 @@ static int pair_offset(const LevelBuf& L) {
 // all be resident at once -- sweep B spins on sweep A, so co-residency is required.
 // the largest clusters (fewest cross-cluster handoffs) with which both halves of
 // level k's grid can be resident at once, or cs = 0 (none: two single sweeps)
-static int pair_shape(Ctx* c, int k, bool forward, bool zero_a, int* cs_out, int* ncl_out) {
+static int pair_shape(Ctx* c, int k, bool forward, bool zero_a, int* cs_out, int* ncl_out, int cs_cap = 16) {
   LevelBuf& L = c->lv[k];
   const int bands = div_up(L.d.ny, gs::R);
   const void* fn = forward ? (zero_a ? (const void*)k_gs_pair<true, true> : (const void*)k_gs_pair<true, false>)
@@ -2094,7 +2163,7 @@ static int pair_shape(Ctx* c, int k, bool forward, bool zero_a, int* cs_out, int
   static int max_clusters[3][17] = {};
   const int kind = forward ? (zero_a ? 0 : 1) : 2;
   *cs_out = *ncl_out = 0;
-  for (int n = div_up(bands, 16); n <= bands; ++n) {
+  for (int n = div_up(bands, std::max(1, std::min(cs_cap, 16))); n <= bands; ++n) {
     const int size = div_up(bands, n);
     if (div_up(bands, size) != n) continue;  // same cluster size as a smaller n
     if (max_clusters[kind][size] == 0) {
@@ -2126,7 +2195,8 @@ static int gs_pair(Ctx* c, int k, const double* b, double* x, bool forward, bool
   LevelBuf& L = c->lv[k];
   const int bands = div_up(L.d.ny, gs::R);
   int cs = 0, ncl = 0;
-  if (int rc = pair_shape(c, k, forward, zero_a, &cs, &ncl)) return rc;
+  if (int rc = pair_shape(c, k, forward, zero_a, &cs, &ncl, pair_cs_cap(c, k, forward, (mode & 1) != 0))) return rc;
+  if ((mode & 1) && pair_interleave()) mode |= 4;
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(32 * gs::kWarpsPair);
   cfg.dynamicSmemBytes = sizeof(gs::Smem);
@@ -2236,21 +2306,6 @@ static bool fused_bottom_enabled() {
   return on;
 }
 
-// items per block of the overlap passes (VTS_DOVL_DIV / VTS_OVL_DIV, A/B timing)
-static int env_int(const char* name, int dflt) {
-  const char* e = getenv(name);
-  return e ? std::max(1, atoi(e)) : dflt;
-}
-// per-level override "n_top,n_top-1,..." (VTS_DOVL_BLOCKS / VTS_OVL_BLOCKS, tuning runs): 0 = default
-static int env_level(const char* name, int depth) {
-  const char* e = getenv(name);
-  if (!e) return 0;
-  for (int i = 0; i < depth && e; ++i) {
-    e = strchr(e, ',');
-    if (e) ++e;
-  }
-  return e ? std::max(0, atoi(e)) : 0;
-}
 // blocks of the overlap passes of level k (each holds an SM)
 static int dovl_blocks(const Ctx* c, int k) {  // k_residual_restrict_rows, level k -> k-1
   static const int div = env_int("VTS_DOVL_DIV", 6);  // 6: 888 vs 878 it/s for 8 (tools/checks/tune_overlap.py)
@@ -2349,7 +2404,7 @@ int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
       const unsigned long long rtag = ++L.rdone_epoch, ctag = ++C.bready_epoch;
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(dovl_blocks(c, k));
-      cfg.blockDim = dim3(1024);
+      cfg.blockDim = dim3(kRRThreads);
       cfg.stream = c->stream;
       cudaLaunchAttribute at[1];
       at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -2416,7 +2471,7 @@ int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
       cudaLaunchConfig_t cfg = {};
       // blocks scale with the level's items (every block holds an SM the pairs need)
       cfg.gridDim = dim3(aovl_blocks(c, k));
-      cfg.blockDim = dim3(1024);
+      cfg.blockDim = dim3(kPRThreads);
       cfg.stream = c->stream;
       cudaLaunchAttribute at[1];
       at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -180,15 +180,28 @@ int main(int argc, char** argv) {
       }
     }
 #ifdef VTS_GS_PROBE
-    if (rep == 1) {  // bands of the last pair of the V-cycle (the finest ascent pair)
-      std::vector<long long> pr(4 * 256);
+    if (rep == 1) {  // bands of the ascent pair of the level VTS_PROBE_LEVEL (default: finest) inside the V-cycle
+      const int plev = getenv("VTS_PROBE_LEVEL") ? atoi(getenv("VTS_PROBE_LEVEL")) : levels - 1;
+      const int pnx = c->lv[plev].d.nx;
+      cudaMemcpyToSymbol(vts::g_gs_probe_nx, &pnx, 4);
+      vts::vcycle_grid(c, xin, yout, nullptr);
+      cudaDeviceSynchronize();
+      std::vector<long long> pr(4 * 256), p2(2 * 256), p3(2 * 256);
       cudaMemcpyFromSymbol(pr.data(), vts::g_gs_probe, pr.size() * 8);
-      const int bands = (c->lv[levels - 1].d.ny + vts::gs::R - 1) / vts::gs::R;
+      cudaMemcpyFromSymbol(p2.data(), vts::g_gs_probe2, p2.size() * 8);
+      cudaMemcpyFromSymbol(p3.data(), vts::g_gs_probe3, p3.size() * 8);
+      const int zero = 0;
+      cudaMemcpyToSymbol(vts::g_gs_probe_nx, &zero, 4);
+      const int bands = (c->lv[plev].d.ny + vts::gs::R - 1) / vts::gs::R;
+      long long b0 = pr[0];
+      printf("  level %d asc pair bands (us from A band 0's start; wait-above / wait-in / wait-out / loops):\n", plev);
       for (int b = 0; b < bands; ++b)
-        printf("  finest asc band %2d: A start %7.1f first %7.1f end %7.1f | B start %7.1f first %7.1f end %7.1f\n", b,
-               (pr[4 * b] - (long long)t0) / 1e3, (pr[4 * b + 1] - (long long)t0) / 1e3, (pr[4 * b + 2] - (long long)t0) / 1e3,
-               (pr[4 * (b + 128)] - (long long)t0) / 1e3, (pr[4 * (b + 128) + 1] - (long long)t0) / 1e3,
-               (pr[4 * (b + 128) + 2] - (long long)t0) / 1e3);
+        for (int h = 0; h < 2; ++h) {
+          const int i = b + 128 * h;
+          printf("   %c band %2d: start %7.1f first %7.1f end %7.1f | above %6.1f in %6.1f out %6.1f loops %6.1f\n", h ? 'B' : 'A', b,
+                 (pr[4 * i] - b0) / 1e3, (pr[4 * i + 1] - b0) / 1e3, (pr[4 * i + 2] - b0) / 1e3, pr[4 * i + 3] / 1e3,
+                 p2[2 * i] / 1e3, p2[2 * i + 1] / 1e3, p3[2 * i] / 1e3);
+        }
     }
 #endif
   }

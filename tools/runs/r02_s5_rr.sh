@@ -1,0 +1,16 @@
+#!/bin/bash
+# overlap passes: block size (512 threads) and residual items with all loads in flight (ordered loads / cp.async staging)
+cd $GRAFT_REPO_ROOT; O=gpurun_out/s5rr; mkdir -p $O
+run() { local label=$1; shift; env "$@" timeout 150 python tools/checks/quick_time.py $label >> $O/times.jsonl 2>> $O/err.log; echo "$label rc=$?" >> $O/status.txt; }
+for r in 1 2 3; do
+  run base A=1
+  for v in "$@"; do run $v VTS_LIB=$PWD/_ab/lib_$v.so; done
+done
+python - <<'PY'
+import json,collections
+d=collections.defaultdict(list)
+for l in open('gpurun_out/s5rr/times.jsonl'):
+    j=json.loads(l); d[j['label']].append(j)
+for k,v in d.items():
+    print(f"{k:12s} its/s {sum(x['its_per_s'] for x in v)/len(v):7.1f}  vcycle {sum(x['vcycle_ms'] for x in v)/len(v):.4f}  xsum {v[0]['xsum']!r}")
+PY
