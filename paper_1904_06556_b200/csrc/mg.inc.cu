@@ -861,6 +861,12 @@ constexpr int NSA = 4;     // window slots of the previous band's row
 #endif
 constexpr int SKEW = VTS_GS_SKEW;  // columns between consecutive rows of the wavefront (2, or 3: the
                                    // previous row's newest value is needed a step after it arrives)
+#ifndef VTS_GS_HALFWARP
+#define VTS_GS_HALFWARP 1
+#endif
+#ifndef VTS_GS_WAIT3
+#define VTS_GS_WAIT3 0
+#endif
 constexpr int kWarps = 5;  // compute, loader, storer, publisher, stager
 constexpr int kBuild = 6;  // pipelined pair, sweep B: builder warps (<= 2 nodes of a window's R x W box each)
 // Pair CTAs have 16 warps.  Warp w runs on SM sub-partition w % 4: the compute
@@ -1453,6 +1459,18 @@ __device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int b
                                            const double* __restrict__ x) {
   using namespace gs;
   const int lane = threadIdx.x & 31;
+  // Only the R lanes that own a row run the loop (VTS_GS_HALFWARP): the step is bound by
+  // what the lone warp can issue, and its shared-memory loads and stores cost issue
+  // time per 128-byte wavefront -- 32 active lanes (the upper 16 as clamped copies of
+  // row R-1) make every one of them twice as long (tools/probe/step_probe3.cu: 115 ->
+  // 107 cycles per step).
+#if VTS_GS_HALFWARP
+  static_assert(R == 16, "the active mask below is the lower half-warp");
+  constexpr unsigned kLanes = 0x0000ffffu;
+  if (lane >= R) return;
+#else
+  constexpr unsigned kLanes = 0xffffffffu;
+#endif
   auto above_bytes = [&](int a) -> unsigned {
     const int c0 = W * (a - 1) + SKEW;
     const int lo = max(c0, 0), hi = min(c0 + W, nx);
@@ -1478,7 +1496,7 @@ __device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int b
 #pragma unroll
       for (int c = 0; c < SKEW; ++c) win[1 + c] = S.above[0][W - SKEW + c];
     }
-    __syncwarp();
+    __syncwarp(kLanes);
     if (l == 0) {
       if (dsm_in) {
         if (NSA <= nwin) mbar_expect_tx(&S.full_above[0], above_bytes(NSA));
@@ -1504,6 +1522,20 @@ __device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int b
       t_wait_in += t1 - t0;
       t_wait_out += gtimer() - t1;
     }
+#elif VTS_GS_WAIT3
+    {
+      // the window's three barriers polled together: one round trip when all are complete
+      // (the usual case) instead of three dependent ones
+      const int sa3 = (w + 1) % NSA;
+      bool ok_in = mbar_try_wait(&S.full_in[s], (w / NS) & 1);
+      bool ok_out = w >= NS ? mbar_try_wait(&S.empty_out[s], ((w / NS) - 1) & 1) : true;
+      bool ok_ab = has_above ? mbar_try_wait(&S.full_above[sa3], ((w + 1) / NSA) & 1) : true;
+      while (!(ok_in & ok_out & ok_ab)) {
+        if (!ok_in) ok_in = mbar_try_wait(&S.full_in[s], (w / NS) & 1);
+        if (!ok_out) ok_out = mbar_try_wait(&S.empty_out[s], ((w / NS) - 1) & 1);
+        if (!ok_ab) ok_ab = mbar_try_wait(&S.full_above[sa3], ((w + 1) / NSA) & 1);
+      }
+    }
 #else
     mbar_wait(&S.full_in[s], (w / NS) & 1);
     if (w >= NS) mbar_wait(&S.empty_out[s], ((w / NS) - 1) & 1);
@@ -1515,7 +1547,9 @@ __device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int b
     t_wait_above += gtimer() - tw0;
     if (w == 0 && l == 0) t_first = gtimer();
 #endif
+#if !VTS_GS_WAIT3 || defined(VTS_GS_PROBE)
     if (has_above) mbar_wait(&S.full_above[sa], ((w + 1) / NSA) & 1);
+#endif
     const InSlot& in = S.in[s];
 #ifdef VTS_GS_PROBE
     const long long tl0 = gtimer();
@@ -1603,8 +1637,8 @@ __device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int b
       // valid position is an exact zero (no neighbour / Dirichlet)
       wprev = nv;
       if (l < R) S.out[s][l][pos] = nv;
-      const double r0s = __shfl_up_sync(0xffffffffu, nv.x, 1);
-      const double r1s = __shfl_up_sync(0xffffffffu, nv.y, 1);
+      const double r0s = __shfl_up_sync(kLanes, nv.x, 1);
+      const double r1s = __shfl_up_sync(kLanes, nv.y, 1);
       const double r0 = l == 0 ? av.x : r0s;
       const double r1 = l == 0 ? av.y : r1s;
 #pragma unroll
@@ -1616,7 +1650,7 @@ __device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int b
     const long long tl1 = gtimer();
     t_loop += tl1 - tl0;
 #endif
-    __syncwarp();
+    __syncwarp(kLanes);
     if (l == 0) {
       mbar_arrive(&S.empty_in[s]);
       mbar_arrive(&S.full_out[s]);
@@ -1629,7 +1663,7 @@ __device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int b
       }
     }
 #ifdef VTS_GS_PROBE
-    __syncwarp();
+    __syncwarp(kLanes);
     t_end += gtimer() - tl1;
 #endif
   }
