@@ -864,9 +864,6 @@ constexpr int SKEW = VTS_GS_SKEW;  // columns between consecutive rows of the wa
 #ifndef VTS_GS_HALFWARP
 #define VTS_GS_HALFWARP 1
 #endif
-#ifndef VTS_GS_WAIT3
-#define VTS_GS_WAIT3 0
-#endif
 constexpr int kWarps = 5;  // compute, loader, storer, publisher, stager
 constexpr int kBuild = 6;  // pipelined pair, sweep B: builder warps (<= 2 nodes of a window's R x W box each)
 // Pair CTAs have 16 warps.  Warp w runs on SM sub-partition w % 4: the compute
@@ -1522,20 +1519,6 @@ __device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int b
       t_wait_in += t1 - t0;
       t_wait_out += gtimer() - t1;
     }
-#elif VTS_GS_WAIT3
-    {
-      // the window's three barriers polled together: one round trip when all are complete
-      // (the usual case) instead of three dependent ones
-      const int sa3 = (w + 1) % NSA;
-      bool ok_in = mbar_try_wait(&S.full_in[s], (w / NS) & 1);
-      bool ok_out = w >= NS ? mbar_try_wait(&S.empty_out[s], ((w / NS) - 1) & 1) : true;
-      bool ok_ab = has_above ? mbar_try_wait(&S.full_above[sa3], ((w + 1) / NSA) & 1) : true;
-      while (!(ok_in & ok_out & ok_ab)) {
-        if (!ok_in) ok_in = mbar_try_wait(&S.full_in[s], (w / NS) & 1);
-        if (!ok_out) ok_out = mbar_try_wait(&S.empty_out[s], ((w / NS) - 1) & 1);
-        if (!ok_ab) ok_ab = mbar_try_wait(&S.full_above[sa3], ((w + 1) / NSA) & 1);
-      }
-    }
 #else
     mbar_wait(&S.full_in[s], (w / NS) & 1);
     if (w >= NS) mbar_wait(&S.empty_out[s], ((w / NS) - 1) & 1);
@@ -1547,9 +1530,7 @@ __device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int b
     t_wait_above += gtimer() - tw0;
     if (w == 0 && l == 0) t_first = gtimer();
 #endif
-#if !VTS_GS_WAIT3 || defined(VTS_GS_PROBE)
     if (has_above) mbar_wait(&S.full_above[sa], ((w + 1) / NSA) & 1);
-#endif
     const InSlot& in = S.in[s];
 #ifdef VTS_GS_PROBE
     const long long tl0 = gtimer();
