@@ -864,6 +864,9 @@ constexpr int SKEW = VTS_GS_SKEW;  // columns between consecutive rows of the wa
 #ifndef VTS_GS_HALFWARP
 #define VTS_GS_HALFWARP 1
 #endif
+#ifndef VTS_CLUSTER_CLOSE
+#define VTS_CLUSTER_CLOSE 0  // 1: every CTA of a cluster stays until the cluster's last band is done (A/B)
+#endif
 constexpr int kWarps = 5;  // compute, loader, storer, publisher, stager
 constexpr int kBuild = 6;  // pipelined pair, sweep B: builder warps (<= 2 nodes of a window's R x W box each)
 // Pair CTAs have 16 warps.  Warp w runs on SM sub-partition w % 4: the compute
@@ -1375,8 +1378,16 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
     };
     for (int w = 0; w < nwin; ++w) build(w);
   }
+#if VTS_CLUSTER_CLOSE
   // no CTA leaves while a cluster peer may still write into its shared memory
   asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+#endif
+  // No closing cluster barrier: the only remote writes into this CTA's shared memory are
+  // the previous band's pushes into the above ring (all consumed by the compute warp
+  // before it ends) and the next band's `armed` counter, whose last write (a_last,
+  // gs_compute) the publisher has waited for before its last push.  A band's SM is free
+  // when the band is done, not when the last band of its cluster is (up to 10 band lags
+  // later): the coarser levels' pairs and passes of the overlapped V-cycle wait for SMs.
 }
 
 template <bool FWD, bool ZERO>
@@ -1475,6 +1486,12 @@ __device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int b
   };
   // the producer's `armed` counter as a cluster address
   uint32_t r_armed = 0;
+  // The last above-ring chunk that holds columns of the row (chunk a: sweep columns
+  // W (a-1) + SKEW + [0, W)).  The producer's publisher waits for `armed` to reach it
+  // before its last push, and nothing is written into the producer's shared memory
+  // after that (later chunks are empty and need no arming): the producer may leave as
+  // soon as its own band is done, without a closing cluster barrier.
+  const int a_last = (nx - 1 + W - SKEW) / W;
   if (dsm_in) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r_armed) : "r"(smem_u32(&S.armed)), "r"(crank - 1));
   }
@@ -1497,7 +1514,7 @@ __device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int b
     if (l == 0) {
       if (dsm_in) {
         if (NSA <= nwin) mbar_expect_tx(&S.full_above[0], above_bytes(NSA));
-        asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(r_armed), "r"(NSA) : "memory");
+        if (NSA <= a_last) asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(r_armed), "r"(NSA) : "memory");
       } else {
         mbar_arrive(&S.empty_above[0]);
       }
@@ -1638,7 +1655,7 @@ __device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int b
       if (dsm_in) {
         const int an = w + 1 + NSA;  // re-arm this slot for its next chunk and tell the producer
         if (an <= nwin) mbar_expect_tx(&S.full_above[sa], above_bytes(an));
-        asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(r_armed), "r"(an) : "memory");
+        if (an <= a_last) asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(r_armed), "r"(an) : "memory");
       } else if (has_above) {
         mbar_arrive(&S.empty_above[sa]);
       }
