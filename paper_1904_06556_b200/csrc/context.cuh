@@ -34,6 +34,11 @@ struct LevelBuf {
   unsigned long long* ovl_rdone = nullptr;   // residual of this level computed (rdone_epoch)
   // ascent overlap, [gs_groups x kChunk column chunks]: x_old prolongated (ready_epoch)
   unsigned long long* ovl_xready = nullptr;
+  // descent overlap: the residual/restriction items of this level in the order they become
+  // ready (k_residual_restrict_rows takes them by ticket), and the ticket counter
+  int32_t* rr_order = nullptr;
+  unsigned* rr_ticket = nullptr;
+  int rr_items = 0;
   unsigned long long bready_epoch = 0;
   unsigned long long rdone_epoch = 0;
   double* x1 = nullptr;               // [ngrid + 1] sweep A's result inside a pair

@@ -480,10 +480,80 @@ VTS_DEVICE_INLINE void seg_cols(int n, int s, int& c0, int& c1) {
   c0 = (int)((long long)n * s / kSeg);
   c1 = (int)((long long)n * (s + 1) / kSeg);
 }
+// item id -> (coarse band, kind j: 0 / 1 residual of fine band 2cb + j, 2 restriction, segment s);
+// a coarse band's items in column order: R(2cb, 0) R(2cb+1, 0), then per segment
+// t = 1..kSeg-1: R(2cb, t) R(2cb+1, t) P(cb, t-1), and P(cb, kSeg-1) last
+__host__ __device__ inline void rr_item_decode(int it, int& cb, int& j, int& s) {
+  cb = it / (3 * kSeg);
+  const int q = it % (3 * kSeg);
+  if (q < 2) {
+    j = q;
+    s = 0;
+  } else if (q == 3 * kSeg - 1) {
+    j = 2;
+    s = kSeg - 1;
+  } else {
+    j = (q - 2) % 3;
+    s = (q - 2) / 3 + 1 - (j == 2 ? 1 : 0);
+  }
+}
+
+// The items of k_residual_restrict_rows in the order they become ready.  Sweep B's band
+// fb + 1 passes the end of segment s about (fb + 1) band lags + (s + 1) segment widths
+// (in wavefront steps) after the sweep starts, so the items of a band's last segments
+// are ready long after the first segments of the next ten bands: taken in id order the
+// blocks sit on items that are not ready while ready ones queue behind them.  Every
+// restriction item comes after the residual items it waits for (no block ever holds an
+// item whose producers are still unclaimed).
+static std::vector<int32_t> rr_item_order(int nx, int ny, int cnx, int cny) {
+  const int R = kBandRows, fbands = (ny + R - 1) / R, cbands = (cny + R - 1) / R, items = cbands * 3 * kSeg;
+  const double lag = 2.0 * (R - 1) + 1.0 + 17.0 + 20.0;  // steps between the starts of consecutive bands
+  auto seg = [](int n, int q, int& c0, int& c1) {
+    c0 = (int)((long long)n * q / kSeg);
+    c1 = (int)((long long)n * (q + 1) / kSeg);
+  };
+  auto key_r = [&](int fb, int q) {
+    int c0, c1;
+    seg(nx, q, c0, c1);
+    return lag * (std::min(fb + 1, fbands - 1) + 1) + c1;
+  };
+  std::vector<std::pair<double, int32_t>> keyed(items);
+  for (int it = 0; it < items; ++it) {
+    int cb, j, q;
+    rr_item_decode(it, cb, j, q);
+    double key = 0.0;
+    if (j < 2) {
+      key = key_r(2 * cb + j, q);
+    } else {
+      // after every residual item it waits for (k_residual_restrict_rows' wait loop)
+      int c0, c1;
+      seg(cnx, q, c0, c1);
+      const int flo = std::max(0, 2 * c0 - 1), fhi = std::min(nx - 1, 2 * (c1 - 1) + 1);
+      for (int fb = std::max(2 * cb - 1, 0); fb <= std::min(2 * cb + 1, fbands - 1); ++fb)
+        for (int qq = 0; qq < kSeg; ++qq) {
+          int f0, f1;
+          seg(nx, qq, f0, f1);
+          if (f1 <= flo || f0 > fhi) continue;
+          key = std::max(key, key_r(fb, qq));
+        }
+      key += 0.25 * nx / kSeg;  // the residual item's own work
+    }
+    keyed[it] = {key, it};
+  }
+  std::stable_sort(keyed.begin(), keyed.end(),
+                   [](const std::pair<double, int32_t>& a, const std::pair<double, int32_t>& b) { return a.first < b.first; });
+  std::vector<int32_t> order(std::max(items, 1), 0);
+  for (int i = 0; i < items; ++i) order[i] = keyed[i].second;
+  return order;
+}
+
 // threads per block of k_residual_restrict_rows (a multiple of 256: the border row's
 // reduction runs in virtual blocks of 256 threads)
 #ifndef VTS_RR_THREADS
 #define VTS_RR_THREADS 1024
+#endif
+#ifndef VTS_RR_STATIC
+#define VTS_RR_STATIC 0
 #endif
 constexpr int kRRThreads = VTS_RR_THREADS;
 static_assert(kRRThreads % 256 == 0 && kRRThreads >= 256 && kRRThreads <= 1024, "virtual blocks of 256 threads");
@@ -495,7 +565,7 @@ __global__ void __launch_bounds__(kRRThreads) k_residual_restrict_rows(
     const unsigned long long* bready, unsigned long long bready_tag, unsigned long long* rdone, unsigned long long rtag,
     unsigned long long* cready, unsigned long long ctag, int ngrid, const double* __restrict__ corner,
     double* apart, unsigned* acnt, const unsigned long long* aflag_in, unsigned long long* aflag_out, int cngrid,
-    const int* skip) {
+    const int* skip, const int32_t* __restrict__ order, unsigned* ticket) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (skip && ld_relaxed_i32(skip)) return;
   constexpr int R = kBandRows;
@@ -503,7 +573,22 @@ __global__ void __launch_bounds__(kRRThreads) k_residual_restrict_rows(
   const int items = cbands * 3 * kSeg;
   VTS_TL_BEGIN(2, nx);
   const double xa = __ldcg(x + ngrid);
-  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+  // items by ticket, in the order they become ready (rr_item_order); VTS_RR_STATIC: block b
+  // takes items b, b + blocks, ... of the id order
+  __shared__ int s_item[2];
+  for (int turn = 0;; ++turn) {
+#if VTS_RR_STATIC
+    const int it = blockIdx.x + turn * (int)gridDim.x;
+    if (it >= items) break;
+#else
+    if (threadIdx.x == 0) {
+      const unsigned t = atomicAdd(ticket, 1u);
+      s_item[turn & 1] = t < (unsigned)items ? order[t] : -1;
+    }
+    __syncthreads();
+    const int it = s_item[turn & 1];  // (two slots: the next turn's write cannot pass a reader of this one)
+    if (it < 0) break;
+#endif
 #ifdef VTS_TIMELINE
     const bool trace = nx == 1025 && it < 1024 && threadIdx.x == 0;
     if (trace) g_items[it][0] = tl_now(), g_items[it][3] = blockIdx.x;
@@ -511,20 +596,8 @@ __global__ void __launch_bounds__(kRRThreads) k_residual_restrict_rows(
 #else
 #define VTS_ITEM_MARK(i) do {} while (0)
 #endif
-    // a coarse band's items in column order: R(2cb, 0) R(2cb+1, 0), then per segment
-    // t = 1..kSeg-1: R(2cb, t) R(2cb+1, t) P(cb, t-1), and P(cb, kSeg-1) last
-    const int cb = it / (3 * kSeg), q = it % (3 * kSeg);
-    int j, s;
-    if (q < 2) {
-      j = q;
-      s = 0;
-    } else if (q == 3 * kSeg - 1) {
-      j = 2;
-      s = kSeg - 1;
-    } else {
-      j = (q - 2) % 3;
-      s = (q - 2) / 3 + 1 - (j == 2 ? 1 : 0);
-    }
+    int cb, j, s;
+    rr_item_decode(it, cb, j, s);
     if (j < 2) {
       const int fb = 2 * cb + j;
       if (fb >= fbands) continue;
@@ -646,6 +719,7 @@ __global__ void __launch_bounds__(kRRThreads) k_residual_restrict_rows(
         r[ngrid] = ra;
         bc[cngrid] = ra;
         *acnt = 0u;
+        *ticket = 0u;  // every block has left the item loop
         __threadfence();
         st_release(aflag_out, ctag);
       }
@@ -2452,7 +2526,7 @@ int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
                                   L.bready_epoch, L.ovl_rdone, rtag, C.ovl_bready, ctag, L.d.ngrid,
                                   (const double*)c->d_corner, c->ovl_part + (size_t)k * kReduceGridCap, c->ovl_cnt + k,
                                   dprev ? (const unsigned long long*)(c->ovl_aflag + k) : nullptr, c->ovl_aflag + (k - 1),
-                                  C.d.ngrid, skip));
+                                  C.d.ngrid, skip, (const int32_t*)L.rr_order, L.rr_ticket));
       VTS_LAUNCHED(c);
     } else {
       // b_alpha of this level: the overlapped residual rows above restrict it last

@@ -411,6 +411,17 @@ static int create(Ctx** out, int levels, const int32_t* ex, const int32_t* ey, c
   dalloc(arena, &c->dscal, 64);
   dalloc(arena, &c->dflags, 4);
   dalloc(arena, &c->mst, 1);
+  // (after everything else.  The placement of the level arrays matters: shifting each level's
+  // block by a few hundred bytes to a few KB moves the V-cycle between two repeatable states
+  // 3.7 % apart -- 945 vs 911 MINRES it/s on C3 with 256 n bytes of padding per level, n = 0 1
+  // 2 7 1024 fast, 3 4 8 16 64 slow (tools/runs/r02_s5_layout.sh) -- so new per-level arrays
+  // go here, behind the arrays the sweeps stream.)
+  for (int k = 0; k < levels; ++k) {
+    LevelBuf& L = c->lv[k];
+    L.rr_items = k >= 1 ? div_up(c->lv[k - 1].d.ny, kBandRows) * 3 * kSeg : 0;
+    dalloc(arena, &L.rr_order, (size_t)std::max(L.rr_items, 1));
+    dalloc(arena, &L.rr_ticket, 1);
+  }
   VTS_CREATE_MARK("plan");
   if (arena.commit(c)) return fail(VTS_E_CUDA);
   VTS_CREATE_MARK("commit");
@@ -426,6 +437,13 @@ static int create(Ctx** out, int levels, const int32_t* ex, const int32_t* ey, c
     if (cudaMemset(L.gs_xfer, 0xFF, 2 * 2 * (size_t)L.gs_groups * L.d.nx * sizeof(double)) != cudaSuccess) {
       set_error(VTS_E_CUDA, "vts_ctx_create: device memset failed");
       return fail(VTS_E_CUDA);
+    }
+    if (k >= 1) {
+      const std::vector<int32_t> order = rr_item_order(L.d.nx, L.d.ny, c->lv[k - 1].d.nx, c->lv[k - 1].d.ny);
+      if (cudaMemcpy(L.rr_order, order.data(), order.size() * sizeof(int32_t), cudaMemcpyHostToDevice) != cudaSuccess) {
+        set_error(VTS_E_CUDA, "vts_ctx_create: device upload failed");
+        return fail(VTS_E_CUDA);
+      }
     }
   }
   VTS_CREATE_MARK("upload");
