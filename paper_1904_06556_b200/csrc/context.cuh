@@ -39,6 +39,11 @@ struct LevelBuf {
   int32_t* rr_order = nullptr;
   unsigned* rr_ticket = nullptr;
   int rr_items = 0;
+  // ascent overlap: k_prolong_rows' items (band x column chunk) in diagonal order, ticket and exit counters
+  int32_t* pr_order = nullptr;
+  unsigned* pr_ticket = nullptr;  // grows by pr_items + blocks per launch (pr_base: the next launch's first ticket)
+  unsigned pr_base = 0;
+  int pr_items = 0;
   unsigned long long bready_epoch = 0;
   unsigned long long rdone_epoch = 0;
   double* x1 = nullptr;               // [ngrid + 1] sweep A's result inside a pair

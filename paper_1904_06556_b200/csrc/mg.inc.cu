@@ -401,19 +401,31 @@ __global__ void __launch_bounds__(kPRThreads) k_prolong_rows(int fnx, int fny, c
                                                        int cW, int cspan, int cnwin,
                                                        const unsigned long long* cready, unsigned long long cready_tag,
                                                        unsigned long long* ready, unsigned long long tag, const int* skip,
-                                                       int coff) {
+                                                       int coff, const int32_t* __restrict__ order, unsigned* ticket,
+                                                       unsigned ticket_base) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  if (skip && ld_relaxed_i32(skip)) return;
   constexpr int R = kBandRows;
   const int fbands = (fny + R - 1) / R, nch = (fnx + kChunk - 1) / kChunk;
+  // The ticket counter only ever grows: every launch draws fbands nch + gridDim.x tickets
+  // (one failing draw per block) from ticket_base on, which the host counts per level
+  // (LevelBuf::pr_base); a skipped launch draws them all at once.
+  if (skip && ld_relaxed_i32(skip)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(ticket, (unsigned)(fbands * nch) + gridDim.x);
+    return;
+  }
   VTS_TL_BEGIN(3, fnx);
-  int g = 0;
-  for (int d = 0; d <= fbands - 1 + 2 * (nch - 1); ++d) {
-    for (int fb = 0; fb < fbands && fb <= d; ++fb) {
-      if ((d - fb) & 1) continue;
-      const int j = (d - fb) >> 1;
-      if (j >= nch) continue;
-      if (g++ % (int)gridDim.x != (int)blockIdx.x) continue;
+  // items (fine band fb, chunk j) by ticket, in the diagonal order fb + 2 j (pr_item_order)
+  __shared__ int s_item[2];
+  {
+    for (int turn = 0;; ++turn) {
+      if (threadIdx.x == 0) {
+        const unsigned t = atomicAdd(ticket, 1u) - ticket_base;
+        s_item[turn & 1] = t < (unsigned)(fbands * nch) ? order[t] : -1;
+      }
+      __syncthreads();
+      const int item = s_item[turn & 1];
+      if (item < 0) break;
+      const int fb = item / nch, j = item - fb * nch;
       const int yhi = fny - 1 - fb * R, ylo = max(0, yhi - R + 1);
       const int c0 = max(0, fnx - kChunk * (j + 1)), c1 = fnx - kChunk * j;
       if (threadIdx.x == 0) {
@@ -458,6 +470,20 @@ __global__ void __launch_bounds__(kPRThreads) k_prolong_rows(int fnx, int fny, c
     }
   }
   VTS_TL_END(3, fnx);
+}
+
+// k_prolong_rows' items in the order the coarser pair's windows complete: diagonals d = fb + 2 j
+static std::vector<int32_t> pr_item_order(int fnx, int fny) {
+  const int fbands = (fny + kBandRows - 1) / kBandRows, nch = (fnx + kChunk - 1) / kChunk;
+  std::vector<int32_t> order;
+  order.reserve((size_t)fbands * nch);
+  for (int d = 0; d <= fbands - 1 + 2 * (nch - 1); ++d)
+    for (int fb = 0; fb < fbands && fb <= d; ++fb) {
+      if ((d - fb) & 1) continue;
+      const int j = (d - fb) >> 1;
+      if (j < nch) order.push_back(fb * nch + j);
+    }
+  return order;
 }
 
 // Descent overlap: level k's residual r = b - A x and its restriction into the
@@ -2588,7 +2614,9 @@ int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
                                   (const uint8_t*)C.d.free_mask, (const double*)C.x,
                                   (const unsigned long long*)C.gs_flags, C.pair_epoch, gs::W, gs::SKEW * (gs::R - 1),
                                   pair_nwin(C), prev_ovl ? (const unsigned long long*)C.ovl_xready : nullptr,
-                                  C.ready_epoch, ready, tag, skip, pair_offset(C)));
+                                  C.ready_epoch, ready, tag, skip, pair_offset(C), (const int32_t*)L.pr_order, L.pr_ticket,
+                                  L.pr_base));
+      L.pr_base += (unsigned)L.pr_items + cfg.gridDim.x;
       VTS_LAUNCHED(c);
       bool launched = false;
       if (int rc = gs_pair(c, k, b, x, false, false, skip, &launched, 1 | mode, ready, tag, nch)) return rc;

@@ -421,6 +421,9 @@ static int create(Ctx** out, int levels, const int32_t* ex, const int32_t* ey, c
     L.rr_items = k >= 1 ? div_up(c->lv[k - 1].d.ny, kBandRows) * 3 * kSeg : 0;
     dalloc(arena, &L.rr_order, (size_t)std::max(L.rr_items, 1));
     dalloc(arena, &L.rr_ticket, 1);
+    L.pr_items = div_up(L.d.ny, kBandRows) * div_up(L.d.nx, kChunk);
+    dalloc(arena, &L.pr_order, (size_t)L.pr_items);
+    dalloc(arena, &L.pr_ticket, 1);
   }
   VTS_CREATE_MARK("plan");
   if (arena.commit(c)) return fail(VTS_E_CUDA);
@@ -437,6 +440,13 @@ static int create(Ctx** out, int levels, const int32_t* ex, const int32_t* ey, c
     if (cudaMemset(L.gs_xfer, 0xFF, 2 * 2 * (size_t)L.gs_groups * L.d.nx * sizeof(double)) != cudaSuccess) {
       set_error(VTS_E_CUDA, "vts_ctx_create: device memset failed");
       return fail(VTS_E_CUDA);
+    }
+    {
+      const std::vector<int32_t> order = pr_item_order(L.d.nx, L.d.ny);
+      if (cudaMemcpy(L.pr_order, order.data(), order.size() * sizeof(int32_t), cudaMemcpyHostToDevice) != cudaSuccess) {
+        set_error(VTS_E_CUDA, "vts_ctx_create: device upload failed");
+        return fail(VTS_E_CUDA);
+      }
     }
     if (k >= 1) {
       const std::vector<int32_t> order = rr_item_order(L.d.nx, L.d.ny, c->lv[k - 1].d.nx, c->lv[k - 1].d.ny);
