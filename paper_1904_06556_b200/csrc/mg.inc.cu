@@ -375,7 +375,7 @@ __global__ void k_prolong_add(int fnx, int fny, const uint8_t* __restrict__ ffm,
 #define VTS_OVL_SLEEP 128
 #endif
 #ifndef VTS_KCHUNK
-#define VTS_KCHUNK 128
+#define VTS_KCHUNK 64  // taken by ticket (k_prolong_rows), 64-column items beat 128 (970 vs 960 MINRES it/s on C3)
 #endif
 constexpr int kChunk = VTS_KCHUNK;
 // cluster-size cap of the overlapped ascent pairs (pair_cs_cap)

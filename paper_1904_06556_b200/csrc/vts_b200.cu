@@ -372,6 +372,10 @@ static int create(Ctx** out, int levels, const int32_t* ex, const int32_t* ey, c
     LevelBuf& L = c->lv[k];
     const size_t ng = L.d.ngrid;
     L.pad_nodes = (size_t)kPadRows * L.d.nx;
+    if (const char* e = getenv("VTS_ARENA_PAD")) {  // placement diagnostic (see below): n x 256 bytes before each level
+      static char* unused[64];
+      dalloc(arena, &unused[k & 63], (size_t)std::max(1, atoi(e)) * 256);
+    }
     dalloc_pad(arena, &L.d.stL, (size_t)L.d.nnodes * kHalf, L.pad_nodes * kHalf);
     dalloc_pad(arena, &L.d.stU, (size_t)L.d.nnodes * kHalf, L.pad_nodes * kHalf);
     dalloc_pad(arena, &L.d.border, ng + 1, 2 * L.pad_nodes);

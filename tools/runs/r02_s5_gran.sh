@@ -1,0 +1,19 @@
+#!/bin/bash
+# item granularity under the ticket queues (16 / 12 column segments, 64-column chunks), each at several placements
+cd $GRAFT_REPO_ROOT; O=gpurun_out/s5gran; mkdir -p $O; rm -f $O/times.jsonl
+run() { local label=$1; shift; env "$@" timeout 150 python tools/checks/quick_time.py $label >> $O/times.jsonl 2>> $O/err.log; echo "$label rc=$?" >> $O/status.txt; }
+for v in base seg16 seg12 chunk64; do
+  for n in 0 1 3 7; do
+    if [ $v = base ]; then L=""; else L="VTS_LIB=$PWD/_ab/lib_$v.so"; fi
+    if [ $n = 0 ]; then run ${v}_p0 A=1 $L; else run ${v}_p$n VTS_ARENA_PAD=$n $L; fi
+  done
+done
+python - <<'PY'
+import json,collections
+d=collections.defaultdict(list)
+for l in open('gpurun_out/s5gran/times.jsonl'):
+    j=json.loads(l); d[j['label']].append(j)
+for k,v in d.items():
+    print(f"{k:14s} its/s {' '.join('%.1f'%x['its_per_s'] for x in v)}  vcycle {sum(x['vcycle_ms'] for x in v)/len(v):.4f}")
+PY
+tail -3 $O/err.log
