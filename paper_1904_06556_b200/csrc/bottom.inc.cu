@@ -18,15 +18,19 @@
 
 constexpr int kBotThreads = 512;  // 128 registers: the wavefront warp keeps two steps of operands live
 #ifdef VTS_BOT_PROBE
+// time marks of one launch: kept in shared memory while the kernel runs (a global
+// read-modify-write per mark cost ~2 us each and hid the picture), written out at the end
 __device__ long long g_bot_probe[64];
 __device__ int g_bot_n;
-#define BOT_MARK()                                                           \
-  do {                                                                       \
-    if (threadIdx.x == 0) {                                                  \
-      long long t_;                                                          \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                 \
-      if (g_bot_n < 64) g_bot_probe[g_bot_n++] = t_;                         \
-    }                                                                        \
+__shared__ long long s_bot_marks[64];
+__shared__ int s_bot_n;
+#define BOT_MARK()                                                 \
+  do {                                                             \
+    if (threadIdx.x == 0 && s_bot_n < 64) {                        \
+      long long t_;                                                \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));       \
+      s_bot_marks[s_bot_n++] = t_;                                 \
+    }                                                              \
   } while (0)
 #else
 #define BOT_MARK() \
@@ -37,7 +41,11 @@ constexpr int kBotMaxLevels = 8;
 #ifndef VTS_BOT_EXP
 #define VTS_BOT_EXP 0  // probe-only timing experiments on bot_coarse (results then wrong)
 #endif
+#ifdef VTS_BOT_PROBE
+constexpr size_t kBotSmemMax = 226 * 1024;  // (the probe's marks take static shared memory)
+#else
 constexpr size_t kBotSmemMax = 227 * 1024;  // the opt-in dynamic shared memory limit of one CTA
+#endif
 
 struct BotLevel {
   int nx, ny, nn, ngrid;
@@ -107,40 +115,53 @@ __device__ __noinline__ void bot_sweep(const BotLevel& L, double* sm, const BotA
   __syncthreads();
   BOT_MARK();  // staged
   BOT_MARK();  // (old pass: part of staging)
-  if (tid < 32) {
+  // only the lanes that own a row: every shared-memory load and store of the loop costs
+  // issue time per 128-byte wavefront
+  const int nlanes = min(L.ny, 32);
+  if (tid < nlanes) {
     // the wavefront of k_gs_tri on a single band: lane l = sweep row, skew 2,
     // software-pipelined, branch-free like k_gs_tri: every lane streams its row
     // through the padded stage with a pointer that moves one node per step;
-    // positions off the row (and lanes below the grid, clamped to the last row)
-    // compute on finite real-neighbour or zero-pad data and are never stored;
-    // every coupling that reads them at a valid position is an exact zero
+    // positions off the row compute on finite real-neighbour or zero-pad data and
+    // are never stored; every coupling that reads them at a valid position is an
+    // exact zero
+    const unsigned lanes = nlanes == 32 ? 0xffffffffu : ((1u << nlanes) - 1u);
     const int l = tid;
     const int nx = L.nx, ny = L.ny;  // registers: the loop must not re-read L through a generic pointer
-    const int lc = l < ny ? l : ny - 1;
     constexpr int d0 = FWD ? 0 : 1;
     constexpr int d1 = 1 - d0;
     constexpr int dir = FWD ? 1 : -1;
-    // node of (row lc, sweep column t - 2 l) at t = 0, in padded stage order
-    const int n0 = FWD ? lc * nx - 2 * l : (ny - 1 - lc) * nx + nx - 1 + 2 * l;
+    // node of (row l, sweep column t - 2 l) at t = 0, in padded stage order
+    const int n0 = FWD ? l * nx - 2 * l : (ny - 1 - l) * nx + nx - 1 + 2 * l;
     const double* ap = stage + (size_t)(kBotPad + n0) * kHalf;
     const double* pp = pst + (size_t)(kBotPad + n0) * 2;
     double* xp_out = sx + 2 * (ptrdiff_t)n0;
     struct StepData {
       double q0, q1, e00, e01, e10, e11, w00, w01, w10, w11, c, r0, r1;
     };
-    // gs_pre / gs_rec2 of k_gs_tri's skew-2 steps, so both paths compute the same bits
-    auto prepare = [&](const double* a, const double* pv, const double2 xm, const double2 xz) {
+    // a step's shared-memory operands, loaded two steps ahead of the step that uses
+    // them (as gs_compute): the loads' latency and gs_pre run in the shadow of the
+    // recurrence of the steps in between
+    struct Raw {
       double r[19];
+      double2 pq;
+    };
+    auto load_raw = [&](int t, Raw& o) {
+      const double* a = ap + (ptrdiff_t)t * dir * kHalf;
 #pragma unroll
       for (int i = 0; i < 9; ++i) {
         const double2 v = reinterpret_cast<const double2*>(a)[i];
-        r[2 * i] = v.x;
-        r[2 * i + 1] = v.y;
+        o.r[2 * i] = v.x;
+        o.r[2 * i + 1] = v.y;
       }
-      r[18] = a[18];
-      const double2 pq = *reinterpret_cast<const double2*>(pv);
+      o.r[18] = a[18];
+      o.pq = *reinterpret_cast<const double2*>(pp + 2 * dir * t);
+    };
+    // gs_pre / gs_rec2 of k_gs_tri's skew-2 steps, so both paths compute the same bits
+    auto prepare = [&](const Raw& in, const double2 xm, const double2 xz) {
+      const double* r = in.r;
       StepData o;
-      gs_pre<d0>(r, pq.x, pq.y, xm, xz, o.q0, o.q1);
+      gs_pre<d0>(r, in.pq.x, in.pq.y, xm, xz, o.q0, o.q1);
       o.e00 = r[8 + 2 * d0];
       o.e01 = r[9 + 2 * d0];
       o.e10 = r[8 + 2 * d1];
@@ -157,24 +178,25 @@ __device__ __noinline__ void bot_sweep(const BotLevel& L, double* sm, const BotA
     double2 win[3] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
     double2 wprev = make_double2(0.0, 0.0);
     const int T = nx + 2 * (ny - 1);
-    StepData cur = prepare(ap, pp, win[0], win[1]);
-    const bool row_ok = l < ny;
+    Raw ra;
+    load_raw(0, ra);
+    StepData cur = prepare(ra, win[0], win[1]);
+    load_raw(1, ra);  // (reads at most two nodes past the last step: inside the stage's zero pad)
     double* const trash = sm + A.off_red;  // stores of off-row positions land here (unused during sweeps)
 #pragma unroll 4
     for (int t = 0; t < T; ++t) {
       const int j = t - 2 * l;
       const double2 nv = gs_rec2<d0>(cur.q0, cur.q1, cur.w00, cur.w01, cur.w10, cur.w11, cur.e00, cur.e01, cur.e10,
                                      cur.e11, cur.c, cur.r0, cur.r1, wprev, win[2]);
-      // the next step's loads before this step's store (shared memory: the store
-      // would otherwise order them behind it)
-      const StepData nxt = prepare(ap + (size_t)((t + 1) * dir * kHalf), pp + 2 * dir * (t + 1), win[1], win[2]);
+      const StepData nxt = prepare(ra, win[1], win[2]);
+      load_raw(t + 2, ra);
       // branch-free store: off-row positions write the scratch slot instead
-      double* dst = (row_ok && j >= 0 && j < nx) ? xp_out + 2 * dir * t : trash;
+      double* dst = (j >= 0 && j < nx) ? xp_out + 2 * dir * t : trash;
       *reinterpret_cast<double2*>(dst) = nv;
       wprev = nv;
       double2 up;
-      up.x = __shfl_up_sync(0xffffffffu, nv.x, 1);
-      up.y = __shfl_up_sync(0xffffffffu, nv.y, 1);
+      up.x = __shfl_up_sync(lanes, nv.x, 1);
+      up.y = __shfl_up_sync(lanes, nv.y, 1);
       if (l == 0) up = make_double2(0.0, 0.0);  // a single band: no previous row
       win[0] = win[1];
       win[1] = win[2];
@@ -379,11 +401,17 @@ __global__ void __launch_bounds__(kBotThreads, 1) k_vcycle_bottom(const __grid_c
   VTS_TL_BEGIN(4, 5);
   extern __shared__ __align__(16) double sm[];
   const int tid = threadIdx.x;
+#ifdef VTS_BOT_PROBE
+  if (tid == 0) s_bot_n = 0;
+  __syncthreads();
+  BOT_MARK();
+#endif
   {
     const BotLevel& T = A.lv[A.kb];
     for (int i = tid; i <= T.ngrid; i += blockDim.x) sm[T.off_b + i] = A.gb[i];
   }
   __syncthreads();
+  BOT_MARK();  // right-hand side loaded
   for (int k = A.kb; k >= 1; --k) {  // descent (multigrid.py:115-131)
     const BotLevel& L = A.lv[k];
     if (tid == 0) sm[L.off_x + L.ngrid] = 0.0;  // k_alpha_init on a coarse level
@@ -400,6 +428,7 @@ __global__ void __launch_bounds__(kBotThreads, 1) k_vcycle_bottom(const __grid_c
             restrict_node(L.nx, L.ny, L.fm, sm + L.off_r, C.nx, C.fm, cn);
     }
     __syncthreads();
+    BOT_MARK();  // restricted
   }
   BOT_MARK();
   bot_coarse(A.lv[0], sm, A);
@@ -414,6 +443,7 @@ __global__ void __launch_bounds__(kBotThreads, 1) k_vcycle_bottom(const __grid_c
             prolong_node(L.nx, L.fm, sm + L.off_x, C.nx, C.fm, sm + C.off_x, fi);
     }
     __syncthreads();
+    BOT_MARK();  // prolongated
     bot_sweep<false, false>(L, sm, A, true);
     bot_sweep<false, false>(L, sm, A, false);
   }
@@ -421,6 +451,14 @@ __global__ void __launch_bounds__(kBotThreads, 1) k_vcycle_bottom(const __grid_c
     const BotLevel& T = A.lv[A.kb];
     for (int i = tid; i <= T.ngrid; i += blockDim.x) A.gx[i] = sm[T.off_x + i];
   }
+#ifdef VTS_BOT_PROBE
+  BOT_MARK();
+  __syncthreads();
+  if (tid == 0) {
+    for (int i = 0; i < s_bot_n; ++i) g_bot_probe[i] = s_bot_marks[i];
+    g_bot_n = s_bot_n;
+  }
+#endif
   VTS_TL_END(4, 5);
 }
 

@@ -207,16 +207,14 @@ int main(int argc, char** argv) {
   }
 #endif
 #ifdef VTS_BOT_PROBE
-  {
-    int zero = 0;
-    cudaMemcpyToSymbol(vts::g_bot_n, &zero, 4);
-    vts::vcycle_grid(c, xin, yout, nullptr);
+  {  // marks of the fused bottom in the last of several back-to-back V-cycles
+    for (int r = 0; r < 6; ++r) vts::vcycle_grid(c, xin, yout, nullptr);
     cudaDeviceSynchronize();
     int n = 0;
     long long pr[64];
     cudaMemcpyFromSymbol(&n, vts::g_bot_n, 4);
     cudaMemcpyFromSymbol(pr, vts::g_bot_probe, 64 * 8);
-    for (int i = 1; i < n; ++i) printf("bottom mark %2d: +%6.2f us\n", i, (pr[i] - pr[i - 1]) / 1e3);
+    for (int i = 1; i < n; ++i) printf("bottom mark %2d: +%6.2f us  (at %7.2f)\n", i, (pr[i] - pr[i - 1]) / 1e3, (pr[i] - pr[0]) / 1e3);
     printf("bottom total (first to last mark): %.1f us\n", (pr[n - 1] - pr[0]) / 1e3);
   }
 #endif
