@@ -378,6 +378,13 @@ __global__ void k_prolong_add(int fnx, int fny, const uint8_t* __restrict__ ffm,
 #define VTS_KCHUNK 64  // taken by ticket (k_prolong_rows), 64-column items beat 128 (970 vs 960 MINRES it/s on C3)
 #endif
 constexpr int kChunk = VTS_KCHUNK;
+// k_prolong_rows' item of band fb covers sweep rows R fb + 1 .. R fb + R (band 0 also row 0):
+// the finer pair's band b reads rows R b .. R b + R (its own and the next band's first), that
+// is items b - 1 and b instead of b and b + 1 -- its first band no longer waits for the item
+// behind it, which waits for the coarser pair's next band.  0: items are the bands' own rows.
+#ifndef VTS_PR_SHIFT
+#define VTS_PR_SHIFT 1
+#endif
 // cluster-size cap of the overlapped ascent pairs (pair_cs_cap)
 #ifndef VTS_ASC_CS
 #define VTS_ASC_CS 16
@@ -426,9 +433,13 @@ __global__ void __launch_bounds__(kPRThreads) k_prolong_rows(int fnx, int fny, c
       const int item = s_item[turn & 1];
       if (item < 0) break;
       const int fb = item / nch, j = item - fb * nch;
+#if VTS_PR_SHIFT
+      const int yhi = fny - 1 - (fb == 0 ? 0 : fb * R + 1), ylo = max(0, fny - 1 - (fb * R + R));
+#else
       const int yhi = fny - 1 - fb * R, ylo = max(0, yhi - R + 1);
+#endif
       const int c0 = max(0, fnx - kChunk * (j + 1)), c1 = fnx - kChunk * j;
-      if (threadIdx.x == 0) {
+      if (threadIdx.x == 0 && yhi >= ylo) {
         // coarse rows ylo/2 .. (yhi+1)/2 in the coarse backward bands (cny-1-row)/R, their
         // columns >= c0/2: stored once every row of the band is through window w
         // (row R-1 lags: columns >= cnx - cW (w+1) + cspan)
@@ -1344,7 +1355,7 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
         if (chunked) {
           const int need = min(G.ready_seg, (W * (w + 1) + 1 + gs_chunk - 1) / gs_chunk);
           if (need > got) {
-            for (int bb = band; bb <= min(band + 1, bands - 1); ++bb)
+            for (int bb = VTS_PR_SHIFT ? max(band - 1, 0) : band; bb <= (VTS_PR_SHIFT ? band : min(band + 1, bands - 1)); ++bb)
               for (int j = got; j < need; ++j)
                 while (ld_acquire(G.ready + (size_t)bb * G.ready_seg + j) < G.ready_tag) {
                 }
@@ -2262,12 +2273,16 @@ static bool pair_interleave() {
 
 // row offset of a pair's sweep B (GsBand::offset): R/2 when its bands still fit the grid
 // (VTS_PAIR_OFFSET=0: aligned bands, A/B checks)
-static int pair_offset(const LevelBuf& L) {
+// Backward pairs (the ascent) use R/2 - 1: sweep B's band 0 then holds sweep rows 0 .. R/2,
+// all the coarse rows the finer level's first band is prolongated from (rows 0 .. R + 1 of
+// the finer level), so the finer pair starts behind this pair's band 0, not its band 1
+// (VTS_PR_SHIFT, k_prolong_rows).
+static int pair_offset(const LevelBuf& L, bool forward = true) {
   static const bool on = [] {
     const char* e = getenv("VTS_PAIR_OFFSET");
     return !(e && e[0] == '0');
   }();
-  const int h = gs::R / 2;
+  const int h = gs::R / 2 - ((VTS_PR_SHIFT && !forward) ? 1 : 0);
   return (on && div_up(L.d.ny + h, gs::R) <= div_up(L.d.ny, gs::R)) ? h : 0;
 }
 
@@ -2370,7 +2385,8 @@ static int gs_pair(Ctx* c, int k, const double* b, double* x, bool forward, bool
   else
     VTS_CUDA(cudaLaunchKernelEx(&cfg, k_gs_pair<false, false>, L.d.nx, L.d.ny, L.d.ngrid, (int)L.pad_nodes, bands,
                                 mSA, mPA, mQA, mSB, mBB, mQB, mXB, mUB, mXA, L.x1, x, L.gs_flags, L.gs_xfer, L.gs_groups, epoch, b,
-                                (const double*)L.d.border, old_half, ready, ready_tag, ready_seg, mode, skip, pair_offset(L)));
+                                (const double*)L.d.border, old_half, ready, ready_tag, ready_seg, mode, skip,
+                                pair_offset(L, false)));
   VTS_LAUNCHED(c);
   if (pe) VTS_CUDA(cudaEventRecord(pe->b, c->stream));
   *launched = true;
@@ -2614,7 +2630,7 @@ int vcycle_grid(Ctx* c, const double* b_top, double* z_top, const int* skip) {
                                   (const uint8_t*)C.d.free_mask, (const double*)C.x,
                                   (const unsigned long long*)C.gs_flags, C.pair_epoch, gs::W, gs::SKEW * (gs::R - 1),
                                   pair_nwin(C), prev_ovl ? (const unsigned long long*)C.ovl_xready : nullptr,
-                                  C.ready_epoch, ready, tag, skip, pair_offset(C), (const int32_t*)L.pr_order, L.pr_ticket,
+                                  C.ready_epoch, ready, tag, skip, pair_offset(C, false), (const int32_t*)L.pr_order, L.pr_ticket,
                                   L.pr_base));
       L.pr_base += (unsigned)L.pr_items + cfg.gridDim.x;
       VTS_LAUNCHED(c);
