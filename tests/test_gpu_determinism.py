@@ -85,3 +85,18 @@ def test_fast_paths_are_bitwise_identical_to_the_plain_path(tmp_path, switch, ke
     fast = _run_ab(tmp_path, "fast", {}, key)
     plain = _run_ab(tmp_path, "plain", {switch: "1"}, key)
     assert np.array_equal(fast, plain)
+
+
+@pytest.mark.parametrize("env_extra", [{"VTS_PAIR_CS_ASC": "4,4,4,4", "VTS_PAIR_CS_DESC": "6,5,3,3"},
+                                       {"VTS_PAIR_INTERLEAVE": "1", "VTS_PAIR_CS_ASC": "3"},
+                                       {"VTS_ARENA_PAD": "3"},
+                                       {"VTS_DOVL_BLOCKS": "7,3,2,2", "VTS_OVL_BLOCKS": "5,2,1,1"}])
+def test_scheduling_switches_do_not_change_a_bit(tmp_path, env_extra):
+    """Cluster sizes of the pairs (more bands handed over through global memory), the order of
+    the two sweeps' clusters in the grid, the placement of the level arrays and the number of
+    blocks that draw residual / restriction / prolongation items by ticket only change when
+    and where work runs: the V-cycle output and a MINRES solution on C3 (nine levels, five
+    of them overlapped) keep every bit."""
+    ref = _run_ab(tmp_path, "default", {}, "C3")
+    alt = _run_ab(tmp_path, "switched", env_extra, "C3")
+    assert np.array_equal(ref, alt)
