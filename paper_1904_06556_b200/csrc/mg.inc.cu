@@ -975,6 +975,12 @@ constexpr int SKEW = VTS_GS_SKEW;  // columns between consecutive rows of the wa
 #ifndef VTS_GS_HALFWARP
 #define VTS_GS_HALFWARP 1
 #endif
+// The publisher pushes the part of a window that completes a chunk of the next band's ring
+// (the steps before kSplit) as soon as the compute warp has passed them, not at the window's
+// end: the consumer's chunk is complete two steps and a window boundary earlier
+#ifndef VTS_GS_SPLIT_PUSH
+#define VTS_GS_SPLIT_PUSH 1
+#endif
 #ifndef VTS_CLUSTER_CLOSE
 #define VTS_CLUSTER_CLOSE 0  // 1: every CTA of a cluster stays until the cluster's last band is done (A/B)
 #endif
@@ -1000,6 +1006,8 @@ struct __align__(128) InSlot {  // the compute warp's ring
   double p[R][W][2];   // P (TMA box, or written by sweep B's builders)
   double q[R][W][2];   // border (zero-guess sweeps)
 };
+constexpr int kSplit = SKEW * R - W;  // row R-1's steps [0, kSplit) of a window end chunk w - 1, the rest start chunk w
+static_assert(!VTS_GS_SPLIT_PUSH || (kSplit > 0 && kSplit < W), "a window of row R-1 spans two chunks");
 constexpr int NSB = 2;  // sweep B: builder-input ring (refilled as soon as the builders are done)
 struct __align__(128) BSlot {  // sweep B's builder inputs
   double u[R][W][18];  // the old-value half-stencil (18 of its 22 doubles)
@@ -1014,6 +1022,7 @@ struct Smem {
   double2 out[NS][R][W];
   double2 above[NSA][W];
   unsigned long long full_in[NS], empty_in[NS], full_out[NS], empty_out[NS];
+  unsigned long long split_out[NS];  // the compute warp has stored a window's steps before kSplit (split push)
   unsigned long long loaded[NSB];    // sweep B: a builder slot's static TMA boxes have landed
   unsigned long long xloaded[NSB];   // sweep B: a builder slot's x_A box has landed
   unsigned long long bempty[NSB];    // sweep B: the builders are done with a builder slot
@@ -1049,7 +1058,7 @@ static_assert(((W * kHalf * 8) / 16) % 2 == 1, "lane stride must be an odd multi
 template <bool FWD, bool ZERO>
 __device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int band, int rows_here, bool has_above,
                                            bool dsm_in, unsigned crank, int nwin,
-                                           const double* __restrict__ x);
+                                           const double* __restrict__ x, bool dsm_out);
 
 // One band of a wavefront sweep.  ROLE 0: a single sweep (P by TMA box).  In
 // the pipelined pair (k_gs_pair) of two consecutive sweeps, ROLE 1 is sweep A
@@ -1128,6 +1137,7 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
       mbar_init(&S.empty_in[s], 1);
       mbar_init(&S.full_out[s], 1);
       mbar_init(&S.empty_out[s], 2);
+      mbar_init(&S.split_out[s], 1);
     }
     for (int s = 0; s < NSB; ++s) {
       mbar_init(&S.loaded[s], 1);
@@ -1229,8 +1239,36 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
       asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r_above) : "r"(smem_u32(&S.above[0][0])), "r"(crank + 1));
       asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r_mbar) : "r"(smem_u32(&S.full_above[0])), "r"(crank + 1));
     }
+    // the next band's ring: row R-1's values of window w at the steps [st0, st1)
+    auto push = [&](int w, int s, int st0, int st1) {
+      const int l = R - 1;
+      const int jlo = W * w - SKEW * (R - 1);
+      const int jhi = min(jlo + st1 - 1, nx - 1);
+      const int amax = jhi < max(jlo + st0, 0) ? -1 : (jhi + W - SKEW) / W;
+      if (lane == 0)
+        while (*reinterpret_cast<volatile int*>(&S.armed) < amax) {
+        }
+      __syncwarp();
+      const int st = FWD ? lane : W - 1 - lane;
+      const int j = jlo + st;
+      if (lane < W && st >= st0 && st < st1 && j >= 0 && j < nx) {
+        const int a = (j + W - SKEW) / W;
+        const int sl = a % NSA;
+        const uint32_t dst = r_above + (uint32_t)((sl * W + (j - SKEW - W * (a - 1))) * 16);
+        const double2 v = S.out[s][l][lane];
+        asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(dst),
+                     "d"(v.x), "d"(v.y), "r"(r_mbar + (uint32_t)(sl * 8))
+                     : "memory");
+      }
+    };
     for (int w = 0; w < nwin; ++w) {
       const int s = w % NS;
+#if VTS_GS_SPLIT_PUSH
+      if (pub && dsm_out && R - 1 < l_hi) {
+        mbar_wait(&S.split_out[s], (w / NS) & 1);
+        push(w, s, 0, kSplit);
+      }
+#endif
       mbar_wait(&S.full_out[s], (w / NS) & 1);
       if (!pub) {
         // in a pair the storer also stores the last row, so its stored counter alone
@@ -1260,28 +1298,10 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
                             make_double2(xfer_canon(v.x), xfer_canon(v.y)));
           }
         }
-        if (dsm_out) {
-          // hand the row to the next band of the cluster: one st.async per column into
-          // its above ring, completing on that slot's mbarrier (above slot a holds
-          // sweep columns W*(a-1) + SKEW + [0, W)), once the consumer has armed it
-          const int jlo = W * w - SKEW * (R - 1);
-          const int jmax = min(jlo + W - 1, nx - 1);
-          const int amax = jmax < 0 ? -1 : (jmax + W - SKEW) / W;
-          if (lane == 0)
-            while (*reinterpret_cast<volatile int*>(&S.armed) < amax) {
-            }
-          __syncwarp();
-          const int j = jlo + (FWD ? lane : W - 1 - lane);
-          if (lane < W && j >= 0 && j < nx) {
-            const int a = (j + W - SKEW) / W;
-            const int sl = a % NSA;
-            const uint32_t dst = r_above + (uint32_t)((sl * W + (j - SKEW - W * (a - 1))) * 16);
-            const double2 v = S.out[s][l][lane];
-            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(dst),
-                         "d"(v.x), "d"(v.y), "r"(r_mbar + (uint32_t)(sl * 8))
-                         : "memory");
-          }
-        }
+        // hand the row to the next band of the cluster: one st.async per column into
+        // its above ring, completing on that slot's mbarrier (above slot a holds
+        // sweep columns W*(a-1) + SKEW + [0, W)), once the consumer has armed it
+        if (dsm_out) push(w, s, VTS_GS_SPLIT_PUSH ? kSplit : 0, W);
       }
       __syncwarp();
       if (lane == 0) {
@@ -1317,7 +1337,7 @@ __device__ __forceinline__ void gs_band(const GsBand& G) {
     }
   } else if (warp == 0) {
     gs_compute<FWD, ZERO>(S, nx, ngrid, band + (ROLE == 2 ? 128 : 0), l_hi, has_above, dsm_in, crank, nwin,
-                          G.xa_src);  // (band only labels the probe timeline)
+                          G.xa_src, dsm_out);  // (band only labels the probe timeline)
   } else if ((ROLE == 1 || G.bdone) && warp == kReleaseWarp) {  // ---------------- stored-window counter
     // (sweep B with G.bdone: the same counter for the finer level's prolongation or
     // this level's residual, which read the band's final rows window by window)
@@ -1575,7 +1595,7 @@ __global__ void __launch_bounds__(32 * gs::kWarpsPair, 1)
 template <bool FWD, bool ZERO>
 __device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int band, int rows_here, bool has_above,
                                            bool dsm_in, unsigned crank, int nwin,
-                                           const double* __restrict__ x) {
+                                           const double* __restrict__ x, bool dsm_out) {
   using namespace gs;
   const int lane = threadIdx.x & 31;
   // Only the R lanes that own a row run the loop (VTS_GS_HALFWARP): the step is bound by
@@ -1746,6 +1766,12 @@ __device__ __forceinline__ void gs_compute(gs::Smem& S, int nx, int ngrid, int b
       // valid position is an exact zero (no neighbour / Dirichlet)
       wprev = nv;
       if (l < R) S.out[s][l][pos] = nv;
+#if VTS_GS_SPLIT_PUSH
+      if (st == kSplit - 1 && dsm_out) {  // row R-1's values that complete the consumer's chunk are stored
+        __syncwarp(kLanes);
+        if (l == 0) mbar_arrive(&S.split_out[s]);
+      }
+#endif
       const double r0s = __shfl_up_sync(kLanes, nv.x, 1);
       const double r1s = __shfl_up_sync(kLanes, nv.y, 1);
       const double r0 = l == 0 ? av.x : r0s;
