@@ -450,18 +450,30 @@ def main() -> None:
 
         gc.collect()
         torch.cuda.synchronize()
-        t_p = time.perf_counter()
-        rep = vts.solve_pbm(vts.build_config("C4"))
-        pbm = {"config": "C4 full PBM 1024x512 cantilever", "wall_s": time.perf_counter() - t_p,
-               "note": "one solve_pbm call, context creation included (device arena recycled from the "
-                       "microbenchmark context); each Newton step one vts_newton_step (device-resident, "
-                       "CUDA graphs, one host synchronisation per step)",
+        def timed_solves(reps):
+            walls, last = [], None
+            for _ in range(reps):
+                torch.cuda.synchronize()
+                t_p = time.perf_counter()
+                last = vts.solve_pbm(vts.build_config("C4"))
+                torch.cuda.synchronize()
+                walls.append(time.perf_counter() - t_p)
+            return walls, last
+
+        # three solves per mode (each: mesh build, context creation, solve): the first one of a
+        # process also pays one-time costs (graph instantiation, pool growth) that vary by 0.1 s
+        walls, rep = timed_solves(3)
+        pbm = {"config": "C4 full PBM 1024x512 cantilever", "wall_s": sorted(walls)[1], "wall_s_runs": walls,
+               "note": "median of three solve_pbm calls, each with its mesh build and context creation (device "
+                       "arena recycled from the microbenchmark context); each Newton step one vts_newton_step "
+                       "(device-resident, CUDA graphs, one host synchronisation per step); wall_s_runs[0] is "
+                       "the process's first solve",
                "outer": rep.outer_iterations, **rep.totals(), "compliance": rep.objective,
                "converged": rep.converged}
         os.environ["VTS_HOST_NEWTON"] = "1"  # the call-by-call host orchestration, same kernels (same bits)
-        t_p = time.perf_counter()
-        rep_h = vts.solve_pbm(vts.build_config("C4"))
-        pbm["host_orchestrated_wall_s"] = time.perf_counter() - t_p
+        walls_h, rep_h = timed_solves(3)
+        pbm["host_orchestrated_wall_s"] = sorted(walls_h)[1]
+        pbm["host_orchestrated_wall_s_runs"] = walls_h
         pbm["host_orchestrated_same_result"] = bool(rep_h.objective == rep.objective and rep_h.rows == rep.rows)
         os.environ.pop("VTS_HOST_NEWTON")
     cpu = None
