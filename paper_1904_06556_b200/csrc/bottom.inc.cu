@@ -41,11 +41,17 @@ constexpr int kBotMaxLevels = 8;
 #ifndef VTS_BOT_EXP
 #define VTS_BOT_EXP 0  // probe-only timing experiments on bot_coarse (results then wrong)
 #endif
-#ifdef VTS_BOT_PROBE
-constexpr size_t kBotSmemMax = 226 * 1024;  // (the probe's marks take static shared memory)
-#else
-constexpr size_t kBotSmemMax = 227 * 1024;  // the opt-in dynamic shared memory limit of one CTA
+// the opt-in shared memory limit of one CTA less 1 KB of static shared memory (the prefetch
+// barrier, the probe's marks)
+constexpr size_t kBotSmemMax = 226 * 1024;
+// The top fused level's first half-stencil (99 KB on C3) is fetched by one bulk copy issued
+// BEFORE the kernel waits for the grids ahead of it (the stencils date from mg_setup): the
+// first sweep's staging, 8.5 us of dependent global loads, shrinks to a barrier wait.
+// VTS_BOT_PREFETCH=0: every staging by the block's threads.
+#ifndef VTS_BOT_PREFETCH
+#define VTS_BOT_PREFETCH 1
 #endif
+__shared__ unsigned long long s_bot_bar;
 
 struct BotLevel {
   int nx, ny, nn, ngrid;
@@ -79,7 +85,8 @@ struct BotArgs {
 // after its first use; inlined copies per call site ran 3.6x slower cold)
 constexpr int kBotPad = 64;  // zero nodes before/after the staged level (>= 2 x 31, the largest skew)
 template <bool FWD, bool ZERO>
-__device__ __noinline__ void bot_sweep(const BotLevel& L, double* sm, const BotArgs& A, bool restage) {
+// restage: 0 the stage still holds this level's half, 1 copy it, 2 it was prefetched (wait for the bulk copy)
+__device__ __noinline__ void bot_sweep(const BotLevel& L, double* sm, const BotArgs& A, int restage) {
   double* sb = sm + L.off_b;
   double* sx = sm + L.off_x;
   double* stage = sm + A.off_stage;  // [(nn + 2 pad) * kHalf] the half the wavefront solves with
@@ -93,8 +100,9 @@ __device__ __noinline__ void bot_sweep(const BotLevel& L, double* sm, const BotA
     const double2* src = reinterpret_cast<const double2*>(solve_half);
     double2* dst = reinterpret_cast<double2*>(stage);
     const int lo = kBotPad * kHalf / 2, hi = (kBotPad + nn) * kHalf / 2, end = (2 * kBotPad + nn) * kHalf / 2;
-    if (restage)  // the second sweep of a smoothing step solves with the same half: still staged
+    if (restage == 1)  // the second sweep of a smoothing step solves with the same half: still staged
       for (int i = tid; i < end; i += blockDim.x) dst[i] = (i >= lo && i < hi) ? src[i - lo] : make_double2(0.0, 0.0);
+    if (restage == 2) mbar_wait(&s_bot_bar, 0);  // the prefetched half has landed (its pads were zeroed at the start)
     const double xa = sx[L.ngrid];
     double2* pd = reinterpret_cast<double2*>(pst);
     for (int i = tid; i < nn + 2 * kBotPad; i += blockDim.x) {
@@ -396,11 +404,36 @@ __device__ __noinline__ void bot_coarse(const BotLevel& C, double* sm, const Bot
 }
 
 __global__ void __launch_bounds__(kBotThreads, 1) k_vcycle_bottom(const __grid_constant__ BotArgs A, const int* skip) {
-  pdl_enter();
-  if (skip && *skip) return;
-  VTS_TL_BEGIN(4, 5);
   extern __shared__ __align__(16) double sm[];
   const int tid = threadIdx.x;
+#if VTS_BOT_PREFETCH
+  {
+    // before the wait: nothing here depends on the grids ahead (read-only setup data -> shared memory)
+    const BotLevel& T = A.lv[A.kb];
+    double* stage = sm + A.off_stage;
+    const unsigned bytes = (unsigned)((size_t)T.nn * kHalf * sizeof(double));
+    if (tid == 0) {
+      mbar_init(&s_bot_bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(&s_bot_bar, bytes);
+      bulk_g2s(stage + (size_t)kBotPad * kHalf, T.stL, bytes, &s_bot_bar);
+    }
+    double2* dst = reinterpret_cast<double2*>(stage);
+    const int lo = kBotPad * kHalf / 2, hi = (kBotPad + T.nn) * kHalf / 2, end = (2 * kBotPad + T.nn) * kHalf / 2;
+    for (int i = tid; i < lo; i += blockDim.x) dst[i] = make_double2(0.0, 0.0);
+    for (int i = hi + tid; i < end; i += blockDim.x) dst[i] = make_double2(0.0, 0.0);
+  }
+#endif
+  pdl_enter();
+  if (skip && *skip) {
+#if VTS_BOT_PREFETCH
+    __syncthreads();  // (the barrier's initialisation)
+    mbar_wait(&s_bot_bar, 0);  // no bulk copy may still be writing into this CTA's shared memory
+#endif
+    return;
+  }
+  VTS_TL_BEGIN(4, 5);
 #ifdef VTS_BOT_PROBE
   if (tid == 0) s_bot_n = 0;
   __syncthreads();
@@ -416,8 +449,8 @@ __global__ void __launch_bounds__(kBotThreads, 1) k_vcycle_bottom(const __grid_c
     const BotLevel& L = A.lv[k];
     if (tid == 0) sm[L.off_x + L.ngrid] = 0.0;  // k_alpha_init on a coarse level
     __syncthreads();
-    bot_sweep<true, true>(L, sm, A, true);
-    bot_sweep<true, false>(L, sm, A, false);
+    bot_sweep<true, true>(L, sm, A, (VTS_BOT_PREFETCH && k == A.kb) ? 2 : 1);
+    bot_sweep<true, false>(L, sm, A, 0);
     bot_residual(L, sm, A);
     BOT_MARK();  // residual
     const BotLevel& C = A.lv[k - 1];
@@ -444,8 +477,8 @@ __global__ void __launch_bounds__(kBotThreads, 1) k_vcycle_bottom(const __grid_c
     }
     __syncthreads();
     BOT_MARK();  // prolongated
-    bot_sweep<false, false>(L, sm, A, true);
-    bot_sweep<false, false>(L, sm, A, false);
+    bot_sweep<false, false>(L, sm, A, 1);
+    bot_sweep<false, false>(L, sm, A, 0);
   }
   {
     const BotLevel& T = A.lv[A.kb];
