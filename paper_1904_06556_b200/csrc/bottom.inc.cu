@@ -48,6 +48,10 @@ constexpr size_t kBotSmemMax = 226 * 1024;
 // BEFORE the kernel waits for the grids ahead of it (the stencils date from mg_setup): the
 // first sweep's staging, 8.5 us of dependent global loads, shrinks to a barrier wait.
 // VTS_BOT_PREFETCH=0: every staging by the block's threads.
+#ifndef VTS_BOT_UNROLL
+#define VTS_BOT_UNROLL 4  // steps per trip of the wavefront loop (code size against loop overhead)
+#endif
+constexpr int kBotUnroll = VTS_BOT_UNROLL;
 #ifndef VTS_BOT_PREFETCH
 #define VTS_BOT_PREFETCH 1
 #endif
@@ -191,7 +195,7 @@ __device__ __noinline__ void bot_sweep(const BotLevel& L, double* sm, const BotA
     StepData cur = prepare(ra, win[0], win[1]);
     load_raw(1, ra);  // (reads at most two nodes past the last step: inside the stage's zero pad)
     double* const trash = sm + A.off_red;  // stores of off-row positions land here (unused during sweeps)
-#pragma unroll 4
+#pragma unroll kBotUnroll
     for (int t = 0; t < T; ++t) {
       const int j = t - 2 * l;
       const double2 nv = gs_rec2<d0>(cur.q0, cur.q1, cur.w00, cur.w01, cur.w10, cur.w11, cur.e00, cur.e01, cur.e10,
