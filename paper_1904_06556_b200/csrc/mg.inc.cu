@@ -989,14 +989,22 @@ constexpr int kBuild = 6;  // pipelined pair, sweep B: builder warps (<= 2 nodes
 // Pair CTAs have 16 warps.  Warp w runs on SM sub-partition w % 4: the compute
 // warp (0) must keep its sub-partition's issue slots and fp64 pipe, so the
 // builders sit on warps with w % 4 in {1, 2} (5 6 9 10 13 14), away from the
-// compute warp's and the publisher's sub-partitions (0, 3); warps 8 and 12
+// compute warp's and the publisher's sub-partitions (0, 3); warps 11 and 15
 // issue sweep B's builder-input boxes (x_A after an acquire-poll, and U, b,
 // border), warp 4 is the (cross-cluster) stager: all light loops.
 constexpr int kWarpsPair = 16;
 constexpr int gs_chunk = kChunk;  // columns per k_prolong_rows item
-constexpr int kXLoadWarp = 8;
+// (the two polling loader warps sit on sub-partition 3 with the publisher and the releaser, not
+// on the compute warp's: warps 11 / 15 instead of 8 / 12 -- finest pairs 266 -> 263 us and 280 -> 277 us)
+#ifndef VTS_XLOAD_WARP
+#define VTS_XLOAD_WARP 11
+#endif
+#ifndef VTS_BLOAD_WARP
+#define VTS_BLOAD_WARP 15
+#endif
+constexpr int kXLoadWarp = VTS_XLOAD_WARP;
 constexpr int kReleaseWarp = 7;  // sweep A: publishes the stored-window counters (backs off while waiting)
-constexpr int kBLoadWarp = 12;
+constexpr int kBLoadWarp = VTS_BLOAD_WARP;
 VTS_DEVICE_INLINE int builder_index(int warp) {  // -1: not a builder warp (sub-partitions 1 and 2 only)
   return (warp < kWarps || (warp & 3) == 0 || (warp & 3) == 3) ? -1 : 2 * ((warp - kWarps) / 4) + ((warp - kWarps) & 1);
 }
